@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""Benchmark: batched malloc/free trace replay (Scalene, arXiv 2212.07597) on B200.
+
+Contract (driver): ``python bench.py --gpus N --steps K --warmup W [--impl reference]``
+prints ONE JSON line on rank 0.  A step is one pass of the whole hot path
+a1..a6 over the resident workload: scl_replay_run (streaming
+replay kernel + per-sample reduce) -> [N>1: NCCL all-reduce of the int64 site
+table] -> scl_finalize (probabilities, flags, report order, rows).
+
+Workload (N=1): BASELINE configs[1] = config 2, 64 traces x 1M events, 1000
+sites, 4 planted leaks, T = next_prime(10 MiB).  N>1: weak scaling -- every
+rank replays its own 64-trace batch (trace ids rank*64 ...), and the per-site
+tables are summed with one all-reduce (the method's only exchange step).
+
+--impl reference: the CPU oracle (oracle/oracle.c) as it stands, on the host
+cores, on the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "malloc/free events/sec replayed (1/2/4/8 B200) and % of HBM peak"
+BYTES_PER_EVENT = 16
+SAMPLE_BYTES = 32
+ROW_BYTES_TABLE = 80
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--traces", type=int, default=0, help="override traces per rank (testing)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def workload(cfg, n_traces_rank, world):
+    return {"workload": f"{cfg.name}: {n_traces_rank} traces/GPU x {cfg.events_per_trace} events, "
+                        f"{cfg.n_sites} sites (Zipf {cfg.zipf_s}), {cfg.n_planted} planted leaks, T={cfg.T}",
+            "traces_per_gpu": n_traces_rank, "events_per_trace": cfg.events_per_trace,
+            "n_sites": cfg.n_sites, "threshold": cfg.T, "event_bytes": BYTES_PER_EVENT,
+            "l2": f"inputs larger than L2 ({n_traces_rank * cfg.events_per_trace * 16 / 1e9:.2f} GB > 0.126 GB); no flush needed",
+            "parallelism": f"dp{world} (trace shards, int64 all-reduce of the site table)"}
+
+
+class ClockSampler:
+    """NVML polling of SM clock and throttle reasons during the timed region."""
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.stop = [], set(), threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+            self.max = None
+
+    def _run(self):
+        nv = self.nv
+        names = {getattr(nv, k, None): k for k in (
+            "nvmlClocksEventReasonGpuIdle", "nvmlClocksEventReasonApplicationsClocksSetting",
+            "nvmlClocksEventReasonSwPowerCap", "nvmlClocksEventReasonHwSlowdown",
+            "nvmlClocksEventReasonSwThermalSlowdown", "nvmlClocksEventReasonHwThermalSlowdown",
+            "nvmlClocksEventReasonHwPowerBrakeSlowdown", "nvmlClocksEventReasonSyncBoost")}
+        while not self.stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in names.items():
+                    if bit and (r & bit):
+                        self.reasons.add(name.replace("nvmlClocksEventReason", "").lower())
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self.stop.set()
+            self.t.join()
+
+    def summary(self):
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max, "reasons": sorted(self.reasons - {"gpuidle"}),
+                "n_samples": len(self.samples), "source": "nvml, 2 ms polling during the timed region"}
+
+
+def measured_peak():
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(mp["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy_ read+write, measured)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def ncu_traffic(config_id):
+    """dram bytes per replay_kernel launch from the committed ncu --set full capture, if any."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        e = d.get(f"cfg{config_id}")
+        return e["dram_bytes_per_launch"] if e else None
+    except Exception:
+        return None
+
+
+def cpu_oracle_baseline(ev, off, cfg, reps=3):
+    """The oracle as it stands, on all host cores and on 1 core, on the full
+    rank-0 workload (a few core-seconds, bounded)."""
+    import oracle
+    lib = oracle._load()
+    nt = len(off) - 1
+    cap = oracle.sample_bound(ev, off, cfg.T)
+    soff = np.zeros(nt + 1, dtype=np.uint64)
+    soff[1:] = np.cumsum(cap)
+    samples = np.zeros(max(int(soff[-1]), 1), dtype=oracle.SAMPLE_DTYPE)
+    summ = np.zeros(nt, dtype=oracle.SUMMARY_DTYPE)
+    table = np.zeros((cfg.n_sites, oracle.NCOL), dtype=np.uint64)
+    cores = os.cpu_count() or 1
+    res = {}
+    for threads in (cores, 1):
+        best = None
+        for _ in range(reps if threads > 1 else 1):
+            t0 = time.perf_counter()
+            lib.orc_replay_all(oracle._ptr(ev), oracle._ptr(off), nt, cfg.n_sites, cfg.T, 0, threads,
+                               oracle._ptr(samples), oracle._ptr(soff), oracle._ptr(summ), oracle._ptr(table))
+            num, den, op = oracle.gate(summ)
+            prob, rate, flag = oracle.finalize(table, op, oracle.elapsed_ns(off))
+            oracle.report_order(rate, flag)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        res[threads] = len(ev) / best
+    return {"value": res[cores], "unit": "events/s", "cores": cores, "kind": "oracle",
+            "value_1core": res[1],
+            "sample": f"the full rank-0 workload ({len(ev)} events, {nt} traces), a1..a6, best of {reps}"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle on the host cores (rank 0 only)."""
+    import tracegen
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = tracegen.CONFIGS[args.config]
+    ntr = args.traces or cfg.n_traces
+    ev, off = tracegen.generate(cfg.with_traces(ntr))
+    import oracle
+    lib = oracle._load()
+    nt = len(off) - 1
+    cap = oracle.sample_bound(ev, off, cfg.T)
+    soff = np.zeros(nt + 1, dtype=np.uint64)
+    soff[1:] = np.cumsum(cap)
+    samples = np.zeros(max(int(soff[-1]), 1), dtype=oracle.SAMPLE_DTYPE)
+    summ = np.zeros(nt, dtype=oracle.SUMMARY_DTYPE)
+    table = np.zeros((cfg.n_sites, oracle.NCOL), dtype=np.uint64)
+    cores = os.cpu_count() or 1
+
+    def step():
+        lib.orc_replay_all(oracle._ptr(ev), oracle._ptr(off), nt, cfg.n_sites, cfg.T, 0, cores,
+                           oracle._ptr(samples), oracle._ptr(soff), oracle._ptr(summ), oracle._ptr(table))
+        num, den, op = oracle.gate(summ)
+        prob, rate, flag = oracle.finalize(table, op, oracle.elapsed_ns(off))
+        oracle.report_order(rate, flag)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    v = len(ev) * args.steps / dt
+    print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": "events/s",
+                      "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                      "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+                      "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+                      "config": workload(cfg, ntr, 1),
+                      "cpu_baseline": {"value": v, "unit": "events/s", "cores": cores, "kind": "oracle",
+                                       "sample": f"full workload ({len(ev)} events) per step"},
+                      "e2e": {"value": v, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2212_07597_b200 as scl
+    import tracegen
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = tracegen.CONFIGS[args.config]
+    ntr = args.traces or cfg.n_traces
+    gcfg = cfg.with_traces(ntr * world)
+    # pinned host copy of this rank's traces (inputs of the e2e leg)
+    n_ev = ntr * cfg.events_per_trace
+    pinned = torch.empty(n_ev * 2, dtype=torch.int64, pin_memory=True)
+    host_ev = pinned.numpy().view(tracegen.EVENT_DTYPE)
+    _, off_local = tracegen.generate(gcfg, rank * ntr, (rank + 1) * ntr, out=host_ev)
+    stream = torch.cuda.current_stream()
+    elapsed_ns = cfg.events_per_trace * 1000          # global max n_t * tick (all traces equal)
+
+    tr = scl.scl_trace_load(host_ev, off_local, cfg.n_sites, device=local)
+    r = None
+
+    def step(r):
+        r = scl.scl_replay_run(cfg.T, tr, stream=stream, out=r, defer_finalize=world > 1, elapsed_ns=elapsed_ns)
+        if world > 1:
+            dist.all_reduce(scl.device_table_tensor(r))
+            scl.scl_finalize(r, elapsed_ns)
+        return r
+
+    for _ in range(max(args.warmup, 3)):
+        r = step(r)
+    kern_ms, n_samples = [], 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            r = step(r)
+            kern_ms.append(scl.scl_result_timing(r)[0])
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    total_events = n_ev * world * args.steps
+    value = total_events / (ms_max / 1e3)
+
+    summ = scl.scl_trace_summaries(r)
+    n_samples = int(summ["n_samples"].sum())
+    kern_avg = statistics.mean(kern_ms)
+    alg_bytes = n_ev * BYTES_PER_EVENT + n_samples * SAMPLE_BYTES + cfg.n_sites * ROW_BYTES_TABLE
+    achieved = alg_bytes / (kern_avg / 1e3) / 1e9
+    peak, peak_src = measured_peak()
+    traffic = ncu_traffic(args.config)
+
+    # e2e through the public API: H2D of this step's events from pinned memory, replay, report D2H
+    e2e = None
+    if not args.no_e2e:
+        torch.cuda.synchronize()
+        reps = max(2, min(5, args.steps))
+        tr2 = scl.scl_trace_load(host_ev, off_local, cfg.n_sites, device=local)   # warm allocator
+        tr2.free()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            trx = scl.scl_trace_load(host_ev, off_local, cfg.n_sites, device=local)
+            rx = scl.scl_replay_run(cfg.T, trx, stream=stream, defer_finalize=world > 1, elapsed_ns=elapsed_ns)
+            if world > 1:
+                dist.all_reduce(scl.device_table_tensor(rx))
+                scl.scl_finalize(rx, elapsed_ns)
+            rows = scl.scl_site_report(rx)
+            rx.free()
+            trx.free()
+        torch.cuda.synchronize()
+        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e = {"value": n_ev * world * reps / float(dt.item()), "unit": "events/s",
+               "h2d_bytes_per_step": int(n_ev * 16 + off_local.nbytes),
+               "d2h_bytes_per_step": int(rows.nbytes + 24),
+               "note": "scl_trace_load(pinned host events) + scl_replay_run + scl_site_report per step"}
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu:
+            cpu = cpu_oracle_baseline(host_ev, off_local, cfg)
+        out = {
+            "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic (tracegen, seeded)",
+            "config": workload(cfg, ntr, world),
+            "hbm_gbs_step": total_events * BYTES_PER_EVENT / (ms_max / 1e3) / 1e9,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "scl::replay_kernel",
+                         "kernel_ms": kern_avg, "peak_source": peak_src,
+                         "alg_bytes_per_launch": alg_bytes,
+                         "alg_bytes_rule": "16 B/event read + 32 B/sample written + 80 B/site table flush",
+                         "frac_of_8tbs_spec": achieved / 8000.0},
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "gpu_launches": 4 * args.steps,
+            "gpu_launches_note": "per step: replay_kernel, samples_kernel, finalize_kernel, rows_kernel "
+                                 "(+ CUB radix-sort kernels for the report order, library)",
+            "n_samples_per_step": n_samples,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,181 @@
+/*
+ * include/scl.h -- C-ABI of the B200 trace-replay library (libscl.so).
+ *
+ * What it computes: batched replay of recorded malloc/free traces through
+ * Scalene's memory-profiling method (Berger et al., arXiv 2212.07597;
+ * "P:a-b" = lines of PAPER.md):
+ *   a1 footprint prefix sum ........ P:430-431
+ *   a2 high-water-mark prefix max .. P:24-25
+ *   a3 threshold sampler ........... P:429-438 ("|A - F| >= T" then reset)
+ *   a4 leak tracker + ptr match .... P:20-39
+ *   a5 per-(file,line) reduce ...... P:488-494
+ *   a6 leak probability/filter/rate
+ * Every trace is replayed independently (its own sampler and tracker); only
+ * the per-site table is summed over traces (and over GPUs).  Readings where
+ * the paper is silent are DESIGN.md §3.
+ *
+ * Conventions
+ *  - Every call returns scl_status (0 = OK, negative = error);
+ *    scl_last_error() returns a thread-local message for the last failure.
+ *  - Pointers passed IN may be host or device memory (detected with
+ *    cudaPointerGetAttributes); the library copies what it keeps.  The
+ *    caller always owns its arrays; the library owns handles until *_free.
+ *  - Size queries: pass cap = 0 (out buffer may be NULL) to get the count.
+ *  - All work is queued on opts->cuda_stream (NULL = the legacy default
+ *    stream) and is complete when the call returns, unless stated otherwise.
+ *  - A handle is not safe for concurrent use from several threads.
+ *  - There is no CPU fallback: without a CUDA device every compute call
+ *    fails with SCL_ECUDA.
+ */
+#ifndef SCL_H
+#define SCL_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SCL_OK = 0,
+    SCL_EINVAL = -1,     /* bad argument: threshold 0, site >= n_sites, size 0, kind 3, NULL ... */
+    SCL_ENOMEM = -2,     /* device or host allocation failed */
+    SCL_ECUDA = -3,      /* CUDA runtime error or no device */
+    SCL_ETRACE = -4,     /* invalid trace (validate = 1): message names trace and first bad event */
+    SCL_EOVERFLOW = -5,  /* a result does not fit (e.g. > 2^21 sites) */
+    SCL_EIO = -6,        /* trace file unreadable or malformed */
+    SCL_ENCCL = -7       /* reserved: collective failure */
+} scl_status;
+
+/* One trace event, 16 bytes, 16-byte aligned, array-of-structs.
+ *   ptr : the address passed to / returned by the allocator (pointer identity)
+ *   meta: bits  0..39  size in bytes, 1 .. 2^40-1
+ *         bits 40..41  kind: 0 alloc, 1 free, 2 copy (ignored by a1..a6: copies
+ *                      do not change the footprint), 3 invalid
+ *         bit  42      domain (0 native, 1 Python-managed; carried, unused by a1..a6)
+ *         bits 43..63  site id (< 2^21): dense index of a (file, line) pair */
+typedef struct { uint64_t ptr; uint64_t meta; } scl_event;
+
+#define SCL_META(kind, size, site) \
+    (((uint64_t)(size) & 0xFFFFFFFFFFull) | ((uint64_t)(kind) << 40) | ((uint64_t)(site) << 43))
+
+/* One threshold-sampler entry (the sampling-file entry of P:433-434), 32 bytes.
+ *   idx       event index within its trace that triggered the sample
+ *   net       signed bytes since the previous sample (the counter value, |net| >= T)
+ *   footprint F at that event
+ *   site      site of the triggering event (reading Q14)
+ *   kind      0 growth (net > 0, always an alloc), 1 decline (always a free)
+ *   new_max   1 if a growth sample reached a new high-water mark (episode start) */
+typedef struct {
+    uint64_t idx; int64_t net; int64_t footprint;
+    uint32_t site; uint8_t kind; uint8_t new_max; uint16_t pad;
+} scl_sample;
+
+/* Site-table columns (one uint64 row of SCL_NCOL per site, a5). */
+enum {
+    SCL_COL_N_MALLOC = 0, SCL_COL_N_FREE, SCL_COL_MALLOC_BYTES, SCL_COL_FREE_BYTES,
+    SCL_COL_N_GROWTH, SCL_COL_N_DECLINE, SCL_COL_GROWTH_BYTES, SCL_COL_DECLINE_BYTES,
+    SCL_COL_LEAK_MALLOCS, SCL_COL_LEAK_FREES, SCL_NCOL
+};
+
+/* One report row (a6).  leak_prob = 1 - (f+1)/(m-f+2), fp64, unclamped (P:55-57,
+ * reading Q8); leak_rate_mbps = malloc_bytes / 2^20 / elapsed_s (Q11);
+ * leak_flag = gate open AND p > 0.95, decided as m > 21 f + 18 (Q9). */
+typedef struct {
+    uint32_t site; uint32_t leak_flag;
+    uint64_t col[SCL_NCOL];
+    double leak_prob; double leak_rate_mbps;
+} scl_site_row;
+
+typedef struct {
+    int64_t f_final;          /* footprint after the last event = sum of signed sizes (a1) */
+    int64_t hwm;              /* max(0, max_i F_i) (a2) */
+    uint64_t n_samples;       /* threshold samples in the trace (a3) */
+    uint64_t n_episodes;      /* leak-tracking episodes = new-max growth samples (a4) */
+    int64_t f_first_sample;   /* footprint at the first / last sample (0 if none): */
+    int64_t f_last_sample;    /*   the footprint trend endpoints used by the gate */
+} scl_trace_summary;
+
+enum { SCL_HWM_PREFIX = 0 };                          /* reading Q3 (prefix max) */
+enum { SCL_FORMULA_PAPER = 0, SCL_FORMULA_TEXTBOOK = 1 };
+
+typedef struct {
+    uint64_t tick_ns;        /* synthetic time base: event i at (i+1)*tick_ns; 0 -> 1000 */
+    int hwm_mode;            /* SCL_HWM_PREFIX only */
+    int formula;             /* SCL_FORMULA_PAPER (default) or SCL_FORMULA_TEXTBOOK (Laplace) */
+    int defer_finalize;      /* 1: stop after the site table (a1-a5); the caller may sum the
+                                device table across GPUs (scl_result_device_table) and then
+                                call scl_finalize.  0: finalize immediately. */
+    int reserved;
+    uint64_t elapsed_ns;     /* 0: max_t n_t * tick_ns over this handle's traces */
+    void* cuda_stream;       /* cudaStream_t, NULL = default stream */
+} scl_run_opts;
+
+typedef struct scl_traces scl_traces;  /* opaque: device copy of events + offsets + segment plan */
+typedef struct scl_result scl_result;  /* opaque: samples, summaries, site table, report */
+
+/* Load traces into library-owned device memory.
+ *   path      binary trace file ("SCLTRC01" format) or NULL to use the arrays
+ *   events    n = offsets[n_traces] events (host or device pointer)
+ *   offsets   n_traces+1 uint64 event offsets, offsets[0] = 0, non-decreasing (host or device)
+ *   n_sites   number of distinct sites (1 .. 2^21); every event site must be < n_sites
+ *   device    CUDA device ordinal
+ *   validate  1: host-side validity check (reading Q16); returns SCL_ETRACE naming the trace
+ *             and first bad event.  0: skip (an invalid trace gives undefined results).
+ * Errors: SCL_EINVAL (NULL, n_sites 0 or > 2^21, bad offsets), SCL_ETRACE, SCL_ENOMEM,
+ *         SCL_ECUDA, SCL_EIO. */
+scl_status scl_trace_load(const char* path, const scl_event* events, const uint64_t* offsets,
+                          uint32_t n_traces, uint32_t n_sites, int device, int validate,
+                          scl_traces** out);
+
+/* Replay every trace at threshold T (used verbatim; P:436-438 picks a prime slightly
+ * above 10 MB -- see scl_next_prime).  Runs a1..a5 on the GPU and, unless
+ * opts->defer_finalize, a6.  threshold == 0 -> SCL_EINVAL. */
+scl_status scl_replay_run(uint64_t threshold, const scl_traces* traces,
+                          const scl_run_opts* opts, scl_result** out);
+
+/* Device pointer to the result's summable int64 table: n_sites*SCL_NCOL site-table
+ * values followed by 3 gate values (sum of F_last-F_first, sum of max(F_first,1),
+ * number of traces with >= 2 samples).  Summing it element-wise across GPUs (an
+ * int64 all-reduce) gives the multi-GPU table. */
+scl_status scl_result_device_table(scl_result* r, int64_t** dev_ptr, size_t* n_int64);
+
+/* a6 on the (possibly all-reduced) table: probabilities, rates, flags, report order.
+ * elapsed_ns 0 -> keep the run's value (use the global max across GPUs otherwise). */
+scl_status scl_finalize(scl_result* r, uint64_t elapsed_ns);
+
+/* Report rows in report order: flagged sites by (rate desc, site asc), then the rest by
+ * site asc (a6).  rows may be NULL with cap 0; *n_rows = n_sites. */
+scl_status scl_site_report(const scl_result* r, scl_site_row* rows, size_t cap, size_t* n_rows);
+
+/* Samples of one trace, in event order (host buffer).  *n = the trace's sample count. */
+scl_status scl_samples(const scl_result* r, uint32_t trace, scl_sample* out, size_t cap, size_t* n);
+
+/* All traces' summaries (host buffer of n_traces). */
+scl_status scl_trace_summaries(const scl_result* r, scl_trace_summary* out, size_t cap, size_t* n);
+
+/* Gate of P:62-65 (reading Q10): num = sum(F_last - F_first), den = sum max(F_first,1)
+ * over traces with >= 2 samples; open iff some trace qualifies and 100*num >= den. */
+scl_status scl_gate(const scl_result* r, int64_t* num, int64_t* den, int* open);
+
+/* Device time of the last run, in ms, from CUDA events on the run's stream:
+ *   replay_kernel_ms  the streaming a1..a5 kernel alone (the roofline kernel)
+ *   run_ms            a1..a5 including per-run clears and the per-sample reduce
+ *   finalize_ms       a6 (probabilities, flags, report order, rows) */
+scl_status scl_result_timing(const scl_result* r, float* replay_kernel_ms, float* run_ms, float* finalize_ms);
+
+void scl_traces_free(scl_traces* t);
+void scl_result_free(scl_result* r);
+const char* scl_last_error(void);
+
+/* Smallest prime >= base ("a prime number slightly above 10MB"). */
+uint64_t scl_next_prime(uint64_t base);
+
+/* Number of events / traces / sites held by a handle. */
+scl_status scl_traces_info(const scl_traces* t, uint64_t* n_events, uint32_t* n_traces,
+                           uint32_t* n_sites);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCL_H */

@@ -1,0 +1,267 @@
+"""B200-native batched replay of malloc/free traces through Scalene's memory
+profiling method (arXiv 2212.07597): footprint / high-water mark, threshold
+sampler, leak tracker and per-site leak report.
+
+This package is a thin ctypes binding over ``libscl.so`` (C-ABI in
+``include/scl.h``); it only marshals arguments.  Every step of the hot path runs
+in the sm_100a kernels of ``csrc/``.  There is no CPU fallback: if the library
+cannot be loaded, importing this package raises, and without a CUDA device
+every compute call raises ``SclError`` (SCL_ECUDA).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import _build
+
+__all__ = ["SclError", "Traces", "Result", "scl_trace_load", "scl_replay_run", "scl_finalize",
+           "scl_site_report", "scl_samples", "scl_trace_summaries", "scl_gate", "scl_result_device_table",
+           "scl_result_timing", "scl_next_prime", "scl_traces_info", "EVENT_DTYPE", "SAMPLE_DTYPE",
+           "SUMMARY_DTYPE", "SITE_ROW_DTYPE", "COLS", "device_table_tensor", "write_trace_file"]
+
+EVENT_DTYPE = np.dtype([("ptr", "<u8"), ("meta", "<u8")])
+SAMPLE_DTYPE = np.dtype([("idx", "<u8"), ("net", "<i8"), ("footprint", "<i8"), ("site", "<u4"),
+                         ("kind", "u1"), ("new_max", "u1"), ("pad", "<u2")])
+SUMMARY_DTYPE = np.dtype([("f_final", "<i8"), ("hwm", "<i8"), ("n_samples", "<u8"), ("n_episodes", "<u8"),
+                          ("f_first_sample", "<i8"), ("f_last_sample", "<i8")])
+SITE_ROW_DTYPE = np.dtype([("site", "<u4"), ("leak_flag", "<u4"), ("col", "<u8", (10,)),
+                           ("leak_prob", "<f8"), ("leak_rate_mbps", "<f8")])
+COLS = ("n_malloc", "n_free", "malloc_bytes", "free_bytes", "n_growth", "n_decline",
+        "growth_bytes", "decline_bytes", "leak_mallocs", "leak_frees")
+STATUS = {0: "SCL_OK", -1: "SCL_EINVAL", -2: "SCL_ENOMEM", -3: "SCL_ECUDA", -4: "SCL_ETRACE",
+          -5: "SCL_EOVERFLOW", -6: "SCL_EIO", -7: "SCL_ENCCL"}
+assert SAMPLE_DTYPE.itemsize == 32 and SUMMARY_DTYPE.itemsize == 48 and SITE_ROW_DTYPE.itemsize == 104
+
+
+class SclError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _RunOpts(ctypes.Structure):
+    _fields_ = [("tick_ns", ctypes.c_uint64), ("hwm_mode", ctypes.c_int), ("formula", ctypes.c_int),
+                ("defer_finalize", ctypes.c_int), ("reserved", ctypes.c_int), ("elapsed_ns", ctypes.c_uint64),
+                ("cuda_stream", ctypes.c_void_p)]
+
+
+def _load():
+    if not os.path.exists(_build.LIB):
+        raise ImportError(f"{_build.LIB} is missing: run __graft_entry__.build() (nvcc for sm_100a)")
+    lib = ctypes.CDLL(_build.LIB)
+    P, U64, U32, I32, SZ = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_size_t
+    sig = {
+        "scl_trace_load": [ctypes.c_char_p, P, P, U32, U32, I32, I32, P],
+        "scl_replay_run": [U64, P, P, P],
+        "scl_result_device_table": [P, P, P],
+        "scl_finalize": [P, U64],
+        "scl_site_report": [P, P, SZ, P],
+        "scl_samples": [P, U32, P, SZ, P],
+        "scl_trace_summaries": [P, P, SZ, P],
+        "scl_gate": [P, P, P, P],
+        "scl_result_timing": [P, P, P, P],
+        "scl_traces_info": [P, P, P, P],
+    }
+    for name, args in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int
+    lib.scl_traces_free.argtypes = [P]
+    lib.scl_traces_free.restype = None
+    lib.scl_result_free.argtypes = [P]
+    lib.scl_result_free.restype = None
+    lib.scl_last_error.restype = ctypes.c_char_p
+    lib.scl_next_prime.argtypes = [U64]
+    lib.scl_next_prime.restype = U64
+    return lib
+
+
+lib = _load()
+
+
+def _check(st: int):
+    if st != 0:
+        raise SclError(st, (lib.scl_last_error() or b"").decode())
+
+
+def _addr(x):
+    """Host numpy array or CUDA tensor -> raw address."""
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    return x.ctypes.data
+
+
+class Traces:
+    """Owning handle of scl_traces (device copy of events + offsets + segment plan)."""
+
+    def __init__(self, handle, n_traces, n_sites):
+        self._h = ctypes.c_void_p(handle)
+        self.n_traces, self.n_sites = n_traces, n_sites
+
+    @property
+    def handle(self):
+        return self._h
+
+    def free(self):
+        if self._h:
+            lib.scl_traces_free(self._h)
+            self._h = ctypes.c_void_p(None)
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class Result:
+    """Owning handle of scl_result."""
+
+    def __init__(self, traces: Traces):
+        self._h = ctypes.c_void_p(None)
+        self.traces = traces
+
+    @property
+    def handle(self):
+        return self._h
+
+    def free(self):
+        if self._h:
+            lib.scl_result_free(self._h)
+            self._h = ctypes.c_void_p(None)
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def scl_trace_load(events=None, offsets=None, n_sites: int = 0, device: int = 0, validate: bool = False,
+                   path: str | None = None) -> Traces:
+    """events: host EVENT_DTYPE array or CUDA tensor (int64 / uint8 view of 16-B events);
+    offsets: uint64 [n_traces+1] (host or CUDA)."""
+    out = ctypes.c_void_p()
+    if path is not None:
+        _check(lib.scl_trace_load(path.encode(), None, None, 0, 0, device, int(validate), ctypes.byref(out)))
+    else:
+        if isinstance(offsets, np.ndarray):
+            offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        if isinstance(events, np.ndarray):
+            events = np.ascontiguousarray(events)
+        n_traces = len(offsets) - 1
+        _check(lib.scl_trace_load(None, _addr(events), _addr(offsets), n_traces, n_sites, device,
+                                  int(validate), ctypes.byref(out)))
+    nev, nt, ns = ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_uint32()
+    _check(lib.scl_traces_info(out, ctypes.byref(nev), ctypes.byref(nt), ctypes.byref(ns)))
+    t = Traces(out.value, nt.value, ns.value)
+    t.n_events = nev.value
+    return t
+
+
+def scl_replay_run(threshold: int, traces: Traces, tick_ns: int = 0, formula: int = 0,
+                   defer_finalize: bool = False, elapsed_ns: int = 0, stream=None,
+                   out: Result | None = None) -> Result:
+    """Replay all traces at threshold T; ``out`` (a previous Result of the same
+    traces) is reused in place.  stream: torch.cuda.Stream / raw handle / None."""
+    o = _RunOpts()
+    o.tick_ns, o.hwm_mode, o.formula = tick_ns, 0, formula
+    o.defer_finalize, o.elapsed_ns = int(defer_finalize), elapsed_ns
+    if stream is not None:
+        o.cuda_stream = getattr(stream, "cuda_stream", stream)
+    r = out if out is not None else Result(traces)
+    h = ctypes.c_void_p(r._h.value)
+    _check(lib.scl_replay_run(threshold, traces.handle, ctypes.byref(o), ctypes.byref(h)))
+    r._h = h
+    return r
+
+
+def scl_result_device_table(r: Result):
+    ptr, n = ctypes.c_void_p(), ctypes.c_size_t()
+    _check(lib.scl_result_device_table(r.handle, ctypes.byref(ptr), ctypes.byref(n)))
+    return ptr.value, n.value
+
+
+def device_table_tensor(r: Result):
+    """torch.int64 CUDA view of the summable table (site table + 3 gate sums),
+    for an all-reduce across ranks before scl_finalize."""
+    import torch
+    ptr, n = scl_result_device_table(r)
+
+    class _Iface:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (ptr, False), "version": 2}
+    return torch.as_tensor(_Iface(), device="cuda")
+
+
+def scl_finalize(r: Result, elapsed_ns: int = 0):
+    _check(lib.scl_finalize(r.handle, elapsed_ns))
+
+
+def scl_site_report(r: Result) -> np.ndarray:
+    n = ctypes.c_size_t()
+    _check(lib.scl_site_report(r.handle, None, 0, ctypes.byref(n)))
+    rows = np.zeros(n.value, dtype=SITE_ROW_DTYPE)
+    _check(lib.scl_site_report(r.handle, rows.ctypes.data, n.value, ctypes.byref(n)))
+    return rows
+
+
+def scl_samples(r: Result, trace: int) -> np.ndarray:
+    n = ctypes.c_size_t()
+    _check(lib.scl_samples(r.handle, trace, None, 0, ctypes.byref(n)))
+    out = np.zeros(n.value, dtype=SAMPLE_DTYPE)
+    if n.value:
+        _check(lib.scl_samples(r.handle, trace, out.ctypes.data, n.value, ctypes.byref(n)))
+    return out
+
+
+def scl_trace_summaries(r: Result) -> np.ndarray:
+    n = ctypes.c_size_t()
+    _check(lib.scl_trace_summaries(r.handle, None, 0, ctypes.byref(n)))
+    out = np.zeros(n.value, dtype=SUMMARY_DTYPE)
+    if n.value:
+        _check(lib.scl_trace_summaries(r.handle, out.ctypes.data, n.value, ctypes.byref(n)))
+    return out
+
+
+def scl_gate(r: Result):
+    num, den, op = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
+    _check(lib.scl_gate(r.handle, ctypes.byref(num), ctypes.byref(den), ctypes.byref(op)))
+    return num.value, den.value, bool(op.value)
+
+
+def scl_result_timing(r: Result):
+    """(replay_kernel_ms, run_ms, finalize_ms) of the last run (CUDA events)."""
+    a, b, c = ctypes.c_float(), ctypes.c_float(), ctypes.c_float()
+    _check(lib.scl_result_timing(r.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+    return a.value, b.value, c.value
+
+
+def scl_next_prime(base: int) -> int:
+    return int(lib.scl_next_prime(base))
+
+
+def scl_traces_info(t: Traces):
+    nev, nt, ns = ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_uint32()
+    _check(lib.scl_traces_info(t.handle, ctypes.byref(nev), ctypes.byref(nt), ctypes.byref(ns)))
+    return nev.value, nt.value, ns.value
+
+
+def write_trace_file(path: str, events: np.ndarray, offsets: np.ndarray, n_sites: int, tick_ns: int = 1000,
+                     site_names=None):
+    """Binary trace file: "SCLTRC01", u32 version=1, u32 n_traces,
+    u32 n_sites, u32 0, u64 tick_ns, u64 offsets[n+1], 16-B events, then an
+    optional site table of "file\\tline\\n" strings (ignored by the loader)."""
+    offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+    with open(path, "wb") as f:
+        f.write(b"SCLTRC01")
+        f.write(np.array([1, len(offsets) - 1, n_sites, 0], dtype=np.uint32).tobytes())
+        f.write(np.array([tick_ns], dtype=np.uint64).tobytes())
+        f.write(offsets.tobytes())
+        f.write(np.ascontiguousarray(events).tobytes())
+        if site_names:
+            f.write("".join(f"{a}\t{b}\n" for a, b in site_names).encode())

@@ -1,0 +1,88 @@
+// scl_internal.cuh -- device-side layout shared by the replay kernels and the
+// host API of libscl.so (not part of the public ABI; see include/scl.h).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include "../../include/scl.h"
+
+namespace scl {
+
+// ---- segment geometry --------------------------------------
+// A segment is 256 rows of 128 B = 8 events per row, one row per thread:
+// 2048 events = 32 KiB staged in shared memory by one 2-D TMA load with the
+// 128-byte swizzle, so that every thread reads its own 8 consecutive events
+// with conflict-free LDS.128.
+constexpr int kThreads = 256;
+constexpr int kEpt = 8;                       // events per thread (one 128-B row)
+constexpr int kSeg = kThreads * kEpt;         // events per segment
+constexpr int kSegBytes = kSeg * 16;
+constexpr int kStages = 2;                    // TMA ring depth per CTA
+constexpr int kHot = 1024;                    // sites with shared-memory Tier-E counters
+constexpr int kCtasPerSm = 2;
+constexpr long long kNeg = -(1ll << 62);      // "no event" sentinels for max / min
+constexpr long long kPos = (1ll << 62);
+constexpr unsigned long long kNoEp = ~0ull;
+
+// ---- event decoding (include/scl.h) ----------------------------------------
+__host__ __device__ inline uint64_t ev_size(uint64_t meta) { return meta & 0xFFFFFFFFFFull; }
+__host__ __device__ inline unsigned ev_kind(uint64_t meta) { return (unsigned)(meta >> 40) & 3u; }
+__host__ __device__ inline uint32_t ev_site(uint64_t meta) { return (uint32_t)(meta >> 43); }
+
+// ---- chained-scan state of one segment (decoupled look-back) ---------------
+// flag = epoch*4 + {1: aggregate published, 2: inclusive published}.
+struct __align__(16) SegState {
+    long long sum, mx, mn;            // aggregate: sum of d, max / min prefix of the local running sum
+    long long F, M, B;                // inclusive: footprint, high-water mark, footprint at last sample
+    unsigned long long n, nep;        // samples / episodes in the trace so far
+    unsigned long long ep, ep_ptr;    // current episode: sample slot of its start, tracked pointer
+    unsigned int flag, pad0, pad1, pad2;
+};
+
+// Per-segment list entry of episodes started inside the segment (phase 4).
+struct EpStart { unsigned long long ep, ptr; unsigned int pos, pad; };
+
+struct ReplayParams {
+    const scl_event* ev;              // padded device copy (multiple of 8 events)
+    const unsigned long long* off;    // [n_traces+1]
+    const unsigned int* tk_trace;     // ticket -> trace
+    const unsigned int* tk_k;         // ticket -> segment index (bit 31: last segment of the trace)
+    const unsigned int* seg_base;     // trace -> first state slot
+    SegState* state;                  // [n_segs]
+    unsigned int* ticket;             // global ticket counter (zeroed per run)
+    unsigned int n_segs;
+    unsigned int epoch;
+    unsigned int n_sites;
+    unsigned int n_traces;
+    long long T;
+    unsigned long long* table;        // [n_sites*SCL_NCOL + 3]
+    scl_sample* samples;              // [capacity]
+    unsigned int* ep_flag;            // [capacity]  reclaimed flag per episode-start sample
+    const unsigned long long* sbase;  // trace -> first sample slot
+    scl_trace_summary* summ;          // [n_traces]
+    EpStart* ep_scratch;              // [grid * kSeg]
+};
+
+struct FinalParams {
+    const unsigned long long* table;  // [n_sites*SCL_NCOL + 3]
+    unsigned int n_sites;
+    int formula;
+    double elapsed_ns;
+    double* prob; double* rate; unsigned char* flag;
+    unsigned long long* key1; unsigned int* val;   // sort inputs
+};
+
+// launch wrappers (replay.cu)
+cudaError_t launch_load_stats(const scl_event* ev, const unsigned long long* off, unsigned n_traces,
+                              unsigned n_sites, unsigned long long* sabs, unsigned long long* err,
+                              cudaStream_t st);
+cudaError_t launch_replay(const CUtensorMap* tmap, const ReplayParams& p, int grid, cudaStream_t st);
+cudaError_t launch_samples(const ReplayParams& p, cudaStream_t st);
+cudaError_t launch_finalize(const FinalParams& p, cudaStream_t st);
+cudaError_t launch_rows(const unsigned long long* table, const double* prob, const double* rate,
+                        const unsigned char* flag, const unsigned int* order, unsigned n_sites,
+                        scl_site_row* rows, cudaStream_t st);
+size_t replay_smem_bytes();
+int replay_occupancy(int* grid);
+
+}  // namespace scl

@@ -1,0 +1,192 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle, element by
+element, on seeded synthetic inputs shaped like the paper's workloads."""
+import os
+import tempfile
+
+import numpy as np
+import pytest
+
+import _golden
+import oracle
+import paper_2212_07597_b200 as scl
+import tracegen
+from parity import compare, gpu_run
+
+pytestmark = pytest.mark.gpu
+
+
+def _concat(traces):
+    """list of lists of (kind, ptr, size, site) -> events, offsets"""
+    ev = tracegen.from_tuples([e for tr in traces for e in tr])
+    off = np.zeros(len(traces) + 1, dtype=np.uint64)
+    off[1:] = np.cumsum([len(t) for t in traces])
+    return ev, off
+
+
+@pytest.mark.parametrize("name", _golden.all_names())
+def test_golden(name):
+    g = _golden.load(name)
+    if g["hwm"] != "prefix":
+        pytest.skip("hwm_mode SAMPLE is oracle-only (NEXT-4)")
+    n_sites = max(max(e[3] for e in g["events"]) + 1, max(g["sites"], default=0) + 1)
+    ev, off = _concat([g["events"]])
+    _, r = gpu_run(ev, off, n_sites, g["T"])
+    smp = scl.scl_samples(r, 0)
+    got = [(int(s["idx"]), "G" if s["kind"] == 0 else "D", int(s["net"]), int(s["footprint"]), int(s["site"]),
+            bool(s["new_max"])) for s in smp]
+    assert got == g["samples"]
+    compare(ev, off, n_sites, g["T"], r)
+
+
+def test_random_small_ragged():
+    """Hundreds of small random traces of ragged lengths (incl. empty ones and
+    lengths that straddle rows, threads and segments) at several T."""
+    rng = np.random.default_rng(1)
+    traces = []
+    for i in range(400):
+        n = int(rng.choice([0, 1, 3, 7, 8, 9, 31, 255, 256, 257, 2047, 2048, 2049, 5000, int(rng.integers(1, 9000))]))
+        traces.append(tracegen.random_small_trace(rng, n, n_sites=37, max_size=int(rng.integers(1, 200)),
+                                                  max_ptrs=int(rng.integers(2, 40))))
+    ev, off = _concat(traces)
+    tr = scl.scl_trace_load(ev, off, 37, validate=True)
+    r = None
+    for T in (1, 2, 7, 64, 401, 5000, 10**9):
+        r = scl.scl_replay_run(T, tr, out=r)
+        compare(ev, off, 37, T, r)
+
+
+def test_config1():
+    cfg = tracegen.CONFIGS[1]
+    ev, off = tracegen.generate(cfg)
+    _, r = gpu_run(ev, off, cfg.n_sites, cfg.T, validate=True)
+    ref = compare(ev, off, cfg.n_sites, cfg.T, r)
+    pl = tracegen.planted_sites(cfg)
+    rows = scl.scl_site_report(r)
+    flagged = set(rows["site"][rows["leak_flag"] == 1].tolist())
+    assert set(pl.tolist()) <= flagged and ref["gate"][2]
+
+
+def test_config2_full():
+    """BASELINE configs[1] at full size (64 x 1M events) -- the bench workload."""
+    cfg = tracegen.CONFIGS[2]
+    ev, off = tracegen.generate(cfg)
+    tr, r = gpu_run(ev, off, cfg.n_sites, cfg.T)
+    compare(ev, off, cfg.n_sites, cfg.T, r)
+    # same handle, smaller thresholds (dense samples, many episodes, P:436-438 sweep values)
+    for T in (1048583, 65537):
+        r = scl.scl_replay_run(T, tr, out=r)
+        compare(ev, off, cfg.n_sites, T, r)
+
+
+def test_config2_small_T_subset():
+    cfg = tracegen.CONFIGS[2].with_traces(4)
+    ev, off = tracegen.generate(cfg)
+    tr = scl.scl_trace_load(ev, off, cfg.n_sites)
+    r = None
+    for T in (4099, 521, 16):
+        r = scl.scl_replay_run(T, tr, out=r)
+        compare(ev, off, cfg.n_sites, T, r)
+
+
+def test_config3_subset_cold_sites():
+    """50k sites (most beyond the shared-memory hot range) on 24 traces of config 3."""
+    cfg = tracegen.CONFIGS[3].with_traces(24)
+    ev, off = tracegen.generate(cfg)
+    _, r = gpu_run(ev, off, cfg.n_sites, cfg.T)
+    compare(ev, off, cfg.n_sites, cfg.T, r)
+
+
+def test_huge_sizes_and_copies():
+    """Sizes >= 2^32 (L2 reduction path), 32-bit byte-counter carries, copy events (ignored)."""
+    rng = np.random.default_rng(5)
+    traces = []
+    for t in range(20):
+        tr_ = []
+        live = []
+        for i in range(3000):
+            if live and rng.random() < 0.4:
+                p, s = live.pop(int(rng.integers(len(live))))
+                tr_.append(("f", p, s, int(rng.integers(0, 3))))
+            elif rng.random() < 0.1:
+                tr_.append(("c", 0, int(rng.integers(1, 1 << 30)), 2))
+            else:
+                s = int(rng.choice([16, 4096, (1 << 31) + 17, (1 << 33) + 5, (1 << 39) + 3]))
+                p = 0x1000 + 0x10000000000 * i
+                live.append((p, s))
+                tr_.append(("a", p, s, int(rng.integers(0, 3))))
+        traces.append(tr_)
+    ev, off = _concat(traces)
+    for T in (1 << 20, (1 << 34) + 7):
+        _, r = gpu_run(ev, off, 3, T)
+        compare(ev, off, 3, T, r)
+
+
+def test_reuse_and_textbook_and_ticks():
+    cfg = tracegen.CONFIGS[1]
+    ev, off = tracegen.generate(cfg)
+    tr = scl.scl_trace_load(ev, off, cfg.n_sites)
+    r = None
+    for it in range(3):
+        r = scl.scl_replay_run(cfg.T, tr, out=r)
+        compare(ev, off, cfg.n_sites, cfg.T, r)
+    r = scl.scl_replay_run(cfg.T, tr, out=r, formula=1, tick_ns=777)
+    compare(ev, off, cfg.n_sites, cfg.T, r, formula=1, tick_ns=777)
+
+
+def test_device_pointers_and_file():
+    import torch
+    cfg = tracegen.CONFIGS[2].with_traces(3)
+    ev, off = tracegen.generate(cfg)
+    dev_ev = torch.from_numpy(ev.view(np.int64).copy()).cuda()
+    dev_off = torch.from_numpy(off.view(np.int64).copy()).cuda()
+    tr = scl.scl_trace_load(dev_ev, dev_off, cfg.n_sites)
+    r = scl.scl_replay_run(cfg.T, tr)
+    ref = compare(ev, off, cfg.n_sites, cfg.T, r)
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "t.scltrc")
+        scl.write_trace_file(path, ev, off, cfg.n_sites)
+        tr2 = scl.scl_trace_load(path=path)
+        r2 = scl.scl_replay_run(cfg.T, tr2)
+        compare(ev, off, cfg.n_sites, cfg.T, r2, ref=ref)
+
+
+def test_errors():
+    ev = tracegen.from_tuples([("a", 1, 8, 0), ("f", 2, 8, 0)])
+    off = np.array([0, 2], dtype=np.uint64)
+    with pytest.raises(scl.SclError) as e:
+        scl.scl_trace_load(ev, off, 1, validate=True)
+    assert e.value.status == -4 and "trace 0 event 1" in str(e.value)
+    with pytest.raises(scl.SclError) as e:
+        scl.scl_trace_load(ev, off, 1, validate=False).n_sites
+        scl.scl_trace_load(tracegen.from_tuples([("a", 1, 8, 3)]), np.array([0, 1], dtype=np.uint64), 2)
+    assert e.value.status == -1
+    tr = scl.scl_trace_load(tracegen.from_tuples([("a", 1, 8, 0)]), np.array([0, 1], dtype=np.uint64), 1)
+    with pytest.raises(scl.SclError):
+        scl.scl_replay_run(0, tr)
+
+
+def test_defer_finalize_table_sum():
+    """Two 'ranks' (halves of the traces) on one GPU: summing their device
+    tables element-wise then finalizing equals the single-run report (the
+    multi-GPU reduction of SURVEY §8(e), exercised without a second GPU)."""
+    import torch
+    cfg = tracegen.CONFIGS[2].with_traces(8)
+    ev, off = tracegen.generate(cfg)
+    h = int(off[4])
+    a_ev, a_off = ev[:h], off[:5]
+    b_ev, b_off = ev[h:], off[4:] - off[4]
+    ta = scl.scl_trace_load(a_ev, a_off, cfg.n_sites)
+    tb = scl.scl_trace_load(b_ev, b_off, cfg.n_sites)
+    ra = scl.scl_replay_run(cfg.T, ta, defer_finalize=True)
+    rb = scl.scl_replay_run(cfg.T, tb, defer_finalize=True)
+    xa, xb = scl.device_table_tensor(ra), scl.device_table_tensor(rb)
+    xa += xb
+    torch.cuda.synchronize()
+    scl.scl_finalize(ra, elapsed_ns=oracle.elapsed_ns(off))
+    ref = oracle.full(ev, off, cfg.n_sites, cfg.T)
+    rows = scl.scl_site_report(ra)
+    assert np.array_equal(rows["site"], ref["order"])
+    assert np.array_equal(rows["col"], ref["result"].site_table[ref["order"]])
+    assert np.array_equal(rows["leak_flag"], ref["flag"][ref["order"]].astype(np.uint32))
+    assert np.array_equal(rows["leak_prob"], ref["prob"][ref["order"]])
+    assert scl.scl_gate(ra) == ref["gate"]
