@@ -35,9 +35,7 @@ struct scl_traces {
     unsigned long long* d_off = nullptr;       // n_traces + 1
     std::vector<uint64_t> h_off, h_sabs;
     uint32_t n_segs = 0;
-    unsigned int* d_tk_trace = nullptr;
-    unsigned int* d_tk_k = nullptr;
-    unsigned int* d_seg_base = nullptr;
+    TicketInfo* d_tk = nullptr;
     SegState* d_state = nullptr;
     unsigned int* d_ticket = nullptr;
     mutable unsigned int epoch = 0;
@@ -216,25 +214,28 @@ extern "C" scl_status scl_trace_load(const char* path, const scl_event* events, 
         const uint64_t a = h_off[t], b = h_off[t + 1];
         tr->max_len = std::max<uint64_t>(tr->max_len, b - a);
         uint32_t ns = 0;
-        if (b > a) { uint64_t r = (b + 7) / 8 - a / 8; ns = (uint32_t)((r + kThreads - 1) / kThreads); }
+        if (b > a) { uint64_t r = (b + 7) / 8 - a / 8; ns = (uint32_t)((r + kUnitRows - 1) / kUnitRows); }
         nseg[t] = ns; seg_base[t] = total; total += ns; maxk = std::max(maxk, ns);
     }
-    std::vector<uint32_t> tk_t, tk_k;
-    tk_t.reserve(total); tk_k.reserve(total);
+    std::vector<TicketInfo> tk;
+    tk.reserve(total);
     for (uint32_t k = 0; k < maxk; ++k)
         for (uint32_t t = 0; t < n_traces; ++t)
-            if (k < nseg[t]) { tk_t.push_back(t); tk_k.push_back(k | (k + 1 == nseg[t] ? 0x80000000u : 0u)); }
+            if (k < nseg[t]) {
+                TicketInfo ti;
+                ti.off_t = (long long)h_off[t]; ti.n_t = (long long)(h_off[t + 1] - h_off[t]);
+                ti.t = t; ti.kraw = k | (k + 1 == nseg[t] ? 0x80000000u : 0u); ti.slot = seg_base[t] + k;
+                const uint64_t row_base = h_off[t] / 8 + (uint64_t)k * kUnitRows;
+                const uint64_t rows_left = (h_off[t + 1] + 7) / 8 - row_base;
+                ti.nbox = (unsigned)std::min<uint64_t>((rows_left + kThreads - 1) / kThreads, kSub);
+                tk.push_back(ti);
+            }
     tr->n_segs = total;
-    const size_t nn = std::max<size_t>(total, 1), nt = std::max<size_t>(n_traces, 1);
-    if (cudaMalloc(&tr->d_tk_trace, nn * 4) != cudaSuccess || cudaMalloc(&tr->d_tk_k, nn * 4) != cudaSuccess ||
-        cudaMalloc(&tr->d_seg_base, nt * 4) != cudaSuccess || cudaMalloc(&tr->d_state, nn * sizeof(SegState)) != cudaSuccess ||
-        cudaMalloc(&tr->d_ticket, 4) != cudaSuccess)
+    const size_t nn = std::max<size_t>(total, 1);
+    if (cudaMalloc(&tr->d_tk, nn * sizeof(TicketInfo)) != cudaSuccess ||
+        cudaMalloc(&tr->d_state, nn * sizeof(SegState)) != cudaSuccess || cudaMalloc(&tr->d_ticket, 4) != cudaSuccess)
         { cudaGetLastError(); return cleanup(fail(SCL_ENOMEM, "segment plan")); }
-    if (total) {
-        cudaMemcpy(tr->d_tk_trace, tk_t.data(), total * 4, cudaMemcpyHostToDevice);
-        cudaMemcpy(tr->d_tk_k, tk_k.data(), total * 4, cudaMemcpyHostToDevice);
-    }
-    if (n_traces) cudaMemcpy(tr->d_seg_base, seg_base.data(), n_traces * 4, cudaMemcpyHostToDevice);
+    if (total) cudaMemcpy(tr->d_tk, tk.data(), total * sizeof(TicketInfo), cudaMemcpyHostToDevice);
     cudaMemset(tr->d_state, 0, nn * sizeof(SegState));
 
     // TMA descriptor: rows of 32 x u32 (128 B), box 32 x 256 rows, 128-B swizzle
@@ -255,8 +256,7 @@ extern "C" scl_status scl_trace_load(const char* path, const scl_event* events, 
 
 extern "C" void scl_traces_free(scl_traces* t) {
     if (!t) return;
-    cudaFree(t->d_ev); cudaFree(t->d_off); cudaFree(t->d_tk_trace); cudaFree(t->d_tk_k);
-    cudaFree(t->d_seg_base); cudaFree(t->d_state); cudaFree(t->d_ticket);
+    cudaFree(t->d_ev); cudaFree(t->d_off); cudaFree(t->d_tk); cudaFree(t->d_state); cudaFree(t->d_ticket);
     delete t;
 }
 
@@ -286,7 +286,7 @@ static scl_status alloc_result(scl_result* r, const scl_traces* tr) {
     CU(cudaMalloc(&r->d_table, (S * SCL_NCOL + 3) * 8));
     CU(cudaMalloc(&r->d_sbase, nt * 8));
     CU(cudaMalloc(&r->d_summ, nt * sizeof(scl_trace_summary)));
-    CU(cudaMalloc(&r->d_scratch, (size_t)grid * kSeg * sizeof(EpStart)));
+    CU(cudaMalloc(&r->d_scratch, (size_t)grid * kLBWarps * kUnit * sizeof(EpStart)));
     CU(cudaMalloc(&r->d_prob, S * 8)); CU(cudaMalloc(&r->d_rate, S * 8)); CU(cudaMalloc(&r->d_flag, S));
     CU(cudaMalloc(&r->d_key, S * 8)); CU(cudaMalloc(&r->d_key2, S * 8));
     CU(cudaMalloc(&r->d_val, S * 4)); CU(cudaMalloc(&r->d_order, S * 4));
@@ -354,7 +354,7 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
     CU(cudaMemsetAsync(tr->d_ticket, 0, 4, st));
 
     ReplayParams p{};
-    p.ev = tr->d_ev; p.off = tr->d_off; p.tk_trace = tr->d_tk_trace; p.tk_k = tr->d_tk_k; p.seg_base = tr->d_seg_base;
+    p.ev = tr->d_ev; p.off = tr->d_off; p.tk = tr->d_tk;
     p.state = tr->d_state; p.ticket = tr->d_ticket; p.n_segs = tr->n_segs; p.epoch = tr->epoch;
     p.n_sites = tr->n_sites; p.n_traces = NT; p.T = (long long)threshold;
     p.table = r->d_table; p.samples = r->d_samples; p.ep_flag = r->d_epflag; p.sbase = r->d_sbase;

@@ -1,0 +1,66 @@
+// ptx.cuh -- inline-PTX helpers for sm_100a (mbarrier, TMA, acquire/release, warp shuffles).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+
+namespace scl {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+// Wait until the phase with the given parity has completed (acquire.cta).
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile("{\n\t.reg .pred p;\n"
+                 "SCL_WAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra SCL_WAIT_%=;\n}" :: "r"(smem_u32(b)), "r"(parity) : "memory");
+}
+// 2-D TMA tile load (box = the tensor map's box) into shared memory, completing on bar.
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                 :: "r"(smem_u32(dst)), "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(threads) : "memory");
+}
+
+__device__ __forceinline__ long long shfl_ll(long long v, int src) { return __shfl_sync(kFull, v, src); }
+__device__ __forceinline__ long long shfl_up_ll(long long v, int d) { return __shfl_up_sync(kFull, v, d); }
+__device__ __forceinline__ long long shfl_down_ll(long long v, int d) { return __shfl_down_sync(kFull, v, d); }
+__device__ __forceinline__ long long llmax(long long a, long long b) { return a > b ? a : b; }
+__device__ __forceinline__ long long llmin(long long a, long long b) { return a < b ? a : b; }
+__device__ __forceinline__ long long warp_max(long long v) {
+    #pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v = llmax(v, __shfl_xor_sync(kFull, v, d));
+    return v;
+}
+__device__ __forceinline__ long long warp_min(long long v) {
+    #pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v = llmin(v, __shfl_xor_sync(kFull, v, d));
+    return v;
+}
+__device__ __forceinline__ long long warp_sum(long long v) {
+    #pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(kFull, v, d);
+    return v;
+}
+
+}  // namespace scl

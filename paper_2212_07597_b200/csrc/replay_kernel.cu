@@ -1,0 +1,509 @@
+// replay_kernel.cu -- the streaming hot path a1..a5 in one pass over the events.
+//
+// Paper (PAPER.md lines): threshold sampler P:429-438 ("|A - F| >= T ... resets
+// the counters"), footprint P:430-431 / P:490-494, high-water mark P:24-25,
+// leak tracker with the free-pointer comparison P:20-39, per-line statistics
+// P:488-494.  Readings Q1-Q16: DESIGN.md §3.
+//
+// One persistent CTA per SM, warp-specialised:
+//   producer warp   one ticket per 8192-event unit (tickets ordered (unit index,
+//                   trace), so the units of one trace are spread over time);
+//                   issues the unit's 2-D TMA boxes (32 KiB, 128-B swizzle)
+//                   into a kStages-deep shared-memory ring;
+//   8 compute warps one 256-event chunk per box each: signed sizes, chunk sum
+//                   and max/min prefix, Tier-E site counters (32-bit shared
+//                   atomics + carry word), a 2048-bit Bloom filter of freed
+//                   pointers; the last warp to finish a unit composes the 32
+//                   chunk summaries and publishes the unit aggregate at once;
+//   3 look-back warps take whole units round-robin: find the incoming state by
+//                   a decoupled look-back over the trace's earlier units
+//                   (aggregates are composed while the sampler band provably
+//                   stays closed; the warp waits only at the first unit where
+//                   a sample could fire), resolve the samples (re-reading only
+//                   the chunks whose range leaves the band, through L2),
+//                   publish the inclusive state, then check the frees against
+//                   the tracked pointer (Bloom query per chunk, exact re-check
+//                   of positives).
+#include "scl_internal.cuh"
+#include "ptx.cuh"
+
+namespace scl {
+
+struct SegInfo {                     // one unit ticket, as the producer resolved it
+    unsigned u, t, kraw, slot;       // ticket, trace, unit index (| last << 31), state slot
+    long long off_t, n_t, row_base;  // trace start, trace length, first global row of the unit
+    unsigned nbox, pad;              // boxes of this unit that overlap the trace
+};
+struct Slot {                        // compute -> look-back summary of one unit
+    SegInfo info;
+    long long csum[kChunks], cmx[kChunks], cmn[kChunks];   // per chunk, relative to the chunk start
+    long long Pc[kChunks], ax[kChunks], an[kChunks];       // chunk prefix; max/min relative to the unit start
+    long long usum, umx, umn;                              // unit aggregate
+    unsigned done, pad;
+    unsigned bloom[kChunks][kBloomWords];
+};
+struct __align__(16) Smem {
+    unsigned cnt[2 * kHot];          // Tier-E per (kind, hot site): event count
+    unsigned blo[2 * kHot];          //   bytes, low 32 bits
+    unsigned bhi[2 * kHot];          //   carries out of blo
+    Slot slot[kSlots];
+    SegInfo info[kStages];
+    unsigned sub[kStages];           // box index within the unit
+    uint64_t full[kStages], empty[kStages], sfull[kSlots], sempty[kSlots];
+};
+
+size_t replay_smem_bytes() { return 1024 + (size_t)kStages * kSegBytes + sizeof(Smem); }
+
+__device__ __forceinline__ unsigned bloom_bit(unsigned long long ptr) {
+    return (unsigned)((ptr * 0x9E3779B97F4A7C15ull) >> 53);          // 11 bits: 0..2047
+}
+
+// The 8 events of one global row, through L2 (re-read path).
+__device__ __forceinline__ void load_row_global(const scl_event* ev, long long row, unsigned long long* ptr,
+                                                unsigned long long* meta) {
+    const ulonglong2* q = reinterpret_cast<const ulonglong2*>(ev + row * kEpt);
+    #pragma unroll
+    for (int j = 0; j < kEpt; ++j) { ulonglong2 v = __ldcg(q + j); ptr[j] = v.x; meta[j] = v.y; }
+}
+
+// ============================================================================ compute warps
+__device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stage, int w, int lane)
+{
+    const unsigned want = p.epoch * 4u;
+    for (unsigned it = 0;; ++it) {
+        const int st = it % kStages;
+        mbar_wait(&s.full[st], (it / kStages) & 1u);
+        const SegInfo inf = s.info[st];
+        const unsigned g = s.sub[st];
+        const unsigned itu = it / kSub;                   // unit iteration of this CTA
+        const int sl = itu % kSlots;
+        if (inf.u == kInvalid) {
+            // propagate termination to every look-back warp (one invalid unit slot each)
+            for (unsigned m = 0; m < (unsigned)kLBWarps; ++m) {
+                const unsigned itm = itu + m;
+                const int slm = itm % kSlots;
+                mbar_wait(&s.sempty[slm], ((itm / kSlots) & 1u) ^ 1u);
+                if (w == 0 && lane == 0) { s.slot[slm].info.u = kInvalid; mbar_arrive(&s.sfull[slm]); }
+                __syncwarp();
+            }
+            return;
+        }
+        if (g == 0) mbar_wait(&s.sempty[sl], ((itu / kSlots) & 1u) ^ 1u);
+        Slot& S = s.slot[sl];
+        const int c = g * kComputeWarps + w;              // chunk index within the unit
+        S.bloom[c][lane] = 0u; S.bloom[c][lane + 32] = 0u;
+        if (g == 0 && w == 0 && lane == 0) S.info = inf;
+        __syncwarp();
+
+        long long run = 0, tmx = kNeg, tmn = kPos;
+        if (g < inf.nbox) {
+            // ---- the 8 events of row 32w+lane (16-B chunk j of row r sits at j ^ (r & 7))
+            const int r = w * 32 + lane;
+            const unsigned char* rowp = stage + (size_t)st * kSegBytes + (size_t)r * 128;
+            unsigned long long ptr[kEpt], meta[kEpt];
+            #pragma unroll
+            for (int j = 0; j < kEpt; ++j) {
+                ulonglong2 v = *reinterpret_cast<const ulonglong2*>(rowp + ((j ^ (r & 7)) << 4));
+                ptr[j] = v.x; meta[j] = v.y;
+            }
+            const long long e0 = (inf.row_base + (long long)g * kThreads + r) * kEpt - inf.off_t;
+            #pragma unroll
+            for (int j = 0; j < kEpt; ++j) {
+                const long long ie = e0 + j;
+                const unsigned kind = ev_kind(meta[j]);
+                const bool af = ie >= 0 && ie < inf.n_t && kind < 2;
+                const unsigned long long size = ev_size(meta[j]);
+                run += af ? (kind == 0 ? (long long)size : -(long long)size) : 0;     // a1: signed size
+                if (af) {
+                    tmx = llmax(tmx, run); tmn = llmin(tmn, run);
+                    const unsigned site = ev_site(meta[j]);
+                    if (site < (unsigned)kHot && size < (1ull << 32)) {              // a5 Tier E (shared)
+                        const int x = kind * kHot + site;
+                        atomicAdd(&s.cnt[x], 1u);
+                        const unsigned sz = (unsigned)size;
+                        const unsigned old = atomicAdd(&s.blo[x], sz);
+                        if (old + sz < old) atomicAdd(&s.bhi[x], 1u);
+                    } else {                                                          // cold site / huge size
+                        unsigned long long* row = p.table + (size_t)site * SCL_NCOL;
+                        atomicAdd(&row[SCL_COL_N_MALLOC + kind], 1ull);
+                        atomicAdd(&row[SCL_COL_MALLOC_BYTES + kind], size);
+                    }
+                    if (kind == 1) {                                                  // freed pointer -> Bloom
+                        const unsigned b = bloom_bit(ptr[j]);
+                        atomicOr(&S.bloom[c][b >> 5], 1u << (b & 31));
+                    }
+                }
+            }
+        }
+        // ---- chunk summary: sum, max / min prefix relative to the chunk start
+        long long incl = run;
+        #pragma unroll
+        for (int d = 1; d < 32; d <<= 1) { long long o = shfl_up_ll(incl, d); if (lane >= d) incl += o; }
+        const long long Pl = incl - run;
+        const long long cmx = warp_max(Pl + tmx), cmn = warp_min(Pl + tmn);
+        if (lane == 31) { S.csum[c] = incl; S.cmx[c] = cmx; S.cmn[c] = cmn; }
+        __syncwarp();
+        mbar_arrive(&s.empty[st]);                        // box consumed
+        unsigned old = 0;
+        if (lane == 0) { __threadfence_block(); old = atomicAdd(&S.done, 1u); __threadfence_block(); }
+        old = __shfl_sync(kFull, old, 0);
+        if (old == kChunks - 1) {
+            // last chunk of the unit: compose the 32 chunk summaries (lane = chunk) and publish
+            const long long cs = S.csum[lane], cx = S.cmx[lane], cn = S.cmn[lane];
+            long long ci = cs;
+            #pragma unroll
+            for (int d = 1; d < 32; d <<= 1) { long long o = shfl_up_ll(ci, d); if (lane >= d) ci += o; }
+            const long long Pc = ci - cs, ax = Pc + cx, an = Pc + cn;
+            S.Pc[lane] = Pc; S.ax[lane] = ax; S.an[lane] = an;
+            const long long usum = shfl_ll(ci, 31), umx = warp_max(ax), umn = warp_min(an);
+            if (lane == 0) {
+                S.usum = usum; S.umx = umx; S.umn = umn;
+                SegState* my = &p.state[S.info.slot];
+                my->sum = usum; my->mx = umx; my->mn = umn;
+                st_release(&my->flag, want + 1);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.sfull[sl]);
+        }
+    }
+}
+
+// ============================================================================ producer warp
+__device__ void producer_role(const ReplayParams& p, const CUtensorMap* tmap, Smem& s, unsigned char* stage, int lane)
+{
+    if (lane != 0) return;
+    auto resolve = [&](unsigned u) {
+        SegInfo inf; inf.u = kInvalid; inf.nbox = 0;
+        if (u < p.n_segs) {
+            const TicketInfo ti = p.tk[u];
+            inf.u = u; inf.t = ti.t; inf.kraw = ti.kraw; inf.slot = ti.slot; inf.nbox = ti.nbox;
+            inf.off_t = ti.off_t; inf.n_t = ti.n_t;
+            inf.row_base = (ti.off_t >> 3) + (long long)(ti.kraw & 0x7fffffffu) * kUnitRows;
+        }
+        return inf;
+    };
+    // two tickets in flight: the atomic for unit i+2 and the record load for unit i+1
+    // are issued before unit i's boxes, and consumed after them
+    SegInfo cur = resolve(atomicAdd(p.ticket, 1u));
+    unsigned u_next = cur.u == kInvalid ? kInvalid : atomicAdd(p.ticket, 1u);
+    unsigned it = 0;
+    for (;;) {
+        const SegInfo nxt = resolve(u_next);
+        const unsigned u_after = nxt.u == kInvalid ? kInvalid : atomicAdd(p.ticket, 1u);
+        for (unsigned g = 0; g < (unsigned)kSub; ++g, ++it) {
+            const int st = it % kStages;
+            mbar_wait(&s.empty[st], ((it / kStages) & 1u) ^ 1u);
+            s.info[st] = cur; s.sub[st] = g;
+            if (cur.u == kInvalid || g >= cur.nbox) {
+                mbar_arrive(&s.full[st]);                  // sentinel / box outside the trace
+            } else {
+                mbar_expect_tx(&s.full[st], kSegBytes);
+                tma_load_2d(stage + (size_t)st * kSegBytes, tmap, 0, (int)(cur.row_base + (long long)g * kThreads),
+                            &s.full[st]);
+            }
+            if (cur.u == kInvalid) return;
+        }
+        cur = nxt;
+        u_next = u_after;
+    }
+}
+
+// ============================================================================ look-back warps
+struct InState { long long F, M, B; unsigned long long n, nep, ep, eptr; };
+
+// The 7 inclusive words of a SegState (F, M, B, n, nep, ep, ep_ptr are consecutive):
+// lanes 0..6 load one word each, then broadcast.
+__device__ __forceinline__ InState load_inclusive_warp(const SegState* q, int lane) {
+    const unsigned long long* w = reinterpret_cast<const unsigned long long*>(&q->F);
+    unsigned long long v = lane < 7 ? __ldcg(w + lane) : 0ull;
+    InState x;
+    x.F = (long long)__shfl_sync(kFull, v, 0); x.M = (long long)__shfl_sync(kFull, v, 1);
+    x.B = (long long)__shfl_sync(kFull, v, 2); x.n = __shfl_sync(kFull, v, 3);
+    x.nep = __shfl_sync(kFull, v, 4); x.ep = __shfl_sync(kFull, v, 5); x.eptr = __shfl_sync(kFull, v, 6);
+    return x;
+}
+
+// State before unit k of a trace (a1-a4 carries).  Units k-1, k-2, ... are
+// examined 32 at a time (lane i <-> unit k-1-i).  From the nearest inclusive
+// state ("base") the aggregates of the units after it are applied in order
+// while the sampler provably does not fire (every prefix of the carry stays
+// in (-T, T)); at the first unit where it could fire, the warp waits for that
+// unit's inclusive state and continues from there.
+__device__ InState look_back(const ReplayParams& p, const SegState* ts, unsigned k, unsigned want, int lane)
+{
+    InState b{0, 0, 0, 0, 0, kNoEp, 0};
+    if (k == 0) return b;
+    const int j = (int)k - 1;
+    const int idx = j - lane;
+    unsigned fl = 0;
+    if (idx >= 0) {
+        const unsigned* fp = &ts[idx].flag;
+        do { fl = ld_acquire(fp); } while (fl < want + 1);
+    }
+    const unsigned im = __ballot_sync(kFull, idx >= 0 && fl >= want + 2);
+    if (!im && j - 31 > 0) {
+        // no inclusive state within 32 units: wait for the predecessor's (rare)
+        if (lane == 0) { unsigned f; do { f = ld_acquire(&ts[k - 1].flag); } while (f < want + 2); }
+        __syncwarp();
+        return load_inclusive_warp(&ts[k - 1], lane);
+    }
+    int stop = im ? __ffs(im) - 1 : 32;                    // lanes < stop: units after the base
+    long long a_s = 0, a_x = kNeg, a_n = kPos;
+    if (lane < stop && idx >= 0) {
+        const SegState* q = &ts[idx];
+        a_s = __ldcg(&q->sum); a_x = __ldcg(&q->mx); a_n = __ldcg(&q->mn);
+    }
+    if (im) b = load_inclusive_warp(&ts[j - stop], lane);  // else base = trace start
+    for (;;) {
+        // forward order = decreasing lane; E = sum over earlier units (higher lanes < stop)
+        const long long v = lane < stop ? a_s : 0;
+        long long inc = v;
+        #pragma unroll
+        for (int d = 1; d < 32; d <<= 1) { long long o = shfl_down_ll(inc, d); if (lane + d < 32) inc += o; }
+        const long long E = inc - v;
+        const long long c = b.F - b.B + E;
+        const bool bad = lane < stop && (c + a_x >= p.T || c + a_n <= -p.T);
+        const unsigned bm = __ballot_sync(kFull, bad);
+        if (!bm) {
+            const long long tot = shfl_ll(inc, 0);
+            const long long mx = warp_max(lane < stop ? E + a_x : kNeg);
+            b.M = llmax(b.M, b.F + mx);
+            b.F += tot;
+            return b;
+        }
+        const int jf = 31 - __clz(bm);                     // earliest unit where a sample may fire
+        const SegState* q = &ts[j - jf];
+        if (lane == 0) { unsigned f; do { f = ld_acquire(&q->flag); } while (f < want + 2); }
+        __syncwarp();
+        b = load_inclusive_warp(q, lane);
+        stop = jf;
+    }
+}
+
+__device__ void lookback_role(const ReplayParams& p, Smem& s, int lbw, int lane)
+{
+    const unsigned want = p.epoch * 4u;
+    EpStart* eplist = p.ep_scratch + ((size_t)blockIdx.x * kLBWarps + lbw) * kUnit;
+    for (unsigned it = lbw;; it += kLBWarps) {
+        const int sl = it % kSlots;
+        mbar_wait(&s.sfull[sl], (it / kSlots) & 1u);
+        Slot& S = s.slot[sl];
+        const SegInfo inf = S.info;
+        if (inf.u == kInvalid) return;
+        const unsigned k = inf.kraw & 0x7fffffffu;
+        const bool last = (inf.kraw >> 31) != 0;
+        SegState* my = &p.state[inf.slot];
+        const long long usum = S.usum, umx = S.umx, umn = S.umn;
+
+        // ---- incoming state (chain)
+        const InState in = look_back(p, &p.state[inf.slot - k], k, want, lane);
+
+        // ---- a3/a4: samples of this unit (band test per chunk; exact re-scan only where needed)
+        long long B = in.B;
+        unsigned long long n = in.n, nep = in.nep, ep = in.ep, eptr = in.eptr;
+        unsigned nl = 0;
+        const long long F0 = in.F;
+        if (F0 - B + umx >= p.T || F0 - B + umn <= -p.T) {
+            const unsigned long long sb = __ldg(p.sbase + inf.t);
+            const long long myax = S.ax[lane], myan = S.an[lane], myPc = S.Pc[lane];
+            long long Mrun = in.M;                             // max F over events before the chunk
+            for (int c = 0; c < kChunks; ++c) {
+                const long long Pw = shfl_ll(myPc, c), hi = F0 + shfl_ll(myax, c), lo = F0 + shfl_ll(myan, c);
+                if (!(hi >= B + p.T || lo <= B - p.T)) { Mrun = llmax(Mrun, hi); continue; }
+                // re-read the chunk: lane l <-> row 32c+l of the unit (8 events)
+                const long long row = inf.row_base + (long long)c * 32 + lane;
+                unsigned long long rp[kEpt], rm[kEpt];
+                load_row_global(p.ev, row, rp, rm);
+                const long long e0 = row * kEpt - inf.off_t;
+                long long d[kEpt], run = 0, lmx = kNeg, lmn = kPos;
+                #pragma unroll
+                for (int jj = 0; jj < kEpt; ++jj) {
+                    const long long ie = e0 + jj;
+                    const unsigned kind = ev_kind(rm[jj]);
+                    const bool af = ie >= 0 && ie < inf.n_t && kind < 2;
+                    const long long sz = (long long)ev_size(rm[jj]);
+                    d[jj] = af ? (kind == 0 ? sz : -sz) : 0;
+                    run += d[jj];
+                    if (af) { lmx = llmax(lmx, run); lmn = llmin(lmn, run); }
+                }
+                long long li = run;
+                #pragma unroll
+                for (int dd = 1; dd < 32; dd <<= 1) { long long o = shfl_up_ll(li, dd); if (lane >= dd) li += o; }
+                const long long Fl = F0 + Pw + (li - run);          // F before this lane's first event
+                long long pmx = Fl + lmx;                             // max F over lanes <= lane
+                #pragma unroll
+                for (int dd = 1; dd < 32; dd <<= 1) { long long o = shfl_up_ll(pmx, dd); if (lane >= dd) pmx = llmax(pmx, o); }
+                long long PMl = shfl_up_ll(pmx, 1);
+                if (lane == 0) PMl = kNeg;
+                int cur = 0;
+                for (;;) {
+                    const bool cand = lane >= cur && (Fl + lmx >= B + p.T || Fl + lmn <= B - p.T);
+                    const unsigned cm = __ballot_sync(kFull, cand);
+                    if (!cm) break;
+                    const int l0 = __ffs(cm) - 1;
+                    // lanes 0..7 take the 8 events of lane l0
+                    long long de = 0; unsigned long long pe = 0, me = 0;
+                    #pragma unroll
+                    for (int jj = 0; jj < kEpt; ++jj) {
+                        const long long v = shfl_ll(d[jj], l0);
+                        const unsigned long long pv = __shfl_sync(kFull, rp[jj], l0), mv = __shfl_sync(kFull, rm[jj], l0);
+                        if (lane == jj) { de = v; pe = pv; me = mv; }
+                    }
+                    const long long iev = shfl_ll(e0, l0) + lane;
+                    const bool af = lane < kEpt && iev >= 0 && iev < inf.n_t && ev_kind(me) < 2;
+                    long long L = de;
+                    #pragma unroll
+                    for (int dd = 1; dd < kEpt; dd <<= 1) { long long o = shfl_up_ll(L, dd); if (lane >= dd) L += o; }
+                    const long long Fe = shfl_ll(Fl, l0) + L;
+                    const long long Mbase = llmax(Mrun, shfl_ll(PMl, l0));
+                    int ef = 0;
+                    for (;;) {                                      // successive first exits of (B-T, B+T)
+                        const bool ex = af && lane >= ef && (Fe >= B + p.T || Fe <= B - p.T);
+                        const unsigned em = __ballot_sync(kFull, ex);
+                        if (!em) break;
+                        const int e = __ffs(em) - 1;
+                        const long long Fs = shfl_ll(Fe, e);
+                        const long long Mprev = llmax(Mbase, warp_max((af && lane < e) ? Fe : kNeg));   // M_{i-1}
+                        const long long net = Fs - B;              // the |A - F| counter
+                        const bool growth = net > 0;
+                        const bool nm = growth && Fs > Mprev;      // new high-water mark (Q3, Q4)
+                        const unsigned long long slot_s = sb + n;
+                        if (lane == e) {
+                            scl_sample smp;
+                            smp.idx = (unsigned long long)iev; smp.net = net; smp.footprint = Fs;
+                            smp.site = ev_site(me); smp.kind = growth ? 0 : 1; smp.new_max = nm ? 1 : 0; smp.pad = 0;
+                            p.samples[slot_s] = smp;
+                            if (nm) {
+                                p.ep_flag[slot_s] = 0u;
+                                EpStart es; es.ep = slot_s; es.ptr = pe; es.pos = (unsigned)((c * 32 + l0) * kEpt + e); es.pad = 0;
+                                eplist[nl] = es;
+                            }
+                        }
+                        if (nm) { ep = slot_s; eptr = __shfl_sync(kFull, pe, e); ++nep; ++nl; }
+                        ++n; B = Fs; ef = e + 1;                   // "resets the counters"
+                    }
+                    cur = l0 + 1;
+                }
+                Mrun = llmax(Mrun, hi);
+            }
+        }
+        // ---- publish the inclusive state (the end of the chain's critical path)
+        if (lane == 0) {
+            my->F = F0 + usum; my->M = llmax(in.M, F0 + umx); my->B = B;
+            my->n = n; my->nep = nep; my->ep = ep; my->ep_ptr = eptr;
+            st_release(&my->flag, want + 2);
+            if (last) {
+                scl_trace_summary* sm = &p.summ[inf.t];
+                sm->f_final = F0 + usum; sm->hwm = llmax(in.M, F0 + umx);
+                sm->n_samples = n; sm->n_episodes = nep;
+            }
+        }
+        __syncwarp();
+
+        // ---- a4 free-pointer match, "a pointer comparison that is almost always false":
+        // lane c decides whether chunk c may hold a free of an active tracked pointer (Bloom)
+        if (in.ep != kNoEp || nl > 0) {
+            const unsigned cbeg = (unsigned)lane * 32 * kEpt, cend = cbeg + 32 * kEpt;
+            unsigned li = 0;
+            unsigned long long cptr = in.eptr; bool cval = in.ep != kNoEp;
+            while (li < nl && eplist[li].pos < cbeg) { cptr = eplist[li].ptr; cval = true; ++li; }
+            bool need = false;
+            for (;;) {
+                if (cval) { const unsigned b = bloom_bit(cptr); if ((S.bloom[lane][b >> 5] >> (b & 31)) & 1u) need = true; }
+                if (li < nl && eplist[li].pos < cend) { cptr = eplist[li].ptr; cval = true; ++li; } else break;
+            }
+            unsigned nm = __ballot_sync(kFull, need);
+            if (nm && in.ep != kNoEp && nl == 0) {
+                // the incoming episode may already be known reclaimed: nothing left to learn
+                unsigned f0 = lane == 0 ? __ldcg(&p.ep_flag[in.ep]) : 0u;
+                if (__shfl_sync(kFull, f0, 0)) nm = 0;
+            }
+            while (nm) {
+                const int c = __ffs(nm) - 1;
+                nm &= nm - 1;
+                const long long row = inf.row_base + (long long)c * 32 + lane;
+                unsigned long long rp[kEpt], rm[kEpt];
+                load_row_global(p.ev, row, rp, rm);
+                const long long e0 = row * kEpt - inf.off_t;
+                const unsigned pos0 = (unsigned)(c * 32 + lane) * kEpt;
+                unsigned lk = 0;
+                unsigned long long aep = in.ep, aptr = in.eptr;
+                while (lk < nl && eplist[lk].pos < pos0) { aep = eplist[lk].ep; aptr = eplist[lk].ptr; ++lk; }
+                #pragma unroll
+                for (int jj = 0; jj < kEpt; ++jj) {
+                    while (lk < nl && eplist[lk].pos <= pos0 + jj) { aep = eplist[lk].ep; aptr = eplist[lk].ptr; ++lk; }
+                    const long long ie = e0 + jj;
+                    if (aep != kNoEp && ie >= 0 && ie < inf.n_t && ev_kind(rm[jj]) == 1 && rp[jj] == aptr)
+                        atomicOr(&p.ep_flag[aep], 1u);
+                }
+            }
+        }
+        if (lane == 0) S.done = 0;
+        __syncwarp();
+        mbar_arrive(&s.sempty[sl]);
+    }
+}
+
+// ============================================================================ kernel
+__global__ void __maxnreg__(168)
+replay_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ ReplayParams p)
+{
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    unsigned char* stage = base;                                     // kStages x 32 KiB, 1024-aligned
+    Smem& s = *reinterpret_cast<Smem*>(base + (size_t)kStages * kSegBytes);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    for (int x = tid; x < 2 * kHot; x += kCtaThreads) { s.cnt[x] = 0; s.blo[x] = 0; s.bhi[x] = 0; }
+    for (int x = tid; x < kSlots; x += kCtaThreads) s.slot[x].done = 0;
+    if (tid == 0) {
+        for (int i = 0; i < kStages; ++i) { mbar_init(&s.full[i], 1); mbar_init(&s.empty[i], kComputeWarps * 32); }
+        for (int i = 0; i < kSlots; ++i) { mbar_init(&s.sfull[i], 1); mbar_init(&s.sempty[i], 32); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" :: "l"((uint64_t)&tmap) : "memory");
+    }
+    __syncthreads();
+
+    if (warp < kComputeWarps) {
+        compute_role(p, s, stage, warp, lane);
+        named_bar(1, kComputeWarps * 32);                            // all compute warps done
+        for (int x = tid; x < 2 * kHot; x += kComputeWarps * 32) {   // flush Tier-E counters
+            const unsigned c = s.cnt[x];
+            if (c) {
+                const int kind = x / kHot, site = x % kHot;
+                unsigned long long* row = p.table + (size_t)site * SCL_NCOL;
+                atomicAdd(&row[SCL_COL_N_MALLOC + kind], (unsigned long long)c);
+                atomicAdd(&row[SCL_COL_MALLOC_BYTES + kind], ((unsigned long long)s.bhi[x] << 32) | s.blo[x]);
+            }
+        }
+    } else if (warp == kProducerWarp) {
+        producer_role(p, &tmap, s, stage, lane);
+    } else {
+        lookback_role(p, s, warp - kProducerWarp - 1, lane);
+    }
+}
+
+int replay_occupancy(int* grid)
+{
+    int dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    *grid = nsm;
+    return 1;
+}
+
+cudaError_t launch_replay(const CUtensorMap* tmap, const ReplayParams& p, int grid, cudaStream_t st)
+{
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)replay_smem_bytes());
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    if (p.n_segs == 0) return cudaSuccess;
+    replay_kernel<<<grid, kCtaThreads, replay_smem_bytes(), st>>>(*tmap, p);
+    return cudaGetLastError();
+}
+
+}  // namespace scl

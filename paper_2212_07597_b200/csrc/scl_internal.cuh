@@ -8,21 +8,37 @@
 
 namespace scl {
 
-// ---- segment geometry --------------------------------------
-// A segment is 256 rows of 128 B = 8 events per row, one row per thread:
-// 2048 events = 32 KiB staged in shared memory by one 2-D TMA load with the
-// 128-byte swizzle, so that every thread reads its own 8 consecutive events
-// with conflict-free LDS.128.
-constexpr int kThreads = 256;
-constexpr int kEpt = 8;                       // events per thread (one 128-B row)
-constexpr int kSeg = kThreads * kEpt;         // events per segment
+// ---- geometry and CTA roles -----------------------------------
+// Events are viewed as 128-B rows of 8.  A TMA box is 256 rows (2048 events,
+// 32 KiB), staged in shared memory with the 128-byte swizzle so that each
+// compute lane reads its own row with conflict-free LDS.128.  A chain UNIT
+// (the look-back granule) is kSub = 4 boxes = 8192 events = 32 chunks of 256
+// events (one chunk per compute warp per box).  One persistent CTA per SM:
+//   warps 0..7   compute: stream boxes (one chunk per warp), no CTA barriers;
+//                the last warp to finish a unit publishes its aggregate
+//   warp  8      producer: tickets (one per unit) + TMA issue into a kStages ring
+//   warps 9..11  look-back: chain the units of a trace, resolve samples,
+//                match frees against the tracked pointer, publish
+constexpr int kThreads = 256;                 // rows per box = compute threads
+constexpr int kEpt = 8;                       // events per row
+constexpr int kSeg = kThreads * kEpt;         // events per box
 constexpr int kSegBytes = kSeg * 16;
-constexpr int kStages = 2;                    // TMA ring depth per CTA
+constexpr int kSub = 4;                       // boxes per unit
+constexpr int kUnitRows = kThreads * kSub;
+constexpr int kUnit = kSeg * kSub;            // events per unit (8192)
+constexpr int kChunks = 32;                   // 256-event chunks per unit (one per look-back lane)
+constexpr int kComputeWarps = 8;
+constexpr int kLBWarps = 3;                   // 12 warps total: 3 per SM sub-partition (register budget)
+constexpr int kProducerWarp = kComputeWarps;
+constexpr int kCtaThreads = (kComputeWarps + 1 + kLBWarps) * 32;
+constexpr int kStages = 4;                    // TMA ring depth
+constexpr int kSlots = 6;                     // compute -> look-back unit summary ring
+constexpr int kBloomWords = 64;               // 2048-bit Bloom filter of freed pointers per chunk
 constexpr int kHot = 1024;                    // sites with shared-memory Tier-E counters
-constexpr int kCtasPerSm = 2;
 constexpr long long kNeg = -(1ll << 62);      // "no event" sentinels for max / min
 constexpr long long kPos = (1ll << 62);
 constexpr unsigned long long kNoEp = ~0ull;
+constexpr unsigned kInvalid = 0xffffffffu;
 
 // ---- event decoding (include/scl.h) ----------------------------------------
 __host__ __device__ inline uint64_t ev_size(uint64_t meta) { return meta & 0xFFFFFFFFFFull; }
@@ -42,12 +58,16 @@ struct __align__(16) SegState {
 // Per-segment list entry of episodes started inside the segment (phase 4).
 struct EpStart { unsigned long long ep, ptr; unsigned int pos, pad; };
 
+// One unit ticket, resolved on the host at load time (one 32-B load per ticket).
+struct __align__(16) TicketInfo {
+    long long off_t, n_t;             // trace start (global event index), trace length
+    unsigned t, kraw, slot, nbox;     // trace, unit index (| last << 31), state slot, boxes overlapping the trace
+};
+
 struct ReplayParams {
     const scl_event* ev;              // padded device copy (multiple of 8 events)
     const unsigned long long* off;    // [n_traces+1]
-    const unsigned int* tk_trace;     // ticket -> trace
-    const unsigned int* tk_k;         // ticket -> segment index (bit 31: last segment of the trace)
-    const unsigned int* seg_base;     // trace -> first state slot
+    const TicketInfo* tk;             // [n_segs] in ticket order (unit index, trace)
     SegState* state;                  // [n_segs]
     unsigned int* ticket;             // global ticket counter (zeroed per run)
     unsigned int n_segs;
@@ -60,7 +80,7 @@ struct ReplayParams {
     unsigned int* ep_flag;            // [capacity]  reclaimed flag per episode-start sample
     const unsigned long long* sbase;  // trace -> first sample slot
     scl_trace_summary* summ;          // [n_traces]
-    EpStart* ep_scratch;              // [grid * kSeg]
+    EpStart* ep_scratch;              // [grid * kLBWarps * kUnit]
 };
 
 struct FinalParams {

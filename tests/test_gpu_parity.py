@@ -44,7 +44,8 @@ def test_random_small_ragged():
     rng = np.random.default_rng(1)
     traces = []
     for i in range(400):
-        n = int(rng.choice([0, 1, 3, 7, 8, 9, 31, 255, 256, 257, 2047, 2048, 2049, 5000, int(rng.integers(1, 9000))]))
+        n = int(rng.choice([0, 1, 3, 7, 8, 9, 31, 255, 256, 257, 2047, 2048, 2049, 5000, 8191, 8192, 8193,
+                            16385, 40000, int(rng.integers(1, 9000))]))
         traces.append(tracegen.random_small_trace(rng, n, n_sites=37, max_size=int(rng.integers(1, 200)),
                                                   max_ptrs=int(rng.integers(2, 40))))
     ev, off = _concat(traces)
