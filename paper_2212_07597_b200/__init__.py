@@ -49,9 +49,10 @@ class _RunOpts(ctypes.Structure):
 
 
 def _load():
-    if not os.path.exists(_build.LIB):
-        raise ImportError(f"{_build.LIB} is missing: run __graft_entry__.build() (nvcc for sm_100a)")
-    lib = ctypes.CDLL(_build.LIB)
+    path = os.environ.get("SCL_LIB", _build.LIB)     # SCL_LIB: the debug build (libscl_prof.so)
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: run __graft_entry__.build() (nvcc for sm_100a)")
+    lib = ctypes.CDLL(path)
     P, U64, U32, I32, SZ = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_size_t
     sig = {
         "scl_trace_load": [ctypes.c_char_p, P, P, U32, U32, I32, I32, P],

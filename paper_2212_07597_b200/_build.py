@@ -26,13 +26,15 @@ def up_to_date() -> bool:
     return os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(p) for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, lib: str = LIB, extra=()) -> str:
+    """Compile csrc/*.cu -> lib.  extra: additional nvcc flags (e.g. -DSCL_PROFILE for
+    the debug build with per-role cycle counters, libscl_prof.so)."""
+    if not force and lib == LIB and up_to_date():
         return LIB
     objs = []
     for src in sources():
-        obj = os.path.join(CSRC, os.path.basename(src)[:-3] + ".o")
-        cmd = [NVCC, *FLAGS, "-c", src, "-o", obj]
+        obj = os.path.join(CSRC, os.path.basename(src)[:-3] + (".prof.o" if extra else ".o"))
+        cmd = [NVCC, *FLAGS, *extra, "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if verbose or r.returncode != 0:
             print(" ".join(cmd))
@@ -40,17 +42,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}")
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         print(r.stdout + r.stderr)
         raise RuntimeError("link of libscl.so failed")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     for o in objs:
         os.remove(o)
-    return LIB
+    return lib
 
+
+PROF_LIB = os.path.join(HERE, "libscl_prof.so")
 
 if __name__ == "__main__":
-    build(force=True, verbose=True)
+    import sys
+    if "prof" in sys.argv[1:]:
+        build(force=True, lib=PROF_LIB, extra=("-DSCL_PROFILE",))
+    else:
+        build(force=True, verbose=True)

@@ -66,6 +66,7 @@ struct scl_result {
     bool finalized = false;
     cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     float kern_ms = 0;
+    unsigned long long* d_prof = nullptr;     // SCL_PROFILE builds only
     float run_ms = 0, fin_ms = 0;
 };
 
@@ -273,7 +274,7 @@ extern "C" void scl_result_free(scl_result* r) {
     if (!r) return;
     cudaFree(r->d_table); cudaFree(r->d_samples); cudaFree(r->d_epflag); cudaFree(r->d_sbase);
     cudaFree(r->d_summ); cudaFree(r->d_scratch); cudaFree(r->d_prob); cudaFree(r->d_rate); cudaFree(r->d_flag);
-    cudaFree(r->d_key); cudaFree(r->d_key2); cudaFree(r->d_val); cudaFree(r->d_order); cudaFree(r->d_cub); cudaFree(r->d_rows);
+    cudaFree(r->d_prof); cudaFree(r->d_key); cudaFree(r->d_key2); cudaFree(r->d_val); cudaFree(r->d_order); cudaFree(r->d_cub); cudaFree(r->d_rows);
     for (auto& e : r->ev) if (e) cudaEventDestroy(e);
     delete r;
 }
@@ -359,6 +360,11 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
     p.n_sites = tr->n_sites; p.n_traces = NT; p.T = (long long)threshold;
     p.table = r->d_table; p.samples = r->d_samples; p.ep_flag = r->d_epflag; p.sbase = r->d_sbase;
     p.summ = r->d_summ; p.ep_scratch = r->d_scratch;
+#ifdef SCL_PROFILE
+    if (!r->d_prof) CU(cudaMalloc(&r->d_prof, 32 * 8));
+    CU(cudaMemsetAsync(r->d_prof, 0, 32 * 8, st));
+    p.prof = r->d_prof;
+#endif
     CU(cudaEventRecord(r->ev[4], st));
     CU(launch_replay(&tr->tmap, p, r->grid, st));
     CU(cudaEventRecord(r->ev[5], st));
@@ -476,6 +482,15 @@ extern "C" scl_status scl_result_timing(const scl_result* r, float* replay_kerne
     if (finalize_ms) *finalize_ms = r->fin_ms;
     return SCL_OK;
 }
+
+#ifdef SCL_PROFILE
+// Debug build only: per-role cycle sums of the last run (compute 0..7, producer 8..15, look-back 16..23).
+extern "C" scl_status scl_debug_prof(const scl_result* r, unsigned long long* out) {
+    if (!r || !r->d_prof) return fail(SCL_EINVAL, "no profile");
+    CU(cudaMemcpy(out, r->d_prof, 32 * 8, cudaMemcpyDeviceToHost));
+    return SCL_OK;
+}
+#endif
 
 // "a prime number slightly above 10MB" -- smallest prime >= base (trial division)
 extern "C" uint64_t scl_next_prime(uint64_t base) {

@@ -42,6 +42,22 @@ __device__ __forceinline__ void named_bar(int id, int threads) {
     asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(threads) : "memory");
 }
 
+// Predicated shared-memory reductions / atomics (no divergent branch around them).
+__device__ __forceinline__ void red_add_if(uint32_t addr, unsigned v, bool c) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.shared.add.u32 [%0], %1;\n}"
+                 :: "r"(addr), "r"(v), "r"((unsigned)c) : "memory");
+}
+__device__ __forceinline__ void red_or_if(uint32_t addr, unsigned v, bool c) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.shared.or.b32 [%0], %1;\n}"
+                 :: "r"(addr), "r"(v), "r"((unsigned)c) : "memory");
+}
+__device__ __forceinline__ unsigned atom_add_if(uint32_t addr, unsigned v, bool c) {
+    unsigned old = 0;
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p atom.shared.add.u32 %0, [%1], %3;\n}"
+                 : "+r"(old) : "r"(addr), "r"((unsigned)c), "r"(v) : "memory");
+    return old;
+}
+
 __device__ __forceinline__ long long shfl_ll(long long v, int src) { return __shfl_sync(kFull, v, src); }
 __device__ __forceinline__ long long shfl_up_ll(long long v, int d) { return __shfl_up_sync(kFull, v, d); }
 __device__ __forceinline__ long long shfl_down_ll(long long v, int d) { return __shfl_down_sync(kFull, v, d); }

@@ -24,6 +24,7 @@
 //                   publish the inclusive state, then check the frees against
 //                   the tracked pointer (Bloom query per chunk, exact re-check
 //                   of positives).
+#include <climits>
 #include "scl_internal.cuh"
 #include "ptx.cuh"
 
@@ -39,7 +40,7 @@ struct Slot {                        // compute -> look-back summary of one unit
     long long csum[kChunks], cmx[kChunks], cmn[kChunks];   // per chunk, relative to the chunk start
     long long Pc[kChunks], ax[kChunks], an[kChunks];       // chunk prefix; max/min relative to the unit start
     long long usum, umx, umn;                              // unit aggregate
-    unsigned done, pad;
+    unsigned done, itu;                                    // chunks finished; CTA unit iteration
     unsigned bloom[kChunks][kBloomWords];
 };
 struct __align__(16) Smem {
@@ -49,14 +50,29 @@ struct __align__(16) Smem {
     Slot slot[kSlots];
     SegInfo info[kStages];
     unsigned sub[kStages];           // box index within the unit
-    uint64_t full[kStages], empty[kStages], sfull[kSlots], sempty[kSlots];
+    uint64_t full[kStages], empty[kStages], sempty[kSlots];
+    unsigned sstate[kSlots];         // 0 compute-owned, 1 full (ready for look-back), 2 claimed
+    unsigned situ[kSlots];           // priority of a full slot (unit iteration; + 10^6 after a failed try)
+    unsigned n_units;                // units handed to this CTA (known at the end of the tickets)
+    unsigned n_done;                 // units finished by the look-back warps
 };
 
 size_t replay_smem_bytes() { return 1024 + (size_t)kStages * kSegBytes + sizeof(Smem); }
 
 __device__ __forceinline__ unsigned bloom_bit(unsigned long long ptr) {
-    return (unsigned)((ptr * 0x9E3779B97F4A7C15ull) >> 53);          // 11 bits: 0..2047
+    return ((unsigned)(ptr >> 4) * 0x9E3779B1u) >> 21;               // 11 bits: 0..2047
 }
+
+// Optional per-role cycle accounting (debug build with -DSCL_PROFILE only).
+#ifdef SCL_PROFILE
+#define PROF_DECL unsigned long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long pt = clock64();
+#define PROF_MARK(i) { const long long now_ = clock64(); pacc[i] += now_ - pt; pt = now_; }
+#define PROF_FLUSH(base) if (lane == 0 && p.prof) { for (int q_ = 0; q_ < 8; ++q_) atomicAdd(&p.prof[(base) + q_], pacc[q_]); }
+#else
+#define PROF_DECL
+#define PROF_MARK(i)
+#define PROF_FLUSH(base)
+#endif
 
 // The 8 events of one global row, through L2 (re-read path).
 __device__ __forceinline__ void load_row_global(const scl_event* ev, long long row, unsigned long long* ptr,
@@ -67,38 +83,43 @@ __device__ __forceinline__ void load_row_global(const scl_event* ev, long long r
 }
 
 // ============================================================================ compute warps
-__device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stage, int w, int lane)
+// Two groups of 8 warps alternate boxes (group 0: boxes 0 and 2 of a unit, group 1: 1 and 3);
+// warp w8 of a group takes rows 32*w8 .. 32*w8+31 of its box = chunk g*8 + w8 of the unit.
+__device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stage, int grp, int w8, int lane)
 {
     const unsigned want = p.epoch * 4u;
-    for (unsigned it = 0;; ++it) {
+    const uint32_t cnt_s = smem_u32(s.cnt), blo_s = smem_u32(s.blo), bhi_s = smem_u32(s.bhi);
+    PROF_DECL
+    for (unsigned it = grp;; it += 2) {
         const int st = it % kStages;
+        PROF_MARK(3)
         mbar_wait(&s.full[st], (it / kStages) & 1u);
+        PROF_MARK(0)
         const SegInfo inf = s.info[st];
         const unsigned g = s.sub[st];
         const unsigned itu = it / kSub;                   // unit iteration of this CTA
         const int sl = itu % kSlots;
         if (inf.u == kInvalid) {
-            // propagate termination to every look-back warp (one invalid unit slot each)
-            for (unsigned m = 0; m < (unsigned)kLBWarps; ++m) {
-                const unsigned itm = itu + m;
-                const int slm = itm % kSlots;
-                mbar_wait(&s.sempty[slm], ((itm / kSlots) & 1u) ^ 1u);
-                if (w == 0 && lane == 0) { s.slot[slm].info.u = kInvalid; mbar_arrive(&s.sfull[slm]); }
-                __syncwarp();
-            }
+            // the look-back warps stop once all `itu` units of this CTA are published
+            if (grp == 0 && w8 == 0 && lane == 0) atomicExch(&s.n_units, itu);
+            PROF_FLUSH(0)
             return;
         }
-        if (g == 0) mbar_wait(&s.sempty[sl], ((itu / kSlots) & 1u) ^ 1u);
+        if (g == (unsigned)grp) mbar_wait(&s.sempty[sl], ((itu / kSlots) & 1u) ^ 1u);   // group's first box of the unit
+        PROF_MARK(1)
         Slot& S = s.slot[sl];
-        const int c = g * kComputeWarps + w;              // chunk index within the unit
+        const int c = g * 8 + w8;                         // chunk index within the unit
         S.bloom[c][lane] = 0u; S.bloom[c][lane + 32] = 0u;
-        if (g == 0 && w == 0 && lane == 0) S.info = inf;
+        if (g == 0 && w8 == 0 && lane == 0) S.info = inf;
         __syncwarp();
+        const uint32_t bl_s = smem_u32(&S.bloom[c][0]);
 
         long long run = 0, tmx = kNeg, tmn = kPos;
+        int r32 = 0, mx32 = INT_MIN, mn32 = INT_MAX;
+        bool small = true;                                // 32-bit chunk summary is exact for this lane
         if (g < inf.nbox) {
-            // ---- the 8 events of row 32w+lane (16-B chunk j of row r sits at j ^ (r & 7))
-            const int r = w * 32 + lane;
+            // ---- the 8 events of row 32*w8+lane (16-B chunk j of row r sits at j ^ (r & 7))
+            const int r = w8 * 32 + lane;
             const unsigned char* rowp = stage + (size_t)st * kSegBytes + (size_t)r * 128;
             unsigned long long ptr[kEpt], meta[kEpt];
             #pragma unroll
@@ -107,43 +128,103 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
                 ptr[j] = v.x; meta[j] = v.y;
             }
             const long long e0 = (inf.row_base + (long long)g * kThreads + r) * kEpt - inf.off_t;
+            unsigned big = 0;                                 // any size >= 2^27 in the row?
             #pragma unroll
-            for (int j = 0; j < kEpt; ++j) {
-                const long long ie = e0 + j;
-                const unsigned kind = ev_kind(meta[j]);
-                const bool af = ie >= 0 && ie < inf.n_t && kind < 2;
-                const unsigned long long size = ev_size(meta[j]);
-                run += af ? (kind == 0 ? (long long)size : -(long long)size) : 0;     // a1: signed size
-                if (af) {
-                    tmx = llmax(tmx, run); tmn = llmin(tmn, run);
-                    const unsigned site = ev_site(meta[j]);
-                    if (site < (unsigned)kHot && size < (1ull << 32)) {              // a5 Tier E (shared)
-                        const int x = kind * kHot + site;
-                        atomicAdd(&s.cnt[x], 1u);
-                        const unsigned sz = (unsigned)size;
-                        const unsigned old = atomicAdd(&s.blo[x], sz);
-                        if (old + sz < old) atomicAdd(&s.bhi[x], 1u);
-                    } else {                                                          // cold site / huge size
-                        unsigned long long* row = p.table + (size_t)site * SCL_NCOL;
-                        atomicAdd(&row[SCL_COL_N_MALLOC + kind], 1ull);
-                        atomicAdd(&row[SCL_COL_MALLOC_BYTES + kind], size);
-                    }
-                    if (kind == 1) {                                                  // freed pointer -> Bloom
-                        const unsigned b = bloom_bit(ptr[j]);
-                        atomicOr(&S.bloom[c][b >> 5], 1u << (b & 31));
+            for (int j = 0; j < kEpt; ++j) big |= ((unsigned)meta[j] >> 27) | ((unsigned)(meta[j] >> 32) & 0xffu);
+            unsigned cold = 0;                                // events for the L2 (cold site) path
+            if (e0 >= 0 && e0 + kEpt <= inf.n_t && big == 0) {
+                // fast path: the whole row is in the trace and |partial sums| < 2^30: 32-bit running
+                // sum / max / min (a copy's d = 0 repeats an F already seen: harmless), predicated
+                // shared atomics issued back to back, carries checked after all of them
+                unsigned old[kEpt];
+                #pragma unroll
+                for (int j = 0; j < kEpt; ++j) {
+                    const unsigned hi = (unsigned)(meta[j] >> 32), lo = (unsigned)meta[j];
+                    const unsigned kind = (hi >> 8) & 3u, site = hi >> 11;
+                    r32 += kind == 0 ? (int)lo : (kind == 1 ? -(int)lo : 0);          // a1: signed size
+                    mx32 = max(mx32, r32); mn32 = min(mn32, r32);
+                    const bool h = kind < 2 && site < (unsigned)kHot;
+                    cold |= (kind < 2 && !h ? 1u : 0u) << j;
+                    const uint32_t x = ((kind & 1u) * kHot + (h ? site : 0u)) * 4u;
+                    red_add_if(cnt_s + x, 1u, h);                                     // a5 Tier E
+                    old[j] = atom_add_if(blo_s + x, lo, h);
+                    const unsigned b = bloom_bit(ptr[j]);                             // freed pointer -> Bloom
+                    red_or_if(bl_s + (b >> 5) * 4u, 1u << (b & 31), kind == 1);
+                }
+                #pragma unroll
+                for (int j = 0; j < kEpt; ++j) {
+                    const unsigned hi = (unsigned)(meta[j] >> 32), lo = (unsigned)meta[j];
+                    const unsigned kind = (hi >> 8) & 3u, site = hi >> 11;
+                    const bool h = kind < 2 && site < (unsigned)kHot;
+                    red_add_if(bhi_s + ((kind & 1u) * kHot + (h ? site : 0u)) * 4u, 1u, h && old[j] + lo < old[j]);
+                }
+                run = r32;
+                tmx = mx32; tmn = mn32;
+                small = r32 > -(1 << 25) && r32 < (1 << 25) && mx32 < (1 << 25) && mn32 > -(1 << 25);
+            } else {
+                // exact 64-bit path: rows crossing a trace boundary or holding a size >= 2^27
+                small = false;
+                #pragma unroll
+                for (int j = 0; j < kEpt; ++j) {
+                    const long long ie = e0 + j;
+                    const unsigned kind = ev_kind(meta[j]);
+                    const bool af = ie >= 0 && ie < inf.n_t && kind < 2;
+                    const unsigned long long size = ev_size(meta[j]);
+                    run += af ? (kind == 0 ? (long long)size : -(long long)size) : 0;     // a1: signed size
+                    if (af) {
+                        tmx = llmax(tmx, run); tmn = llmin(tmn, run);
+                        const unsigned site = ev_site(meta[j]);
+                        if (site < (unsigned)kHot && size < (1ull << 32)) {
+                            const int x = kind * kHot + site;
+                            atomicAdd(&s.cnt[x], 1u);
+                            const unsigned old = atomicAdd(&s.blo[x], (unsigned)size);
+                            if (old + (unsigned)size < old) atomicAdd(&s.bhi[x], 1u);
+                        } else {
+                            cold |= 1u << j;
+                        }
+                        if (kind == 1) {
+                            const unsigned b = bloom_bit(ptr[j]);
+                            atomicOr(&S.bloom[c][b >> 5], 1u << (b & 31));
+                        }
                     }
                 }
             }
+            while (cold) {                                    // cold site / huge size: L2 reductions
+                const int j = __ffs(cold) - 1;
+                cold &= cold - 1;
+                unsigned long long mj = 0;
+                #pragma unroll
+                for (int q = 0; q < kEpt; ++q) if (q == j) mj = meta[q];
+                const unsigned kind = ev_kind(mj);
+                unsigned long long* row = p.table + (size_t)ev_site(mj) * SCL_NCOL;
+                atomicAdd(&row[SCL_COL_N_MALLOC + kind], 1ull);
+                atomicAdd(&row[SCL_COL_MALLOC_BYTES + kind], ev_size(mj));
+            }
         }
+        PROF_MARK(4)
         // ---- chunk summary: sum, max / min prefix relative to the chunk start
-        long long incl = run;
-        #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) { long long o = shfl_up_ll(incl, d); if (lane >= d) incl += o; }
-        const long long Pl = incl - run;
-        const long long cmx = warp_max(Pl + tmx), cmn = warp_min(Pl + tmn);
-        if (lane == 31) { S.csum[c] = incl; S.cmx[c] = cmx; S.cmn[c] = cmn; }
+        long long csum, cmx, cmn;
+        if (__all_sync(kFull, small)) {                       // 32-bit scan + REDUX
+            int incl = r32;
+            #pragma unroll
+            for (int d = 1; d < 32; d <<= 1) { int o = __shfl_up_sync(kFull, incl, d); if (lane >= d) incl += o; }
+            const int a = mx32 == INT_MIN ? INT_MIN : incl - r32 + mx32;
+            const int b = mn32 == INT_MAX ? INT_MAX : incl - r32 + mn32;
+            const int am = __reduce_max_sync(kFull, a), bm = __reduce_min_sync(kFull, b);
+            csum = __shfl_sync(kFull, incl, 31);
+            cmx = am == INT_MIN ? kNeg : am; cmn = bm == INT_MAX ? kPos : bm;
+        } else {
+            long long incl = run;
+            #pragma unroll
+            for (int d = 1; d < 32; d <<= 1) { long long o = shfl_up_ll(incl, d); if (lane >= d) incl += o; }
+            const long long Pl = incl - run;
+            cmx = warp_max(Pl + tmx); cmn = warp_min(Pl + tmn);
+            csum = shfl_ll(incl, 31);
+        }
+        if (lane == 0) { S.csum[c] = csum; S.cmx[c] = cmx; S.cmn[c] = cmn; }
         __syncwarp();
         mbar_arrive(&s.empty[st]);                        // box consumed
+        PROF_MARK(2)
         unsigned old = 0;
         if (lane == 0) { __threadfence_block(); old = atomicAdd(&S.done, 1u); __threadfence_block(); }
         old = __shfl_sync(kFull, old, 0);
@@ -163,7 +244,7 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
                 st_release(&my->flag, want + 1);
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&s.sfull[sl]);
+            if (lane == 0) { S.itu = itu; ((volatile unsigned*)s.situ)[sl] = itu; __threadfence_block(); atomicExch(&s.sstate[sl], 1u); }
         }
     }
 }
@@ -172,6 +253,7 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
 __device__ void producer_role(const ReplayParams& p, const CUtensorMap* tmap, Smem& s, unsigned char* stage, int lane)
 {
     if (lane != 0) return;
+    PROF_DECL
     auto resolve = [&](unsigned u) {
         SegInfo inf; inf.u = kInvalid; inf.nbox = 0;
         if (u < p.n_segs) {
@@ -192,16 +274,19 @@ __device__ void producer_role(const ReplayParams& p, const CUtensorMap* tmap, Sm
         const unsigned u_after = nxt.u == kInvalid ? kInvalid : atomicAdd(p.ticket, 1u);
         for (unsigned g = 0; g < (unsigned)kSub; ++g, ++it) {
             const int st = it % kStages;
+            PROF_MARK(1)
             mbar_wait(&s.empty[st], ((it / kStages) & 1u) ^ 1u);
+            PROF_MARK(0)
             s.info[st] = cur; s.sub[st] = g;
             if (cur.u == kInvalid || g >= cur.nbox) {
                 mbar_arrive(&s.full[st]);                  // sentinel / box outside the trace
+                if (cur.u == kInvalid && g == 0) continue; // the sentinel goes to both compute groups
             } else {
                 mbar_expect_tx(&s.full[st], kSegBytes);
                 tma_load_2d(stage + (size_t)st * kSegBytes, tmap, 0, (int)(cur.row_base + (long long)g * kThreads),
                             &s.full[st]);
             }
-            if (cur.u == kInvalid) return;
+            if (cur.u == kInvalid) { PROF_FLUSH(8) return; }
         }
         cur = nxt;
         u_next = u_after;
@@ -223,31 +308,31 @@ __device__ __forceinline__ InState load_inclusive_warp(const SegState* q, int la
     return x;
 }
 
-// State before unit k of a trace (a1-a4 carries).  Units k-1, k-2, ... are
-// examined 32 at a time (lane i <-> unit k-1-i).  From the nearest inclusive
-// state ("base") the aggregates of the units after it are applied in order
-// while the sampler provably does not fire (every prefix of the carry stays
-// in (-T, T)); at the first unit where it could fire, the warp waits for that
-// unit's inclusive state and continues from there.
-__device__ InState look_back(const ReplayParams& p, const SegState* ts, unsigned k, unsigned want, int lane)
+// State before unit k of a trace (a1-a4 carries), NON-BLOCKING: returns false if
+// a state it needs is not published yet (the caller retries later).  Units
+// k-1, k-2, ... are examined 32 at a time (lane i <-> unit k-1-i).  From the
+// nearest inclusive state ("base") the aggregates of the units after it are
+// applied in order while the sampler provably does not fire (every prefix of
+// the carry stays in (-T, T)); at the first unit where it could fire, that
+// unit's inclusive state is needed.
+__device__ bool look_back(const ReplayParams& p, const SegState* ts, unsigned k, unsigned want, int lane, InState& b)
 {
-    InState b{0, 0, 0, 0, 0, kNoEp, 0};
-    if (k == 0) return b;
+    b = InState{0, 0, 0, 0, 0, kNoEp, 0};
+    if (k == 0) return true;
     const int j = (int)k - 1;
     const int idx = j - lane;
-    unsigned fl = 0;
-    if (idx >= 0) {
-        const unsigned* fp = &ts[idx].flag;
-        do { fl = ld_acquire(fp); } while (fl < want + 1);
-    }
+    const unsigned fl = idx >= 0 ? ld_acquire(&ts[idx].flag) : 0u;
     const unsigned im = __ballot_sync(kFull, idx >= 0 && fl >= want + 2);
     if (!im && j - 31 > 0) {
-        // no inclusive state within 32 units: wait for the predecessor's (rare)
-        if (lane == 0) { unsigned f; do { f = ld_acquire(&ts[k - 1].flag); } while (f < want + 2); }
-        __syncwarp();
-        return load_inclusive_warp(&ts[k - 1], lane);
+        // no inclusive state within 32 units: the predecessor's is needed (rare)
+        unsigned f = lane == 0 ? ld_acquire(&ts[k - 1].flag) : 0u;
+        if (__shfl_sync(kFull, f, 0) < want + 2) return false;
+        b = load_inclusive_warp(&ts[k - 1], lane);
+        return true;
     }
     int stop = im ? __ffs(im) - 1 : 32;                    // lanes < stop: units after the base
+    const unsigned lowmask = stop >= 32 ? kFull : ((1u << stop) - 1u);
+    if (__ballot_sync(kFull, idx >= 0 && fl < want + 1) & lowmask) return false;   // aggregate missing
     long long a_s = 0, a_x = kNeg, a_n = kPos;
     if (lane < stop && idx >= 0) {
         const SegState* q = &ts[idx];
@@ -269,12 +354,12 @@ __device__ InState look_back(const ReplayParams& p, const SegState* ts, unsigned
             const long long mx = warp_max(lane < stop ? E + a_x : kNeg);
             b.M = llmax(b.M, b.F + mx);
             b.F += tot;
-            return b;
+            return true;
         }
         const int jf = 31 - __clz(bm);                     // earliest unit where a sample may fire
         const SegState* q = &ts[j - jf];
-        if (lane == 0) { unsigned f; do { f = ld_acquire(&q->flag); } while (f < want + 2); }
-        __syncwarp();
+        unsigned f = lane == 0 ? ld_acquire(&q->flag) : 0u;
+        if (__shfl_sync(kFull, f, 0) < want + 2) return false;
         b = load_inclusive_warp(q, lane);
         stop = jf;
     }
@@ -284,19 +369,51 @@ __device__ void lookback_role(const ReplayParams& p, Smem& s, int lbw, int lane)
 {
     const unsigned want = p.epoch * 4u;
     EpStart* eplist = p.ep_scratch + ((size_t)blockIdx.x * kLBWarps + lbw) * kUnit;
-    for (unsigned it = lbw;; it += kLBWarps) {
-        const int sl = it % kSlots;
-        mbar_wait(&s.sfull[sl], (it / kSlots) & 1u);
+    PROF_DECL
+    for (;;) {
+        // claim the oldest full slot whose incoming state is available (any look-back warp
+        // may take any slot, so a unit waiting on its chain never blocks the others)
+        int sl = -1;
+        unsigned best = kInvalid;
+        if (lane < kSlots) {
+            const unsigned stt = ((volatile unsigned*)s.sstate)[lane];
+            if (stt == 1) best = ((volatile unsigned*)s.situ)[lane];
+        }
+        #pragma unroll
+        for (int d = 16; d > 0; d >>= 1) best = min(best, __shfl_xor_sync(kFull, best, d));
+        if (best == kInvalid) {
+            const unsigned nu = ((volatile unsigned*)&s.n_units)[0], nd = ((volatile unsigned*)&s.n_done)[0];
+            if (nu != kInvalid && nd >= nu) { PROF_FLUSH(16) return; }
+            PROF_MARK(0)
+            __nanosleep(64);
+            continue;
+        }
+        const unsigned cand = __ballot_sync(kFull, lane < kSlots && ((volatile unsigned*)s.sstate)[lane] == 1 &&
+                                                    ((volatile unsigned*)s.situ)[lane] == best);
+        if (!cand) continue;
+        const int q = __ffs(cand) - 1;
+        unsigned got = 0;
+        if (lane == 0) got = atomicCAS(&s.sstate[q], 1u, 2u);
+        if (__shfl_sync(kFull, got, 0) != 1u) continue;
+        sl = q;
+        __threadfence_block();
+        PROF_MARK(0)
         Slot& S = s.slot[sl];
         const SegInfo inf = S.info;
-        if (inf.u == kInvalid) return;
         const unsigned k = inf.kraw & 0x7fffffffu;
         const bool last = (inf.kraw >> 31) != 0;
         SegState* my = &p.state[inf.slot];
         const long long usum = S.usum, umx = S.umx, umn = S.umn;
 
-        // ---- incoming state (chain)
-        const InState in = look_back(p, &p.state[inf.slot - k], k, want, lane);
+        // ---- incoming state (chain); not available yet -> release the claim, retry later
+        InState in;
+        const bool ready = look_back(p, &p.state[inf.slot - k], k, want, lane, in);
+        PROF_MARK(1)
+        if (!ready) {
+            if (lane == 0) { ((volatile unsigned*)s.situ)[sl] = S.itu + 1000000u; __threadfence_block(); atomicExch(&s.sstate[sl], 1u); }
+            __syncwarp();
+            continue;
+        }
 
         // ---- a3/a4: samples of this unit (band test per chunk; exact re-scan only where needed)
         long long B = in.B;
@@ -387,6 +504,7 @@ __device__ void lookback_role(const ReplayParams& p, Smem& s, int lbw, int lane)
                 Mrun = llmax(Mrun, hi);
             }
         }
+        PROF_MARK(2)
         // ---- publish the inclusive state (the end of the chain's critical path)
         if (lane == 0) {
             my->F = F0 + usum; my->M = llmax(in.M, F0 + umx); my->B = B;
@@ -400,6 +518,7 @@ __device__ void lookback_role(const ReplayParams& p, Smem& s, int lbw, int lane)
         }
         __syncwarp();
 
+        PROF_MARK(3)
         // ---- a4 free-pointer match, "a pointer comparison that is almost always false":
         // lane c decides whether chunk c may hold a free of an active tracked pointer (Bloom)
         if (in.ep != kNoEp || nl > 0) {
@@ -438,34 +557,40 @@ __device__ void lookback_role(const ReplayParams& p, Smem& s, int lbw, int lane)
                 }
             }
         }
-        if (lane == 0) S.done = 0;
+        PROF_MARK(4)
+        if (lane == 0) {
+            S.done = 0; __threadfence_block();
+            atomicExch(&s.sstate[sl], 0u); mbar_arrive(&s.sempty[sl]); atomicAdd(&s.n_done, 1u);
+        }
         __syncwarp();
-        mbar_arrive(&s.sempty[sl]);
     }
 }
 
 // ============================================================================ kernel
-__global__ void __maxnreg__(168)
+__global__ void __maxnreg__(96)
 replay_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ ReplayParams p)
 {
-    extern __shared__ unsigned char smem_raw[];
-    unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    unsigned char* stage = base;                                     // kStages x 32 KiB, 1024-aligned
-    Smem& s = *reinterpret_cast<Smem*>(base + (size_t)kStages * kSegBytes);
+    // Pointers into dynamic shared memory are derived by pointer arithmetic only (never through
+    // an integer), so that ptxas keeps the shared state space: LDS / ATOMS, not generic LD / ATOM.
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* stage = smem_raw;                                 // kStages x 32 KiB, 1024-aligned (swizzle)
+    Smem& s = *reinterpret_cast<Smem*>(smem_raw + (size_t)kStages * kSegBytes);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0 && (smem_u32(smem_raw) & 1023u) != 0) __trap();     // the 128-B swizzle needs 1024-B alignment
 
     for (int x = tid; x < 2 * kHot; x += kCtaThreads) { s.cnt[x] = 0; s.blo[x] = 0; s.bhi[x] = 0; }
     for (int x = tid; x < kSlots; x += kCtaThreads) s.slot[x].done = 0;
     if (tid == 0) {
-        for (int i = 0; i < kStages; ++i) { mbar_init(&s.full[i], 1); mbar_init(&s.empty[i], kComputeWarps * 32); }
-        for (int i = 0; i < kSlots; ++i) { mbar_init(&s.sfull[i], 1); mbar_init(&s.sempty[i], 32); }
+        for (int i = 0; i < kStages; ++i) { mbar_init(&s.full[i], 1); mbar_init(&s.empty[i], 8 * 32); }
+        for (int i = 0; i < kSlots; ++i) { mbar_init(&s.sempty[i], 1); s.sstate[i] = 0; s.situ[i] = 0; }
+        s.n_units = kInvalid; s.n_done = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" :: "l"((uint64_t)&tmap) : "memory");
     }
     __syncthreads();
 
     if (warp < kComputeWarps) {
-        compute_role(p, s, stage, warp, lane);
+        compute_role(p, s, stage, warp / 8, warp % 8, lane);
         named_bar(1, kComputeWarps * 32);                            // all compute warps done
         for (int x = tid; x < 2 * kHot; x += kComputeWarps * 32) {   // flush Tier-E counters
             const unsigned c = s.cnt[x];

@@ -14,10 +14,10 @@ namespace scl {
 // compute lane reads its own row with conflict-free LDS.128.  A chain UNIT
 // (the look-back granule) is kSub = 4 boxes = 8192 events = 32 chunks of 256
 // events (one chunk per compute warp per box).  One persistent CTA per SM:
-//   warps 0..7   compute: stream boxes (one chunk per warp), no CTA barriers;
+//   warps 0..15  compute: two groups of 8 alternate boxes (one chunk per warp), no CTA barriers;
 //                the last warp to finish a unit publishes its aggregate
-//   warp  8      producer: tickets (one per unit) + TMA issue into a kStages ring
-//   warps 9..11  look-back: chain the units of a trace, resolve samples,
+//   warp  16     producer: tickets (one per unit) + TMA issue into a kStages ring
+//   warps 17..19 look-back: chain the units of a trace, resolve samples,
 //                match frees against the tracked pointer, publish
 constexpr int kThreads = 256;                 // rows per box = compute threads
 constexpr int kEpt = 8;                       // events per row
@@ -27,8 +27,8 @@ constexpr int kSub = 4;                       // boxes per unit
 constexpr int kUnitRows = kThreads * kSub;
 constexpr int kUnit = kSeg * kSub;            // events per unit (8192)
 constexpr int kChunks = 32;                   // 256-event chunks per unit (one per look-back lane)
-constexpr int kComputeWarps = 8;
-constexpr int kLBWarps = 3;                   // 12 warps total: 3 per SM sub-partition (register budget)
+constexpr int kComputeWarps = 16;                // two groups of 8, alternating boxes
+constexpr int kLBWarps = 3;                   // 20 warps total (5 per SM sub-partition, 96 registers)
 constexpr int kProducerWarp = kComputeWarps;
 constexpr int kCtaThreads = (kComputeWarps + 1 + kLBWarps) * 32;
 constexpr int kStages = 4;                    // TMA ring depth
@@ -81,6 +81,7 @@ struct ReplayParams {
     const unsigned long long* sbase;  // trace -> first sample slot
     scl_trace_summary* summ;          // [n_traces]
     EpStart* ep_scratch;              // [grid * kLBWarps * kUnit]
+    unsigned long long* prof;         // debug build only (SCL_PROFILE): per-role cycle sums, else NULL
 };
 
 struct FinalParams {
