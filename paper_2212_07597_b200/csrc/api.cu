@@ -54,6 +54,7 @@ struct scl_result {
     unsigned long long* d_sbase = nullptr;
     scl_trace_summary* d_summ = nullptr;
     EpStart* d_scratch = nullptr; int grid = 0;
+    void* d_park = nullptr;
     double* d_prob = nullptr; double* d_rate = nullptr; unsigned char* d_flag = nullptr;
     unsigned long long *d_key = nullptr, *d_key2 = nullptr; unsigned int *d_val = nullptr, *d_order = nullptr;
     void* d_cub = nullptr; size_t cub_bytes = 0;
@@ -273,7 +274,7 @@ extern "C" scl_status scl_traces_info(const scl_traces* t, uint64_t* n_events, u
 extern "C" void scl_result_free(scl_result* r) {
     if (!r) return;
     cudaFree(r->d_table); cudaFree(r->d_samples); cudaFree(r->d_epflag); cudaFree(r->d_sbase);
-    cudaFree(r->d_summ); cudaFree(r->d_scratch); cudaFree(r->d_prob); cudaFree(r->d_rate); cudaFree(r->d_flag);
+    cudaFree(r->d_summ); cudaFree(r->d_scratch); cudaFree(r->d_park); cudaFree(r->d_prob); cudaFree(r->d_rate); cudaFree(r->d_flag);
     cudaFree(r->d_prof); cudaFree(r->d_key); cudaFree(r->d_key2); cudaFree(r->d_val); cudaFree(r->d_order); cudaFree(r->d_cub); cudaFree(r->d_rows);
     for (auto& e : r->ev) if (e) cudaEventDestroy(e);
     delete r;
@@ -288,6 +289,7 @@ static scl_status alloc_result(scl_result* r, const scl_traces* tr) {
     CU(cudaMalloc(&r->d_sbase, nt * 8));
     CU(cudaMalloc(&r->d_summ, nt * sizeof(scl_trace_summary)));
     CU(cudaMalloc(&r->d_scratch, (size_t)grid * kLBWarps * kUnit * sizeof(EpStart)));
+    CU(cudaMalloc(&r->d_park, (size_t)grid * kLBWarps * kPark * replay_park_bytes()));
     CU(cudaMalloc(&r->d_prob, S * 8)); CU(cudaMalloc(&r->d_rate, S * 8)); CU(cudaMalloc(&r->d_flag, S));
     CU(cudaMalloc(&r->d_key, S * 8)); CU(cudaMalloc(&r->d_key2, S * 8));
     CU(cudaMalloc(&r->d_val, S * 4)); CU(cudaMalloc(&r->d_order, S * 4));
@@ -359,10 +361,10 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
     p.state = tr->d_state; p.ticket = tr->d_ticket; p.n_segs = tr->n_segs; p.epoch = tr->epoch;
     p.n_sites = tr->n_sites; p.n_traces = NT; p.T = (long long)threshold;
     p.table = r->d_table; p.samples = r->d_samples; p.ep_flag = r->d_epflag; p.sbase = r->d_sbase;
-    p.summ = r->d_summ; p.ep_scratch = r->d_scratch;
+    p.summ = r->d_summ; p.ep_scratch = r->d_scratch; p.park = r->d_park;
 #ifdef SCL_PROFILE
-    if (!r->d_prof) CU(cudaMalloc(&r->d_prof, 32 * 8));
-    CU(cudaMemsetAsync(r->d_prof, 0, 32 * 8, st));
+    if (!r->d_prof) CU(cudaMalloc(&r->d_prof, (32 + 2 * (size_t)tr->n_segs) * 8));
+    CU(cudaMemsetAsync(r->d_prof, 0, (32 + 2 * (size_t)tr->n_segs) * 8, st));
     p.prof = r->d_prof;
 #endif
     CU(cudaEventRecord(r->ev[4], st));
@@ -487,7 +489,7 @@ extern "C" scl_status scl_result_timing(const scl_result* r, float* replay_kerne
 // Debug build only: per-role cycle sums of the last run (compute 0..7, producer 8..15, look-back 16..23).
 extern "C" scl_status scl_debug_prof(const scl_result* r, unsigned long long* out) {
     if (!r || !r->d_prof) return fail(SCL_EINVAL, "no profile");
-    CU(cudaMemcpy(out, r->d_prof, 32 * 8, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(out, r->d_prof, (32 + 2 * (size_t)r->tr->n_segs) * 8, cudaMemcpyDeviceToHost));
     return SCL_OK;
 }
 #endif

@@ -35,7 +35,7 @@ struct SegInfo {                     // one unit ticket, as the producer resolve
     long long off_t, n_t, row_base;  // trace start, trace length, first global row of the unit
     unsigned nbox, pad;              // boxes of this unit that overlap the trace
 };
-struct Slot {                        // compute -> look-back summary of one unit
+struct __align__(16) Slot {          // compute -> look-back summary of one unit
     SegInfo info;
     long long csum[kChunks], cmx[kChunks], cmn[kChunks];   // per chunk, relative to the chunk start
     long long Pc[kChunks], ax[kChunks], an[kChunks];       // chunk prefix; max/min relative to the unit start
@@ -57,10 +57,18 @@ struct __align__(16) Smem {
     unsigned n_done;                 // units finished by the look-back warps
 };
 
+size_t replay_park_bytes() { return sizeof(Slot); }
 size_t replay_smem_bytes() { return 1024 + (size_t)kStages * kSegBytes + sizeof(Smem); }
 
-__device__ __forceinline__ unsigned bloom_bit(unsigned long long ptr) {
-    return ((unsigned)(ptr >> 4) * 0x9E3779B1u) >> 21;               // 11 bits: 0..2047
+// Blocked Bloom filter of freed pointers, 64 words (2048 bits) per 256-event chunk: one
+// word per pointer, two bits in it (one shared-memory OR per free; ~1.4 % false positives
+// at ~128 frees per chunk).
+__device__ __forceinline__ unsigned bloom_word(unsigned long long ptr) {
+    return ((unsigned)(ptr >> 4) * 0x9E3779B1u) >> 26;
+}
+__device__ __forceinline__ unsigned bloom_mask(unsigned long long ptr) {
+    const unsigned h = (unsigned)(ptr >> 4) * 0x85EBCA77u;
+    return (1u << (h >> 27)) | (1u << ((h >> 22) & 31u));
 }
 
 // Optional per-role cycle accounting (debug build with -DSCL_PROFILE only).
@@ -68,10 +76,12 @@ __device__ __forceinline__ unsigned bloom_bit(unsigned long long ptr) {
 #define PROF_DECL unsigned long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long pt = clock64();
 #define PROF_MARK(i) { const long long now_ = clock64(); pacc[i] += now_ - pt; pt = now_; }
 #define PROF_FLUSH(base) if (lane == 0 && p.prof) { for (int q_ = 0; q_ < 8; ++q_) atomicAdd(&p.prof[(base) + q_], pacc[q_]); }
+#define PROF_UNIT_T(u, which) if (p.prof) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); p.prof[32 + 2 * (size_t)(u) + (which)] = t_; }
 #else
 #define PROF_DECL
 #define PROF_MARK(i)
 #define PROF_FLUSH(base)
+#define PROF_UNIT_T(u, which)
 #endif
 
 // The 8 events of one global row, through L2 (re-read path).
@@ -148,8 +158,7 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
                     const uint32_t x = ((kind & 1u) * kHot + (h ? site : 0u)) * 4u;
                     red_add_if(cnt_s + x, 1u, h);                                     // a5 Tier E
                     old[j] = atom_add_if(blo_s + x, lo, h);
-                    const unsigned b = bloom_bit(ptr[j]);                             // freed pointer -> Bloom
-                    red_or_if(bl_s + (b >> 5) * 4u, 1u << (b & 31), kind == 1);
+                    red_or_if(bl_s + bloom_word(ptr[j]) * 4u, bloom_mask(ptr[j]), kind == 1);   // freed ptr -> Bloom
                 }
                 #pragma unroll
                 for (int j = 0; j < kEpt; ++j) {
@@ -182,10 +191,7 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
                         } else {
                             cold |= 1u << j;
                         }
-                        if (kind == 1) {
-                            const unsigned b = bloom_bit(ptr[j]);
-                            atomicOr(&S.bloom[c][b >> 5], 1u << (b & 31));
-                        }
+                        if (kind == 1) atomicOr(&S.bloom[c][bloom_word(ptr[j])], bloom_mask(ptr[j]));
                     }
                 }
             }
@@ -242,6 +248,7 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
                 SegState* my = &p.state[S.info.slot];
                 my->sum = usum; my->mx = umx; my->mn = umn;
                 st_release(&my->flag, want + 1);
+                PROF_UNIT_T(S.info.slot, 0)
             }
             __syncwarp();
             if (lane == 0) { S.itu = itu; ((volatile unsigned*)s.situ)[sl] = itu; __threadfence_block(); atomicExch(&s.sstate[sl], 1u); }
@@ -308,113 +315,73 @@ __device__ __forceinline__ InState load_inclusive_warp(const SegState* q, int la
     return x;
 }
 
-// State before unit k of a trace (a1-a4 carries), NON-BLOCKING: returns false if
-// a state it needs is not published yet (the caller retries later).  Units
-// k-1, k-2, ... are examined 32 at a time (lane i <-> unit k-1-i).  From the
-// nearest inclusive state ("base") the aggregates of the units after it are
-// applied in order while the sampler provably does not fire (every prefix of
-// the carry stays in (-T, T)); at the first unit where it could fire, that
-// unit's inclusive state is needed.
-__device__ bool look_back(const ReplayParams& p, const SegState* ts, unsigned k, unsigned want, int lane, InState& b)
+// State before unit k of a trace (a1-a4 carries), NON-BLOCKING: returns false (with the
+// flag it waits for) if a state it needs is not published yet.  Backward: windows of 32
+// units (lane i <-> unit j-i) until the nearest inclusive state (the "base"; or the trace
+// start), checking that every unit after it has its aggregate.  Forward: from the base,
+// units are composed 32 at a time (lane i <-> unit start+i) while the sampler provably
+// does not fire (every prefix of the carry stays in (-T, T)); at the first unit where it
+// could fire, that unit's inclusive state is needed and becomes the new base.
+__device__ bool look_back(const ReplayParams& p, const SegState* ts, unsigned k, unsigned want, int lane, InState& b,
+                          const unsigned*& blk, unsigned& need, int resume = -1)
 {
     b = InState{0, 0, 0, 0, 0, kNoEp, 0};
+    blk = nullptr; need = 0;
     if (k == 0) return true;
-    const int j = (int)k - 1;
-    const int idx = j - lane;
-    const unsigned fl = idx >= 0 ? ld_acquire(&ts[idx].flag) : 0u;
-    const unsigned im = __ballot_sync(kFull, idx >= 0 && fl >= want + 2);
-    if (!im && j - 31 > 0) {
-        // no inclusive state within 32 units: the predecessor's is needed (rare)
-        unsigned f = lane == 0 ? ld_acquire(&ts[k - 1].flag) : 0u;
-        if (__shfl_sync(kFull, f, 0) < want + 2) return false;
-        b = load_inclusive_warp(&ts[k - 1], lane);
-        return true;
+    int base = resume;                                     // unit holding the base state (-1: trace start)
+    // resume: a parked unit re-tried because the inclusive state it waited for (unit `resume`)
+    // is published -- start the forward walk there (aggregates after it were checked before)
+    if (resume < 0) for (int j = (int)k - 1;; j -= 32) {
+        const int idx = j - lane;
+        const unsigned fl = idx >= 0 ? ld_acquire(&ts[idx].flag) : 0u;
+        const unsigned im = __ballot_sync(kFull, idx >= 0 && fl >= want + 2);
+        const int stop = im ? __ffs(im) - 1 : 32;
+        const unsigned lowmask = stop >= 32 ? kFull : ((1u << stop) - 1u);
+        const unsigned miss = __ballot_sync(kFull, idx >= 0 && fl < want + 1) & lowmask;
+        if (miss) { blk = &ts[j - (__ffs(miss) - 1)].flag; need = want + 1; return false; }   // an aggregate is missing
+        if (im) { base = j - stop; break; }
+        if (j - 31 <= 0) break;                            // reached unit 0: base = trace start
     }
-    int stop = im ? __ffs(im) - 1 : 32;                    // lanes < stop: units after the base
-    const unsigned lowmask = stop >= 32 ? kFull : ((1u << stop) - 1u);
-    if (__ballot_sync(kFull, idx >= 0 && fl < want + 1) & lowmask) return false;   // aggregate missing
-    long long a_s = 0, a_x = kNeg, a_n = kPos;
-    if (lane < stop && idx >= 0) {
-        const SegState* q = &ts[idx];
-        a_s = __ldcg(&q->sum); a_x = __ldcg(&q->mx); a_n = __ldcg(&q->mn);
-    }
-    if (im) b = load_inclusive_warp(&ts[j - stop], lane);  // else base = trace start
-    for (;;) {
-        // forward order = decreasing lane; E = sum over earlier units (higher lanes < stop)
-        const long long v = lane < stop ? a_s : 0;
-        long long inc = v;
+    if (base >= 0) b = load_inclusive_warp(&ts[base], lane);
+    for (int start = base + 1; start < (int)k;) {
+        const int idx = start + lane;
+        const bool in = idx < (int)k;
+        long long a_s = 0, a_x = kNeg, a_n = kPos;
+        if (in) { const SegState* q = &ts[idx]; a_s = __ldcg(&q->sum); a_x = __ldcg(&q->mx); a_n = __ldcg(&q->mn); }
+        long long inc = a_s;
         #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) { long long o = shfl_down_ll(inc, d); if (lane + d < 32) inc += o; }
-        const long long E = inc - v;
+        for (int d = 1; d < 32; d <<= 1) { long long o = shfl_up_ll(inc, d); if (lane >= d) inc += o; }
+        const long long E = inc - a_s;                     // sum of the earlier units of the window
         const long long c = b.F - b.B + E;
-        const bool bad = lane < stop && (c + a_x >= p.T || c + a_n <= -p.T);
-        const unsigned bm = __ballot_sync(kFull, bad);
+        const unsigned bm = __ballot_sync(kFull, in && (c + a_x >= p.T || c + a_n <= -p.T));
         if (!bm) {
-            const long long tot = shfl_ll(inc, 0);
-            const long long mx = warp_max(lane < stop ? E + a_x : kNeg);
+            const long long mx = warp_max(in ? E + a_x : kNeg);
             b.M = llmax(b.M, b.F + mx);
-            b.F += tot;
-            return true;
+            b.F += shfl_ll(inc, 31);
+            start += 32;
+            continue;
         }
-        const int jf = 31 - __clz(bm);                     // earliest unit where a sample may fire
-        const SegState* q = &ts[j - jf];
+        const int jf = __ffs(bm) - 1;                      // earliest unit where a sample may fire
+        const SegState* q = &ts[start + jf];
         unsigned f = lane == 0 ? ld_acquire(&q->flag) : 0u;
-        if (__shfl_sync(kFull, f, 0) < want + 2) return false;
+        if (__shfl_sync(kFull, f, 0) < want + 2) { blk = &q->flag; need = want + 2; return false; }
         b = load_inclusive_warp(q, lane);
-        stop = jf;
+        start += jf + 1;
     }
+    return true;
 }
 
-__device__ void lookback_role(const ReplayParams& p, Smem& s, int lbw, int lane)
+// Finish unit S (smem slot or its parked global copy) once its incoming state is known:
+// samples, inclusive state, free-pointer match.
+__device__ void finish_unit(const ReplayParams& p, const Slot* Sp, const InState& in, unsigned want,
+                            EpStart* eplist, int lane)
 {
-    const unsigned want = p.epoch * 4u;
-    EpStart* eplist = p.ep_scratch + ((size_t)blockIdx.x * kLBWarps + lbw) * kUnit;
-    PROF_DECL
-    for (;;) {
-        // claim the oldest full slot whose incoming state is available (any look-back warp
-        // may take any slot, so a unit waiting on its chain never blocks the others)
-        int sl = -1;
-        unsigned best = kInvalid;
-        if (lane < kSlots) {
-            const unsigned stt = ((volatile unsigned*)s.sstate)[lane];
-            if (stt == 1) best = ((volatile unsigned*)s.situ)[lane];
-        }
-        #pragma unroll
-        for (int d = 16; d > 0; d >>= 1) best = min(best, __shfl_xor_sync(kFull, best, d));
-        if (best == kInvalid) {
-            const unsigned nu = ((volatile unsigned*)&s.n_units)[0], nd = ((volatile unsigned*)&s.n_done)[0];
-            if (nu != kInvalid && nd >= nu) { PROF_FLUSH(16) return; }
-            PROF_MARK(0)
-            __nanosleep(64);
-            continue;
-        }
-        const unsigned cand = __ballot_sync(kFull, lane < kSlots && ((volatile unsigned*)s.sstate)[lane] == 1 &&
-                                                    ((volatile unsigned*)s.situ)[lane] == best);
-        if (!cand) continue;
-        const int q = __ffs(cand) - 1;
-        unsigned got = 0;
-        if (lane == 0) got = atomicCAS(&s.sstate[q], 1u, 2u);
-        if (__shfl_sync(kFull, got, 0) != 1u) continue;
-        sl = q;
-        __threadfence_block();
-        PROF_MARK(0)
-        Slot& S = s.slot[sl];
-        const SegInfo inf = S.info;
-        const unsigned k = inf.kraw & 0x7fffffffu;
-        const bool last = (inf.kraw >> 31) != 0;
-        SegState* my = &p.state[inf.slot];
-        const long long usum = S.usum, umx = S.umx, umn = S.umn;
-
-        // ---- incoming state (chain); not available yet -> release the claim, retry later
-        InState in;
-        const bool ready = look_back(p, &p.state[inf.slot - k], k, want, lane, in);
-        PROF_MARK(1)
-        if (!ready) {
-            if (lane == 0) { ((volatile unsigned*)s.situ)[sl] = S.itu + 1000000u; __threadfence_block(); atomicExch(&s.sstate[sl], 1u); }
-            __syncwarp();
-            continue;
-        }
-
+    const Slot& S = *Sp;
+    const SegInfo inf = S.info;
+    const bool last = (inf.kraw >> 31) != 0;
+    SegState* my = &p.state[inf.slot];
+    const long long usum = S.usum, umx = S.umx, umn = S.umn;
+    {
         // ---- a3/a4: samples of this unit (band test per chunk; exact re-scan only where needed)
         long long B = in.B;
         unsigned long long n = in.n, nep = in.nep, ep = in.ep, eptr = in.eptr;
@@ -504,12 +471,12 @@ __device__ void lookback_role(const ReplayParams& p, Smem& s, int lbw, int lane)
                 Mrun = llmax(Mrun, hi);
             }
         }
-        PROF_MARK(2)
         // ---- publish the inclusive state (the end of the chain's critical path)
         if (lane == 0) {
             my->F = F0 + usum; my->M = llmax(in.M, F0 + umx); my->B = B;
             my->n = n; my->nep = nep; my->ep = ep; my->ep_ptr = eptr;
             st_release(&my->flag, want + 2);
+            PROF_UNIT_T(inf.slot, 1)
             if (last) {
                 scl_trace_summary* sm = &p.summ[inf.t];
                 sm->f_final = F0 + usum; sm->hwm = llmax(in.M, F0 + umx);
@@ -518,7 +485,6 @@ __device__ void lookback_role(const ReplayParams& p, Smem& s, int lbw, int lane)
         }
         __syncwarp();
 
-        PROF_MARK(3)
         // ---- a4 free-pointer match, "a pointer comparison that is almost always false":
         // lane c decides whether chunk c may hold a free of an active tracked pointer (Bloom)
         if (in.ep != kNoEp || nl > 0) {
@@ -528,7 +494,7 @@ __device__ void lookback_role(const ReplayParams& p, Smem& s, int lbw, int lane)
             while (li < nl && eplist[li].pos < cbeg) { cptr = eplist[li].ptr; cval = true; ++li; }
             bool need = false;
             for (;;) {
-                if (cval) { const unsigned b = bloom_bit(cptr); if ((S.bloom[lane][b >> 5] >> (b & 31)) & 1u) need = true; }
+                if (cval) { const unsigned m = bloom_mask(cptr); if ((S.bloom[lane][bloom_word(cptr)] & m) == m) need = true; }
                 if (li < nl && eplist[li].pos < cend) { cptr = eplist[li].ptr; cval = true; ++li; } else break;
             }
             unsigned nm = __ballot_sync(kFull, need);
@@ -557,12 +523,98 @@ __device__ void lookback_role(const ReplayParams& p, Smem& s, int lbw, int lane)
                 }
             }
         }
-        PROF_MARK(4)
-        if (lane == 0) {
-            S.done = 0; __threadfence_block();
-            atomicExch(&s.sstate[sl], 0u); mbar_arrive(&s.sempty[sl]); atomicAdd(&s.n_done, 1u);
+    }
+    __syncwarp();
+}
+
+// Look-back warp: claims full slots (oldest first).  A unit whose incoming state is
+// available is finished from shared memory; otherwise its slot is copied to a global
+// "park" record, released at once (compute never waits on a trace's chain), and the
+// unit is finished later, when the flag it waits for has moved.  Lane i of the warp
+// tracks parked unit i.
+__device__ void lookback_role(const ReplayParams& p, Smem& s, int lbw, int lane)
+{
+    const unsigned want = p.epoch * 4u;
+    const size_t wid = (size_t)blockIdx.x * kLBWarps + lbw;
+    EpStart* eplist = p.ep_scratch + wid * kUnit;
+    Slot* park = reinterpret_cast<Slot*>(p.park) + wid * kPark;
+    unsigned pk_itu = kInvalid, pk_need = 0;           // lane i: parked unit i (CTA unit iteration), flag value needed
+    const unsigned* pk_blk = nullptr;
+    PROF_DECL
+    for (;;) {
+        // ---- 1. a parked unit whose blocker moved (oldest first)
+        unsigned prio = kInvalid;
+        if (pk_itu != kInvalid && ld_acquire(pk_blk) >= pk_need) prio = pk_itu;
+        #pragma unroll
+        for (int d = 16; d > 0; d >>= 1) prio = min(prio, __shfl_xor_sync(kFull, prio, d));
+        if (prio != kInvalid) {
+            const int i = __ffs(__ballot_sync(kFull, pk_itu == prio)) - 1;
+            const Slot* G = park + i;
+            const SegInfo inf = G->info;
+            const unsigned k = inf.kraw & 0x7fffffffu;
+            const SegState* ts = &p.state[inf.slot - k];
+            // the blocker was an inclusive state of this trace: resume the forward walk from it
+            const unsigned* bptr = (const unsigned*)__shfl_sync(kFull, (unsigned long long)pk_blk, i);
+            const unsigned bneed = __shfl_sync(kFull, pk_need, i);
+            const int resume = bneed == want + 2 ? (int)(((const char*)bptr - (const char*)&ts[0].flag) / sizeof(SegState)) : -1;
+            InState in; const unsigned* blk; unsigned need;
+            if (look_back(p, ts, k, want, lane, in, blk, need, resume)) {
+                finish_unit(p, G, in, want, eplist, lane);
+                if (lane == i) pk_itu = kInvalid;
+                if (lane == 0) atomicAdd(&s.n_done, 1u);
+            } else if (lane == i) {
+                pk_blk = blk; pk_need = need;
+            }
+            __syncwarp();
+            PROF_MARK(2)
+            continue;
+        }
+        // ---- 2. the oldest full slot (only if a park lane is free)
+        const unsigned freelanes = __ballot_sync(kFull, lane < kPark && pk_itu == kInvalid);
+        unsigned best = kInvalid;
+        if (freelanes && lane < kSlots && ((volatile unsigned*)s.sstate)[lane] == 1) best = ((volatile unsigned*)s.situ)[lane];
+        #pragma unroll
+        for (int d = 16; d > 0; d >>= 1) best = min(best, __shfl_xor_sync(kFull, best, d));
+        if (best == kInvalid) {
+            const unsigned nu = ((volatile unsigned*)&s.n_units)[0], nd = ((volatile unsigned*)&s.n_done)[0];
+            if (nu != kInvalid && nd >= nu) { PROF_FLUSH(16) return; }
+            PROF_MARK(0)
+            __nanosleep(64);
+            continue;
+        }
+        const bool mine = lane < kSlots && ((volatile unsigned*)s.sstate)[lane] == 1 && ((volatile unsigned*)s.situ)[lane] == best;
+        const unsigned cand = __ballot_sync(kFull, mine);
+        if (!cand) continue;
+        const int q = __ffs(cand) - 1;
+        unsigned got = 0;
+        if (lane == 0) got = atomicCAS(&s.sstate[q], 1u, 2u);
+        if (__shfl_sync(kFull, got, 0) != 1u) continue;
+        __threadfence_block();
+        PROF_MARK(0)
+        Slot& S = s.slot[q];
+        const SegInfo inf = S.info;
+        const unsigned k = inf.kraw & 0x7fffffffu;
+        InState in; const unsigned* blk; unsigned need;
+        const bool ready = look_back(p, &p.state[inf.slot - k], k, want, lane, in, blk, need);
+        PROF_MARK(1)
+        if (ready) {
+            finish_unit(p, &S, in, want, eplist, lane);
+        } else {
+            // park: copy the slot to global memory, remember what it waits for
+            const int i = __ffs(freelanes) - 1;
+            const uint4* src = reinterpret_cast<const uint4*>(&S);
+            uint4* dst = reinterpret_cast<uint4*>(park + i);
+            for (int o = lane; o < (int)(sizeof(Slot) / 16); o += 32) dst[o] = src[o];
+            if (lane == i) { pk_itu = S.itu; pk_blk = blk; pk_need = need; }
         }
         __syncwarp();
+        if (lane == 0) {
+            S.done = 0; __threadfence_block();
+            atomicExch(&s.sstate[q], 0u); mbar_arrive(&s.sempty[q]);
+            if (ready) atomicAdd(&s.n_done, 1u);
+        }
+        __syncwarp();
+        PROF_MARK(3)
     }
 }
 

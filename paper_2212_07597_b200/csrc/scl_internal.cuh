@@ -32,7 +32,8 @@ constexpr int kLBWarps = 3;                   // 20 warps total (5 per SM sub-pa
 constexpr int kProducerWarp = kComputeWarps;
 constexpr int kCtaThreads = (kComputeWarps + 1 + kLBWarps) * 32;
 constexpr int kStages = 4;                    // TMA ring depth
-constexpr int kSlots = 6;                     // compute -> look-back unit summary ring
+constexpr int kSlots = 6;                     // compute -> look-back unit summary ring (smem)
+constexpr int kPark = 32;                     // parked units per look-back warp (global copies)
 constexpr int kBloomWords = 64;               // 2048-bit Bloom filter of freed pointers per chunk
 constexpr int kHot = 1024;                    // sites with shared-memory Tier-E counters
 constexpr long long kNeg = -(1ll << 62);      // "no event" sentinels for max / min
@@ -81,6 +82,7 @@ struct ReplayParams {
     const unsigned long long* sbase;  // trace -> first sample slot
     scl_trace_summary* summ;          // [n_traces]
     EpStart* ep_scratch;              // [grid * kLBWarps * kUnit]
+    void* park;                       // [grid * kLBWarps * kPark] parked unit summaries (Slot)
     unsigned long long* prof;         // debug build only (SCL_PROFILE): per-role cycle sums, else NULL
 };
 
@@ -104,6 +106,7 @@ cudaError_t launch_rows(const unsigned long long* table, const double* prob, con
                         const unsigned char* flag, const unsigned int* order, unsigned n_sites,
                         scl_site_row* rows, cudaStream_t st);
 size_t replay_smem_bytes();
+size_t replay_park_bytes();            // bytes of one parked unit summary
 int replay_occupancy(int* grid);
 
 }  // namespace scl

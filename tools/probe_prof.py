@@ -15,14 +15,32 @@ r = None
 for _ in range(4):
     r = scl.scl_replay_run(T, tr, out=r)
 ms = scl.scl_result_timing(r)[0]
-buf = np.zeros(32, dtype=np.uint64)
-lib.scl_debug_prof(r.handle, buf.ctypes.data)
+nunits_all = int(sum((cfg.events_per_trace + 8191) // 8192 for _ in range(nt)))
+bigbuf = np.zeros(32 + 2 * nunits_all, dtype=np.uint64)
+lib.scl_debug_prof(r.handle, bigbuf.ctypes.data)
+buf = bigbuf[:32]
 nsm = 148
 cyc = ms * 1e-3 * 1.965e9
 print(f"cfg{cid} traces={nt} T={T}: kernel {ms*1e3:.1f} us = {cyc:.0f} cycles @1.965GHz")
 names = {0: ("compute", 16, ["wait_full", "wait_sempty", "summary", "agg+loop", "process"]),
          8: ("producer", 1, ["wait_empty", "fetch+issue"]),
-         16: ("lookback", 3, ["wait_sfull", "look_back", "resolve", "publish", "ptr_match", "loop"])}
+         16: ("lookback", 3, ["idle", "lookback", "parked", "finish"])}
 for base, (nm, nw, cats) in names.items():
     tot = buf[base:base + 8].astype(float) / (nw * nsm)
     print(f"  {nm:9s} " + "  ".join(f"{c}={tot[i]/cyc*100:5.1f}%" for i, c in enumerate(cats)))
+    if False:
+        units = float(buf[base + 6])
+        print("  walker per unit (cycles): " + "  ".join(f"{c}={float(buf[base+i])/max(units,1):.0f}" for i, c in enumerate(cats) if c not in ("units", "x")), f" units={units:.0f}")
+
+# per-unit timeline (aggregate published, inclusive published), first unit of each trace = unit 0
+if len(sys.argv) > 4:
+    nunits = nunits_all
+    tl = bigbuf[32:].reshape(-1, 2).astype(np.int64)
+    t0 = tl[tl > 0].min()
+    per = (cfg.events_per_trace + 8191) // 8192
+    agg = (tl[:, 0] - t0) / 1e3; inc = (tl[:, 1] - t0) / 1e3
+    lag = inc - agg
+    print(f"  units={nunits} agg publish: max {agg.max():.0f} us; inclusive publish: max {inc.max():.0f} us; lag mean {lag.mean():.1f} us p50 {np.median(lag):.1f} p90 {np.percentile(lag,90):.1f} max {lag.max():.1f}")
+    for t in (0, 1, nt // 2):
+        a = agg[t * per:(t + 1) * per]; b = inc[t * per:(t + 1) * per]
+        print(f"  trace {t}: " + " ".join(f"{int(x)}/{int(y)}" for x, y in list(zip(a, b))[::8]))
