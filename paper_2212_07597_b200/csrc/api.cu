@@ -36,7 +36,12 @@ struct scl_traces {
     std::vector<uint64_t> h_off, h_sabs;
     uint32_t n_segs = 0;
     TicketInfo* d_tk = nullptr;
-    SegState* d_state = nullptr;
+    void* d_urec = nullptr;                    // per unit: published summary record
+    unsigned int* d_uready = nullptr;          // per unit: run epoch when published
+    unsigned int* d_tr_nseg = nullptr;         // per trace: number of units
+    unsigned int* d_tr_base = nullptr;         // per trace: first unit id
+    RunState* d_run = nullptr;                 // per trace: runner state (zeroed per run)
+    UnitEntry* d_uent = nullptr;               // per unit: state entering it (runner -> reclaim pass)
     unsigned int* d_ticket = nullptr;
     mutable unsigned int epoch = 0;
     CUtensorMap tmap;
@@ -53,8 +58,7 @@ struct scl_result {
     scl_sample* d_samples = nullptr; unsigned int* d_epflag = nullptr; size_t cap = 0;
     unsigned long long* d_sbase = nullptr;
     scl_trace_summary* d_summ = nullptr;
-    EpStart* d_scratch = nullptr; int grid = 0;
-    void* d_park = nullptr;
+    int grid = 0;
     double* d_prob = nullptr; double* d_rate = nullptr; unsigned char* d_flag = nullptr;
     unsigned long long *d_key = nullptr, *d_key2 = nullptr; unsigned int *d_val = nullptr, *d_order = nullptr;
     void* d_cub = nullptr; size_t cub_bytes = 0;
@@ -235,10 +239,26 @@ extern "C" scl_status scl_trace_load(const char* path, const scl_event* events, 
     tr->n_segs = total;
     const size_t nn = std::max<size_t>(total, 1);
     if (cudaMalloc(&tr->d_tk, nn * sizeof(TicketInfo)) != cudaSuccess ||
-        cudaMalloc(&tr->d_state, nn * sizeof(SegState)) != cudaSuccess || cudaMalloc(&tr->d_ticket, 4) != cudaSuccess)
+        cudaMalloc(&tr->d_urec, nn * replay_urec_bytes()) != cudaSuccess || cudaMalloc(&tr->d_uready, nn * 4) != cudaSuccess ||
+        cudaMalloc(&tr->d_tr_nseg, std::max<size_t>(n_traces, 1) * 4) != cudaSuccess ||
+        cudaMalloc(&tr->d_tr_base, std::max<size_t>(n_traces, 1) * 4) != cudaSuccess ||
+        cudaMalloc(&tr->d_run, std::max<size_t>(n_traces, 1) * sizeof(RunState)) != cudaSuccess ||
+        cudaMalloc(&tr->d_uent, nn * sizeof(UnitEntry)) != cudaSuccess ||
+        cudaMalloc(&tr->d_ticket, 4) != cudaSuccess)
         { cudaGetLastError(); return cleanup(fail(SCL_ENOMEM, "segment plan")); }
     if (total) cudaMemcpy(tr->d_tk, tk.data(), total * sizeof(TicketInfo), cudaMemcpyHostToDevice);
-    cudaMemset(tr->d_state, 0, nn * sizeof(SegState));
+    cudaMemset(tr->d_uready, 0, nn * 4);
+    {   // every trace needs a runner lane: n_traces <= grid * kRunners * 32
+        int grid = 0;
+        replay_occupancy(&grid);
+        if ((uint64_t)n_traces > (uint64_t)grid * kRunners * 32)
+            return cleanup(fail(SCL_EOVERFLOW, "too many traces for one launch (max " +
+                                std::to_string((uint64_t)grid * kRunners * 32) + "): load them in waves"));
+    }
+    if (n_traces) {
+        cudaMemcpy(tr->d_tr_nseg, nseg.data(), n_traces * 4, cudaMemcpyHostToDevice);
+        cudaMemcpy(tr->d_tr_base, seg_base.data(), n_traces * 4, cudaMemcpyHostToDevice);
+    }
 
     // TMA descriptor: rows of 32 x u32 (128 B), box 32 x 256 rows, 128-B swizzle
     auto enc = get_encode();
@@ -258,7 +278,8 @@ extern "C" scl_status scl_trace_load(const char* path, const scl_event* events, 
 
 extern "C" void scl_traces_free(scl_traces* t) {
     if (!t) return;
-    cudaFree(t->d_ev); cudaFree(t->d_off); cudaFree(t->d_tk); cudaFree(t->d_state); cudaFree(t->d_ticket);
+    cudaFree(t->d_ev); cudaFree(t->d_off); cudaFree(t->d_tk); cudaFree(t->d_urec); cudaFree(t->d_uready);
+    cudaFree(t->d_tr_nseg); cudaFree(t->d_tr_base); cudaFree(t->d_run); cudaFree(t->d_uent); cudaFree(t->d_ticket);
     delete t;
 }
 
@@ -274,7 +295,7 @@ extern "C" scl_status scl_traces_info(const scl_traces* t, uint64_t* n_events, u
 extern "C" void scl_result_free(scl_result* r) {
     if (!r) return;
     cudaFree(r->d_table); cudaFree(r->d_samples); cudaFree(r->d_epflag); cudaFree(r->d_sbase);
-    cudaFree(r->d_summ); cudaFree(r->d_scratch); cudaFree(r->d_park); cudaFree(r->d_prob); cudaFree(r->d_rate); cudaFree(r->d_flag);
+    cudaFree(r->d_summ); cudaFree(r->d_prob); cudaFree(r->d_rate); cudaFree(r->d_flag);
     cudaFree(r->d_prof); cudaFree(r->d_key); cudaFree(r->d_key2); cudaFree(r->d_val); cudaFree(r->d_order); cudaFree(r->d_cub); cudaFree(r->d_rows);
     for (auto& e : r->ev) if (e) cudaEventDestroy(e);
     delete r;
@@ -288,8 +309,6 @@ static scl_status alloc_result(scl_result* r, const scl_traces* tr) {
     CU(cudaMalloc(&r->d_table, (S * SCL_NCOL + 3) * 8));
     CU(cudaMalloc(&r->d_sbase, nt * 8));
     CU(cudaMalloc(&r->d_summ, nt * sizeof(scl_trace_summary)));
-    CU(cudaMalloc(&r->d_scratch, (size_t)grid * kLBWarps * kUnit * sizeof(EpStart)));
-    CU(cudaMalloc(&r->d_park, (size_t)grid * kLBWarps * kPark * replay_park_bytes()));
     CU(cudaMalloc(&r->d_prob, S * 8)); CU(cudaMalloc(&r->d_rate, S * 8)); CU(cudaMalloc(&r->d_flag, S));
     CU(cudaMalloc(&r->d_key, S * 8)); CU(cudaMalloc(&r->d_key2, S * 8));
     CU(cudaMalloc(&r->d_val, S * 4)); CU(cudaMalloc(&r->d_order, S * 4));
@@ -347,7 +366,7 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
     }
 
     // epoch-tagged look-back flags: no per-run clear of the state array
-    if (tr->epoch >= (1u << 29)) { CU(cudaMemsetAsync(tr->d_state, 0, (size_t)std::max<uint32_t>(tr->n_segs, 1) * sizeof(SegState), st)); tr->epoch = 0; }
+    if (tr->epoch >= (1u << 30)) { CU(cudaMemsetAsync(tr->d_uready, 0, (size_t)std::max<uint32_t>(tr->n_segs, 1) * 4, st)); tr->epoch = 0; }
     tr->epoch += 1;
 
     CU(cudaEventRecord(r->ev[0], st));
@@ -355,21 +374,24 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
     CU(cudaMemsetAsync(r->d_table, 0, ((size_t)tr->n_sites * SCL_NCOL + 3) * 8, st));
     CU(cudaMemsetAsync(r->d_summ, 0, (size_t)std::max<uint32_t>(NT, 1) * sizeof(scl_trace_summary), st));
     CU(cudaMemsetAsync(tr->d_ticket, 0, 4, st));
+    CU(cudaMemsetAsync(tr->d_run, 0, (size_t)std::max<uint32_t>(NT, 1) * sizeof(RunState), st));
 
     ReplayParams p{};
     p.ev = tr->d_ev; p.off = tr->d_off; p.tk = tr->d_tk;
-    p.state = tr->d_state; p.ticket = tr->d_ticket; p.n_segs = tr->n_segs; p.epoch = tr->epoch;
+    p.urec = tr->d_urec; p.uready = tr->d_uready; p.run = tr->d_run; p.tr_nseg = tr->d_tr_nseg; p.tr_base = tr->d_tr_base;
+    p.ticket = tr->d_ticket; p.n_segs = tr->n_segs; p.epoch = tr->epoch;
     p.n_sites = tr->n_sites; p.n_traces = NT; p.T = (long long)threshold;
     p.table = r->d_table; p.samples = r->d_samples; p.ep_flag = r->d_epflag; p.sbase = r->d_sbase;
-    p.summ = r->d_summ; p.ep_scratch = r->d_scratch; p.park = r->d_park;
+    p.summ = r->d_summ; p.uent = tr->d_uent;
 #ifdef SCL_PROFILE
-    if (!r->d_prof) CU(cudaMalloc(&r->d_prof, (32 + 2 * (size_t)tr->n_segs) * 8));
-    CU(cudaMemsetAsync(r->d_prof, 0, (32 + 2 * (size_t)tr->n_segs) * 8, st));
+    if (!r->d_prof) CU(cudaMalloc(&r->d_prof, (48 + 4 * (size_t)tr->n_segs) * 8));
+    CU(cudaMemsetAsync(r->d_prof, 0, (48 + 4 * (size_t)tr->n_segs) * 8, st));
     p.prof = r->d_prof;
 #endif
     CU(cudaEventRecord(r->ev[4], st));
     CU(launch_replay(&tr->tmap, p, r->grid, st));
     CU(cudaEventRecord(r->ev[5], st));
+    CU(launch_reclaim(p, st));
     CU(launch_samples(p, st));
     CU(cudaEventRecord(r->ev[1], st));
     *out = r;
@@ -489,7 +511,7 @@ extern "C" scl_status scl_result_timing(const scl_result* r, float* replay_kerne
 // Debug build only: per-role cycle sums of the last run (compute 0..7, producer 8..15, look-back 16..23).
 extern "C" scl_status scl_debug_prof(const scl_result* r, unsigned long long* out) {
     if (!r || !r->d_prof) return fail(SCL_EINVAL, "no profile");
-    CU(cudaMemcpy(out, r->d_prof, (32 + 2 * (size_t)r->tr->n_segs) * 8, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(out, r->d_prof, (48 + 4 * (size_t)r->tr->n_segs) * 8, cudaMemcpyDeviceToHost));
     return SCL_OK;
 }
 #endif

@@ -43,6 +43,7 @@ struct __align__(16) Slot {          // compute -> look-back summary of one unit
     unsigned done, itu;                                    // chunks finished; CTA unit iteration
     unsigned bloom[kChunks][kBloomWords];
 };
+
 struct __align__(16) Smem {
     unsigned cnt[2 * kHot];          // Tier-E per (kind, hot site): event count
     unsigned blo[2 * kHot];          //   bytes, low 32 bits
@@ -57,7 +58,7 @@ struct __align__(16) Smem {
     unsigned n_done;                 // units finished by the look-back warps
 };
 
-size_t replay_park_bytes() { return sizeof(Slot); }
+size_t replay_urec_bytes() { return sizeof(Slot); }
 size_t replay_smem_bytes() { return 1024 + (size_t)kStages * kSegBytes + sizeof(Smem); }
 
 // Blocked Bloom filter of freed pointers, 64 words (2048 bits) per 256-event chunk: one
@@ -76,12 +77,14 @@ __device__ __forceinline__ unsigned bloom_mask(unsigned long long ptr) {
 #define PROF_DECL unsigned long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long pt = clock64();
 #define PROF_MARK(i) { const long long now_ = clock64(); pacc[i] += now_ - pt; pt = now_; }
 #define PROF_FLUSH(base) if (lane == 0 && p.prof) { for (int q_ = 0; q_ < 8; ++q_) atomicAdd(&p.prof[(base) + q_], pacc[q_]); }
-#define PROF_UNIT_T(u, which) if (p.prof) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); p.prof[32 + 2 * (size_t)(u) + (which)] = t_; }
+#define RPROF_ADD(i, v) if (p.prof && lane == 0) atomicAdd(&p.prof[24 + (i)], (unsigned long long)(v));
+#define PROF_UNIT_T(u, which) if (p.prof) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); p.prof[48 + 4 * (size_t)(u) + (which)] = t_; }
 #else
 #define PROF_DECL
 #define PROF_MARK(i)
 #define PROF_FLUSH(base)
 #define PROF_UNIT_T(u, which)
+#define RPROF_ADD(i, v)
 #endif
 
 // The 8 events of one global row, through L2 (re-read path).
@@ -97,7 +100,6 @@ __device__ __forceinline__ void load_row_global(const scl_event* ev, long long r
 // warp w8 of a group takes rows 32*w8 .. 32*w8+31 of its box = chunk g*8 + w8 of the unit.
 __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stage, int grp, int w8, int lane)
 {
-    const unsigned want = p.epoch * 4u;
     const uint32_t cnt_s = smem_u32(s.cnt), blo_s = smem_u32(s.blo), bhi_s = smem_u32(s.bhi);
     PROF_DECL
     for (unsigned it = grp;; it += 2) {
@@ -243,13 +245,7 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
             const long long Pc = ci - cs, ax = Pc + cx, an = Pc + cn;
             S.Pc[lane] = Pc; S.ax[lane] = ax; S.an[lane] = an;
             const long long usum = shfl_ll(ci, 31), umx = warp_max(ax), umn = warp_min(an);
-            if (lane == 0) {
-                S.usum = usum; S.umx = umx; S.umn = umn;
-                SegState* my = &p.state[S.info.slot];
-                my->sum = usum; my->mx = umx; my->mn = umn;
-                st_release(&my->flag, want + 1);
-                PROF_UNIT_T(S.info.slot, 0)
-            }
+            if (lane == 0) { S.usum = usum; S.umx = umx; S.umn = umn; PROF_UNIT_T(S.info.slot, 0) }
             __syncwarp();
             if (lane == 0) { S.itu = itu; ((volatile unsigned*)s.situ)[sl] = itu; __threadfence_block(); atomicExch(&s.sstate[sl], 1u); }
         }
@@ -300,322 +296,276 @@ __device__ void producer_role(const ReplayParams& p, const CUtensorMap* tmap, Sm
     }
 }
 
-// ============================================================================ look-back warps
-struct InState { long long F, M, B; unsigned long long n, nep, ep, eptr; };
+// ============================================================================ runner warps
+// Each trace has one RUNNER lane (static assignment) that advances it strictly in order over
+// every published unit, with the exact sequential state in registers.  Units without a sample
+// are composed 32 at a time from their aggregates (sampler band test, HWM); only units in
+// which a sample fires are resolved chunk by chunk.  The runner does no pointer matching: it
+// records the state entering each unit (UnitEntry) and the reclaim pass settles every episode
+// afterwards, all units in parallel -- the chain carries only what the sampler needs.
+struct RState { long long F, M, B; unsigned long long n, nep, ep1; unsigned next; };
 
-// The 7 inclusive words of a SegState (F, M, B, n, nep, ep, ep_ptr are consecutive):
-// lanes 0..6 load one word each, then broadcast.
-__device__ __forceinline__ InState load_inclusive_warp(const SegState* q, int lane) {
-    const unsigned long long* w = reinterpret_cast<const unsigned long long*>(&q->F);
-    unsigned long long v = lane < 7 ? __ldcg(w + lane) : 0ull;
-    InState x;
+__device__ __forceinline__ RState load_rstate(const RunState* rs, int lane) {
+    const unsigned long long* w = reinterpret_cast<const unsigned long long*>(rs);
+    unsigned long long v = lane < 7 ? __ldcg(w + lane) : 0ull;      // F M B n nep ep1 {next,pad}
+    RState x;
     x.F = (long long)__shfl_sync(kFull, v, 0); x.M = (long long)__shfl_sync(kFull, v, 1);
     x.B = (long long)__shfl_sync(kFull, v, 2); x.n = __shfl_sync(kFull, v, 3);
-    x.nep = __shfl_sync(kFull, v, 4); x.ep = __shfl_sync(kFull, v, 5); x.eptr = __shfl_sync(kFull, v, 6);
+    x.nep = __shfl_sync(kFull, v, 4); x.ep1 = __shfl_sync(kFull, v, 5);
+    x.next = (unsigned)__shfl_sync(kFull, v, 6);
     return x;
 }
-
-// State before unit k of a trace (a1-a4 carries), NON-BLOCKING: returns false (with the
-// flag it waits for) if a state it needs is not published yet.  Backward: windows of 32
-// units (lane i <-> unit j-i) until the nearest inclusive state (the "base"; or the trace
-// start), checking that every unit after it has its aggregate.  Forward: from the base,
-// units are composed 32 at a time (lane i <-> unit start+i) while the sampler provably
-// does not fire (every prefix of the carry stays in (-T, T)); at the first unit where it
-// could fire, that unit's inclusive state is needed and becomes the new base.
-__device__ bool look_back(const ReplayParams& p, const SegState* ts, unsigned k, unsigned want, int lane, InState& b,
-                          const unsigned*& blk, unsigned& need, int resume = -1)
-{
-    b = InState{0, 0, 0, 0, 0, kNoEp, 0};
-    blk = nullptr; need = 0;
-    if (k == 0) return true;
-    int base = resume;                                     // unit holding the base state (-1: trace start)
-    // resume: a parked unit re-tried because the inclusive state it waited for (unit `resume`)
-    // is published -- start the forward walk there (aggregates after it were checked before)
-    if (resume < 0) for (int j = (int)k - 1;; j -= 32) {
-        const int idx = j - lane;
-        const unsigned fl = idx >= 0 ? ld_acquire(&ts[idx].flag) : 0u;
-        const unsigned im = __ballot_sync(kFull, idx >= 0 && fl >= want + 2);
-        const int stop = im ? __ffs(im) - 1 : 32;
-        const unsigned lowmask = stop >= 32 ? kFull : ((1u << stop) - 1u);
-        const unsigned miss = __ballot_sync(kFull, idx >= 0 && fl < want + 1) & lowmask;
-        if (miss) { blk = &ts[j - (__ffs(miss) - 1)].flag; need = want + 1; return false; }   // an aggregate is missing
-        if (im) { base = j - stop; break; }
-        if (j - 31 <= 0) break;                            // reached unit 0: base = trace start
-    }
-    if (base >= 0) b = load_inclusive_warp(&ts[base], lane);
-    for (int start = base + 1; start < (int)k;) {
-        const int idx = start + lane;
-        const bool in = idx < (int)k;
-        long long a_s = 0, a_x = kNeg, a_n = kPos;
-        if (in) { const SegState* q = &ts[idx]; a_s = __ldcg(&q->sum); a_x = __ldcg(&q->mx); a_n = __ldcg(&q->mn); }
-        long long inc = a_s;
-        #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) { long long o = shfl_up_ll(inc, d); if (lane >= d) inc += o; }
-        const long long E = inc - a_s;                     // sum of the earlier units of the window
-        const long long c = b.F - b.B + E;
-        const unsigned bm = __ballot_sync(kFull, in && (c + a_x >= p.T || c + a_n <= -p.T));
-        if (!bm) {
-            const long long mx = warp_max(in ? E + a_x : kNeg);
-            b.M = llmax(b.M, b.F + mx);
-            b.F += shfl_ll(inc, 31);
-            start += 32;
-            continue;
-        }
-        const int jf = __ffs(bm) - 1;                      // earliest unit where a sample may fire
-        const SegState* q = &ts[start + jf];
-        unsigned f = lane == 0 ? ld_acquire(&q->flag) : 0u;
-        if (__shfl_sync(kFull, f, 0) < want + 2) { blk = &q->flag; need = want + 2; return false; }
-        b = load_inclusive_warp(q, lane);
-        start += jf + 1;
-    }
-    return true;
+__device__ __forceinline__ void store_rstate(RunState* rs, const RState& x, int lane) {
+    if (lane == 0) { rs->F = x.F; rs->M = x.M; rs->B = x.B; rs->n = x.n; rs->nep = x.nep; rs->ep1 = x.ep1; rs->next = x.next; }
 }
 
-// Finish unit S (smem slot or its parked global copy) once its incoming state is known:
-// samples, inclusive state, free-pointer match.
-__device__ void finish_unit(const ReplayParams& p, const Slot* Sp, const InState& in, unsigned want,
-                            EpStart* eplist, int lane)
-{
-    const Slot& S = *Sp;
-    const SegInfo inf = S.info;
-    const bool last = (inf.kraw >> 31) != 0;
-    SegState* my = &p.state[inf.slot];
-    const long long usum = S.usum, umx = S.umx, umn = S.umn;
-    {
-        // ---- a3/a4: samples of this unit (band test per chunk; exact re-scan only where needed)
-        long long B = in.B;
-        unsigned long long n = in.n, nep = in.nep, ep = in.ep, eptr = in.eptr;
-        unsigned nl = 0;
-        const long long F0 = in.F;
-        if (F0 - B + umx >= p.T || F0 - B + umn <= -p.T) {
-            const unsigned long long sb = __ldg(p.sbase + inf.t);
-            const long long myax = S.ax[lane], myan = S.an[lane], myPc = S.Pc[lane];
-            long long Mrun = in.M;                             // max F over events before the chunk
-            for (int c = 0; c < kChunks; ++c) {
-                const long long Pw = shfl_ll(myPc, c), hi = F0 + shfl_ll(myax, c), lo = F0 + shfl_ll(myan, c);
-                if (!(hi >= B + p.T || lo <= B - p.T)) { Mrun = llmax(Mrun, hi); continue; }
-                // re-read the chunk: lane l <-> row 32c+l of the unit (8 events)
-                const long long row = inf.row_base + (long long)c * 32 + lane;
-                unsigned long long rp[kEpt], rm[kEpt];
-                load_row_global(p.ev, row, rp, rm);
-                const long long e0 = row * kEpt - inf.off_t;
-                long long d[kEpt], run = 0, lmx = kNeg, lmn = kPos;
-                #pragma unroll
-                for (int jj = 0; jj < kEpt; ++jj) {
-                    const long long ie = e0 + jj;
-                    const unsigned kind = ev_kind(rm[jj]);
-                    const bool af = ie >= 0 && ie < inf.n_t && kind < 2;
-                    const long long sz = (long long)ev_size(rm[jj]);
-                    d[jj] = af ? (kind == 0 ? sz : -sz) : 0;
-                    run += d[jj];
-                    if (af) { lmx = llmax(lmx, run); lmn = llmin(lmn, run); }
-                }
-                long long li = run;
-                #pragma unroll
-                for (int dd = 1; dd < 32; dd <<= 1) { long long o = shfl_up_ll(li, dd); if (lane >= dd) li += o; }
-                const long long Fl = F0 + Pw + (li - run);          // F before this lane's first event
-                long long pmx = Fl + lmx;                             // max F over lanes <= lane
-                #pragma unroll
-                for (int dd = 1; dd < 32; dd <<= 1) { long long o = shfl_up_ll(pmx, dd); if (lane >= dd) pmx = llmax(pmx, o); }
-                long long PMl = shfl_up_ll(pmx, 1);
-                if (lane == 0) PMl = kNeg;
-                int cur = 0;
-                for (;;) {
-                    const bool cand = lane >= cur && (Fl + lmx >= B + p.T || Fl + lmn <= B - p.T);
-                    const unsigned cm = __ballot_sync(kFull, cand);
-                    if (!cm) break;
-                    const int l0 = __ffs(cm) - 1;
-                    // lanes 0..7 take the 8 events of lane l0
-                    long long de = 0; unsigned long long pe = 0, me = 0;
-                    #pragma unroll
-                    for (int jj = 0; jj < kEpt; ++jj) {
-                        const long long v = shfl_ll(d[jj], l0);
-                        const unsigned long long pv = __shfl_sync(kFull, rp[jj], l0), mv = __shfl_sync(kFull, rm[jj], l0);
-                        if (lane == jj) { de = v; pe = pv; me = mv; }
-                    }
-                    const long long iev = shfl_ll(e0, l0) + lane;
-                    const bool af = lane < kEpt && iev >= 0 && iev < inf.n_t && ev_kind(me) < 2;
-                    long long L = de;
-                    #pragma unroll
-                    for (int dd = 1; dd < kEpt; dd <<= 1) { long long o = shfl_up_ll(L, dd); if (lane >= dd) L += o; }
-                    const long long Fe = shfl_ll(Fl, l0) + L;
-                    const long long Mbase = llmax(Mrun, shfl_ll(PMl, l0));
-                    int ef = 0;
-                    for (;;) {                                      // successive first exits of (B-T, B+T)
-                        const bool ex = af && lane >= ef && (Fe >= B + p.T || Fe <= B - p.T);
-                        const unsigned em = __ballot_sync(kFull, ex);
-                        if (!em) break;
-                        const int e = __ffs(em) - 1;
-                        const long long Fs = shfl_ll(Fe, e);
-                        const long long Mprev = llmax(Mbase, warp_max((af && lane < e) ? Fe : kNeg));   // M_{i-1}
-                        const long long net = Fs - B;              // the |A - F| counter
-                        const bool growth = net > 0;
-                        const bool nm = growth && Fs > Mprev;      // new high-water mark (Q3, Q4)
-                        const unsigned long long slot_s = sb + n;
-                        if (lane == e) {
-                            scl_sample smp;
-                            smp.idx = (unsigned long long)iev; smp.net = net; smp.footprint = Fs;
-                            smp.site = ev_site(me); smp.kind = growth ? 0 : 1; smp.new_max = nm ? 1 : 0; smp.pad = 0;
-                            p.samples[slot_s] = smp;
-                            if (nm) {
-                                p.ep_flag[slot_s] = 0u;
-                                EpStart es; es.ep = slot_s; es.ptr = pe; es.pos = (unsigned)((c * 32 + l0) * kEpt + e); es.pad = 0;
-                                eplist[nl] = es;
-                            }
-                        }
-                        if (nm) { ep = slot_s; eptr = __shfl_sync(kFull, pe, e); ++nep; ++nl; }
-                        ++n; B = Fs; ef = e + 1;                   // "resets the counters"
-                    }
-                    cur = l0 + 1;
-                }
-                Mrun = llmax(Mrun, hi);
-            }
-        }
-        // ---- publish the inclusive state (the end of the chain's critical path)
-        if (lane == 0) {
-            my->F = F0 + usum; my->M = llmax(in.M, F0 + umx); my->B = B;
-            my->n = n; my->nep = nep; my->ep = ep; my->ep_ptr = eptr;
-            st_release(&my->flag, want + 2);
-            PROF_UNIT_T(inf.slot, 1)
-            if (last) {
-                scl_trace_summary* sm = &p.summ[inf.t];
-                sm->f_final = F0 + usum; sm->hwm = llmax(in.M, F0 + umx);
-                sm->n_samples = n; sm->n_episodes = nep;
-            }
-        }
-        __syncwarp();
-
-        // ---- a4 free-pointer match, "a pointer comparison that is almost always false":
-        // lane c decides whether chunk c may hold a free of an active tracked pointer (Bloom)
-        if (in.ep != kNoEp || nl > 0) {
-            const unsigned cbeg = (unsigned)lane * 32 * kEpt, cend = cbeg + 32 * kEpt;
-            unsigned li = 0;
-            unsigned long long cptr = in.eptr; bool cval = in.ep != kNoEp;
-            while (li < nl && eplist[li].pos < cbeg) { cptr = eplist[li].ptr; cval = true; ++li; }
-            bool need = false;
-            for (;;) {
-                if (cval) { const unsigned m = bloom_mask(cptr); if ((S.bloom[lane][bloom_word(cptr)] & m) == m) need = true; }
-                if (li < nl && eplist[li].pos < cend) { cptr = eplist[li].ptr; cval = true; ++li; } else break;
-            }
-            unsigned nm = __ballot_sync(kFull, need);
-            if (nm && in.ep != kNoEp && nl == 0) {
-                // the incoming episode may already be known reclaimed: nothing left to learn
-                unsigned f0 = lane == 0 ? __ldcg(&p.ep_flag[in.ep]) : 0u;
-                if (__shfl_sync(kFull, f0, 0)) nm = 0;
-            }
-            while (nm) {
-                const int c = __ffs(nm) - 1;
-                nm &= nm - 1;
-                const long long row = inf.row_base + (long long)c * 32 + lane;
-                unsigned long long rp[kEpt], rm[kEpt];
-                load_row_global(p.ev, row, rp, rm);
-                const long long e0 = row * kEpt - inf.off_t;
-                const unsigned pos0 = (unsigned)(c * 32 + lane) * kEpt;
-                unsigned lk = 0;
-                unsigned long long aep = in.ep, aptr = in.eptr;
-                while (lk < nl && eplist[lk].pos < pos0) { aep = eplist[lk].ep; aptr = eplist[lk].ptr; ++lk; }
-                #pragma unroll
-                for (int jj = 0; jj < kEpt; ++jj) {
-                    while (lk < nl && eplist[lk].pos <= pos0 + jj) { aep = eplist[lk].ep; aptr = eplist[lk].ptr; ++lk; }
-                    const long long ie = e0 + jj;
-                    if (aep != kNoEp && ie >= 0 && ie < inf.n_t && ev_kind(rm[jj]) == 1 && rp[jj] == aptr)
-                        atomicOr(&p.ep_flag[aep], 1u);
-                }
-            }
-        }
+// Exact check of chunk c of a unit: is there a free of `ptr` at unit positions [sbeg, send)?
+__device__ __forceinline__ bool chunk_has_free(const ReplayParams& p, const SegInfo& inf, int c, unsigned long long ptr,
+                                               unsigned sbeg, unsigned send, int lane) {
+    const long long row = inf.row_base + (long long)c * 32 + lane;
+    unsigned long long rp[kEpt], rm[kEpt];
+    load_row_global(p.ev, row, rp, rm);
+    const long long e0 = row * kEpt - inf.off_t;
+    const unsigned pos0 = (unsigned)(c * 32 + lane) * kEpt;
+    bool hit = false;
+    #pragma unroll
+    for (int jj = 0; jj < kEpt; ++jj) {
+        const long long ie = e0 + jj;
+        const unsigned pos = pos0 + jj;
+        hit |= pos >= sbeg && pos < send && ie >= 0 && ie < inf.n_t && ev_kind(rm[jj]) == 1 && rp[jj] == ptr;
     }
+    return __any_sync(kFull, hit);
+}
+
+// A unit in which a sample fires: resolve it chunk by chunk (a3).  x: state before the unit
+// -> state after it.
+__device__ void resolve_unit(const ReplayParams& p, const Slot& S, RState& x, int lane)
+{
+    // every load of the unit record is issued up front (one round trip)
+    const SegInfo inf = S.info;
+    const long long F0 = x.F, M0 = x.M;
+    long long B = x.B;
+    const long long sPc = S.Pc[lane], sax = S.ax[lane], san = S.an[lane], susum = S.usum, sumx = S.umx;
+    unsigned long long n = x.n, nep = x.nep, ep1 = x.ep1;
+    const unsigned long long sb = __ldg(p.sbase + inf.t);
+    const long long myPc = sPc, hiL = F0 + sax, loL = F0 + san;
+    int cnext = 0;                                     // chunks < cnext are resolved for the current B
+    for (;;) {
+        // next chunk whose F range leaves (B-T, B+T): only those can hold a sample
+        const unsigned ccm = __ballot_sync(kFull, lane >= cnext && (hiL >= B + p.T || loL <= B - p.T));
+        if (!ccm) break;
+        const int c = __ffs(ccm) - 1;
+        RPROF_ADD(11, 1)
+        const long long Pw = shfl_ll(myPc, c);
+        const long long Mrun = llmax(M0, warp_max(lane < c ? hiL : kNeg));   // max F before the chunk
+        const long long row = inf.row_base + (long long)c * 32 + lane;      // lane l <-> row 32c+l
+        unsigned long long rp[kEpt], rm[kEpt];
+        load_row_global(p.ev, row, rp, rm);
+        const long long e0 = row * kEpt - inf.off_t;
+        long long d[kEpt], run = 0, lmx = kNeg, lmn = kPos;
+        #pragma unroll
+        for (int jj = 0; jj < kEpt; ++jj) {
+            const long long ie = e0 + jj;
+            const unsigned kind = ev_kind(rm[jj]);
+            const bool af = ie >= 0 && ie < inf.n_t && kind < 2;
+            const long long sz = (long long)ev_size(rm[jj]);
+            d[jj] = af ? (kind == 0 ? sz : -sz) : 0;
+            run += d[jj];
+            if (af) { lmx = llmax(lmx, run); lmn = llmin(lmn, run); }
+        }
+        long long li = run;
+        #pragma unroll
+        for (int dd = 1; dd < 32; dd <<= 1) { long long o = shfl_up_ll(li, dd); if (lane >= dd) li += o; }
+        const long long Fl = F0 + Pw + (li - run);          // F before this lane's first event
+        long long pmx = Fl + lmx;                             // max F over lanes <= lane
+        #pragma unroll
+        for (int dd = 1; dd < 32; dd <<= 1) { long long o = shfl_up_ll(pmx, dd); if (lane >= dd) pmx = llmax(pmx, o); }
+        long long PMl = shfl_up_ll(pmx, 1);
+        if (lane == 0) PMl = kNeg;
+        int cur = 0;
+        for (;;) {
+            const unsigned cm = __ballot_sync(kFull, lane >= cur && (Fl + lmx >= B + p.T || Fl + lmn <= B - p.T));
+            if (!cm) break;
+            const int l0 = __ffs(cm) - 1;
+            // lanes 0..7 take the 8 events of lane l0
+            long long de = 0; unsigned long long me = 0;
+            #pragma unroll
+            for (int jj = 0; jj < kEpt; ++jj) {
+                const long long v = shfl_ll(d[jj], l0);
+                const unsigned long long mv = __shfl_sync(kFull, rm[jj], l0);
+                if (lane == jj) { de = v; me = mv; }
+            }
+            const long long iev = shfl_ll(e0, l0) + lane;
+            const bool af = lane < kEpt && iev >= 0 && iev < inf.n_t && ev_kind(me) < 2;
+            long long L = de;
+            #pragma unroll
+            for (int dd = 1; dd < kEpt; dd <<= 1) { long long o = shfl_up_ll(L, dd); if (lane >= dd) L += o; }
+            const long long Fe = shfl_ll(Fl, l0) + L;
+            const long long Mbase = llmax(Mrun, shfl_ll(PMl, l0));
+            int ef = 0;
+            for (;;) {                                      // successive first exits of (B-T, B+T)
+                const unsigned em = __ballot_sync(kFull, af && lane >= ef && (Fe >= B + p.T || Fe <= B - p.T));
+                if (!em) break;
+                const int e = __ffs(em) - 1;
+                const long long Fs = shfl_ll(Fe, e);
+                const long long Mprev = llmax(Mbase, warp_max((af && lane < e) ? Fe : kNeg));   // M_{i-1}
+                const long long net = Fs - B;              // the |A - F| counter
+                const bool growth = net > 0;
+                const bool nm = growth && Fs > Mprev;      // new high-water mark (Q3, Q4)
+                const unsigned long long slot_s = sb + n;
+                if (lane == e) {
+                    scl_sample smp;
+                    smp.idx = (unsigned long long)iev; smp.net = net; smp.footprint = Fs;
+                    smp.site = ev_site(me); smp.kind = growth ? 0 : 1; smp.new_max = nm ? 1 : 0; smp.pad = 0;
+                    p.samples[slot_s] = smp;
+                    if (nm) p.ep_flag[slot_s] = 0u;        // settled by the reclaim pass
+                }
+                if (nm) { ep1 = slot_s + 1; ++nep; }
+                ++n; B = Fs; ef = e + 1;                   // "resets the counters"
+            }
+            cur = l0 + 1;
+        }
+        cnext = c + 1;
+    }
+    x.F = F0 + susum; x.M = llmax(M0, F0 + sumx); x.B = B;
+    x.n = n; x.nep = nep; x.ep1 = ep1;
     __syncwarp();
 }
 
-// Look-back warp: claims full slots (oldest first).  A unit whose incoming state is
-// available is finished from shared memory; otherwise its slot is copied to a global
-// "park" record, released at once (compute never waits on a trace's chain), and the
-// unit is finished later, when the flag it waits for has moved.  Lane i of the warp
-// tracks parked unit i.
-__device__ void lookback_role(const ReplayParams& p, Smem& s, int lbw, int lane)
+// Advance a trace as far as its units are published (the caller is the trace's runner).
+__device__ void run_trace(const ReplayParams& p, RState& x, unsigned base, unsigned nseg, unsigned ep_tag, int lane)
 {
-    const unsigned want = p.epoch * 4u;
-    const size_t wid = (size_t)blockIdx.x * kLBWarps + lbw;
-    EpStart* eplist = p.ep_scratch + wid * kUnit;
-    Slot* park = reinterpret_cast<Slot*>(p.park) + wid * kPark;
-    unsigned pk_itu = kInvalid, pk_need = 0;           // lane i: parked unit i (CTA unit iteration), flag value needed
-    const unsigned* pk_blk = nullptr;
+    const Slot* rec = reinterpret_cast<const Slot*>(p.urec);
+    RPROF_ADD(0, 1)
+    while (x.next < nseg) {
+        // ready prefix of the next 32 units (lane i <-> unit next+i)
+        const unsigned ui = x.next + (unsigned)lane;
+        const bool rdy = ui < nseg && ld_acquire(&p.uready[base + ui]) == ep_tag;
+        const unsigned nr = ~__ballot_sync(kFull, rdy);
+        const int m = nr ? __ffs(nr) - 1 : 32;               // units next .. next+m-1 are ready
+        if (m == 0) return;
+        RPROF_ADD(1, 1) RPROF_ADD(2, m)
+#ifdef SCL_PROFILE
+        if (lane < m) PROF_UNIT_T(base + x.next + lane, 2)
+#endif
+        const Slot* R = rec + base + x.next;
+        UnitEntry* ue = p.uent + base + x.next;
+        long long us = 0, ux = kNeg, un = kPos;
+        if (lane < m) { us = R[lane].usum; ux = R[lane].umx; un = R[lane].umn; }
+        int j = 0;
+        while (j < m) {
+            // compose units j.. while the sampler band holds; jf = first unit where a sample fires
+            const long long v = (lane >= j && lane < m) ? us : 0;
+            long long inc = v;
+            #pragma unroll
+            for (int d = 1; d < 32; d <<= 1) { long long o = shfl_up_ll(inc, d); if (lane >= d) inc += o; }
+            const long long E = inc - v;                      // sum of units j..lane-1
+            const long long c0 = x.F - x.B + E;
+            const unsigned bm = __ballot_sync(kFull, lane >= j && lane < m && (c0 + ux >= p.T || c0 + un <= -p.T));
+            const int jf = bm ? __ffs(bm) - 1 : m;
+            // units j .. jf (incl. the resolved one) are entered with the same episode and count
+            if (lane >= j && lane <= jf && lane < m) { UnitEntry e; e.ep1 = x.ep1; e.n = x.n; ue[lane] = e; }
+            const long long mx = warp_max((lane >= j && lane < jf) ? E + ux : kNeg);
+            const long long add = shfl_ll(inc, jf > j ? jf - 1 : 0);   // sum of units j..jf-1 (lanes < j hold 0)
+            x.M = llmax(x.M, x.F + mx);
+            x.F += jf > j ? add : 0;
+            if (jf == m) break;
+            // unit jf: a sample fires in it
+#ifdef SCL_PROFILE
+            const long long t_r = clock64();
+#endif
+            resolve_unit(p, R[jf], x, lane);
+            RPROF_ADD(3, 1) RPROF_ADD(4, clock64() - t_r)
+#ifdef SCL_PROFILE
+            if (p.prof && lane == 0) p.prof[48 + 4 * (size_t)(base + x.next + jf) + 3] = clock64() - t_r;
+#endif
+            j = jf + 1;
+        }
+#ifdef SCL_PROFILE
+        if (lane < m) PROF_UNIT_T(base + x.next + lane, 1)
+#endif
+        x.next += (unsigned)m;
+        if (x.next == nseg && lane == 0) {
+            const SegInfo inf = R[m - 1].info;
+            scl_trace_summary* sm = &p.summ[inf.t];
+            sm->f_final = x.F; sm->hwm = x.M; sm->n_samples = x.n; sm->n_episodes = x.nep;
+        }
+    }
+}
+
+// Publisher warp (one per CTA): copies each finished unit's summary from its shared-memory
+// slot to the unit's global record, marks it ready and frees the slot at once.
+__device__ void publisher_role(const ReplayParams& p, Smem& s, int lane)
+{
+    const unsigned ep_tag = p.epoch;
+    Slot* urec = reinterpret_cast<Slot*>(p.urec);
     PROF_DECL
     for (;;) {
-        // ---- 1. a parked unit whose blocker moved (oldest first)
-        unsigned prio = kInvalid;
-        if (pk_itu != kInvalid && ld_acquire(pk_blk) >= pk_need) prio = pk_itu;
-        #pragma unroll
-        for (int d = 16; d > 0; d >>= 1) prio = min(prio, __shfl_xor_sync(kFull, prio, d));
-        if (prio != kInvalid) {
-            const int i = __ffs(__ballot_sync(kFull, pk_itu == prio)) - 1;
-            const Slot* G = park + i;
-            const SegInfo inf = G->info;
-            const unsigned k = inf.kraw & 0x7fffffffu;
-            const SegState* ts = &p.state[inf.slot - k];
-            // the blocker was an inclusive state of this trace: resume the forward walk from it
-            const unsigned* bptr = (const unsigned*)__shfl_sync(kFull, (unsigned long long)pk_blk, i);
-            const unsigned bneed = __shfl_sync(kFull, pk_need, i);
-            const int resume = bneed == want + 2 ? (int)(((const char*)bptr - (const char*)&ts[0].flag) / sizeof(SegState)) : -1;
-            InState in; const unsigned* blk; unsigned need;
-            if (look_back(p, ts, k, want, lane, in, blk, need, resume)) {
-                finish_unit(p, G, in, want, eplist, lane);
-                if (lane == i) pk_itu = kInvalid;
-                if (lane == 0) atomicAdd(&s.n_done, 1u);
-            } else if (lane == i) {
-                pk_blk = blk; pk_need = need;
-            }
-            __syncwarp();
-            PROF_MARK(2)
-            continue;
-        }
-        // ---- 2. the oldest full slot (only if a park lane is free)
-        const unsigned freelanes = __ballot_sync(kFull, lane < kPark && pk_itu == kInvalid);
-        unsigned best = kInvalid;
-        if (freelanes && lane < kSlots && ((volatile unsigned*)s.sstate)[lane] == 1) best = ((volatile unsigned*)s.situ)[lane];
+        unsigned best = kInvalid;                        // the oldest full slot
+        if (lane < kSlots && ((volatile unsigned*)s.sstate)[lane] == 1) best = ((volatile unsigned*)s.situ)[lane];
         #pragma unroll
         for (int d = 16; d > 0; d >>= 1) best = min(best, __shfl_xor_sync(kFull, best, d));
         if (best == kInvalid) {
             const unsigned nu = ((volatile unsigned*)&s.n_units)[0], nd = ((volatile unsigned*)&s.n_done)[0];
             if (nu != kInvalid && nd >= nu) { PROF_FLUSH(16) return; }
             PROF_MARK(0)
-            __nanosleep(64);
+            __nanosleep(32);
             continue;
         }
-        const bool mine = lane < kSlots && ((volatile unsigned*)s.sstate)[lane] == 1 && ((volatile unsigned*)s.situ)[lane] == best;
-        const unsigned cand = __ballot_sync(kFull, mine);
-        if (!cand) continue;
+        const unsigned cand = __ballot_sync(kFull, lane < kSlots && ((volatile unsigned*)s.sstate)[lane] == 1 &&
+                                                    ((volatile unsigned*)s.situ)[lane] == best);
         const int q = __ffs(cand) - 1;
-        unsigned got = 0;
-        if (lane == 0) got = atomicCAS(&s.sstate[q], 1u, 2u);
-        if (__shfl_sync(kFull, got, 0) != 1u) continue;
         __threadfence_block();
-        PROF_MARK(0)
         Slot& S = s.slot[q];
-        const SegInfo inf = S.info;
-        const unsigned k = inf.kraw & 0x7fffffffu;
-        InState in; const unsigned* blk; unsigned need;
-        const bool ready = look_back(p, &p.state[inf.slot - k], k, want, lane, in, blk, need);
-        PROF_MARK(1)
-        if (ready) {
-            finish_unit(p, &S, in, want, eplist, lane);
-        } else {
-            // park: copy the slot to global memory, remember what it waits for
-            const int i = __ffs(freelanes) - 1;
-            const uint4* src = reinterpret_cast<const uint4*>(&S);
-            uint4* dst = reinterpret_cast<uint4*>(park + i);
-            for (int o = lane; o < (int)(sizeof(Slot) / 16); o += 32) dst[o] = src[o];
-            if (lane == i) { pk_itu = S.itu; pk_blk = blk; pk_need = need; }
-        }
+        const unsigned u = S.info.slot;
+        const uint4* src = reinterpret_cast<const uint4*>(&S);
+        uint4* dst = reinterpret_cast<uint4*>(urec + u);
+        for (int o = lane; o < (int)(sizeof(Slot) / 16); o += 32) dst[o] = src[o];
         __syncwarp();
         if (lane == 0) {
+            __threadfence();
+            st_release(&p.uready[u], ep_tag);
             S.done = 0; __threadfence_block();
-            atomicExch(&s.sstate[q], 0u); mbar_arrive(&s.sempty[q]);
-            if (ready) atomicAdd(&s.n_done, 1u);
+            atomicExch(&s.sstate[q], 0u); mbar_arrive(&s.sempty[q]); atomicAdd(&s.n_done, 1u);
         }
         __syncwarp();
-        PROF_MARK(3)
+        PROF_MARK(1)
     }
+}
+
+// Runner warp rw of grid*kRunners: owns traces rw, rw + nr, ...  (lane i <-> its i-th trace,
+// whose next unit index it keeps) and advances whichever of them has its next unit published,
+// with the exact sequential state (kept in p.run between visits).
+__device__ void runner_role(const ReplayParams& p, int ri_local, int lane)
+{
+    const unsigned ep_tag = p.epoch;
+    const unsigned nr = gridDim.x * kRunners, ri = blockIdx.x * kRunners + ri_local;
+    const unsigned cnt = ri < p.n_traces ? (p.n_traces - ri + nr - 1) / nr : 0u;
+    const unsigned my_t = ri + (unsigned)lane * nr;
+    unsigned my_base = 0, my_nseg = 0, my_next = 0;
+    if ((unsigned)lane < cnt) { my_nseg = __ldg(p.tr_nseg + my_t); my_base = __ldg(p.tr_base + my_t); }
+    PROF_DECL
+    for (;;) {
+        const bool alive = (unsigned)lane < cnt && my_next < my_nseg;
+        if (!__any_sync(kFull, alive)) break;
+        const bool ready = alive && ld_acquire(&p.uready[my_base + my_next]) == ep_tag;
+        unsigned rm = __ballot_sync(kFull, ready);
+        if (!rm) { PROF_MARK(0) __nanosleep(64); continue; }
+        PROF_MARK(0)
+        while (rm) {
+            const int i = __ffs(rm) - 1;
+            rm &= rm - 1;
+            const unsigned t = ri + (unsigned)i * nr;
+            RunState* rs = p.run + t;
+            RState x = load_rstate(rs, lane);
+            x.next = __shfl_sync(kFull, my_next, i);
+            run_trace(p, x, __shfl_sync(kFull, my_base, i), __shfl_sync(kFull, my_nseg, i), ep_tag, lane);
+            store_rstate(rs, x, lane);
+            if (lane == i) my_next = x.next;
+        }
+        PROF_MARK(2)
+    }
+    PROF_FLUSH(16)
 }
 
 // ============================================================================ kernel
@@ -641,6 +591,10 @@ replay_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     }
     __syncthreads();
 
+    // register rebalancing per warpgroup (launch: 96/thread): the four compute warpgroups
+    // give 16 each, the producer + look-back warpgroup takes them (no spills in its resolver)
+    if (warp < kComputeWarps) asm volatile("setmaxnreg.dec.sync.aligned.u32 80;\n" ::: "memory");
+    else                      asm volatile("setmaxnreg.inc.sync.aligned.u32 160;\n" ::: "memory");
     if (warp < kComputeWarps) {
         compute_role(p, s, stage, warp / 8, warp % 8, lane);
         named_bar(1, kComputeWarps * 32);                            // all compute warps done
@@ -655,9 +609,74 @@ replay_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         }
     } else if (warp == kProducerWarp) {
         producer_role(p, &tmap, s, stage, lane);
+    } else if (warp == kProducerWarp + 1) {
+        publisher_role(p, s, lane);
     } else {
-        lookback_role(p, s, warp - kProducerWarp - 1, lane);
+        runner_role(p, warp - kProducerWarp - 2, lane);
     }
+}
+
+// ============================================================================ reclaim pass (a4)
+// One warp per unit settles the leak tracker's free-pointer comparison for every
+// episode segment inside the unit: the episode entering it (UnitEntry) up to the first
+// episode started in it, then each episode started in it up to the next.  An episode is
+// reclaimed iff its pointer is freed anywhere in its span, so the segments are independent
+// and every unit is checked in parallel: Bloom query per chunk (lane <-> chunk), exact
+// re-check of the positives through L2.  ep_flag was zeroed by the runner at episode start.
+__global__ void __launch_bounds__(256) reclaim_kernel(const __grid_constant__ ReplayParams p)
+{
+    const unsigned u = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (u >= p.n_segs) return;
+    const Slot& S = reinterpret_cast<const Slot*>(p.urec)[u];
+    const SegInfo inf = S.info;
+    const UnitEntry ent = p.uent[u];
+    const bool last = (inf.kraw >> 31) != 0;
+    const unsigned long long n_out = last ? p.summ[inf.t].n_samples : p.uent[u + 1].n;
+    const unsigned long long sb = __ldg(p.sbase + inf.t);
+    const long long g0 = inf.row_base * kEpt;              // global event index of unit position 0
+    unsigned long long ep1 = ent.ep1;                        // current segment: episode (slot + 1), pointer, start
+    unsigned long long ptr = 0;
+    if (ep1) ptr = __ldg(&p.ev[inf.off_t + (long long)__ldg(&p.samples[ep1 - 1].idx)].ptr);
+    unsigned sbeg = 0;
+    auto check = [&](unsigned send) {                        // settle [sbeg, send) for the current episode
+        if (!ep1 || send <= sbeg) return;
+        const unsigned w = bloom_word(ptr), msk = bloom_mask(ptr);
+        const unsigned cb = (unsigned)lane * 32 * kEpt;
+        const bool pos = cb < send && cb + 32 * kEpt > sbeg && (S.bloom[lane][w] & msk) == msk;
+        unsigned cm = __ballot_sync(kFull, pos);
+        bool found = false;
+        while (cm && !found) {
+            const int c = __ffs(cm) - 1;
+            cm &= cm - 1;
+            found = chunk_has_free(p, inf, c, ptr, sbeg, send, lane);
+        }
+        if (found && lane == 0) p.ep_flag[ep1 - 1] = 1u;
+    };
+    for (unsigned long long s0 = ent.n; s0 < n_out; s0 += 32) {       // samples taken in this unit
+        const unsigned long long si = s0 + (unsigned long long)lane;
+        bool nm = false; long long idx = 0;
+        if (si < n_out) { const scl_sample smp = p.samples[sb + si]; nm = smp.new_max != 0; idx = (long long)smp.idx; }
+        unsigned em = __ballot_sync(kFull, nm);
+        while (em) {
+            const int e = __ffs(em) - 1;
+            em &= em - 1;
+            const long long ie = shfl_ll(idx, e);
+            const unsigned pos = (unsigned)(inf.off_t + ie - g0);
+            check(pos);
+            ep1 = sb + s0 + (unsigned long long)e + 1;
+            ptr = __ldg(&p.ev[inf.off_t + ie].ptr);
+            sbeg = pos;
+        }
+    }
+    check((unsigned)kUnit);
+}
+
+cudaError_t launch_reclaim(const ReplayParams& p, cudaStream_t st)
+{
+    if (p.n_segs == 0) return cudaSuccess;
+    reclaim_kernel<<<(p.n_segs + 7) / 8, 256, 0, st>>>(p);
+    return cudaGetLastError();
 }
 
 int replay_occupancy(int* grid)

@@ -28,12 +28,12 @@ constexpr int kUnitRows = kThreads * kSub;
 constexpr int kUnit = kSeg * kSub;            // events per unit (8192)
 constexpr int kChunks = 32;                   // 256-event chunks per unit (one per look-back lane)
 constexpr int kComputeWarps = 16;                // two groups of 8, alternating boxes
-constexpr int kLBWarps = 3;                   // 20 warps total (5 per SM sub-partition, 96 registers)
+constexpr int kLBWarps = 3;                   // publisher + 2 runners (20 warps total, 96 registers)
+constexpr int kRunners = 2;                   // runner warps per CTA
 constexpr int kProducerWarp = kComputeWarps;
 constexpr int kCtaThreads = (kComputeWarps + 1 + kLBWarps) * 32;
 constexpr int kStages = 4;                    // TMA ring depth
 constexpr int kSlots = 6;                     // compute -> look-back unit summary ring (smem)
-constexpr int kPark = 32;                     // parked units per look-back warp (global copies)
 constexpr int kBloomWords = 64;               // 2048-bit Bloom filter of freed pointers per chunk
 constexpr int kHot = 1024;                    // sites with shared-memory Tier-E counters
 constexpr long long kNeg = -(1ll << 62);      // "no event" sentinels for max / min
@@ -46,18 +46,16 @@ __host__ __device__ inline uint64_t ev_size(uint64_t meta) { return meta & 0xFFF
 __host__ __device__ inline unsigned ev_kind(uint64_t meta) { return (unsigned)(meta >> 40) & 3u; }
 __host__ __device__ inline uint32_t ev_site(uint64_t meta) { return (uint32_t)(meta >> 43); }
 
-// ---- chained-scan state of one segment (decoupled look-back) ---------------
-// flag = epoch*4 + {1: aggregate published, 2: inclusive published}.
-struct __align__(16) SegState {
-    long long sum, mx, mn;            // aggregate: sum of d, max / min prefix of the local running sum
-    long long F, M, B;                // inclusive: footprint, high-water mark, footprint at last sample
-    unsigned long long n, nep;        // samples / episodes in the trace so far
-    unsigned long long ep, ep_ptr;    // current episode: sample slot of its start, tracked pointer
-    unsigned int flag, pad0, pad1, pad2;
+// ---- exact sequential state of one trace between units (owned by the trace's runner) ----
+struct __align__(16) RunState {
+    long long F, M, B;                // footprint, high-water mark, footprint at the last sample
+    unsigned long long n, nep, ep1;   // samples, episodes, current episode (sample slot + 1; 0 none)
+    unsigned next, pad;               // next unit index to run
 };
 
-// Per-segment list entry of episodes started inside the segment (phase 4).
-struct EpStart { unsigned long long ep, ptr; unsigned int pos, pad; };
+// State entering one unit, written by its trace's runner for the reclaim pass: the episode
+// in progress (sample slot + 1; 0 none) and the samples taken before the unit.
+struct __align__(16) UnitEntry { unsigned long long ep1, n; };
 
 // One unit ticket, resolved on the host at load time (one 32-B load per ticket).
 struct __align__(16) TicketInfo {
@@ -69,10 +67,15 @@ struct ReplayParams {
     const scl_event* ev;              // padded device copy (multiple of 8 events)
     const unsigned long long* off;    // [n_traces+1]
     const TicketInfo* tk;             // [n_segs] in ticket order (unit index, trace)
-    SegState* state;                  // [n_segs]
+    void* urec;                       // [n_segs] unit records (summaries published by the look-back warps)
+    unsigned int* uready;             // [n_segs] = epoch when the unit's record is published
+    RunState* run;                    // [n_traces] per-trace runner state (zeroed per run)
+    UnitEntry* uent;                  // [n_segs] state entering each unit (runner -> reclaim pass)
+    const unsigned int* tr_nseg;      // [n_traces] units per trace
+    const unsigned int* tr_base;      // [n_traces] first unit id of the trace
     unsigned int* ticket;             // global ticket counter (zeroed per run)
     unsigned int n_segs;
-    unsigned int epoch;
+    unsigned int epoch;               // run number on this traces handle (ready tag)
     unsigned int n_sites;
     unsigned int n_traces;
     long long T;
@@ -81,8 +84,6 @@ struct ReplayParams {
     unsigned int* ep_flag;            // [capacity]  reclaimed flag per episode-start sample
     const unsigned long long* sbase;  // trace -> first sample slot
     scl_trace_summary* summ;          // [n_traces]
-    EpStart* ep_scratch;              // [grid * kLBWarps * kUnit]
-    void* park;                       // [grid * kLBWarps * kPark] parked unit summaries (Slot)
     unsigned long long* prof;         // debug build only (SCL_PROFILE): per-role cycle sums, else NULL
 };
 
@@ -100,13 +101,14 @@ cudaError_t launch_load_stats(const scl_event* ev, const unsigned long long* off
                               unsigned n_sites, unsigned long long* sabs, unsigned long long* err,
                               cudaStream_t st);
 cudaError_t launch_replay(const CUtensorMap* tmap, const ReplayParams& p, int grid, cudaStream_t st);
+cudaError_t launch_reclaim(const ReplayParams& p, cudaStream_t st);
 cudaError_t launch_samples(const ReplayParams& p, cudaStream_t st);
 cudaError_t launch_finalize(const FinalParams& p, cudaStream_t st);
 cudaError_t launch_rows(const unsigned long long* table, const double* prob, const double* rate,
                         const unsigned char* flag, const unsigned int* order, unsigned n_sites,
                         scl_site_row* rows, cudaStream_t st);
 size_t replay_smem_bytes();
-size_t replay_park_bytes();            // bytes of one parked unit summary
+size_t replay_urec_bytes();            // bytes of one unit record
 int replay_occupancy(int* grid);
 
 }  // namespace scl

@@ -16,7 +16,7 @@ for _ in range(4):
     r = scl.scl_replay_run(T, tr, out=r)
 ms = scl.scl_result_timing(r)[0]
 nunits_all = int(sum((cfg.events_per_trace + 8191) // 8192 for _ in range(nt)))
-bigbuf = np.zeros(32 + 2 * nunits_all, dtype=np.uint64)
+bigbuf = np.zeros(48 + 4 * nunits_all, dtype=np.uint64)
 lib.scl_debug_prof(r.handle, bigbuf.ctypes.data)
 buf = bigbuf[:32]
 nsm = 148
@@ -24,7 +24,7 @@ cyc = ms * 1e-3 * 1.965e9
 print(f"cfg{cid} traces={nt} T={T}: kernel {ms*1e3:.1f} us = {cyc:.0f} cycles @1.965GHz")
 names = {0: ("compute", 16, ["wait_full", "wait_sempty", "summary", "agg+loop", "process"]),
          8: ("producer", 1, ["wait_empty", "fetch+issue"]),
-         16: ("lookback", 3, ["idle", "lookback", "parked", "finish"])}
+         16: ("lookback", 3, ["idle", "publish", "run"])}
 for base, (nm, nw, cats) in names.items():
     tot = buf[base:base + 8].astype(float) / (nw * nsm)
     print(f"  {nm:9s} " + "  ".join(f"{c}={tot[i]/cyc*100:5.1f}%" for i, c in enumerate(cats)))
@@ -32,10 +32,14 @@ for base, (nm, nw, cats) in names.items():
         units = float(buf[base + 6])
         print("  walker per unit (cycles): " + "  ".join(f"{c}={float(buf[base+i])/max(units,1):.0f}" for i, c in enumerate(cats) if c not in ("units", "x")), f" units={units:.0f}")
 
+rc = bigbuf[24:40].astype(float)
+print(f"  runner: invocations {rc[0]:.0f} batches {rc[1]:.0f} units {rc[2]:.0f} resolves {rc[3]:.0f} "
+      f"resolve cyc/each {rc[4]/max(rc[3],1):.0f} ptr-exact {rc[5]:.0f} run cyc/invocation {rc[6]/max(rc[0],1):.0f} lock-fails {rc[7]:.0f}")
+print(f"  resolve parts per resolve: loads {rc[8]/max(rc[3],1):.0f} sampler {rc[9]/max(rc[3],1):.0f} ptrmatch {rc[10]/max(rc[3],1):.0f} cand-chunks {rc[11]/max(rc[3],1):.2f}")
 # per-unit timeline (aggregate published, inclusive published), first unit of each trace = unit 0
 if len(sys.argv) > 4:
     nunits = nunits_all
-    tl = bigbuf[32:].reshape(-1, 2).astype(np.int64)
+    tl4 = bigbuf[48:].reshape(-1, 4).astype(np.int64); tl = tl4[:, :2]
     t0 = tl[tl > 0].min()
     per = (cfg.events_per_trace + 8191) // 8192
     agg = (tl[:, 0] - t0) / 1e3; inc = (tl[:, 1] - t0) / 1e3
@@ -44,3 +48,9 @@ if len(sys.argv) > 4:
     for t in (0, 1, nt // 2):
         a = agg[t * per:(t + 1) * per]; b = inc[t * per:(t + 1) * per]
         print(f"  trace {t}: " + " ".join(f"{int(x)}/{int(y)}" for x, y in list(zip(a, b))[::8]))
+
+    for t in (1,):
+        print(f"  trace {t} per unit: agg / batch-start / batch-end (us) / resolve kcyc")
+        for u in range(t * per, (t + 1) * per):
+            a, bs, be, rc_ = (tl4[u, 0] - t0) / 1e3, (tl4[u, 2] - t0) / 1e3, (tl4[u, 1] - t0) / 1e3, tl4[u, 3] / 1e3
+            print(f"    u{u - t*per:3d} {a:7.1f} {bs:7.1f} {be:7.1f} {rc_:7.1f}")
