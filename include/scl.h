@@ -128,9 +128,26 @@ scl_status scl_trace_load(const char* path, const scl_event* events, const uint6
                           uint32_t n_traces, uint32_t n_sites, int device, int validate,
                           scl_traces** out);
 
+/* Refill an existing handle with new traces (same meaning of the arguments as
+ * scl_trace_load, events/offsets host or device pointers).  The handle's device buffers
+ * are reused while the new traces fit and grown otherwise; the copy, the load checks and
+ * the unit plan are ordered on cuda_stream (cudaStream_t, NULL = default stream), and the
+ * call returns after one synchronisation of that stream (the per-trace sample bounds come
+ * back to the host).  Runs of this handle still in flight on ANOTHER stream must have
+ * finished.  Results of the handle stay valid handles (re-sized on their next run); their
+ * earlier contents are stale.  On SCL_EINVAL from the event check the handle holds no
+ * traces until the next successful reload.
+ * Errors: as scl_trace_load. */
+scl_status scl_trace_reload(scl_traces* traces, const scl_event* events, const uint64_t* offsets,
+                            uint32_t n_traces, uint32_t n_sites, int validate, void* cuda_stream);
+
 /* Replay every trace at threshold T (used verbatim; P:436-438 picks a prime slightly
  * above 10 MB -- see scl_next_prime).  Runs a1..a5 on the GPU and, unless
- * opts->defer_finalize, a6.  threshold == 0 -> SCL_EINVAL. */
+ * opts->defer_finalize, a6.  threshold == 0 -> SCL_EINVAL.
+ * Asynchronous: the work is enqueued on opts->cuda_stream and the call returns without
+ * waiting (it blocks only when the sample buffer must grow).  The accessors below
+ * (report, samples, summaries, gate, timing) wait for the run themselves.
+ * *out: NULL -> a new result; else a result of the same handle, reused. */
 scl_status scl_replay_run(uint64_t threshold, const scl_traces* traces,
                           const scl_run_opts* opts, scl_result** out);
 
@@ -158,11 +175,16 @@ scl_status scl_trace_summaries(const scl_result* r, scl_trace_summary* out, size
  * over traces with >= 2 samples; open iff some trace qualifies and 100*num >= den. */
 scl_status scl_gate(const scl_result* r, int64_t* num, int64_t* den, int* open);
 
-/* Device time of the last run, in ms, from CUDA events on the run's stream:
+/* Device time of the last run, in ms, from CUDA events on the run's stream (waits for it):
  *   replay_kernel_ms  the streaming a1..a5 kernel alone (the roofline kernel)
- *   run_ms            a1..a5 including per-run clears and the per-sample reduce
+ *   run_ms            a1..a5 including the per-run clears, the reclaim pass and the per-sample reduce
  *   finalize_ms       a6 (probabilities, flags, report order, rows) */
 scl_status scl_result_timing(const scl_result* r, float* replay_kernel_ms, float* run_ms, float* finalize_ms);
+
+/* Replay-kernel durations (ms) of the runs enqueued since the previous call (at most the
+ * latest 128), oldest first; waits for them.  Lets a caller time many back-to-back runs
+ * without synchronising between them.  *n = number written (<= cap). */
+scl_status scl_result_kernel_times(const scl_result* r, float* ms, size_t cap, size_t* n);
 
 void scl_traces_free(scl_traces* t);
 void scl_result_free(scl_result* r);

@@ -17,9 +17,9 @@ import numpy as np
 
 from . import _build
 
-__all__ = ["SclError", "Traces", "Result", "scl_trace_load", "scl_replay_run", "scl_finalize",
+__all__ = ["SclError", "Traces", "Result", "scl_trace_load", "scl_trace_reload", "scl_replay_run", "scl_finalize",
            "scl_site_report", "scl_samples", "scl_trace_summaries", "scl_gate", "scl_result_device_table",
-           "scl_result_timing", "scl_next_prime", "scl_traces_info", "EVENT_DTYPE", "SAMPLE_DTYPE",
+           "scl_result_timing", "scl_result_kernel_times", "scl_next_prime", "scl_traces_info", "EVENT_DTYPE", "SAMPLE_DTYPE",
            "SUMMARY_DTYPE", "SITE_ROW_DTYPE", "COLS", "device_table_tensor", "write_trace_file"]
 
 EVENT_DTYPE = np.dtype([("ptr", "<u8"), ("meta", "<u8")])
@@ -56,6 +56,8 @@ def _load():
     P, U64, U32, I32, SZ = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_size_t
     sig = {
         "scl_trace_load": [ctypes.c_char_p, P, P, U32, U32, I32, I32, P],
+        "scl_trace_reload": [P, P, P, U32, U32, I32, P],
+        "scl_result_kernel_times": [P, P, SZ, P],
         "scl_replay_run": [U64, P, P, P],
         "scl_result_device_table": [P, P, P],
         "scl_finalize": [P, U64],
@@ -165,6 +167,22 @@ def scl_trace_load(events=None, offsets=None, n_sites: int = 0, device: int = 0,
     return t
 
 
+def scl_trace_reload(traces: Traces, events, offsets, n_sites: int, validate: bool = False, stream=None) -> Traces:
+    """Refill ``traces`` with new events (host or CUDA), reusing its device buffers while
+    they fit; stream-ordered on ``stream`` (torch.cuda.Stream / raw handle / None)."""
+    if isinstance(offsets, np.ndarray):
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+    if isinstance(events, np.ndarray):
+        events = np.ascontiguousarray(events)
+    st = getattr(stream, "cuda_stream", stream) if stream is not None else None
+    _check(lib.scl_trace_reload(traces.handle, _addr(events), _addr(offsets), len(offsets) - 1, n_sites,
+                                int(validate), st))
+    nev, nt, ns = ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_uint32()
+    _check(lib.scl_traces_info(traces.handle, ctypes.byref(nev), ctypes.byref(nt), ctypes.byref(ns)))
+    traces.n_traces, traces.n_sites, traces.n_events = nt.value, ns.value, nev.value
+    return traces
+
+
 def scl_replay_run(threshold: int, traces: Traces, tick_ns: int = 0, formula: int = 0,
                    defer_finalize: bool = False, elapsed_ns: int = 0, stream=None,
                    out: Result | None = None) -> Result:
@@ -240,6 +258,14 @@ def scl_result_timing(r: Result):
     a, b, c = ctypes.c_float(), ctypes.c_float(), ctypes.c_float()
     _check(lib.scl_result_timing(r.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
     return a.value, b.value, c.value
+
+
+def scl_result_kernel_times(r: Result) -> list:
+    """Replay-kernel durations (ms) of the runs enqueued since the previous call (<= 128)."""
+    buf = (ctypes.c_float * 128)()
+    n = ctypes.c_size_t()
+    _check(lib.scl_result_kernel_times(r.handle, buf, 128, ctypes.byref(n)))
+    return [buf[i] for i in range(n.value)]
 
 
 def scl_next_prime(base: int) -> int:

@@ -31,21 +31,29 @@ struct scl_traces {
     int device = 0;
     uint32_t n_traces = 0, n_sites = 0;
     uint64_t n_events = 0, max_len = 0, tick_ns = 1000;
+    // device buffers, reused by scl_trace_reload while the new traces fit (cap_*)
     scl_event* d_ev = nullptr;                 // padded_rows * 8 events
+    size_t cap_rows = 0;
     unsigned long long* d_off = nullptr;       // n_traces + 1
-    std::vector<uint64_t> h_off, h_sabs;
-    uint32_t n_segs = 0;
-    TicketInfo* d_tk = nullptr;
-    void* d_urec = nullptr;                    // per unit: published summary record
-    unsigned int* d_uready = nullptr;          // per unit: run epoch when published
+    unsigned long long* d_sabs = nullptr;      // per trace: sum |d| (sample-capacity bound)
     unsigned int* d_tr_nseg = nullptr;         // per trace: number of units
     unsigned int* d_tr_base = nullptr;         // per trace: first unit id
     RunState* d_run = nullptr;                 // per trace: runner state (zeroed per run)
+    size_t cap_tr = 0;
+    TicketInfo* d_tk = nullptr;
+    void* d_urec = nullptr;                    // per unit: published summary record
+    unsigned int* d_uready = nullptr;          // per unit: run epoch when published
     UnitEntry* d_uent = nullptr;               // per unit: state entering it (runner -> reclaim pass)
+    size_t cap_segs = 0;
+    unsigned long long* d_err = nullptr;       // first invalid event (load check)
     unsigned int* d_ticket = nullptr;
+    std::vector<uint64_t> h_off, h_sabs;
+    uint32_t n_segs = 0;
     mutable unsigned int epoch = 0;
     CUtensorMap tmap;
 };
+
+constexpr int kRing = 128;                     // replay-kernel timing event pairs kept per result
 
 struct scl_result {
     const scl_traces* tr = nullptr;
@@ -58,6 +66,7 @@ struct scl_result {
     scl_sample* d_samples = nullptr; unsigned int* d_epflag = nullptr; size_t cap = 0;
     unsigned long long* d_sbase = nullptr;
     scl_trace_summary* d_summ = nullptr;
+    size_t cap_sites = 0, cap_tr = 0;
     int grid = 0;
     double* d_prob = nullptr; double* d_rate = nullptr; unsigned char* d_flag = nullptr;
     unsigned long long *d_key = nullptr, *d_key2 = nullptr; unsigned int *d_val = nullptr, *d_order = nullptr;
@@ -66,13 +75,13 @@ struct scl_result {
     // host
     std::vector<unsigned long long> h_sbase;
     std::vector<scl_trace_summary> h_summ;
+    unsigned long long* h_gate = nullptr;      // pinned: gate sums copied at the end of a6
     bool summ_valid = false;
-    long long gate_num = 0, gate_den = 0; unsigned long long gate_cnt = 0;
     bool finalized = false;
-    cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-    float kern_ms = 0;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};   // run begin/end, finalize begin/end
+    cudaEvent_t kev[2 * kRing] = {};           // replay kernel begin/end, one pair per run (ring)
+    uint64_t nrun = 0, nread = 0;
     unsigned long long* d_prof = nullptr;     // SCL_PROFILE builds only
-    float run_ms = 0, fin_ms = 0;
 };
 
 // ---------------------------------------------------------------- helpers
@@ -137,6 +146,141 @@ static scl_status read_file(const char* path, std::vector<scl_event>& ev, std::v
 }
 
 // ---------------------------------------------------------------- load
+template <class T> static bool grow(T*& p, size_t n) {
+    cudaFree(p); p = nullptr;
+    if (cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess) { cudaGetLastError(); p = nullptr; return false; }
+    return true;
+}
+
+// Host offsets (from host or device memory) with their argument checks.
+static scl_status read_offsets(const uint64_t* offsets, uint32_t n_traces, std::vector<uint64_t>& h_off) {
+    h_off.resize((size_t)n_traces + 1);
+    if (is_device_ptr(offsets)) CU(cudaMemcpy(h_off.data(), offsets, h_off.size() * 8, cudaMemcpyDeviceToHost));
+    else memcpy(h_off.data(), offsets, h_off.size() * 8);
+    if (h_off[0] != 0) return fail(SCL_EINVAL, "offsets[0] != 0");
+    for (uint32_t t = 0; t < n_traces; ++t)
+        if (h_off[t + 1] < h_off[t]) return fail(SCL_EINVAL, "offsets not non-decreasing at trace " + std::to_string(t));
+    return SCL_OK;
+}
+
+static scl_status validate_host(const scl_event* src, bool src_dev, const std::vector<uint64_t>& h_off, uint32_t n_traces) {
+    const uint64_t n = h_off[n_traces];
+    if (n == 0) return SCL_OK;
+    std::vector<scl_event> tmp;
+    const scl_event* hv = src;
+    if (src_dev) { tmp.resize(n); CU(cudaMemcpy(tmp.data(), src, n * sizeof(scl_event), cudaMemcpyDeviceToHost)); hv = tmp.data(); }
+    for (uint32_t t = 0; t < n_traces; ++t) {
+        int64_t bad = validate_trace(hv + h_off[t], h_off[t + 1] - h_off[t]);
+        if (bad >= 0) return fail(SCL_ETRACE, "trace " + std::to_string(t) + " event " + std::to_string(bad) +
+                                                  ": free of a non-live pointer, size mismatch or live pointer reused");
+    }
+    return SCL_OK;
+}
+
+// Copy the events into the handle's device buffers (growing them if needed), run the load
+// statistics and build the unit plan.  Stream-ordered on st; one synchronisation at the end
+// (the host needs the per-trace sum |d| to size the sample buffer of each run).
+static scl_status upload(scl_traces* tr, const scl_event* src, bool src_dev, std::vector<uint64_t>&& h_off,
+                         uint32_t n_traces, uint32_t n_sites, cudaStream_t st)
+{
+    const uint64_t n = h_off[n_traces];
+    {   // every trace needs a runner lane: n_traces <= grid * kRunners * 32
+        int grid = 0;
+        replay_occupancy(&grid);
+        if ((uint64_t)n_traces > (uint64_t)grid * kRunners * 32)
+            return fail(SCL_EOVERFLOW, "too many traces for one launch (max " +
+                                       std::to_string((uint64_t)grid * kRunners * 32) + "): load them in waves");
+    }
+    const uint64_t rows_alloc = std::max<uint64_t>((n + 7) / 8, 1);
+    if (rows_alloc > tr->cap_rows) {
+        cudaFree(tr->d_ev); tr->d_ev = nullptr; tr->cap_rows = 0;
+        if (cudaMalloc(&tr->d_ev, rows_alloc * 128) != cudaSuccess) { cudaGetLastError(); tr->d_ev = nullptr; return fail(SCL_ENOMEM, "events"); }
+        tr->cap_rows = rows_alloc;
+    }
+    const size_t nt1 = std::max<uint32_t>(n_traces, 1);
+    if (nt1 > tr->cap_tr) {
+        tr->cap_tr = 0;
+        if (!grow(tr->d_off, nt1 + 1) || !grow(tr->d_sabs, nt1) || !grow(tr->d_tr_nseg, nt1) ||
+            !grow(tr->d_tr_base, nt1) || !grow(tr->d_run, nt1))
+            return fail(SCL_ENOMEM, "per-trace buffers");
+        tr->cap_tr = nt1;
+    }
+    if (!tr->d_err && (!grow(tr->d_err, 1) || !grow(tr->d_ticket, 1))) return fail(SCL_ENOMEM, "counters");
+    if (n > 0) CU(cudaMemcpyAsync(tr->d_ev, src, n * sizeof(scl_event), src_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    if (rows_alloc * 8 > n) CU(cudaMemsetAsync(tr->d_ev + n, 0, (rows_alloc * 8 - n) * sizeof(scl_event), st));
+    CU(cudaMemcpyAsync(tr->d_off, h_off.data(), h_off.size() * 8, cudaMemcpyHostToDevice, st));
+    CU(cudaMemsetAsync(tr->d_sabs, 0, nt1 * 8, st));
+    CU(cudaMemsetAsync(tr->d_err, 0xff, 8, st));
+    CU(launch_load_stats(tr->d_ev, tr->d_off, n_traces, n, n_sites, tr->d_sabs, tr->d_err, st));
+
+    // unit plan (while the copy runs): unit k of trace t covers rows (off_t/8) + 1024k ...;
+    // tickets ordered (k, t) so that one trace's units are spread over the run
+    std::vector<uint32_t> nseg(n_traces), seg_base(n_traces);
+    uint32_t total = 0, maxk = 0;
+    uint64_t max_len = 0;
+    for (uint32_t t = 0; t < n_traces; ++t) {
+        const uint64_t a = h_off[t], b = h_off[t + 1];
+        max_len = std::max<uint64_t>(max_len, b - a);
+        uint32_t ns = 0;
+        if (b > a) { uint64_t r = (b + 7) / 8 - a / 8; ns = (uint32_t)((r + kUnitRows - 1) / kUnitRows); }
+        nseg[t] = ns; seg_base[t] = total; total += ns; maxk = std::max(maxk, ns);
+    }
+    std::vector<TicketInfo> tk;
+    tk.reserve(total);
+    for (uint32_t k = 0; k < maxk; ++k)
+        for (uint32_t t = 0; t < n_traces; ++t)
+            if (k < nseg[t]) {
+                TicketInfo ti;
+                ti.off_t = (long long)h_off[t]; ti.n_t = (long long)(h_off[t + 1] - h_off[t]);
+                ti.t = t; ti.kraw = k | (k + 1 == nseg[t] ? 0x80000000u : 0u); ti.slot = seg_base[t] + k;
+                const uint64_t row_base = h_off[t] / 8 + (uint64_t)k * kUnitRows;
+                const uint64_t rows_left = (h_off[t + 1] + 7) / 8 - row_base;
+                ti.nbox = (unsigned)std::min<uint64_t>((rows_left + kThreads - 1) / kThreads, kSub);
+                tk.push_back(ti);
+            }
+    const size_t nn = std::max<size_t>(total, 1);
+    if (nn > tr->cap_segs) {
+        tr->cap_segs = 0;
+        cudaFree(tr->d_urec); tr->d_urec = nullptr;
+        if (!grow(tr->d_tk, nn) || !grow(tr->d_uready, nn) || !grow(tr->d_uent, nn) ||
+            cudaMalloc(&tr->d_urec, nn * replay_urec_bytes()) != cudaSuccess)
+            { cudaGetLastError(); return fail(SCL_ENOMEM, "unit plan"); }
+        CU(cudaMemsetAsync(tr->d_uready, 0, nn * 4, st));      // epoch tags start at 1
+        tr->cap_segs = nn;
+    }
+    if (total) CU(cudaMemcpyAsync(tr->d_tk, tk.data(), total * sizeof(TicketInfo), cudaMemcpyHostToDevice, st));
+    if (n_traces) {
+        CU(cudaMemcpyAsync(tr->d_tr_nseg, nseg.data(), n_traces * 4, cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(tr->d_tr_base, seg_base.data(), n_traces * 4, cudaMemcpyHostToDevice, st));
+    }
+    unsigned long long err = 0;
+    tr->h_sabs.resize(n_traces);
+    CU(cudaMemcpyAsync(&err, tr->d_err, 8, cudaMemcpyDeviceToHost, st));
+    if (n_traces) CU(cudaMemcpyAsync(tr->h_sabs.data(), tr->d_sabs, n_traces * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    tr->n_traces = n_traces; tr->n_sites = n_sites; tr->n_events = n; tr->max_len = max_len; tr->n_segs = total;
+    tr->h_off = std::move(h_off);
+    if (err != ~0ull) {
+        uint32_t t = (uint32_t)(std::upper_bound(tr->h_off.begin(), tr->h_off.end(), err) - tr->h_off.begin()) - 1;
+        tr->n_traces = 0; tr->n_events = 0; tr->n_segs = 0;     // the handle holds no valid traces
+        return fail(SCL_EINVAL, "trace " + std::to_string(t) + " event " + std::to_string(err - tr->h_off[t]) +
+                                ": size 0, kind 3 or site >= n_sites");
+    }
+
+    // TMA descriptor: rows of 32 x u32 (128 B), box 32 x 256 rows, 128-B swizzle
+    auto enc = get_encode();
+    if (!enc) return fail(SCL_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t gdim[2] = {32, (cuuint64_t)rows_alloc};
+    cuuint64_t gstride[1] = {128};
+    cuuint32_t box[2] = {32, (cuuint32_t)kThreads};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult cr = enc(&tr->tmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, (void*)tr->d_ev, gdim, gstride, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return fail(SCL_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
+    return SCL_OK;
+}
+
 extern "C" scl_status scl_trace_load(const char* path, const scl_event* events, const uint64_t* offsets,
                                      uint32_t n_traces, uint32_t n_sites, int device, int validate,
                                      scl_traces** out)
@@ -158,128 +302,42 @@ extern "C" scl_status scl_trace_load(const char* path, const scl_event* events, 
         src = file_ev.data();
     } else {
         if (!offsets || (n_traces > 0 && !events)) return fail(SCL_EINVAL, "events/offsets is NULL");
-        h_off.resize((size_t)n_traces + 1);
-        if (is_device_ptr(offsets)) CU(cudaMemcpy(h_off.data(), offsets, h_off.size() * 8, cudaMemcpyDeviceToHost));
-        else memcpy(h_off.data(), offsets, h_off.size() * 8);
-        if (h_off[0] != 0) return fail(SCL_EINVAL, "offsets[0] != 0");
-        for (uint32_t t = 0; t < n_traces; ++t)
-            if (h_off[t + 1] < h_off[t]) return fail(SCL_EINVAL, "offsets not non-decreasing at trace " + std::to_string(t));
+        scl_status st = read_offsets(offsets, n_traces, h_off);
+        if (st != SCL_OK) return st;
     }
     if (n_sites == 0 || n_sites > (1u << 21)) return fail(SCL_EINVAL, "n_sites must be in 1..2^21");
     const uint64_t n = h_off[n_traces];
     const bool src_dev = n > 0 && !path && is_device_ptr(src);
-
-    if (validate && n > 0) {
-        std::vector<scl_event> tmp;
-        const scl_event* hv = src;
-        if (src_dev) { tmp.resize(n); CU(cudaMemcpy(tmp.data(), src, n * sizeof(scl_event), cudaMemcpyDeviceToHost)); hv = tmp.data(); }
-        for (uint32_t t = 0; t < n_traces; ++t) {
-            int64_t bad = validate_trace(hv + h_off[t], h_off[t + 1] - h_off[t]);
-            if (bad >= 0) return fail(SCL_ETRACE, "trace " + std::to_string(t) + " event " + std::to_string(bad) +
-                                                      ": free of a non-live pointer, size mismatch or live pointer reused");
-        }
-    }
+    if (validate) { scl_status st = validate_host(src, src_dev, h_off, n_traces); if (st != SCL_OK) return st; }
 
     scl_traces* tr = new scl_traces();
-    tr->device = device; tr->n_traces = n_traces; tr->n_sites = n_sites; tr->n_events = n; tr->tick_ns = tick;
-    tr->h_off = h_off;
-    auto cleanup = [&](scl_status st) { scl_traces_free(tr); return st; };
-
-    const uint64_t rows = (n + 7) / 8;
-    const uint64_t rows_alloc = rows > 0 ? rows : 1;
-    if (cudaMalloc(&tr->d_ev, rows_alloc * 128) != cudaSuccess) { cudaGetLastError(); return cleanup(fail(SCL_ENOMEM, "events")); }
-    if (n > 0 && cudaMemcpy(tr->d_ev, src, n * sizeof(scl_event), src_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice) != cudaSuccess)
-        return cleanup(fail(SCL_ECUDA, "event copy failed"));
-    if (rows_alloc * 8 > n && cudaMemset(tr->d_ev + n, 0, (rows_alloc * 8 - n) * sizeof(scl_event)) != cudaSuccess)
-        return cleanup(fail(SCL_ECUDA, "pad"));
-    if (cudaMalloc(&tr->d_off, h_off.size() * 8) != cudaSuccess) return cleanup(fail(SCL_ENOMEM, "offsets"));
-    if (cudaMemcpy(tr->d_off, h_off.data(), h_off.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) return cleanup(fail(SCL_ECUDA, "off copy"));
-
-    // per-trace sum |d| (sample capacity bound) and argument check, on the device
-    unsigned long long *d_sabs = nullptr, *d_err = nullptr;
-    if (cudaMalloc(&d_sabs, std::max<size_t>(n_traces, 1) * 8) != cudaSuccess || cudaMalloc(&d_err, 8) != cudaSuccess)
-        { cudaFree(d_sabs); return cleanup(fail(SCL_ENOMEM, "stats")); }
-    cudaMemset(d_err, 0xff, 8);
-    launch_load_stats(tr->d_ev, tr->d_off, n_traces, n_sites, d_sabs, d_err, 0);
-    unsigned long long err = 0;
-    tr->h_sabs.resize(n_traces);
-    cudaError_t ce = cudaMemcpy(&err, d_err, 8, cudaMemcpyDeviceToHost);
-    if (ce == cudaSuccess && n_traces) ce = cudaMemcpy(tr->h_sabs.data(), d_sabs, n_traces * 8, cudaMemcpyDeviceToHost);
-    cudaFree(d_sabs); cudaFree(d_err);
-    if (ce != cudaSuccess) return cleanup(fail(SCL_ECUDA, std::string("load stats: ") + cudaGetErrorString(ce)));
-    if (err != ~0ull) {
-        uint32_t t = (uint32_t)(std::upper_bound(h_off.begin(), h_off.end(), err) - h_off.begin()) - 1;
-        return cleanup(fail(SCL_EINVAL, "trace " + std::to_string(t) + " event " + std::to_string(err - h_off[t]) +
-                                        ": size 0, kind 3 or site >= n_sites"));
-    }
-
-    // segment plan: segment k of trace t covers rows (off_t/8) + 256k ... ; tickets ordered (k, t)
-    std::vector<uint32_t> nseg(n_traces), seg_base(n_traces);
-    uint32_t total = 0, maxk = 0;
-    for (uint32_t t = 0; t < n_traces; ++t) {
-        const uint64_t a = h_off[t], b = h_off[t + 1];
-        tr->max_len = std::max<uint64_t>(tr->max_len, b - a);
-        uint32_t ns = 0;
-        if (b > a) { uint64_t r = (b + 7) / 8 - a / 8; ns = (uint32_t)((r + kUnitRows - 1) / kUnitRows); }
-        nseg[t] = ns; seg_base[t] = total; total += ns; maxk = std::max(maxk, ns);
-    }
-    std::vector<TicketInfo> tk;
-    tk.reserve(total);
-    for (uint32_t k = 0; k < maxk; ++k)
-        for (uint32_t t = 0; t < n_traces; ++t)
-            if (k < nseg[t]) {
-                TicketInfo ti;
-                ti.off_t = (long long)h_off[t]; ti.n_t = (long long)(h_off[t + 1] - h_off[t]);
-                ti.t = t; ti.kraw = k | (k + 1 == nseg[t] ? 0x80000000u : 0u); ti.slot = seg_base[t] + k;
-                const uint64_t row_base = h_off[t] / 8 + (uint64_t)k * kUnitRows;
-                const uint64_t rows_left = (h_off[t + 1] + 7) / 8 - row_base;
-                ti.nbox = (unsigned)std::min<uint64_t>((rows_left + kThreads - 1) / kThreads, kSub);
-                tk.push_back(ti);
-            }
-    tr->n_segs = total;
-    const size_t nn = std::max<size_t>(total, 1);
-    if (cudaMalloc(&tr->d_tk, nn * sizeof(TicketInfo)) != cudaSuccess ||
-        cudaMalloc(&tr->d_urec, nn * replay_urec_bytes()) != cudaSuccess || cudaMalloc(&tr->d_uready, nn * 4) != cudaSuccess ||
-        cudaMalloc(&tr->d_tr_nseg, std::max<size_t>(n_traces, 1) * 4) != cudaSuccess ||
-        cudaMalloc(&tr->d_tr_base, std::max<size_t>(n_traces, 1) * 4) != cudaSuccess ||
-        cudaMalloc(&tr->d_run, std::max<size_t>(n_traces, 1) * sizeof(RunState)) != cudaSuccess ||
-        cudaMalloc(&tr->d_uent, nn * sizeof(UnitEntry)) != cudaSuccess ||
-        cudaMalloc(&tr->d_ticket, 4) != cudaSuccess)
-        { cudaGetLastError(); return cleanup(fail(SCL_ENOMEM, "segment plan")); }
-    if (total) cudaMemcpy(tr->d_tk, tk.data(), total * sizeof(TicketInfo), cudaMemcpyHostToDevice);
-    cudaMemset(tr->d_uready, 0, nn * 4);
-    {   // every trace needs a runner lane: n_traces <= grid * kRunners * 32
-        int grid = 0;
-        replay_occupancy(&grid);
-        if ((uint64_t)n_traces > (uint64_t)grid * kRunners * 32)
-            return cleanup(fail(SCL_EOVERFLOW, "too many traces for one launch (max " +
-                                std::to_string((uint64_t)grid * kRunners * 32) + "): load them in waves"));
-    }
-    if (n_traces) {
-        cudaMemcpy(tr->d_tr_nseg, nseg.data(), n_traces * 4, cudaMemcpyHostToDevice);
-        cudaMemcpy(tr->d_tr_base, seg_base.data(), n_traces * 4, cudaMemcpyHostToDevice);
-    }
-
-    // TMA descriptor: rows of 32 x u32 (128 B), box 32 x 256 rows, 128-B swizzle
-    auto enc = get_encode();
-    if (!enc) return cleanup(fail(SCL_ECUDA, "cuTensorMapEncodeTiled unavailable"));
-    cuuint64_t gdim[2] = {32, (cuuint64_t)rows_alloc};
-    cuuint64_t gstride[1] = {128};
-    cuuint32_t box[2] = {32, (cuuint32_t)kThreads};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult cr = enc(&tr->tmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, (void*)tr->d_ev, gdim, gstride, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (cr != CUDA_SUCCESS) return cleanup(fail(SCL_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr)));
-    if (cudaDeviceSynchronize() != cudaSuccess) return cleanup(fail(SCL_ECUDA, "load sync"));
+    tr->device = device; tr->tick_ns = tick;
+    scl_status st = upload(tr, src, src_dev, std::move(h_off), n_traces, n_sites, 0);
+    if (st != SCL_OK) { scl_traces_free(tr); return st; }
     *out = tr;
     return SCL_OK;
 }
 
+extern "C" scl_status scl_trace_reload(scl_traces* tr, const scl_event* events, const uint64_t* offsets,
+                                       uint32_t n_traces, uint32_t n_sites, int validate, void* cuda_stream)
+{
+    if (!tr || !offsets || (n_traces > 0 && !events)) return fail(SCL_EINVAL, "NULL argument");
+    if (n_sites == 0 || n_sites > (1u << 21)) return fail(SCL_EINVAL, "n_sites must be in 1..2^21");
+    CU(cudaSetDevice(tr->device));
+    std::vector<uint64_t> h_off;
+    scl_status st = read_offsets(offsets, n_traces, h_off);
+    if (st != SCL_OK) return st;
+    const uint64_t n = h_off[n_traces];
+    const bool src_dev = n > 0 && is_device_ptr(events);
+    if (validate) { st = validate_host(events, src_dev, h_off, n_traces); if (st != SCL_OK) return st; }
+    return upload(tr, events, src_dev, std::move(h_off), n_traces, n_sites, (cudaStream_t)cuda_stream);
+}
+
 extern "C" void scl_traces_free(scl_traces* t) {
     if (!t) return;
-    cudaFree(t->d_ev); cudaFree(t->d_off); cudaFree(t->d_tk); cudaFree(t->d_urec); cudaFree(t->d_uready);
+    cudaFree(t->d_ev); cudaFree(t->d_off); cudaFree(t->d_sabs); cudaFree(t->d_tk); cudaFree(t->d_urec); cudaFree(t->d_uready);
     cudaFree(t->d_tr_nseg); cudaFree(t->d_tr_base); cudaFree(t->d_run); cudaFree(t->d_uent); cudaFree(t->d_ticket);
+    cudaFree(t->d_err);
     delete t;
 }
 
@@ -292,20 +350,39 @@ extern "C" scl_status scl_traces_info(const scl_traces* t, uint64_t* n_events, u
 }
 
 // ---------------------------------------------------------------- run
+static void free_result_buffers(scl_result* r) {
+    cudaFree(r->d_table); cudaFree(r->d_sbase); cudaFree(r->d_summ); cudaFree(r->d_prob); cudaFree(r->d_rate);
+    cudaFree(r->d_flag); cudaFree(r->d_key); cudaFree(r->d_key2); cudaFree(r->d_val); cudaFree(r->d_order);
+    cudaFree(r->d_cub); cudaFree(r->d_rows);
+    r->d_table = nullptr; r->d_sbase = nullptr; r->d_summ = nullptr; r->d_prob = nullptr; r->d_rate = nullptr;
+    r->d_flag = nullptr; r->d_key = nullptr; r->d_key2 = nullptr; r->d_val = nullptr; r->d_order = nullptr;
+    r->d_cub = nullptr; r->d_rows = nullptr;
+    r->cap_sites = 0; r->cap_tr = 0;
+}
+
 extern "C" void scl_result_free(scl_result* r) {
     if (!r) return;
-    cudaFree(r->d_table); cudaFree(r->d_samples); cudaFree(r->d_epflag); cudaFree(r->d_sbase);
-    cudaFree(r->d_summ); cudaFree(r->d_prob); cudaFree(r->d_rate); cudaFree(r->d_flag);
-    cudaFree(r->d_prof); cudaFree(r->d_key); cudaFree(r->d_key2); cudaFree(r->d_val); cudaFree(r->d_order); cudaFree(r->d_cub); cudaFree(r->d_rows);
+    free_result_buffers(r);
+    cudaFree(r->d_samples); cudaFree(r->d_epflag); cudaFree(r->d_prof);
+    if (r->h_gate) cudaFreeHost(r->h_gate);
     for (auto& e : r->ev) if (e) cudaEventDestroy(e);
+    for (auto& e : r->kev) if (e) cudaEventDestroy(e);
     delete r;
 }
 
+// Per-site and per-trace buffers, sized for the handle (re-sized when a reloaded handle outgrows them).
 static scl_status alloc_result(scl_result* r, const scl_traces* tr) {
     const size_t S = tr->n_sites, nt = std::max<uint32_t>(tr->n_traces, 1);
-    int grid = 0;
-    replay_occupancy(&grid);
-    r->grid = grid;
+    if (!r->ev[0]) {
+        for (auto& e : r->ev) CU(cudaEventCreate(&e));
+        for (auto& e : r->kev) CU(cudaEventCreate(&e));
+        CU(cudaMallocHost(&r->h_gate, 32));
+        int grid = 0;
+        replay_occupancy(&grid);
+        r->grid = grid;
+    }
+    if (S <= r->cap_sites && nt <= r->cap_tr) return SCL_OK;
+    free_result_buffers(r);
     CU(cudaMalloc(&r->d_table, (S * SCL_NCOL + 3) * 8));
     CU(cudaMalloc(&r->d_sbase, nt * 8));
     CU(cudaMalloc(&r->d_summ, nt * sizeof(scl_trace_summary)));
@@ -317,8 +394,7 @@ static scl_status alloc_result(scl_result* r, const scl_traces* tr) {
     cub::DeviceRadixSort::SortPairs(nullptr, tb, r->d_key, r->d_key2, r->d_val, r->d_order, (int)S);
     r->cub_bytes = std::max<size_t>(tb, 1);
     CU(cudaMalloc(&r->d_cub, r->cub_bytes));
-    for (auto& e : r->ev) CU(cudaEventCreate(&e));
-    r->h_sbase.resize(nt + 1);
+    r->cap_sites = S; r->cap_tr = nt;
     return SCL_OK;
 }
 
@@ -336,12 +412,11 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
 
     scl_result* r = *out;
     const bool fresh = (r == nullptr);
-    if (fresh) {
-        r = new scl_result();
+    if (fresh) r = new scl_result();
+    else if (r->tr != tr) return fail(SCL_EINVAL, "*out is a result of another traces handle");
+    {
         scl_status s2 = alloc_result(r, tr);
-        if (s2 != SCL_OK) { scl_result_free(r); return s2; }
-    } else if (r->tr != tr) {
-        return fail(SCL_EINVAL, "*out is a result of another traces handle");
+        if (s2 != SCL_OK) { if (fresh) scl_result_free(r); return s2; }
     }
     r->tr = tr; r->T = threshold; r->formula = o.formula; r->stream = st;
     const uint64_t tick = o.tick_ns ? o.tick_ns : tr->tick_ns;
@@ -349,8 +424,10 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
     r->summ_valid = false; r->finalized = false;
 
     // sample capacity per trace: min(n_t, floor(sum|d| / T)) -- every sample consumes |net| >= T
+    // (prep_kernel computes the same bases on the device; the host copy serves scl_samples)
     const uint32_t NT = tr->n_traces;
     unsigned long long tot = 0;
+    r->h_sbase.resize((size_t)NT + 1);
     for (uint32_t t = 0; t < NT; ++t) {
         r->h_sbase[t] = tot;
         tot += std::min<uint64_t>(tr->h_off[t + 1] - tr->h_off[t], tr->h_sabs[t] / threshold);
@@ -358,7 +435,7 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
     r->h_sbase[NT] = tot;
     if (tot > r->cap || !r->d_samples) {
         cudaFree(r->d_samples); cudaFree(r->d_epflag);
-        r->d_samples = nullptr; r->d_epflag = nullptr;
+        r->d_samples = nullptr; r->d_epflag = nullptr; r->cap = 0;
         const size_t c = std::max<size_t>(tot, 1);
         if (cudaMalloc(&r->d_samples, c * sizeof(scl_sample)) != cudaSuccess ||
             cudaMalloc(&r->d_epflag, c * 4) != cudaSuccess) { cudaGetLastError(); if (fresh) scl_result_free(r); return fail(SCL_ENOMEM, "samples"); }
@@ -366,15 +443,17 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
     }
 
     // epoch-tagged look-back flags: no per-run clear of the state array
-    if (tr->epoch >= (1u << 30)) { CU(cudaMemsetAsync(tr->d_uready, 0, (size_t)std::max<uint32_t>(tr->n_segs, 1) * 4, st)); tr->epoch = 0; }
+    if (tr->epoch >= (1u << 30)) { CU(cudaMemsetAsync(tr->d_uready, 0, tr->cap_segs * 4, st)); tr->epoch = 0; }
     tr->epoch += 1;
 
     CU(cudaEventRecord(r->ev[0], st));
-    CU(cudaMemcpyAsync(r->d_sbase, r->h_sbase.data(), (size_t)std::max<uint32_t>(NT, 1) * 8, cudaMemcpyHostToDevice, st));
-    CU(cudaMemsetAsync(r->d_table, 0, ((size_t)tr->n_sites * SCL_NCOL + 3) * 8, st));
-    CU(cudaMemsetAsync(r->d_summ, 0, (size_t)std::max<uint32_t>(NT, 1) * sizeof(scl_trace_summary), st));
-    CU(cudaMemsetAsync(tr->d_ticket, 0, 4, st));
-    CU(cudaMemsetAsync(tr->d_run, 0, (size_t)std::max<uint32_t>(NT, 1) * sizeof(RunState), st));
+    PrepParams pp{};
+    pp.table = r->d_table; pp.table_words = (size_t)tr->n_sites * SCL_NCOL + 3;
+    pp.summ = reinterpret_cast<unsigned long long*>(r->d_summ); pp.summ_words = (size_t)NT * sizeof(scl_trace_summary) / 8;
+    pp.run = reinterpret_cast<unsigned long long*>(tr->d_run); pp.run_words = (size_t)NT * sizeof(RunState) / 8;
+    pp.ticket = tr->d_ticket; pp.sbase = r->d_sbase; pp.off = tr->d_off; pp.sabs = tr->d_sabs;
+    pp.n_traces = NT; pp.T = threshold;
+    CU(launch_prep(pp, st));
 
     ReplayParams p{};
     p.ev = tr->d_ev; p.off = tr->d_off; p.tk = tr->d_tk;
@@ -384,13 +463,15 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
     p.table = r->d_table; p.samples = r->d_samples; p.ep_flag = r->d_epflag; p.sbase = r->d_sbase;
     p.summ = r->d_summ; p.uent = tr->d_uent;
 #ifdef SCL_PROFILE
-    if (!r->d_prof) CU(cudaMalloc(&r->d_prof, (48 + 4 * (size_t)tr->n_segs) * 8));
+    if (!r->d_prof) CU(cudaMalloc(&r->d_prof, (48 + 4 * (size_t)tr->cap_segs) * 8));
     CU(cudaMemsetAsync(r->d_prof, 0, (48 + 4 * (size_t)tr->n_segs) * 8, st));
     p.prof = r->d_prof;
 #endif
-    CU(cudaEventRecord(r->ev[4], st));
+    const int ks = (int)(r->nrun % kRing);
+    CU(cudaEventRecord(r->kev[2 * ks], st));
     CU(launch_replay(&tr->tmap, p, r->grid, st));
-    CU(cudaEventRecord(r->ev[5], st));
+    CU(cudaEventRecord(r->kev[2 * ks + 1], st));
+    r->nrun += 1;
     CU(launch_reclaim(p, st));
     CU(launch_samples(p, st));
     CU(cudaEventRecord(r->ev[1], st));
@@ -398,10 +479,6 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
     if (!o.defer_finalize) {
         scl_status s3 = scl_finalize(r, 0);
         if (s3 != SCL_OK) return s3;
-    } else {
-        CU(cudaStreamSynchronize(st));
-        cudaEventElapsedTime(&r->run_ms, r->ev[0], r->ev[1]);
-        cudaEventElapsedTime(&r->kern_ms, r->ev[4], r->ev[5]);
     }
     return SCL_OK;
 }
@@ -429,25 +506,22 @@ extern "C" scl_status scl_finalize(scl_result* r, uint64_t elapsed_ns) {
     size_t tb = r->cub_bytes;
     CU(cub::DeviceRadixSort::SortPairs(r->d_cub, tb, r->d_key, r->d_key2, r->d_val, r->d_order, (int)S, 0, 64, st));
     CU(launch_rows(r->d_table, r->d_prob, r->d_rate, r->d_flag, r->d_order, S, r->d_rows, st));
-    unsigned long long g[3];
-    CU(cudaMemcpyAsync(g, r->d_table + (size_t)S * SCL_NCOL, 24, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(r->h_gate, r->d_table + (size_t)S * SCL_NCOL, 24, cudaMemcpyDeviceToHost, st));
     CU(cudaEventRecord(r->ev[3], st));
-    CU(cudaStreamSynchronize(st));
-    r->gate_num = (long long)g[0]; r->gate_den = (long long)g[1]; r->gate_cnt = g[2];
-    cudaEventElapsedTime(&r->run_ms, r->ev[0], r->ev[1]);
-    cudaEventElapsedTime(&r->kern_ms, r->ev[4], r->ev[5]);
-    cudaEventElapsedTime(&r->fin_ms, r->ev[2], r->ev[3]);
     r->finalized = true;
     return SCL_OK;
 }
 
-// ---------------------------------------------------------------- accessors
+// ---------------------------------------------------------------- accessors (wait for the run)
 static scl_status ensure_summ(const scl_result* rc) {
     scl_result* r = const_cast<scl_result*>(rc);
     if (r->summ_valid) return SCL_OK;
     const uint32_t NT = r->tr->n_traces;
     r->h_summ.resize(NT);
-    if (NT) CU(cudaMemcpy(r->h_summ.data(), r->d_summ, NT * sizeof(scl_trace_summary), cudaMemcpyDeviceToHost));
+    if (NT) {
+        CU(cudaMemcpyAsync(r->h_summ.data(), r->d_summ, NT * sizeof(scl_trace_summary), cudaMemcpyDeviceToHost, r->stream));
+        CU(cudaStreamSynchronize(r->stream));
+    }
     r->summ_valid = true;
     return SCL_OK;
 }
@@ -460,7 +534,8 @@ extern "C" scl_status scl_site_report(const scl_result* r, scl_site_row* rows, s
     if (cap == 0) return SCL_OK;
     if (!rows) return fail(SCL_EINVAL, "rows is NULL");
     CU(cudaSetDevice(r->tr->device));
-    CU(cudaMemcpy(rows, r->d_rows, std::min(cap, S) * sizeof(scl_site_row), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyAsync(rows, r->d_rows, std::min(cap, S) * sizeof(scl_site_row), cudaMemcpyDeviceToHost, r->stream));
+    CU(cudaStreamSynchronize(r->stream));
     return SCL_OK;
 }
 
@@ -474,7 +549,9 @@ extern "C" scl_status scl_samples(const scl_result* r, uint32_t trace, scl_sampl
     *n = cnt;
     if (cap == 0 || cnt == 0) return SCL_OK;
     if (!out) return fail(SCL_EINVAL, "out is NULL");
-    CU(cudaMemcpy(out, r->d_samples + r->h_sbase[trace], std::min(cap, cnt) * sizeof(scl_sample), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyAsync(out, r->d_samples + r->h_sbase[trace], std::min(cap, cnt) * sizeof(scl_sample),
+                       cudaMemcpyDeviceToHost, r->stream));
+    CU(cudaStreamSynchronize(r->stream));
     return SCL_OK;
 }
 
@@ -493,17 +570,45 @@ extern "C" scl_status scl_trace_summaries(const scl_result* r, scl_trace_summary
 extern "C" scl_status scl_gate(const scl_result* r, int64_t* num, int64_t* den, int* open) {
     if (!r) return fail(SCL_EINVAL, "NULL result");
     if (!r->finalized) return fail(SCL_EINVAL, "result not finalized");
-    if (num) *num = r->gate_num;
-    if (den) *den = r->gate_den;
-    if (open) *open = r->gate_cnt > 0 && (__int128)100 * (__int128)r->gate_num >= (__int128)r->gate_den;
+    CU(cudaEventSynchronize(r->ev[3]));
+    const long long gn = (long long)r->h_gate[0], gd = (long long)r->h_gate[1];
+    if (num) *num = gn;
+    if (den) *den = gd;
+    if (open) *open = r->h_gate[2] > 0 && (__int128)100 * (__int128)gn >= (__int128)gd;
     return SCL_OK;
 }
 
 extern "C" scl_status scl_result_timing(const scl_result* r, float* replay_kernel_ms, float* run_ms, float* finalize_ms) {
     if (!r) return fail(SCL_EINVAL, "NULL result");
-    if (replay_kernel_ms) *replay_kernel_ms = r->kern_ms;
-    if (run_ms) *run_ms = r->run_ms;
-    if (finalize_ms) *finalize_ms = r->fin_ms;
+    CU(cudaEventSynchronize(r->finalized ? r->ev[3] : r->ev[1]));
+    float k = 0, a = 0, f = 0;
+    if (r->nrun) {
+        const int ks = (int)((r->nrun - 1) % kRing);
+        CU(cudaEventElapsedTime(&k, r->kev[2 * ks], r->kev[2 * ks + 1]));
+    }
+    CU(cudaEventElapsedTime(&a, r->ev[0], r->ev[1]));
+    if (r->finalized) CU(cudaEventElapsedTime(&f, r->ev[2], r->ev[3]));
+    if (replay_kernel_ms) *replay_kernel_ms = k;
+    if (run_ms) *run_ms = a;
+    if (finalize_ms) *finalize_ms = f;
+    return SCL_OK;
+}
+
+extern "C" scl_status scl_result_kernel_times(const scl_result* rc, float* ms, size_t cap, size_t* n) {
+    if (!rc || !n) return fail(SCL_EINVAL, "NULL argument");
+    scl_result* r = const_cast<scl_result*>(rc);
+    const uint64_t avail = std::min<uint64_t>(r->nrun - r->nread, kRing);
+    const uint64_t cnt = std::min<uint64_t>(avail, cap);
+    *n = (size_t)cnt;
+    if (cnt == 0) return SCL_OK;
+    if (!ms) return fail(SCL_EINVAL, "ms is NULL");
+    const uint64_t first = r->nrun - avail;
+    for (uint64_t i = 0; i < cnt; ++i) {
+        const int ks = (int)((first + i) % kRing);
+        CU(cudaEventSynchronize(r->kev[2 * ks + 1]));
+        CU(cudaEventElapsedTime(&ms[i], r->kev[2 * ks], r->kev[2 * ks + 1]));
+    }
+    r->nread = r->nrun;
     return SCL_OK;
 }
 

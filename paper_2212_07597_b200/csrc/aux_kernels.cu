@@ -5,38 +5,91 @@
 //   rows_kernel        report rows in report order
 #include "scl_internal.cuh"
 #include "ptx.cuh"
+#include <algorithm>
 
 namespace scl {
 
 // ============================================================================ load statistics
-// Per trace: sum |d| over alloc/free events (the sample-capacity bound
-// floor(sum|d|/T)), and the first invalid event (size 0, kind 3, site >= n_sites).
+// Per trace: sum |d| over alloc/free events (the sample-capacity bound floor(sum|d|/T)), and
+// the first invalid event (size 0, kind 3, site >= n_sites).  One warp per 256-event chunk
+// (grid-stride, 8 events = one 128-B row per lane); a chunk inside one trace is reduced in the
+// warp before its single atomic.
 __global__ void __launch_bounds__(256) load_stats_kernel(const scl_event* ev, const unsigned long long* off,
-                                                         unsigned n_traces, unsigned n_sites,
-                                                         unsigned long long* sabs, unsigned long long* err)
+                                                         unsigned n_traces, unsigned long long n_events,
+                                                         unsigned n_sites, unsigned long long* sabs,
+                                                         unsigned long long* err)
 {
-    __shared__ unsigned long long red[8];
-    for (unsigned t = blockIdx.x; t < n_traces; t += gridDim.x) {
-        const unsigned long long b = off[t], e = off[t + 1];
+    const int lane = threadIdx.x & 31;
+    const unsigned long long wid = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned long long nw = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    for (unsigned long long base = wid * 256; base < n_events; base += nw * 256) {
+        const unsigned long long i0 = base + (unsigned long long)lane * 8;
+        // trace of event i0: last t with off[t] <= i0 (traces may be empty)
+        unsigned lo = 0, hi = n_traces;                      // invariant: off[lo] <= i0 < off[hi]
+        while (hi - lo > 1) { const unsigned mid = (lo + hi) >> 1; if (off[mid] <= i0) lo = mid; else hi = mid; }
+        unsigned t = lo;
+        unsigned long long tend = off[t + 1];
+        const ulonglong2* q = reinterpret_cast<const ulonglong2*>(ev + i0);
+        ulonglong2 v[8];
+        #pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = i0 + j < n_events ? __ldcs(q + j) : make_ulonglong2(0, 0);
         unsigned long long acc = 0;
-        for (unsigned long long i = b + threadIdx.x; i < e; i += blockDim.x) {
-            const unsigned long long m = ev[i].meta;
+        bool split = false;
+        #pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const unsigned long long i = i0 + j;
+            if (i >= n_events) break;
+            while (i >= tend) {                             // trace boundary inside this lane's row
+                if (acc) atomicAdd(&sabs[t], acc);
+                acc = 0; split = true; ++t; tend = off[t + 1];
+            }
+            const unsigned long long m = v[j].y;
             const unsigned kind = ev_kind(m);
             const unsigned long long sz = ev_size(m);
             if (kind == 3 || ev_site(m) >= n_sites || (kind < 2 && sz == 0)) atomicMin(err, i);
             if (kind < 2) acc += sz;
         }
-        #pragma unroll
-        for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(kFull, acc, d);
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            unsigned long long tot = 0;
-            for (int w = 0; w < 8; ++w) tot += red[w];
-            sabs[t] = tot;
+        const unsigned t_lane0 = __shfl_sync(kFull, t, 0);  // every lane shuffles (never inside a short circuit)
+        const bool uni = __all_sync(kFull, !split && t == t_lane0);
+        if (uni) {
+            #pragma unroll
+            for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(kFull, acc, d);
+            if (lane == 0 && acc) atomicAdd(&sabs[t], acc);
+        } else if (acc) {
+            atomicAdd(&sabs[t], acc);
         }
+    }
+}
+
+// ============================================================================ per-run preparation
+__global__ void __launch_bounds__(1024) prep_kernel(const __grid_constant__ PrepParams p)
+{
+    const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = tid; i < p.table_words; i += nth) p.table[i] = 0;
+    for (size_t i = tid; i < p.summ_words; i += nth) p.summ[i] = 0;
+    for (size_t i = tid; i < p.run_words; i += nth) p.run[i] = 0;
+    if (tid == 0) *p.ticket = 0;
+    if (blockIdx.x != 0) return;
+    // block 0: exclusive scan of the per-trace sample capacities (thread j: a contiguous run of traces)
+    __shared__ unsigned long long part[1024];
+    const unsigned per = (p.n_traces + blockDim.x - 1) / blockDim.x;
+    const unsigned t0 = threadIdx.x * per, t1 = min(p.n_traces, t0 + per);
+    auto cap = [&](unsigned t) {
+        const unsigned long long n = p.off[t + 1] - p.off[t], b = p.sabs[t] / p.T;
+        return n < b ? n : b;
+    };
+    unsigned long long acc = 0;
+    for (unsigned t = t0; t < t1; ++t) acc += cap(t);
+    part[threadIdx.x] = acc;
+    __syncthreads();
+    for (unsigned d = 1; d < blockDim.x; d <<= 1) {          // Hillis-Steele inclusive scan
+        const unsigned long long v = threadIdx.x >= d ? part[threadIdx.x - d] : 0;
+        __syncthreads();
+        part[threadIdx.x] += v;
         __syncthreads();
     }
+    unsigned long long base = part[threadIdx.x] - acc;
+    for (unsigned t = t0; t < t1; ++t) { p.sbase[t] = base; base += cap(t); }
 }
 
 // ============================================================================ per-sample reduce
@@ -119,11 +172,22 @@ __global__ void __launch_bounds__(256) rows_kernel(const unsigned long long* tab
 
 // ============================================================================ launch wrappers
 cudaError_t launch_load_stats(const scl_event* ev, const unsigned long long* off, unsigned n_traces,
-                              unsigned n_sites, unsigned long long* sabs, unsigned long long* err, cudaStream_t st)
+                              unsigned long long n_events, unsigned n_sites, unsigned long long* sabs,
+                              unsigned long long* err, cudaStream_t st)
 {
-    if (n_traces == 0) return cudaSuccess;
-    unsigned grid = n_traces < 4096 ? n_traces : 4096;
-    load_stats_kernel<<<grid, 256, 0, st>>>(ev, off, n_traces, n_sites, sabs, err);
+    if (n_traces == 0 || n_events == 0) return cudaSuccess;
+    const unsigned long long warps = (n_events + 255) / 256;
+    const unsigned blocks = (unsigned)std::min<unsigned long long>((warps + 7) / 8, 148ull * 8);
+    load_stats_kernel<<<blocks, 256, 0, st>>>(ev, off, n_traces, n_events, n_sites, sabs, err);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prep(const PrepParams& p, cudaStream_t st)
+{
+    size_t words = p.table_words > p.summ_words ? p.table_words : p.summ_words;
+    words = words > p.run_words ? words : p.run_words;
+    unsigned blocks = (unsigned)std::min<size_t>((words + 1023) / 1024, 148);
+    prep_kernel<<<blocks ? blocks : 1, 1024, 0, st>>>(p);
     return cudaGetLastError();
 }
 

@@ -319,24 +319,6 @@ __device__ __forceinline__ void store_rstate(RunState* rs, const RState& x, int 
     if (lane == 0) { rs->F = x.F; rs->M = x.M; rs->B = x.B; rs->n = x.n; rs->nep = x.nep; rs->ep1 = x.ep1; rs->next = x.next; }
 }
 
-// Exact check of chunk c of a unit: is there a free of `ptr` at unit positions [sbeg, send)?
-__device__ __forceinline__ bool chunk_has_free(const ReplayParams& p, const SegInfo& inf, int c, unsigned long long ptr,
-                                               unsigned sbeg, unsigned send, int lane) {
-    const long long row = inf.row_base + (long long)c * 32 + lane;
-    unsigned long long rp[kEpt], rm[kEpt];
-    load_row_global(p.ev, row, rp, rm);
-    const long long e0 = row * kEpt - inf.off_t;
-    const unsigned pos0 = (unsigned)(c * 32 + lane) * kEpt;
-    bool hit = false;
-    #pragma unroll
-    for (int jj = 0; jj < kEpt; ++jj) {
-        const long long ie = e0 + jj;
-        const unsigned pos = pos0 + jj;
-        hit |= pos >= sbeg && pos < send && ie >= 0 && ie < inf.n_t && ev_kind(rm[jj]) == 1 && rp[jj] == ptr;
-    }
-    return __any_sync(kFull, hit);
-}
-
 // A unit in which a sample fires: resolve it chunk by chunk (a3).  x: state before the unit
 // -> state after it.
 __device__ void resolve_unit(const ReplayParams& p, const Slot& S, RState& x, int lane)
@@ -646,10 +628,32 @@ __global__ void __launch_bounds__(256) reclaim_kernel(const __grid_constant__ Re
         const bool pos = cb < send && cb + 32 * kEpt > sbeg && (S.bloom[lane][w] & msk) == msk;
         unsigned cm = __ballot_sync(kFull, pos);
         bool found = false;
-        while (cm && !found) {
-            const int c = __ffs(cm) - 1;
-            cm &= cm - 1;
-            found = chunk_has_free(p, inf, c, ptr, sbeg, send, lane);
+        while (cm && !found) {                               // exact re-check, 4 positive chunks at a time:
+            int cs[4];                                       // pointer words first (32 loads in flight per lane),
+            #pragma unroll                                   // the meta word only where the pointer matches
+            for (int k = 0; k < 4; ++k) { cs[k] = cm ? __ffs(cm) - 1 : -1; cm &= cm ? cm - 1 : 0u; }
+            unsigned long long pv[4][kEpt];
+            #pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const long long row = inf.row_base + (long long)(cs[k] < 0 ? cs[0] : cs[k]) * 32 + lane;
+                #pragma unroll
+                for (int jj = 0; jj < kEpt; ++jj) pv[k][jj] = __ldcg(&p.ev[row * kEpt + jj].ptr);
+            }
+            bool hit = false;
+            #pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (cs[k] < 0) continue;
+                const long long row = inf.row_base + (long long)cs[k] * 32 + lane;
+                const unsigned pos0 = (unsigned)(cs[k] * 32 + lane) * kEpt;
+                #pragma unroll
+                for (int jj = 0; jj < kEpt; ++jj) {
+                    const long long ie = row * kEpt + jj - inf.off_t;
+                    const unsigned q = pos0 + jj;
+                    if (pv[k][jj] == ptr && q >= sbeg && q < send && ie >= 0 && ie < inf.n_t)
+                        hit |= ev_kind(__ldcg(&p.ev[row * kEpt + jj].meta)) == 1;
+                }
+            }
+            found = __any_sync(kFull, hit);
         }
         if (found && lane == 0) p.ep_flag[ep1 - 1] = 1u;
     };

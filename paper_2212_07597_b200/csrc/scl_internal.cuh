@@ -96,11 +96,27 @@ struct FinalParams {
     unsigned long long* key1; unsigned int* val;   // sort inputs
 };
 
+// Per-run preparation (one launch instead of memsets + a host copy): zero the site table,
+// the trace summaries, the runner states and the ticket counter; sample slot bases
+// sbase[t] = sum_{t'<t} min(n_t', floor(sum|d|_t' / T)) (the host computes the same bound).
+struct PrepParams {
+    unsigned long long* table; size_t table_words;
+    unsigned long long* summ; size_t summ_words;
+    unsigned long long* run; size_t run_words;
+    unsigned int* ticket;
+    unsigned long long* sbase;        // [n_traces]
+    const unsigned long long* off;    // [n_traces + 1]
+    const unsigned long long* sabs;   // [n_traces]
+    unsigned int n_traces;
+    unsigned long long T;
+};
+
 // launch wrappers (replay.cu)
 cudaError_t launch_load_stats(const scl_event* ev, const unsigned long long* off, unsigned n_traces,
-                              unsigned n_sites, unsigned long long* sabs, unsigned long long* err,
-                              cudaStream_t st);
+                              unsigned long long n_events, unsigned n_sites, unsigned long long* sabs,
+                              unsigned long long* err, cudaStream_t st);
 cudaError_t launch_replay(const CUtensorMap* tmap, const ReplayParams& p, int grid, cudaStream_t st);
+cudaError_t launch_prep(const PrepParams& p, cudaStream_t st);
 cudaError_t launch_reclaim(const ReplayParams& p, cudaStream_t st);
 cudaError_t launch_samples(const ReplayParams& p, cudaStream_t st);
 cudaError_t launch_finalize(const FinalParams& p, cudaStream_t st);

@@ -191,3 +191,38 @@ def test_defer_finalize_table_sum():
     assert np.array_equal(rows["leak_flag"], ref["flag"][ref["order"]].astype(np.uint32))
     assert np.array_equal(rows["leak_prob"], ref["prob"][ref["order"]])
     assert scl.scl_gate(ra) == ref["gate"]
+
+
+def test_reload_grow_shrink_and_kernel_times():
+    """scl_trace_reload: one handle refilled with larger, smaller and different-site traces
+    (buffers grown and reused, results re-sized), each run checked against the oracle; the
+    timing ring returns one replay-kernel duration per run enqueued."""
+    rng = np.random.default_rng(11)
+    batches = []
+    for n_tr, n_sites in ((5, 37), (40, 37), (3, 1500), (64, 9)):
+        traces = [tracegen.random_small_trace(rng, int(rng.integers(0, 30000)), n_sites=n_sites,
+                                              max_size=int(rng.integers(1, 5000)), max_ptrs=30) for _ in range(n_tr)]
+        batches.append((_concat(traces), n_sites))
+    (ev0, off0), s0 = batches[0]
+    tr = scl.scl_trace_load(ev0, off0, s0)
+    r = None
+    for (ev, off), n_sites in batches + batches[:1]:
+        scl.scl_trace_reload(tr, ev, off, n_sites)
+        assert (tr.n_traces, tr.n_sites) == (len(off) - 1, n_sites)
+        for T in (97, 4001):
+            r = scl.scl_replay_run(T, tr, out=r)
+            compare(ev, off, n_sites, T, r)
+    assert len(scl.scl_result_kernel_times(r)) == 2 * (len(batches) + 1)
+    for _ in range(3):
+        r = scl.scl_replay_run(97, tr, out=r)
+    ks = scl.scl_result_kernel_times(r)
+    assert len(ks) == 3 and all(k > 0 for k in ks)
+    assert scl.scl_result_kernel_times(r) == []
+    # a bad event leaves the handle empty, a good reload restores it
+    bad = tracegen.from_tuples([("a", 1, 8, 99)])
+    with pytest.raises(scl.SclError):
+        scl.scl_trace_reload(tr, bad, np.array([0, 1], dtype=np.uint64), 2)
+    (ev, off), n_sites = batches[1]
+    scl.scl_trace_reload(tr, ev, off, n_sites)
+    r = scl.scl_replay_run(97, tr, out=r)
+    compare(ev, off, n_sites, 97, r)
