@@ -42,7 +42,20 @@ __device__ __forceinline__ void named_bar(int id, int threads) {
     asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(threads) : "memory");
 }
 
-// Predicated shared-memory reductions / atomics (no divergent branch around them).
+// Unconditional shared-memory reductions / atomics on a 32-bit shared address.
+__device__ __forceinline__ void red_add(uint32_t addr, unsigned v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" :: "r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_or(uint32_t addr, unsigned v) {
+    asm volatile("red.shared.or.b32 [%0], %1;" :: "r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned atom_add(uint32_t addr, unsigned v) {
+    unsigned old;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
+    return old;
+}
+
+// Predicated shared-memory reductions / atomics (ptxas may still branch around them).
 __device__ __forceinline__ void red_add_if(uint32_t addr, unsigned v, bool c) {
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.shared.add.u32 [%0], %1;\n}"
                  :: "r"(addr), "r"(v), "r"((unsigned)c) : "memory");

@@ -48,6 +48,7 @@ struct __align__(16) Smem {
     unsigned cnt[2 * kHot];          // Tier-E per (kind, hot site): event count
     unsigned blo[2 * kHot];          //   bytes, low 32 bits
     unsigned bhi[2 * kHot];          //   carries out of blo
+    unsigned dummy[kComputeWarps * 32];   // per-lane sink of the unconditional atomics (never read)
     Slot slot[kSlots];
     SegInfo info[kStages];
     unsigned sub[kStages];           // box index within the unit
@@ -63,13 +64,14 @@ size_t replay_smem_bytes() { return 1024 + (size_t)kStages * kSegBytes + sizeof(
 
 // Blocked Bloom filter of freed pointers, 64 words (2048 bits) per 256-event chunk: one
 // word per pointer, two bits in it (one shared-memory OR per free; ~1.4 % false positives
-// at ~128 frees per chunk).
-__device__ __forceinline__ unsigned bloom_word(unsigned long long ptr) {
-    return ((unsigned)(ptr >> 4) * 0x9E3779B1u) >> 26;
+// at ~128 frees per chunk).  One multiply: word = bits 26..31, bits = 21..25 and 16..20.
+__device__ __forceinline__ unsigned bloom_hash(unsigned long long ptr) {
+    return (unsigned)(ptr >> 4) * 0x9E3779B1u;
 }
+__device__ __forceinline__ unsigned bloom_word(unsigned long long ptr) { return bloom_hash(ptr) >> 26; }
 __device__ __forceinline__ unsigned bloom_mask(unsigned long long ptr) {
-    const unsigned h = (unsigned)(ptr >> 4) * 0x85EBCA77u;
-    return (1u << (h >> 27)) | (1u << ((h >> 22) & 31u));
+    const unsigned h = bloom_hash(ptr);
+    return (1u << ((h >> 21) & 31u)) | (1u << ((h >> 16) & 31u));
 }
 
 // Optional per-role cycle accounting (debug build with -DSCL_PROFILE only).
@@ -100,7 +102,8 @@ __device__ __forceinline__ void load_row_global(const scl_event* ev, long long r
 // warp w8 of a group takes rows 32*w8 .. 32*w8+31 of its box = chunk g*8 + w8 of the unit.
 __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stage, int grp, int w8, int lane)
 {
-    const uint32_t cnt_s = smem_u32(s.cnt), blo_s = smem_u32(s.blo), bhi_s = smem_u32(s.bhi);
+    const uint32_t cnt_s = smem_u32(s.cnt), blo_s = smem_u32(s.blo);
+    const uint32_t dum_s = smem_u32(&s.dummy[(grp * 8 + w8) * 32 + lane]);   // this lane's sink word
     PROF_DECL
     for (unsigned it = grp;; it += 2) {
         const int st = it % kStages;
@@ -146,28 +149,37 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
             unsigned cold = 0;                                // events for the L2 (cold site) path
             if (e0 >= 0 && e0 + kEpt <= inf.n_t && big == 0) {
                 // fast path: the whole row is in the trace and |partial sums| < 2^30: 32-bit running
-                // sum / max / min (a copy's d = 0 repeats an F already seen: harmless), predicated
-                // shared atomics issued back to back, carries checked after all of them
-                unsigned old[kEpt];
+                // sum / max / min (a copy's d = 0 repeats an F already seen: harmless).  Every shared
+                // atomic is unconditional (no branch around it): an event that does not count goes
+                // to the lane's dummy word instead; 32-bit byte-counter carries are checked after.
+                unsigned old[kEpt], carry = 0;
                 #pragma unroll
                 for (int j = 0; j < kEpt; ++j) {
                     const unsigned hi = (unsigned)(meta[j] >> 32), lo = (unsigned)meta[j];
                     const unsigned kind = (hi >> 8) & 3u, site = hi >> 11;
-                    r32 += kind == 0 ? (int)lo : (kind == 1 ? -(int)lo : 0);          // a1: signed size
+                    const int d = kind == 1 ? -(int)lo : (int)lo;
+                    r32 += kind < 2 ? d : 0;                                              // a1: signed size
                     mx32 = max(mx32, r32); mn32 = min(mn32, r32);
                     const bool h = kind < 2 && site < (unsigned)kHot;
                     cold |= (kind < 2 && !h ? 1u : 0u) << j;
-                    const uint32_t x = ((kind & 1u) * kHot + (h ? site : 0u)) * 4u;
-                    red_add_if(cnt_s + x, 1u, h);                                     // a5 Tier E
-                    old[j] = atom_add_if(blo_s + x, lo, h);
-                    red_or_if(bl_s + bloom_word(ptr[j]) * 4u, bloom_mask(ptr[j]), kind == 1);   // freed ptr -> Bloom
+                    const uint32_t x = ((kind & 1u) * kHot + site) * 4u;                  // (kind, site) slot
+                    red_add(h ? cnt_s + x : dum_s, 1u);                                   // a5 Tier E
+                    old[j] = atom_add(h ? blo_s + x : dum_s, lo);
+                    red_or(kind == 1 ? bl_s + bloom_word(ptr[j]) * 4u : dum_s, bloom_mask(ptr[j]));   // freed ptr -> Bloom
                 }
                 #pragma unroll
                 for (int j = 0; j < kEpt; ++j) {
                     const unsigned hi = (unsigned)(meta[j] >> 32), lo = (unsigned)meta[j];
                     const unsigned kind = (hi >> 8) & 3u, site = hi >> 11;
-                    const bool h = kind < 2 && site < (unsigned)kHot;
-                    red_add_if(bhi_s + ((kind & 1u) * kHot + (h ? site : 0u)) * 4u, 1u, h && old[j] + lo < old[j]);
+                    carry |= (kind < 2 && site < (unsigned)kHot && old[j] + lo < old[j] ? 1u : 0u) << j;
+                }
+                while (carry) {                                   // rare: a 32-bit byte counter wrapped
+                    const int j = __ffs(carry) - 1;
+                    carry &= carry - 1;
+                    unsigned long long mj = 0;
+                    #pragma unroll
+                    for (int q = 0; q < kEpt; ++q) if (q == j) mj = meta[q];
+                    atomicAdd(&s.bhi[ev_kind(mj) * kHot + ev_site(mj)], 1u);
                 }
                 run = r32;
                 tmx = mx32; tmn = mn32;
