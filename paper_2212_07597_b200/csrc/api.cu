@@ -53,7 +53,8 @@ struct scl_traces {
     CUtensorMap tmap;
 };
 
-constexpr int kRing = 128;                     // replay-kernel timing event pairs kept per result
+constexpr int kRing = 128;
+constexpr unsigned kRTaskCap = 1u << 16;      // reclaim re-check queue (overflow: re-checked in place)                     // replay-kernel timing event pairs kept per result
 
 struct scl_result {
     const scl_traces* tr = nullptr;
@@ -72,6 +73,7 @@ struct scl_result {
     unsigned long long *d_key = nullptr, *d_key2 = nullptr; unsigned int *d_val = nullptr, *d_order = nullptr;
     void* d_cub = nullptr; size_t cub_bytes = 0;
     scl_site_row* d_rows = nullptr;
+    RTask* d_rtask = nullptr;                  // reclaim pass re-check queue
     // host
     std::vector<unsigned long long> h_sbase;
     std::vector<scl_trace_summary> h_summ;
@@ -184,12 +186,13 @@ static scl_status upload(scl_traces* tr, const scl_event* src, bool src_dev, std
                          uint32_t n_traces, uint32_t n_sites, cudaStream_t st)
 {
     const uint64_t n = h_off[n_traces];
-    {   // every trace needs a runner lane: n_traces <= grid * kRunners * 32
+    {   // every trace needs a runner lane: n_traces <= grid * kEmbeddedRunners * 32
         int grid = 0;
         replay_occupancy(&grid);
-        if ((uint64_t)n_traces > (uint64_t)grid * kRunners * 32)
-            return fail(SCL_EOVERFLOW, "too many traces for one launch (max " +
-                                       std::to_string((uint64_t)grid * kRunners * 32) + "): load them in waves");
+        const uint64_t cap = (uint64_t)grid * kEmbeddedRunners * 32;
+        if ((uint64_t)n_traces > cap)
+            return fail(SCL_EOVERFLOW, "too many traces for one launch (max " + std::to_string(cap) +
+                                       "): load them in waves");
     }
     const uint64_t rows_alloc = std::max<uint64_t>((n + 7) / 8, 1);
     if (rows_alloc > tr->cap_rows) {
@@ -205,7 +208,7 @@ static scl_status upload(scl_traces* tr, const scl_event* src, bool src_dev, std
             return fail(SCL_ENOMEM, "per-trace buffers");
         tr->cap_tr = nt1;
     }
-    if (!tr->d_err && (!grow(tr->d_err, 1) || !grow(tr->d_ticket, 1))) return fail(SCL_ENOMEM, "counters");
+    if (!tr->d_err && (!grow(tr->d_err, 1) || !grow(tr->d_ticket, 4))) return fail(SCL_ENOMEM, "counters");
     if (n > 0) CU(cudaMemcpyAsync(tr->d_ev, src, n * sizeof(scl_event), src_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
     if (rows_alloc * 8 > n) CU(cudaMemsetAsync(tr->d_ev + n, 0, (rows_alloc * 8 - n) * sizeof(scl_event), st));
     CU(cudaMemcpyAsync(tr->d_off, h_off.data(), h_off.size() * 8, cudaMemcpyHostToDevice, st));
@@ -363,7 +366,7 @@ static void free_result_buffers(scl_result* r) {
 extern "C" void scl_result_free(scl_result* r) {
     if (!r) return;
     free_result_buffers(r);
-    cudaFree(r->d_samples); cudaFree(r->d_epflag); cudaFree(r->d_prof);
+    cudaFree(r->d_samples); cudaFree(r->d_epflag); cudaFree(r->d_prof); cudaFree(r->d_rtask);
     if (r->h_gate) cudaFreeHost(r->h_gate);
     for (auto& e : r->ev) if (e) cudaEventDestroy(e);
     for (auto& e : r->kev) if (e) cudaEventDestroy(e);
@@ -377,6 +380,7 @@ static scl_status alloc_result(scl_result* r, const scl_traces* tr) {
         for (auto& e : r->ev) CU(cudaEventCreate(&e));
         for (auto& e : r->kev) CU(cudaEventCreate(&e));
         CU(cudaMallocHost(&r->h_gate, 32));
+        CU(cudaMalloc(&r->d_rtask, (size_t)kRTaskCap * sizeof(RTask)));
         int grid = 0;
         replay_occupancy(&grid);
         r->grid = grid;
@@ -459,9 +463,19 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
     p.ev = tr->d_ev; p.off = tr->d_off; p.tk = tr->d_tk;
     p.urec = tr->d_urec; p.uready = tr->d_uready; p.run = tr->d_run; p.tr_nseg = tr->d_tr_nseg; p.tr_base = tr->d_tr_base;
     p.ticket = tr->d_ticket; p.n_segs = tr->n_segs; p.epoch = tr->epoch;
+    {   // runner layout: 2 runner warps in every streaming CTA (default), or dedicated runner CTAs
+        // (SCL_RUNNER_CTAS=1, experiments: measured slower on config 2)
+        static const bool dedicated = getenv("SCL_RUNNER_CTAS") && atoi(getenv("SCL_RUNNER_CTAS")) > 0;
+        if (dedicated && NT <= (unsigned)kMaxRunnerCtas * kRunnersPerCta * 32) {
+            const unsigned rc = std::min<unsigned>(replay_runner_ctas(NT), (unsigned)r->grid - 1);
+            p.n_stream = (unsigned)r->grid - rc; p.n_runners = rc * kRunnersPerCta;
+        } else {
+            p.n_stream = (unsigned)r->grid; p.n_runners = (unsigned)r->grid * kEmbeddedRunners;
+        }
+    }
     p.n_sites = tr->n_sites; p.n_traces = NT; p.T = (long long)threshold;
     p.table = r->d_table; p.samples = r->d_samples; p.ep_flag = r->d_epflag; p.sbase = r->d_sbase;
-    p.summ = r->d_summ; p.uent = tr->d_uent;
+    p.summ = r->d_summ; p.uent = tr->d_uent; p.rtask = r->d_rtask; p.rtask_cap = kRTaskCap;
 #ifdef SCL_PROFILE
     if (!r->d_prof) CU(cudaMalloc(&r->d_prof, (48 + 4 * (size_t)tr->cap_segs) * 8));
     CU(cudaMemsetAsync(r->d_prof, 0, (48 + 4 * (size_t)tr->n_segs) * 8, st));
@@ -472,8 +486,7 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
     CU(launch_replay(&tr->tmap, p, r->grid, st));
     CU(cudaEventRecord(r->kev[2 * ks + 1], st));
     r->nrun += 1;
-    CU(launch_reclaim(p, st));
-    CU(launch_samples(p, st));
+    CU(launch_post(p, st));
     CU(cudaEventRecord(r->ev[1], st));
     *out = r;
     if (!o.defer_finalize) {

@@ -1,6 +1,5 @@
 // aux_kernels.cu -- small sm_100a kernels around the streaming replay kernel:
 //   load_stats_kernel  per-trace sum|d| (sample-capacity bound) + argument check, at load time
-//   samples_kernel     Tier-S, leak (mallocs, frees) and gate sums from the sample lists
 //   finalize_kernel    a6: leak probability, rate, flag, sort key
 //   rows_kernel        report rows in report order
 #include "scl_internal.cuh"
@@ -68,7 +67,7 @@ __global__ void __launch_bounds__(1024) prep_kernel(const __grid_constant__ Prep
     for (size_t i = tid; i < p.table_words; i += nth) p.table[i] = 0;
     for (size_t i = tid; i < p.summ_words; i += nth) p.summ[i] = 0;
     for (size_t i = tid; i < p.run_words; i += nth) p.run[i] = 0;
-    if (tid == 0) *p.ticket = 0;
+    if (tid < 4) p.ticket[tid] = 0;
     if (blockIdx.x != 0) return;
     // block 0: exclusive scan of the per-trace sample capacities (thread j: a contiguous run of traces)
     __shared__ unsigned long long part[1024];
@@ -90,41 +89,6 @@ __global__ void __launch_bounds__(1024) prep_kernel(const __grid_constant__ Prep
     }
     unsigned long long base = part[threadIdx.x] - acc;
     for (unsigned t = t0; t < t1; ++t) { p.sbase[t] = base; base += cap(t); }
-}
-
-// ============================================================================ per-sample reduce
-// One warp per trace: Tier-S columns, leak score (mallocs at episode start,
-// frees if the episode's object was reclaimed), footprint-trend
-// endpoints and the gate sums (reading Q10).
-__global__ void __launch_bounds__(256) samples_kernel(const __grid_constant__ ReplayParams p)
-{
-    const int lane = threadIdx.x & 31;
-    const unsigned wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const unsigned nw = (gridDim.x * blockDim.x) >> 5;
-    unsigned long long* gate = p.table + (size_t)p.n_sites * SCL_NCOL;
-    for (unsigned t = wid; t < p.n_traces; t += nw) {
-        const unsigned long long n = p.summ[t].n_samples, sb = p.sbase[t];
-        for (unsigned long long i = lane; i < n; i += 32) {
-            const scl_sample sm = p.samples[sb + i];
-            unsigned long long* row = p.table + (size_t)sm.site * SCL_NCOL;
-            if (sm.kind == 0) { atomicAdd(&row[SCL_COL_N_GROWTH], 1ull); atomicAdd(&row[SCL_COL_GROWTH_BYTES], (unsigned long long)sm.net); }
-            else              { atomicAdd(&row[SCL_COL_N_DECLINE], 1ull); atomicAdd(&row[SCL_COL_DECLINE_BYTES], (unsigned long long)(-sm.net)); }
-            if (sm.new_max) {
-                atomicAdd(&row[SCL_COL_LEAK_MALLOCS], 1ull);
-                if (p.ep_flag[sb + i]) atomicAdd(&row[SCL_COL_LEAK_FREES], 1ull);
-            }
-        }
-        if (lane == 0) {
-            long long ff = 0, fl = 0;
-            if (n > 0) { ff = p.samples[sb].footprint; fl = p.samples[sb + n - 1].footprint; }
-            p.summ[t].f_first_sample = ff; p.summ[t].f_last_sample = fl;
-            if (n >= 2) {
-                atomicAdd(&gate[0], (unsigned long long)(fl - ff));
-                atomicAdd(&gate[1], (unsigned long long)(ff > 1 ? ff : 1));
-                atomicAdd(&gate[2], 1ull);
-            }
-        }
-    }
 }
 
 // ============================================================================ a6
@@ -188,15 +152,6 @@ cudaError_t launch_prep(const PrepParams& p, cudaStream_t st)
     words = words > p.run_words ? words : p.run_words;
     unsigned blocks = (unsigned)std::min<size_t>((words + 1023) / 1024, 148);
     prep_kernel<<<blocks ? blocks : 1, 1024, 0, st>>>(p);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_samples(const ReplayParams& p, cudaStream_t st)
-{
-    if (p.n_traces == 0) return cudaSuccess;
-    unsigned warps = p.n_traces, blocks = (warps + 7) / 8;
-    if (blocks > 2048) blocks = 2048;
-    samples_kernel<<<blocks, 256, 0, st>>>(p);
     return cudaGetLastError();
 }
 

@@ -25,6 +25,7 @@
 //                   the tracked pointer (Bloom query per chunk, exact re-check
 //                   of positives).
 #include <climits>
+#include <algorithm>
 #include "scl_internal.cuh"
 #include "ptx.cuh"
 
@@ -44,11 +45,13 @@ struct __align__(16) Slot {          // compute -> look-back summary of one unit
     unsigned bloom[kChunks][kBloomWords];
 };
 
+constexpr int kESlots = 2 * kHot + kComputeWarps * 32;
+constexpr uint32_t kBloOff = kESlots * 4;   // byte distance cnt -> blo
+
 struct __align__(16) Smem {
-    unsigned cnt[2 * kHot];          // Tier-E per (kind, hot site): event count
-    unsigned blo[2 * kHot];          //   bytes, low 32 bits
-    unsigned bhi[2 * kHot];          //   carries out of blo
-    unsigned dummy[kComputeWarps * 32];   // per-lane sink of the unconditional atomics (never read)
+    unsigned cnt[kESlots];           // Tier-E per (kind, hot site): event count   (slots >= 2*kHot:
+    unsigned blo[kESlots];           //   bytes, low 32 bits                        per-lane sinks of the
+    unsigned bhi[2 * kHot];          //   carries out of blo                         unconditional atomics)
     Slot slot[kSlots];
     SegInfo info[kStages];
     unsigned sub[kStages];           // box index within the unit
@@ -80,6 +83,7 @@ __device__ __forceinline__ unsigned bloom_mask(unsigned long long ptr) {
 #define PROF_MARK(i) { const long long now_ = clock64(); pacc[i] += now_ - pt; pt = now_; }
 #define PROF_FLUSH(base) if (lane == 0 && p.prof) { for (int q_ = 0; q_ < 8; ++q_) atomicAdd(&p.prof[(base) + q_], pacc[q_]); }
 #define RPROF_ADD(i, v) if (p.prof && lane == 0) atomicAdd(&p.prof[24 + (i)], (unsigned long long)(v));
+#define PROF_TOUCH(v) asm volatile("" : "+l"(v));      /* the value must have arrived before the next clock read */
 #define PROF_UNIT_T(u, which) if (p.prof) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); p.prof[48 + 4 * (size_t)(u) + (which)] = t_; }
 #else
 #define PROF_DECL
@@ -87,6 +91,7 @@ __device__ __forceinline__ unsigned bloom_mask(unsigned long long ptr) {
 #define PROF_FLUSH(base)
 #define PROF_UNIT_T(u, which)
 #define RPROF_ADD(i, v)
+#define PROF_TOUCH(v)
 #endif
 
 // The 8 events of one global row, through L2 (re-read path).
@@ -98,12 +103,50 @@ __device__ __forceinline__ void load_row_global(const scl_event* ev, long long r
 }
 
 // ============================================================================ compute warps
+// Fast path of one row (8 events) in a lane.  Every shared atomic is unconditional (no branch
+// around it): an event that does not count goes to the lane's sink slot (and adds 0 bytes, so
+// the sink never wraps); 32-bit byte-counter carries are gathered as a bitmask.  kAllHot: every
+// site is in the shared-memory table (n_sites <= kHot), no cold-site bookkeeping.
+template <bool kAllHot>
+__device__ __forceinline__ void fast_row(const unsigned long long* ptr, const unsigned long long* meta, uint32_t cnt_s,
+                                         uint32_t bl_s, uint32_t dslot, Smem& s, int& r32, int& mx32, int& mn32,
+                                         unsigned& cold)
+{
+    unsigned old[kEpt], add[kEpt], carry = 0;
+    #pragma unroll
+    for (int j = 0; j < kEpt; ++j) {
+        const unsigned hi = (unsigned)(meta[j] >> 32), lo = (unsigned)meta[j];
+        const unsigned kind = (hi >> 8) & 3u, site = hi >> 11;
+        const int d = kind == 1 ? -(int)lo : (int)lo;
+        r32 += kind < 2 ? d : 0;                                              // a1: signed size
+        mx32 = max(mx32, r32); mn32 = min(mn32, r32);
+        const bool h = kind < 2 && (kAllHot || site < (unsigned)kHot);
+        if (!kAllHot) cold |= (kind < 2 && !h ? 1u : 0u) << j;
+        const uint32_t a = cnt_s + (h ? ((kind & 1u) * kHot + site) * 4u : dslot);   // (kind, site) slot
+        add[j] = h ? lo : 0u;
+        red_add(a, 1u);                                                       // a5 Tier E
+        old[j] = atom_add(a + kBloOff, add[j]);
+        red_or(kind == 1 ? bl_s + bloom_word(ptr[j]) * 4u : cnt_s + dslot, bloom_mask(ptr[j]));   // freed ptr -> Bloom
+    }
+    #pragma unroll
+    for (int j = 0; j < kEpt; ++j) carry |= (old[j] + add[j] < old[j] ? 1u : 0u) << j;
+    while (carry) {                                   // rare: a 32-bit byte counter wrapped
+        const int j = __ffs(carry) - 1;
+        carry &= carry - 1;
+        unsigned long long mj = 0;
+        #pragma unroll
+        for (int q = 0; q < kEpt; ++q) if (q == j) mj = meta[q];
+        atomicAdd(&s.bhi[ev_kind(mj) * kHot + ev_site(mj)], 1u);
+    }
+}
+
 // Two groups of 8 warps alternate boxes (group 0: boxes 0 and 2 of a unit, group 1: 1 and 3);
 // warp w8 of a group takes rows 32*w8 .. 32*w8+31 of its box = chunk g*8 + w8 of the unit.
 __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stage, int grp, int w8, int lane)
 {
-    const uint32_t cnt_s = smem_u32(s.cnt), blo_s = smem_u32(s.blo);
-    const uint32_t dum_s = smem_u32(&s.dummy[(grp * 8 + w8) * 32 + lane]);   // this lane's sink word
+    const uint32_t cnt_s = smem_u32(s.cnt);
+    const uint32_t dslot = (uint32_t)(2 * kHot + (grp * 8 + w8) * 32 + lane) * 4u;   // this lane's sink slot
+    const bool all_hot = p.n_sites <= (unsigned)kHot;       // no cold site: no L2 path to track
     PROF_DECL
     for (unsigned it = grp;; it += 2) {
         const int st = it % kStages;
@@ -149,38 +192,9 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
             unsigned cold = 0;                                // events for the L2 (cold site) path
             if (e0 >= 0 && e0 + kEpt <= inf.n_t && big == 0) {
                 // fast path: the whole row is in the trace and |partial sums| < 2^30: 32-bit running
-                // sum / max / min (a copy's d = 0 repeats an F already seen: harmless).  Every shared
-                // atomic is unconditional (no branch around it): an event that does not count goes
-                // to the lane's dummy word instead; 32-bit byte-counter carries are checked after.
-                unsigned old[kEpt], carry = 0;
-                #pragma unroll
-                for (int j = 0; j < kEpt; ++j) {
-                    const unsigned hi = (unsigned)(meta[j] >> 32), lo = (unsigned)meta[j];
-                    const unsigned kind = (hi >> 8) & 3u, site = hi >> 11;
-                    const int d = kind == 1 ? -(int)lo : (int)lo;
-                    r32 += kind < 2 ? d : 0;                                              // a1: signed size
-                    mx32 = max(mx32, r32); mn32 = min(mn32, r32);
-                    const bool h = kind < 2 && site < (unsigned)kHot;
-                    cold |= (kind < 2 && !h ? 1u : 0u) << j;
-                    const uint32_t x = ((kind & 1u) * kHot + site) * 4u;                  // (kind, site) slot
-                    red_add(h ? cnt_s + x : dum_s, 1u);                                   // a5 Tier E
-                    old[j] = atom_add(h ? blo_s + x : dum_s, lo);
-                    red_or(kind == 1 ? bl_s + bloom_word(ptr[j]) * 4u : dum_s, bloom_mask(ptr[j]));   // freed ptr -> Bloom
-                }
-                #pragma unroll
-                for (int j = 0; j < kEpt; ++j) {
-                    const unsigned hi = (unsigned)(meta[j] >> 32), lo = (unsigned)meta[j];
-                    const unsigned kind = (hi >> 8) & 3u, site = hi >> 11;
-                    carry |= (kind < 2 && site < (unsigned)kHot && old[j] + lo < old[j] ? 1u : 0u) << j;
-                }
-                while (carry) {                                   // rare: a 32-bit byte counter wrapped
-                    const int j = __ffs(carry) - 1;
-                    carry &= carry - 1;
-                    unsigned long long mj = 0;
-                    #pragma unroll
-                    for (int q = 0; q < kEpt; ++q) if (q == j) mj = meta[q];
-                    atomicAdd(&s.bhi[ev_kind(mj) * kHot + ev_site(mj)], 1u);
-                }
+                // sum / max / min (a copy's d = 0 repeats an F already seen: harmless)
+                if (all_hot) fast_row<true>(ptr, meta, cnt_s, bl_s, dslot, s, r32, mx32, mn32, cold);
+                else         fast_row<false>(ptr, meta, cnt_s, bl_s, dslot, s, r32, mx32, mn32, cold);
                 run = r32;
                 tmx = mx32; tmn = mn32;
                 small = r32 > -(1 << 25) && r32 < (1 << 25) && mx32 < (1 << 25) && mn32 > -(1 << 25);
@@ -315,119 +329,149 @@ __device__ void producer_role(const ReplayParams& p, const CUtensorMap* tmap, Sm
 // which a sample fires are resolved chunk by chunk.  The runner does no pointer matching: it
 // records the state entering each unit (UnitEntry) and the reclaim pass settles every episode
 // afterwards, all units in parallel -- the chain carries only what the sampler needs.
-struct RState { long long F, M, B; unsigned long long n, nep, ep1; unsigned next; };
+struct RState { long long F, M, B; unsigned long long n, nep, ep1, eptr; unsigned next; };
 
 __device__ __forceinline__ RState load_rstate(const RunState* rs, int lane) {
     const unsigned long long* w = reinterpret_cast<const unsigned long long*>(rs);
-    unsigned long long v = lane < 7 ? __ldcg(w + lane) : 0ull;      // F M B n nep ep1 {next,pad}
+    unsigned long long v = lane < 8 ? __ldcg(w + lane) : 0ull;      // F M B n nep ep1 eptr {next,pad}
     RState x;
     x.F = (long long)__shfl_sync(kFull, v, 0); x.M = (long long)__shfl_sync(kFull, v, 1);
     x.B = (long long)__shfl_sync(kFull, v, 2); x.n = __shfl_sync(kFull, v, 3);
-    x.nep = __shfl_sync(kFull, v, 4); x.ep1 = __shfl_sync(kFull, v, 5);
-    x.next = (unsigned)__shfl_sync(kFull, v, 6);
+    x.nep = __shfl_sync(kFull, v, 4); x.ep1 = __shfl_sync(kFull, v, 5); x.eptr = __shfl_sync(kFull, v, 6);
+    x.next = (unsigned)__shfl_sync(kFull, v, 7);      // low word: next
     return x;
 }
 __device__ __forceinline__ void store_rstate(RunState* rs, const RState& x, int lane) {
-    if (lane == 0) { rs->F = x.F; rs->M = x.M; rs->B = x.B; rs->n = x.n; rs->nep = x.nep; rs->ep1 = x.ep1; rs->next = x.next; }
+    if (lane == 0) {
+        rs->F = x.F; rs->M = x.M; rs->B = x.B; rs->n = x.n; rs->nep = x.nep; rs->ep1 = x.ep1; rs->eptr = x.eptr;
+        rs->next = x.next;
+    }
 }
 
 // A unit in which a sample fires: resolve it chunk by chunk (a3).  x: state before the unit
-// -> state after it.
-__device__ void resolve_unit(const ReplayParams& p, const Slot& S, RState& x, int lane)
+// -> state after it.  Only chunks whose F range leaves (B-T, B+T) are read (lane l <-> row
+// 32c+l, 8 events); one combined warp scan gives each lane the footprint and the running
+// high-water mark before its first event, and the lane holding the first exit of the band
+// walks its own events sequentially (successive samples included), then broadcasts the state.
+__device__ void resolve_unit(const ReplayParams& p, const Slot& S, RState& x, unsigned long long sb, int lane)
 {
-    // every load of the unit record is issued up front (one round trip)
     const SegInfo inf = S.info;
     const long long F0 = x.F, M0 = x.M;
-    long long B = x.B;
     const long long sPc = S.Pc[lane], sax = S.ax[lane], san = S.an[lane], susum = S.usum, sumx = S.umx;
-    unsigned long long n = x.n, nep = x.nep, ep1 = x.ep1;
-    const unsigned long long sb = __ldg(p.sbase + inf.t);
-    const long long myPc = sPc, hiL = F0 + sax, loL = F0 + san;
-    int cnext = 0;                                     // chunks < cnext are resolved for the current B
+    long long B = x.B;
+    unsigned long long n = x.n, nep = x.nep, ep1 = x.ep1, eptr = x.eptr;
+    const long long hiL = F0 + sax, loL = F0 + san;          // F range of chunk `lane`
+#ifdef SCL_PROFILE
+    const long long t_a = clock64();
+    { long long v0 = sPc, v1 = sax, v2 = san, v3 = susum; PROF_TOUCH(v0) PROF_TOUCH(v1) PROF_TOUCH(v2) PROF_TOUCH(v3) }
+    const long long t_b = clock64(); RPROF_ADD(8, t_b - t_a)          /* record wait */
+    long long t_rows = 0, t_scan = 0, t_walk = 0;
+#endif
+    int cnext = 0;                                           // chunks < cnext are resolved
     for (;;) {
-        // next chunk whose F range leaves (B-T, B+T): only those can hold a sample
         const unsigned ccm = __ballot_sync(kFull, lane >= cnext && (hiL >= B + p.T || loL <= B - p.T));
         if (!ccm) break;
         const int c = __ffs(ccm) - 1;
         RPROF_ADD(11, 1)
-        const long long Pw = shfl_ll(myPc, c);
-        const long long Mrun = llmax(M0, warp_max(lane < c ? hiL : kNeg));   // max F before the chunk
-        const long long row = inf.row_base + (long long)c * 32 + lane;      // lane l <-> row 32c+l
+        const long long row = inf.row_base + (long long)c * 32 + lane;
         unsigned long long rp[kEpt], rm[kEpt];
+#ifdef SCL_PROFILE
+        long long t_l = clock64();
+#endif
         load_row_global(p.ev, row, rp, rm);
-        const long long e0 = row * kEpt - inf.off_t;
-        long long d[kEpt], run = 0, lmx = kNeg, lmn = kPos;
+        // while the rows are in flight: F and the high-water mark before chunk c
+        const long long Fc = F0 + shfl_ll(sPc, c);
+        const long long Mc = llmax(M0, warp_max(lane < c ? hiL : kNeg));
+#ifdef SCL_PROFILE
+        #pragma unroll
+        for (int jj = 0; jj < kEpt; ++jj) { long long v = (long long)rm[jj]; PROF_TOUCH(v) rm[jj] = (unsigned long long)v; }
+        const long long t_r = clock64(); t_rows += t_r - t_l;
+#endif
+        const long long e0 = row * kEpt - inf.off_t;           // trace index of the lane's first event
+        long long fe[kEpt], run = 0, lmx = kNeg, lmn = kPos;   // fe[jj]: F after event jj - F before the lane
+        unsigned live = 0;                                      // events that move F (alloc/free in the trace)
         #pragma unroll
         for (int jj = 0; jj < kEpt; ++jj) {
             const long long ie = e0 + jj;
             const unsigned kind = ev_kind(rm[jj]);
             const bool af = ie >= 0 && ie < inf.n_t && kind < 2;
             const long long sz = (long long)ev_size(rm[jj]);
-            d[jj] = af ? (kind == 0 ? sz : -sz) : 0;
-            run += d[jj];
-            if (af) { lmx = llmax(lmx, run); lmn = llmin(lmn, run); }
+            run += af ? (kind == 0 ? sz : -sz) : 0;
+            fe[jj] = run;
+            if (af) { lmx = llmax(lmx, run); lmn = llmin(lmn, run); live |= 1u << jj; }
         }
-        long long li = run;
+        // combined exclusive scan over lanes of (sum, max prefix): (s1,m1).(s2,m2) = (s1+s2, max(m1, s1+m2))
+        long long ssum = run, smax = lmx;                       // inclusive, relative to the chunk start
         #pragma unroll
-        for (int dd = 1; dd < 32; dd <<= 1) { long long o = shfl_up_ll(li, dd); if (lane >= dd) li += o; }
-        const long long Fl = F0 + Pw + (li - run);          // F before this lane's first event
-        long long pmx = Fl + lmx;                             // max F over lanes <= lane
-        #pragma unroll
-        for (int dd = 1; dd < 32; dd <<= 1) { long long o = shfl_up_ll(pmx, dd); if (lane >= dd) pmx = llmax(pmx, o); }
-        long long PMl = shfl_up_ll(pmx, 1);
-        if (lane == 0) PMl = kNeg;
+        for (int dd = 1; dd < 32; dd <<= 1) {
+            const long long os = shfl_up_ll(ssum, dd), om = shfl_up_ll(smax, dd);
+            if (lane >= dd) { smax = llmax(om, os + smax); ssum = os + ssum; }
+        }
+        const long long Fl = Fc + ssum - run;                  // F before the lane's first event
+        long long Ml = shfl_up_ll(smax, 1);                     // max F over the events of lanes < lane
+        Ml = lane == 0 ? Mc : llmax(Mc, Fc + Ml);
+#ifdef SCL_PROFILE
+        { long long v = Ml; PROF_TOUCH(v) Ml = v; }
+        const long long t_s = clock64(); t_scan += t_s - t_r;
+#endif
         int cur = 0;
         for (;;) {
             const unsigned cm = __ballot_sync(kFull, lane >= cur && (Fl + lmx >= B + p.T || Fl + lmn <= B - p.T));
             if (!cm) break;
             const int l0 = __ffs(cm) - 1;
-            // lanes 0..7 take the 8 events of lane l0
-            long long de = 0; unsigned long long me = 0;
-            #pragma unroll
-            for (int jj = 0; jj < kEpt; ++jj) {
-                const long long v = shfl_ll(d[jj], l0);
-                const unsigned long long mv = __shfl_sync(kFull, rm[jj], l0);
-                if (lane == jj) { de = v; me = mv; }
-            }
-            const long long iev = shfl_ll(e0, l0) + lane;
-            const bool af = lane < kEpt && iev >= 0 && iev < inf.n_t && ev_kind(me) < 2;
-            long long L = de;
-            #pragma unroll
-            for (int dd = 1; dd < kEpt; dd <<= 1) { long long o = shfl_up_ll(L, dd); if (lane >= dd) L += o; }
-            const long long Fe = shfl_ll(Fl, l0) + L;
-            const long long Mbase = llmax(Mrun, shfl_ll(PMl, l0));
-            int ef = 0;
-            for (;;) {                                      // successive first exits of (B-T, B+T)
-                const unsigned em = __ballot_sync(kFull, af && lane >= ef && (Fe >= B + p.T || Fe <= B - p.T));
-                if (!em) break;
-                const int e = __ffs(em) - 1;
-                const long long Fs = shfl_ll(Fe, e);
-                const long long Mprev = llmax(Mbase, warp_max((af && lane < e) ? Fe : kNeg));   // M_{i-1}
-                const long long net = Fs - B;              // the |A - F| counter
-                const bool growth = net > 0;
-                const bool nm = growth && Fs > Mprev;      // new high-water mark (Q3, Q4)
-                const unsigned long long slot_s = sb + n;
-                if (lane == e) {
+            if (lane == l0) {           // this lane's events: exits of the band found in parallel, in order
+                unsigned from = 0;                              // events < from are settled
+                for (;;) {
+                    unsigned ex = 0;
+                    #pragma unroll
+                    for (int jj = 0; jj < kEpt; ++jj) {
+                        const long long F = Fl + fe[jj];
+                        ex |= (F >= B + p.T || F <= B - p.T ? 1u : 0u) << jj;
+                    }
+                    ex &= live & ~((1u << from) - 1u);
+                    if (!ex) break;
+                    const int js = __ffs(ex) - 1;
+                    long long F = 0, Mp = Ml;                   // F at the event, max F before it (M_{i-1})
+                    unsigned long long ms = 0, ps = 0;
+                    #pragma unroll
+                    for (int jj = 0; jj < kEpt; ++jj) {
+                        if (jj < js) Mp = llmax(Mp, Fl + fe[jj]);
+                        if (jj == js) { F = Fl + fe[jj]; ms = rm[jj]; ps = rp[jj]; }
+                    }
+                    const long long net = F - B;              // the |A - F| counter
+                    const bool growth = net > 0;
+                    const bool nm = growth && F > Mp;         // new high-water mark (Q3, Q4)
+                    const unsigned long long slot_s = sb + n;
                     scl_sample smp;
-                    smp.idx = (unsigned long long)iev; smp.net = net; smp.footprint = Fs;
-                    smp.site = ev_site(me); smp.kind = growth ? 0 : 1; smp.new_max = nm ? 1 : 0; smp.pad = 0;
+                    smp.idx = (unsigned long long)(e0 + js); smp.net = net; smp.footprint = F;
+                    smp.site = ev_site(ms); smp.kind = growth ? 0 : 1; smp.new_max = nm ? 1 : 0; smp.pad = 0;
                     p.samples[slot_s] = smp;
-                    if (nm) p.ep_flag[slot_s] = 0u;        // settled by the reclaim pass
+                    if (nm) { p.ep_flag[slot_s] = 0u; ep1 = slot_s + 1; eptr = ps; ++nep; }   // settled by the reclaim pass
+                    ++n; B = F;                               // "resets the counters"
+                    from = (unsigned)js + 1;
                 }
-                if (nm) { ep1 = slot_s + 1; ++nep; }
-                ++n; B = Fs; ef = e + 1;                   // "resets the counters"
             }
+            B = shfl_ll(B, l0); n = __shfl_sync(kFull, n, l0);
+            nep = __shfl_sync(kFull, nep, l0); ep1 = __shfl_sync(kFull, ep1, l0); eptr = __shfl_sync(kFull, eptr, l0);
             cur = l0 + 1;
         }
+#ifdef SCL_PROFILE
+        { long long v = B; PROF_TOUCH(v) B = v; }
+        t_walk += clock64() - t_s;
+#endif
         cnext = c + 1;
     }
     x.F = F0 + susum; x.M = llmax(M0, F0 + sumx); x.B = B;
-    x.n = n; x.nep = nep; x.ep1 = ep1;
+    x.n = n; x.nep = nep; x.ep1 = ep1; x.eptr = eptr;
+#ifdef SCL_PROFILE
+    RPROF_ADD(9, t_rows) RPROF_ADD(10, t_scan) RPROF_ADD(12, t_walk) RPROF_ADD(13, clock64() - t_b - t_rows - t_scan - t_walk)
+#endif
     __syncwarp();
 }
 
 // Advance a trace as far as its units are published (the caller is the trace's runner).
-__device__ void run_trace(const ReplayParams& p, RState& x, unsigned base, unsigned nseg, unsigned ep_tag, int lane)
+__device__ void run_trace(const ReplayParams& p, RState& x, unsigned t, unsigned base, unsigned nseg,
+                          unsigned long long sb, unsigned ep_tag, int lane)
 {
     const Slot* rec = reinterpret_cast<const Slot*>(p.urec);
     RPROF_ADD(0, 1)
@@ -441,47 +485,58 @@ __device__ void run_trace(const ReplayParams& p, RState& x, unsigned base, unsig
         RPROF_ADD(1, 1) RPROF_ADD(2, m)
 #ifdef SCL_PROFILE
         if (lane < m) PROF_UNIT_T(base + x.next + lane, 2)
+        const long long t_bat = clock64();
+        long long t_res = 0;
 #endif
         const Slot* R = rec + base + x.next;
         UnitEntry* ue = p.uent + base + x.next;
         long long us = 0, ux = kNeg, un = kPos;
         if (lane < m) { us = R[lane].usum; ux = R[lane].umx; un = R[lane].umn; }
+        // footprint and high-water mark do not depend on the samples: one combined scan gives F and
+        // M at the start of every unit of the batch ((s1,m1).(s2,m2) = (s1+s2, max(m1, s1+m2)))
+        long long ps = us, pm = ux;                           // inclusive, relative to the batch start
+        #pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const long long os = shfl_up_ll(ps, d), om = shfl_up_ll(pm, d);
+            if (lane >= d) { pm = llmax(om, os + pm); ps = os + ps; }
+        }
+        const long long Pe = ps - us;                         // F at the unit start - F at the batch start
+        long long Me = shfl_up_ll(pm, 1);                      // max F (rel.) over the units before
+        if (lane == 0) Me = kNeg;
+        const long long Fb = x.F, Mb = x.M;
         int j = 0;
-        while (j < m) {
-            // compose units j.. while the sampler band holds; jf = first unit where a sample fires
-            const long long v = (lane >= j && lane < m) ? us : 0;
-            long long inc = v;
-            #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) { long long o = shfl_up_ll(inc, d); if (lane >= d) inc += o; }
-            const long long E = inc - v;                      // sum of units j..lane-1
-            const long long c0 = x.F - x.B + E;
+        for (;;) {
+            // jf = first unit (>= j) whose F range leaves (B-T, B+T): a sample fires in it
+            const long long c0 = Fb + Pe - x.B;
             const unsigned bm = __ballot_sync(kFull, lane >= j && lane < m && (c0 + ux >= p.T || c0 + un <= -p.T));
             const int jf = bm ? __ffs(bm) - 1 : m;
-            // units j .. jf (incl. the resolved one) are entered with the same episode and count
-            if (lane >= j && lane <= jf && lane < m) { UnitEntry e; e.ep1 = x.ep1; e.n = x.n; ue[lane] = e; }
-            const long long mx = warp_max((lane >= j && lane < jf) ? E + ux : kNeg);
-            const long long add = shfl_ll(inc, jf > j ? jf - 1 : 0);   // sum of units j..jf-1 (lanes < j hold 0)
-            x.M = llmax(x.M, x.F + mx);
-            x.F += jf > j ? add : 0;
+            // units j .. jf-1 take no sample: same episode, empty sample range
+            if (lane >= j && lane < jf) { UnitEntry e; e.ep1 = x.ep1; e.eptr = x.eptr; e.s_in = sb + x.n; e.s_out = e.s_in; ue[lane] = e; }
             if (jf == m) break;
-            // unit jf: a sample fires in it
+            UnitEntry ef; ef.ep1 = x.ep1; ef.eptr = x.eptr; ef.s_in = sb + x.n;   // unit jf, before its samples
+            x.F = Fb + shfl_ll(Pe, jf);
+            x.M = llmax(Mb, Fb + shfl_ll(Me, jf));
 #ifdef SCL_PROFILE
             const long long t_r = clock64();
 #endif
-            resolve_unit(p, R[jf], x, lane);
+            resolve_unit(p, R[jf], x, sb, lane);
+            if (lane == 0) { ef.s_out = sb + x.n; ue[jf] = ef; }
             RPROF_ADD(3, 1) RPROF_ADD(4, clock64() - t_r)
 #ifdef SCL_PROFILE
             if (p.prof && lane == 0) p.prof[48 + 4 * (size_t)(base + x.next + jf) + 3] = clock64() - t_r;
+            t_res += clock64() - t_r;
 #endif
             j = jf + 1;
         }
+        x.F = Fb + shfl_ll(ps, m - 1);
+        x.M = llmax(Mb, Fb + shfl_ll(pm, m - 1));
 #ifdef SCL_PROFILE
         if (lane < m) PROF_UNIT_T(base + x.next + lane, 1)
+        RPROF_ADD(14, clock64() - t_bat - t_res)
 #endif
         x.next += (unsigned)m;
         if (x.next == nseg && lane == 0) {
-            const SegInfo inf = R[m - 1].info;
-            scl_trace_summary* sm = &p.summ[inf.t];
+            scl_trace_summary* sm = &p.summ[t];
             sm->f_final = x.F; sm->hwm = x.M; sm->n_samples = x.n; sm->n_episodes = x.nep;
         }
     }
@@ -527,17 +582,18 @@ __device__ void publisher_role(const ReplayParams& p, Smem& s, int lane)
     }
 }
 
-// Runner warp rw of grid*kRunners: owns traces rw, rw + nr, ...  (lane i <-> its i-th trace,
-// whose next unit index it keeps) and advances whichever of them has its next unit published,
-// with the exact sequential state (kept in p.run between visits).
-__device__ void runner_role(const ReplayParams& p, int ri_local, int lane)
+// Runner warp ri of nr (= p.n_runners): owns traces ri, ri + nr, ...  (lane i <-> its i-th
+// trace, whose next unit index it keeps) and advances whichever of them has its next unit
+// published, with the exact sequential state (kept in p.run between visits).
+__device__ void runner_role(const ReplayParams& p, unsigned ri, int lane)
 {
     const unsigned ep_tag = p.epoch;
-    const unsigned nr = gridDim.x * kRunners, ri = blockIdx.x * kRunners + ri_local;
+    const unsigned nr = p.n_runners;
     const unsigned cnt = ri < p.n_traces ? (p.n_traces - ri + nr - 1) / nr : 0u;
     const unsigned my_t = ri + (unsigned)lane * nr;
     unsigned my_base = 0, my_nseg = 0, my_next = 0;
-    if ((unsigned)lane < cnt) { my_nseg = __ldg(p.tr_nseg + my_t); my_base = __ldg(p.tr_base + my_t); }
+    unsigned long long my_sb = 0;
+    if ((unsigned)lane < cnt) { my_nseg = __ldg(p.tr_nseg + my_t); my_base = __ldg(p.tr_base + my_t); my_sb = p.sbase[my_t]; }
     PROF_DECL
     for (;;) {
         const bool alive = (unsigned)lane < cnt && my_next < my_nseg;
@@ -553,13 +609,139 @@ __device__ void runner_role(const ReplayParams& p, int ri_local, int lane)
             RunState* rs = p.run + t;
             RState x = load_rstate(rs, lane);
             x.next = __shfl_sync(kFull, my_next, i);
-            run_trace(p, x, __shfl_sync(kFull, my_base, i), __shfl_sync(kFull, my_nseg, i), ep_tag, lane);
+            run_trace(p, x, t, __shfl_sync(kFull, my_base, i), __shfl_sync(kFull, my_nseg, i), __shfl_sync(kFull, my_sb, i),
+                      ep_tag, lane);
             store_rstate(rs, x, lane);
             if (lane == i) my_next = x.next;
         }
         PROF_MARK(2)
     }
     PROF_FLUSH(16)
+}
+
+// ============================================================================ post pass: reclaim (a4) + per-sample reduce
+// One persistent launch, every block resident (grid = blocks that fit), three phases:
+//  1. one warp per unit settles the leak tracker's free-pointer comparison for every
+//     episode segment inside the unit -- the episode entering it (UnitEntry) up to the first
+//     episode started in it, then each episode started in it up to the next (an episode is
+//     reclaimed iff its pointer is freed anywhere in its span, so units are independent):
+//     Bloom query per chunk (lane <-> chunk); each positive chunk becomes an exact re-check task;
+//  2. after all units: the re-check tasks, spread over all warps (one chunk each, through L2);
+//  3. after all re-checks: the per-sample reduce, one warp per trace.
+// ep_flag was zeroed by the runner at each episode's start; phases 1-2 only set it.
+__device__ __forceinline__ bool chunk_has_free(const ReplayParams& p, long long row0, long long off_t, long long n_t,
+                                               unsigned pos0, unsigned long long ptr, unsigned sbeg, unsigned send, int lane)
+{
+    const long long row = row0 + lane;
+    unsigned long long rp[kEpt], rm[kEpt];
+    load_row_global(p.ev, row, rp, rm);
+    bool hit = false;
+    #pragma unroll
+    for (int jj = 0; jj < kEpt; ++jj) {
+        const long long ie = row * kEpt + jj - off_t;
+        const unsigned q = pos0 + (unsigned)lane * kEpt + jj;
+        hit |= rp[jj] == ptr && q >= sbeg && q < send && ie >= 0 && ie < n_t && ev_kind(rm[jj]) == 1;
+    }
+    return __any_sync(kFull, hit);
+}
+
+__device__ void reclaim_unit(const ReplayParams& p, unsigned u, int lane)
+{
+    const Slot& S = reinterpret_cast<const Slot*>(p.urec)[u];
+    const UnitEntry ent = p.uent[u];
+    const long long row_base = S.info.row_base, off_t = S.info.off_t, n_t = S.info.n_t;
+    const long long g0 = row_base * kEpt;                    // global event index of unit position 0
+    unsigned long long ep1 = ent.ep1, ptr = ent.eptr;        // current segment: episode (slot + 1), pointer, start
+    unsigned sbeg = 0;
+    auto segment = [&](unsigned send) {                      // [sbeg, send) of the current episode
+        if (!ep1 || send <= sbeg) return;
+        const unsigned w = bloom_word(ptr), msk = bloom_mask(ptr);
+        const unsigned cb = (unsigned)lane * 32 * kEpt;
+        const bool pos = cb < send && cb + 32 * kEpt > sbeg && (S.bloom[lane][w] & msk) == msk;
+        const unsigned cm = __ballot_sync(kFull, pos);
+        if (!cm) return;
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(&p.ticket[2], (unsigned)__popc(cm));
+        base = __shfl_sync(kFull, base, 0);
+        if (base + (unsigned)__popc(cm) <= p.rtask_cap) {   // queue one re-check per positive chunk
+            if (pos) {
+                RTask tk;
+                tk.ep1 = ep1; tk.ptr = ptr; tk.row0 = row_base + (long long)lane * 32; tk.off_t = off_t; tk.n_t = n_t;
+                tk.pos0 = cb; tk.sbeg = sbeg; tk.send = send; tk.pad = 0;
+                p.rtask[base + __popc(cm & ((1u << lane) - 1u))] = tk;
+            }
+        } else {                                             // queue full: re-check here, in order
+            bool found = false;
+            for (unsigned c = cm; c && !found; c &= c - 1) {
+                const int ch = __ffs(c) - 1;
+                found = chunk_has_free(p, row_base + (long long)ch * 32, off_t, n_t, (unsigned)ch * 32 * kEpt, ptr, sbeg, send, lane);
+            }
+            if (found && lane == 0) p.ep_flag[ep1 - 1] = 1u;
+        }
+    };
+    for (unsigned long long s0 = ent.s_in; s0 < ent.s_out; s0 += 32) {     // samples taken in this unit
+        const unsigned long long si = s0 + (unsigned long long)lane;
+        bool nm = false; long long idx = 0;
+        if (si < ent.s_out) { const scl_sample smp = p.samples[si]; nm = smp.new_max != 0; idx = (long long)smp.idx; }
+        unsigned em = __ballot_sync(kFull, nm);
+        while (em) {
+            const int e = __ffs(em) - 1;
+            em &= em - 1;
+            const long long ie = shfl_ll(idx, e);
+            const unsigned pos = (unsigned)(off_t + ie - g0);
+            segment(pos);
+            ep1 = s0 + (unsigned long long)e + 1;
+            ptr = __ldcg(&p.ev[off_t + ie].ptr);
+            sbeg = pos;
+        }
+    }
+    segment((unsigned)kUnit);
+}
+
+// Grid-wide barrier on counter ctr (zeroed per run): one arrival and one spinning thread per block.
+__device__ __forceinline__ void grid_barrier(unsigned* ctr) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ctr, 1u);
+        while (ld_acquire(ctr) < gridDim.x) __nanosleep(32);
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) post_kernel(const __grid_constant__ ReplayParams p)
+{
+    const int lane = threadIdx.x & 31;
+    const unsigned wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (unsigned u = wid; u < p.n_segs; u += nw) reclaim_unit(p, u, lane);              // phase 1
+    grid_barrier(&p.ticket[1]);
+    const unsigned ntask = min(ld_acquire(&p.ticket[2]), p.rtask_cap);
+    for (unsigned h = wid; h < ntask; h += nw) {                                          // phase 2
+        const RTask tk = p.rtask[h];
+        if (chunk_has_free(p, tk.row0, tk.off_t, tk.n_t, tk.pos0, tk.ptr, tk.sbeg, tk.send, lane) && lane == 0)
+            p.ep_flag[tk.ep1 - 1] = 1u;
+    }
+    grid_barrier(&p.ticket[3]);
+    for (unsigned t = wid; t < p.n_traces; t += nw) samples_trace(p, t, lane);            // phase 3
+}
+
+cudaError_t launch_post(const ReplayParams& p, cudaStream_t st)
+{
+    static int occ = 0, nsm = 0;
+    if (!occ) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, post_kernel, 256, 0);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) occ = 1;
+    }
+    // every block resident (the phases wait for all warps): a cooperative launch of at most
+    // occupancy x SMs blocks
+    const unsigned need = std::max<unsigned>((std::max(p.n_segs, p.n_traces) + 7) / 8, 1u);
+    const unsigned grid = std::min<unsigned>(need, (unsigned)(occ * nsm));
+    void* args[] = {const_cast<ReplayParams*>(&p)};
+    return cudaLaunchCooperativeKernel((const void*)post_kernel, dim3(grid), dim3(256), args, 0, st);
 }
 
 // ============================================================================ kernel
@@ -587,6 +769,15 @@ replay_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
 
     // register rebalancing per warpgroup (launch: 96/thread): the four compute warpgroups
     // give 16 each, the producer + look-back warpgroup takes them (no spills in its resolver)
+    if (blockIdx.x >= p.n_stream) {
+        // runner CTA: warpgroups 0-1 hand their registers to warpgroups 2-4 (12 runner warps)
+        if (warp < 8) { asm volatile("setmaxnreg.dec.sync.aligned.u32 24;\n" ::: "memory"); return; }
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 144;\n" ::: "memory");   // 8x32x72 released = 12x32x48
+        runner_role(p, (blockIdx.x - p.n_stream) * kRunnersPerCta + (warp - 8), lane);
+        return;
+    }
+    // streaming CTA, per warpgroup (launch: 96/thread): the four compute warpgroups give 16
+    // each, the producer + publisher warpgroup takes them
     if (warp < kComputeWarps) asm volatile("setmaxnreg.dec.sync.aligned.u32 80;\n" ::: "memory");
     else                      asm volatile("setmaxnreg.inc.sync.aligned.u32 160;\n" ::: "memory");
     if (warp < kComputeWarps) {
@@ -605,94 +796,15 @@ replay_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         producer_role(p, &tmap, s, stage, lane);
     } else if (warp == kProducerWarp + 1) {
         publisher_role(p, s, lane);
-    } else {
-        runner_role(p, warp - kProducerWarp - 2, lane);
+    } else if (p.n_stream == gridDim.x) {                             // embedded runners: 2 per CTA
+        runner_role(p, blockIdx.x * kEmbeddedRunners + (warp - kProducerWarp - 2), lane);
     }
 }
 
-// ============================================================================ reclaim pass (a4)
-// One warp per unit settles the leak tracker's free-pointer comparison for every
-// episode segment inside the unit: the episode entering it (UnitEntry) up to the first
-// episode started in it, then each episode started in it up to the next.  An episode is
-// reclaimed iff its pointer is freed anywhere in its span, so the segments are independent
-// and every unit is checked in parallel: Bloom query per chunk (lane <-> chunk), exact
-// re-check of the positives through L2.  ep_flag was zeroed by the runner at episode start.
-__global__ void __launch_bounds__(256) reclaim_kernel(const __grid_constant__ ReplayParams p)
+unsigned replay_runner_ctas(unsigned n_traces)
 {
-    const unsigned u = blockIdx.x * 8 + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (u >= p.n_segs) return;
-    const Slot& S = reinterpret_cast<const Slot*>(p.urec)[u];
-    const SegInfo inf = S.info;
-    const UnitEntry ent = p.uent[u];
-    const bool last = (inf.kraw >> 31) != 0;
-    const unsigned long long n_out = last ? p.summ[inf.t].n_samples : p.uent[u + 1].n;
-    const unsigned long long sb = __ldg(p.sbase + inf.t);
-    const long long g0 = inf.row_base * kEpt;              // global event index of unit position 0
-    unsigned long long ep1 = ent.ep1;                        // current segment: episode (slot + 1), pointer, start
-    unsigned long long ptr = 0;
-    if (ep1) ptr = __ldg(&p.ev[inf.off_t + (long long)__ldg(&p.samples[ep1 - 1].idx)].ptr);
-    unsigned sbeg = 0;
-    auto check = [&](unsigned send) {                        // settle [sbeg, send) for the current episode
-        if (!ep1 || send <= sbeg) return;
-        const unsigned w = bloom_word(ptr), msk = bloom_mask(ptr);
-        const unsigned cb = (unsigned)lane * 32 * kEpt;
-        const bool pos = cb < send && cb + 32 * kEpt > sbeg && (S.bloom[lane][w] & msk) == msk;
-        unsigned cm = __ballot_sync(kFull, pos);
-        bool found = false;
-        while (cm && !found) {                               // exact re-check, 4 positive chunks at a time:
-            int cs[4];                                       // pointer words first (32 loads in flight per lane),
-            #pragma unroll                                   // the meta word only where the pointer matches
-            for (int k = 0; k < 4; ++k) { cs[k] = cm ? __ffs(cm) - 1 : -1; cm &= cm ? cm - 1 : 0u; }
-            unsigned long long pv[4][kEpt];
-            #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const long long row = inf.row_base + (long long)(cs[k] < 0 ? cs[0] : cs[k]) * 32 + lane;
-                #pragma unroll
-                for (int jj = 0; jj < kEpt; ++jj) pv[k][jj] = __ldcg(&p.ev[row * kEpt + jj].ptr);
-            }
-            bool hit = false;
-            #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                if (cs[k] < 0) continue;
-                const long long row = inf.row_base + (long long)cs[k] * 32 + lane;
-                const unsigned pos0 = (unsigned)(cs[k] * 32 + lane) * kEpt;
-                #pragma unroll
-                for (int jj = 0; jj < kEpt; ++jj) {
-                    const long long ie = row * kEpt + jj - inf.off_t;
-                    const unsigned q = pos0 + jj;
-                    if (pv[k][jj] == ptr && q >= sbeg && q < send && ie >= 0 && ie < inf.n_t)
-                        hit |= ev_kind(__ldcg(&p.ev[row * kEpt + jj].meta)) == 1;
-                }
-            }
-            found = __any_sync(kFull, hit);
-        }
-        if (found && lane == 0) p.ep_flag[ep1 - 1] = 1u;
-    };
-    for (unsigned long long s0 = ent.n; s0 < n_out; s0 += 32) {       // samples taken in this unit
-        const unsigned long long si = s0 + (unsigned long long)lane;
-        bool nm = false; long long idx = 0;
-        if (si < n_out) { const scl_sample smp = p.samples[sb + si]; nm = smp.new_max != 0; idx = (long long)smp.idx; }
-        unsigned em = __ballot_sync(kFull, nm);
-        while (em) {
-            const int e = __ffs(em) - 1;
-            em &= em - 1;
-            const long long ie = shfl_ll(idx, e);
-            const unsigned pos = (unsigned)(inf.off_t + ie - g0);
-            check(pos);
-            ep1 = sb + s0 + (unsigned long long)e + 1;
-            ptr = __ldg(&p.ev[inf.off_t + ie].ptr);
-            sbeg = pos;
-        }
-    }
-    check((unsigned)kUnit);
-}
-
-cudaError_t launch_reclaim(const ReplayParams& p, cudaStream_t st)
-{
-    if (p.n_segs == 0) return cudaSuccess;
-    reclaim_kernel<<<(p.n_segs + 7) / 8, 256, 0, st>>>(p);
-    return cudaGetLastError();
+    const unsigned c = (n_traces + kRunnersPerCta - 1) / kRunnersPerCta;   // about one trace per runner warp
+    return c < 1 ? 1 : (c > (unsigned)kMaxRunnerCtas ? (unsigned)kMaxRunnerCtas : c);
 }
 
 int replay_occupancy(int* grid)

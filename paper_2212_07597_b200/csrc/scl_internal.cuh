@@ -28,8 +28,10 @@ constexpr int kUnitRows = kThreads * kSub;
 constexpr int kUnit = kSeg * kSub;            // events per unit (8192)
 constexpr int kChunks = 32;                   // 256-event chunks per unit (one per look-back lane)
 constexpr int kComputeWarps = 16;                // two groups of 8, alternating boxes
-constexpr int kLBWarps = 3;                   // publisher + 2 runners (20 warps total, 96 registers)
-constexpr int kRunners = 2;                   // runner warps per CTA
+constexpr int kLBWarps = 3;                   // publisher + 2 runner warps (20 warps total, 96 registers)
+constexpr int kEmbeddedRunners = 2;           // default layout: warps 18-19 of every streaming CTA run traces
+constexpr int kRunnersPerCta = 12;            // runner CTA: warps 8..19 run traces (144 registers each)
+constexpr int kMaxRunnerCtas = 16;            // at most 16 of the SMs run traces instead of streaming
 constexpr int kProducerWarp = kComputeWarps;
 constexpr int kCtaThreads = (kComputeWarps + 1 + kLBWarps) * 32;
 constexpr int kStages = 4;                    // TMA ring depth
@@ -50,17 +52,27 @@ __host__ __device__ inline uint32_t ev_site(uint64_t meta) { return (uint32_t)(m
 struct __align__(16) RunState {
     long long F, M, B;                // footprint, high-water mark, footprint at the last sample
     unsigned long long n, nep, ep1;   // samples, episodes, current episode (sample slot + 1; 0 none)
+    unsigned long long eptr;          // pointer of the current episode's allocation
     unsigned next, pad;               // next unit index to run
 };
 
-// State entering one unit, written by its trace's runner for the reclaim pass: the episode
-// in progress (sample slot + 1; 0 none) and the samples taken before the unit.
-struct __align__(16) UnitEntry { unsigned long long ep1, n; };
+// One unit's leak-tracker entry, written by its trace's runner for the reclaim pass: the episode
+// in progress when the unit starts (sample slot + 1; 0 none) and its pointer, and the absolute
+// sample slots [s_in, s_out) taken inside the unit.
+struct __align__(16) UnitEntry { unsigned long long ep1, eptr, s_in, s_out; };
 
 // One unit ticket, resolved on the host at load time (one 32-B load per ticket).
 struct __align__(16) TicketInfo {
     long long off_t, n_t;             // trace start (global event index), trace length
     unsigned t, kraw, slot, nbox;     // trace, unit index (| last << 31), state slot, boxes overlapping the trace
+};
+
+// One exact re-check of the reclaim pass: chunk rows [row0, row0 + 32) of a unit, unit positions
+// [sbeg, send), does any free of `ptr` occur?  (pos0: unit position of the chunk's first event.)
+struct __align__(16) RTask {
+    unsigned long long ep1, ptr;
+    long long row0, off_t, n_t;
+    unsigned pos0, sbeg, send, pad;
 };
 
 struct ReplayParams {
@@ -73,8 +85,12 @@ struct ReplayParams {
     UnitEntry* uent;                  // [n_segs] state entering each unit (runner -> reclaim pass)
     const unsigned int* tr_nseg;      // [n_traces] units per trace
     const unsigned int* tr_base;      // [n_traces] first unit id of the trace
-    unsigned int* ticket;             // global ticket counter (zeroed per run)
+    unsigned int* ticket;             // [4]: unit tickets; post pass: units settled, task tail, warps done (zeroed per run)
+    RTask* rtask;                     // [rtask_cap] exact re-checks queued by the reclaim pass
+    unsigned int rtask_cap;
     unsigned int n_segs;
+    unsigned int n_stream;            // CTAs [0, n_stream) stream units, the rest run traces
+    unsigned int n_runners;           // embedded: gridDim.x * 2; dedicated: (gridDim.x - n_stream) * kRunnersPerCta
     unsigned int epoch;               // run number on this traces handle (ready tag)
     unsigned int n_sites;
     unsigned int n_traces;
@@ -103,7 +119,7 @@ struct PrepParams {
     unsigned long long* table; size_t table_words;
     unsigned long long* summ; size_t summ_words;
     unsigned long long* run; size_t run_words;
-    unsigned int* ticket;
+    unsigned int* ticket;             // [4]
     unsigned long long* sbase;        // [n_traces]
     const unsigned long long* off;    // [n_traces + 1]
     const unsigned long long* sabs;   // [n_traces]
@@ -111,14 +127,44 @@ struct PrepParams {
     unsigned long long T;
 };
 
+#ifdef __CUDACC__
+// Per-sample reduce of trace t by one warp: Tier-S columns, leak score (mallocs at episode start,
+// frees if the episode's object was reclaimed), footprint-trend endpoints and the gate
+// sums (reading Q10).
+__device__ __forceinline__ void samples_trace(const ReplayParams& p, unsigned t, int lane)
+{
+    unsigned long long* gate = p.table + (size_t)p.n_sites * SCL_NCOL;
+    const unsigned long long n = p.summ[t].n_samples, sb = p.sbase[t];
+    for (unsigned long long i = lane; i < n; i += 32) {
+        const scl_sample sm = p.samples[sb + i];
+        unsigned long long* row = p.table + (size_t)sm.site * SCL_NCOL;
+        if (sm.kind == 0) { atomicAdd(&row[SCL_COL_N_GROWTH], 1ull); atomicAdd(&row[SCL_COL_GROWTH_BYTES], (unsigned long long)sm.net); }
+        else              { atomicAdd(&row[SCL_COL_N_DECLINE], 1ull); atomicAdd(&row[SCL_COL_DECLINE_BYTES], (unsigned long long)(-sm.net)); }
+        if (sm.new_max) {
+            atomicAdd(&row[SCL_COL_LEAK_MALLOCS], 1ull);
+            if (p.ep_flag[sb + i]) atomicAdd(&row[SCL_COL_LEAK_FREES], 1ull);
+        }
+    }
+    if (lane == 0) {
+        long long ff = 0, fl = 0;
+        if (n > 0) { ff = p.samples[sb].footprint; fl = p.samples[sb + n - 1].footprint; }
+        p.summ[t].f_first_sample = ff; p.summ[t].f_last_sample = fl;
+        if (n >= 2) {
+            atomicAdd(&gate[0], (unsigned long long)(fl - ff));
+            atomicAdd(&gate[1], (unsigned long long)(ff > 1 ? ff : 1));
+            atomicAdd(&gate[2], 1ull);
+        }
+    }
+}
+#endif
+
 // launch wrappers (replay.cu)
 cudaError_t launch_load_stats(const scl_event* ev, const unsigned long long* off, unsigned n_traces,
                               unsigned long long n_events, unsigned n_sites, unsigned long long* sabs,
                               unsigned long long* err, cudaStream_t st);
 cudaError_t launch_replay(const CUtensorMap* tmap, const ReplayParams& p, int grid, cudaStream_t st);
 cudaError_t launch_prep(const PrepParams& p, cudaStream_t st);
-cudaError_t launch_reclaim(const ReplayParams& p, cudaStream_t st);
-cudaError_t launch_samples(const ReplayParams& p, cudaStream_t st);
+cudaError_t launch_post(const ReplayParams& p, cudaStream_t st);
 cudaError_t launch_finalize(const FinalParams& p, cudaStream_t st);
 cudaError_t launch_rows(const unsigned long long* table, const double* prob, const double* rate,
                         const unsigned char* flag, const unsigned int* order, unsigned n_sites,
@@ -126,5 +172,6 @@ cudaError_t launch_rows(const unsigned long long* table, const double* prob, con
 size_t replay_smem_bytes();
 size_t replay_urec_bytes();            // bytes of one unit record
 int replay_occupancy(int* grid);
+unsigned replay_runner_ctas(unsigned n_traces);   // CTAs of the grid that run traces
 
 }  // namespace scl

@@ -35,7 +35,10 @@ for base, (nm, nw, cats) in names.items():
 rc = bigbuf[24:40].astype(float)
 print(f"  runner: invocations {rc[0]:.0f} batches {rc[1]:.0f} units {rc[2]:.0f} resolves {rc[3]:.0f} "
       f"resolve cyc/each {rc[4]/max(rc[3],1):.0f} ptr-exact {rc[5]:.0f} run cyc/invocation {rc[6]/max(rc[0],1):.0f} lock-fails {rc[7]:.0f}")
-print(f"  resolve parts per resolve: loads {rc[8]/max(rc[3],1):.0f} sampler {rc[9]/max(rc[3],1):.0f} ptrmatch {rc[10]/max(rc[3],1):.0f} cand-chunks {rc[11]/max(rc[3],1):.2f}")
+nres = max(rc[3], 1)
+print(f"  resolve parts per resolve (cycles): record {rc[8]/nres:.0f} rows(+Fc,Mc) {rc[9]/nres:.0f} prefix+scan {rc[10]/nres:.0f} "
+      f"walk {rc[12]/nres:.0f} rest {rc[13]/nres:.0f}  cand-chunks {rc[11]/nres:.2f}; batch cycles outside resolves "
+      f"{(rc[14])/max(rc[1],1):.0f}/batch")
 # per-unit timeline (aggregate published, inclusive published), first unit of each trace = unit 0
 if len(sys.argv) > 4:
     nunits = nunits_all
@@ -49,8 +52,18 @@ if len(sys.argv) > 4:
         a = agg[t * per:(t + 1) * per]; b = inc[t * per:(t + 1) * per]
         print(f"  trace {t}: " + " ".join(f"{int(x)}/{int(y)}" for x, y in list(zip(a, b))[::8]))
 
-    for t in (1,):
-        print(f"  trace {t} per unit: agg / batch-start / batch-end (us) / resolve kcyc")
-        for u in range(t * per, (t + 1) * per):
-            a, bs, be, rc_ = (tl4[u, 0] - t0) / 1e3, (tl4[u, 2] - t0) / 1e3, (tl4[u, 1] - t0) / 1e3, tl4[u, 3] / 1e3
-            print(f"    u{u - t*per:3d} {a:7.1f} {bs:7.1f} {be:7.1f} {rc_:7.1f}")
+    fin = []
+    for t in range(nt):
+        us = slice(t * per, (t + 1) * per)
+        agg_t = (tl4[us, 0] - t0) / 1e3; be = (tl4[us, 1] - t0) / 1e3; bs = (tl4[us, 2] - t0) / 1e3
+        rk = tl4[us, 3] / 1e3
+        fin.append((be.max(), agg_t.max(), int((rk > 0).sum()), rk.sum(), t, bs[-1], agg_t[-4:].max()))
+    fin.sort(reverse=True)
+    rk_all = tl4[:, 3].astype(np.float64); bs_all = (tl4[:, 2] - t0) / 1e3
+    end_stream = agg.max()
+    sel_b = (rk_all > 0) & (bs_all < end_stream - 5); sel_a = (rk_all > 0) & (bs_all > end_stream + 2)
+    print(f"  resolve cycles: during stream mean {rk_all[sel_b].mean():.0f} (n={sel_b.sum()}), after stream end mean "
+          f"{rk_all[sel_a].mean() if sel_a.any() else 0:.0f} (n={sel_a.sum()})")
+    print("  slowest traces: finish / last publish / resolves / resolve kcyc / last batch start")
+    for f_, a_, nr_, rk_, t_, bs_, a4 in fin[:12]:
+        print(f"    trace {t_:3d}: finish {f_:6.1f}  last agg {a_:6.1f}  resolves {nr_:3d}  kcyc {rk_:7.1f}  last batch start {bs_:6.1f}")
