@@ -515,10 +515,14 @@ extern "C" scl_status scl_finalize(scl_result* r, uint64_t elapsed_ns) {
     f.table = r->d_table; f.n_sites = S; f.formula = r->formula;
     f.elapsed_ns = (double)(r->elapsed_ns ? r->elapsed_ns : 1);
     f.prob = r->d_prob; f.rate = r->d_rate; f.flag = r->d_flag; f.key1 = r->d_key; f.val = r->d_val;
-    CU(launch_finalize(f, st));
-    size_t tb = r->cub_bytes;
-    CU(cub::DeviceRadixSort::SortPairs(r->d_cub, tb, r->d_key, r->d_key2, r->d_val, r->d_order, (int)S, 0, 64, st));
-    CU(launch_rows(r->d_table, r->d_prob, r->d_rate, r->d_flag, r->d_order, S, r->d_rows, st));
+    if (report_fused(S)) {
+        CU(launch_report(f, r->d_rows, st));
+    } else {
+        CU(launch_finalize(f, st));
+        size_t tb = r->cub_bytes;
+        CU(cub::DeviceRadixSort::SortPairs(r->d_cub, tb, r->d_key, r->d_key2, r->d_val, r->d_order, (int)S, 0, 64, st));
+        CU(launch_rows(r->d_table, r->d_prob, r->d_rate, r->d_flag, r->d_order, S, r->d_rows, st));
+    }
     CU(cudaMemcpyAsync(r->h_gate, r->d_table + (size_t)S * SCL_NCOL, 24, cudaMemcpyDeviceToHost, st));
     CU(cudaEventRecord(r->ev[3], st));
     r->finalized = true;

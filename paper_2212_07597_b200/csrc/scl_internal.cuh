@@ -166,6 +166,8 @@ cudaError_t launch_replay(const CUtensorMap* tmap, const ReplayParams& p, int gr
 cudaError_t launch_prep(const PrepParams& p, cudaStream_t st);
 cudaError_t launch_post(const ReplayParams& p, cudaStream_t st);
 cudaError_t launch_finalize(const FinalParams& p, cudaStream_t st);
+bool report_fused(unsigned n_sites);   // a6 in one block (report_kernel) for tables this small
+cudaError_t launch_report(const FinalParams& p, scl_site_row* rows, cudaStream_t st);
 cudaError_t launch_rows(const unsigned long long* table, const double* prob, const double* rate,
                         const unsigned char* flag, const unsigned int* order, unsigned n_sites,
                         scl_site_row* rows, cudaStream_t st);

@@ -226,3 +226,20 @@ def test_reload_grow_shrink_and_kernel_times():
     scl.scl_trace_reload(tr, ev, off, n_sites)
     r = scl.scl_replay_run(97, tr, out=r)
     compare(ev, off, n_sites, 97, r)
+
+
+def test_report_many_flagged_sites():
+    """a6 with more flagged sites than the fused report kernel's shared list (3000 > 2048):
+    every allocation raises the high-water mark (T=1), none is freed, so each site has
+    m = 20 leak mallocs, f = 0 (flagged: m > 21 f + 18); rates differ by site."""
+    n_sites, reps = 3000, 20
+    ev_t = []
+    ptr = 0x10000
+    for r_ in range(reps):
+        for s_ in range(n_sites):
+            ev_t.append(("a", ptr, 16 + (s_ * 7919) % 4093 + r_, s_))
+            ptr += 0x1000
+    ev, off = _concat([ev_t])
+    _, r = gpu_run(ev, off, n_sites, 1)
+    ref = compare(ev, off, n_sites, 1, r)
+    assert int(ref["flag"].sum()) == n_sites
