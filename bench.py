@@ -231,8 +231,9 @@ def main():
     tr = scl.scl_trace_load(host_ev, off_local, cfg.n_sites, device=local)
     r = None
 
-    def step(r):
-        r = scl.scl_replay_run(cfg.T, tr, stream=stream, out=r, defer_finalize=world > 1, elapsed_ns=elapsed_ns)
+    def step(r, timing=False):
+        r = scl.scl_replay_run(cfg.T, tr, stream=stream, out=r, defer_finalize=world > 1, elapsed_ns=elapsed_ns,
+                               timing=timing)
         if world > 1:
             dist.all_reduce(scl.device_table_tensor(r))
             scl.scl_finalize(r, elapsed_ns)
@@ -245,14 +246,20 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    scl.scl_result_kernel_times(r)                     # drop the warm-up runs' kernel times
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):                    # enqueued back to back: no host sync per step
             r = step(r)
         e1.record(stream)
         torch.cuda.synchronize()
-    kern_ms = scl.scl_result_kernel_times(r)           # replay-kernel durations of the timed steps
+    # the replay kernel's own duration (roofline): the same K steps again with the library's
+    # CUDA events around the kernel (kept out of the timed loop above: ~2.5 us per event record)
+    scl.scl_result_kernel_times(r)
+    with ClockSampler(local) as clk2:
+        for _ in range(args.steps):
+            r = step(r, timing=True)
+        torch.cuda.synchronize()
+    kern_ms = scl.scl_result_kernel_times(r)
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
@@ -327,10 +334,10 @@ def main():
                          "frac_of_8tbs_spec": achieved / 8000.0},
             "clocks": clk.summary(),
             "e2e": e2e,
-            "gpu_launches": 6 * args.steps,
-            "gpu_launches_note": "per step: prep_kernel, replay_kernel, reclaim_kernel, samples_kernel, "
-                                 "finalize_kernel, rows_kernel "
-                                 "(+ CUB radix-sort kernels for the report order, library)",
+            "gpu_launches": 4 * args.steps,
+            "gpu_launches_note": "per step: prep_kernel, replay_kernel, post_kernel, report_kernel "
+                                 "(tables > 16384 sites: finalize + CUB radix sort + rows instead of report)",
+            "kernel_timing": "replay_kernel durations from CUDA events in a second pass of K steps",
             "n_samples_per_step": n_samples,
             "cpu_baseline": cpu,
         }

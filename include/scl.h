@@ -106,7 +106,9 @@ typedef struct {
     int defer_finalize;      /* 1: stop after the site table (a1-a5); the caller may sum the
                                 device table across GPUs (scl_result_device_table) and then
                                 call scl_finalize.  0: finalize immediately. */
-    int reserved;
+    int timing;              /* 1: record CUDA events around the phases and the replay kernel
+                                (scl_result_timing, scl_result_kernel_times); 0: one completion
+                                event only (each event record costs ~2.5 us of stream time) */
     uint64_t elapsed_ns;     /* 0: max_t n_t * tick_ns over this handle's traces */
     void* cuda_stream;       /* cudaStream_t, NULL = default stream */
 } scl_run_opts;
@@ -175,14 +177,15 @@ scl_status scl_trace_summaries(const scl_result* r, scl_trace_summary* out, size
  * over traces with >= 2 samples; open iff some trace qualifies and 100*num >= den. */
 scl_status scl_gate(const scl_result* r, int64_t* num, int64_t* den, int* open);
 
-/* Device time of the last run, in ms, from CUDA events on the run's stream (waits for it):
+/* Device time of the last run, in ms, from CUDA events on the run's stream (waits for it);
+ * -1 for the phases of a run made without opts->timing:
  *   replay_kernel_ms  the streaming a1..a5 kernel alone (the roofline kernel)
  *   run_ms            a1..a5 including the per-run clears, the reclaim pass and the per-sample reduce
  *   finalize_ms       a6 (probabilities, flags, report order, rows) */
 scl_status scl_result_timing(const scl_result* r, float* replay_kernel_ms, float* run_ms, float* finalize_ms);
 
-/* Replay-kernel durations (ms) of the runs enqueued since the previous call (at most the
- * latest 128), oldest first; waits for them.  Lets a caller time many back-to-back runs
+/* Replay-kernel durations (ms) of the runs made with opts->timing since the previous call (at
+ * most the latest 128), oldest first; waits for them.  Lets a caller time many back-to-back runs
  * without synchronising between them.  *n = number written (<= cap). */
 scl_status scl_result_kernel_times(const scl_result* r, float* ms, size_t cap, size_t* n);
 

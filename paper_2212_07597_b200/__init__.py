@@ -44,7 +44,7 @@ class SclError(RuntimeError):
 
 class _RunOpts(ctypes.Structure):
     _fields_ = [("tick_ns", ctypes.c_uint64), ("hwm_mode", ctypes.c_int), ("formula", ctypes.c_int),
-                ("defer_finalize", ctypes.c_int), ("reserved", ctypes.c_int), ("elapsed_ns", ctypes.c_uint64),
+                ("defer_finalize", ctypes.c_int), ("timing", ctypes.c_int), ("elapsed_ns", ctypes.c_uint64),
                 ("cuda_stream", ctypes.c_void_p)]
 
 
@@ -185,12 +185,13 @@ def scl_trace_reload(traces: Traces, events, offsets, n_sites: int, validate: bo
 
 def scl_replay_run(threshold: int, traces: Traces, tick_ns: int = 0, formula: int = 0,
                    defer_finalize: bool = False, elapsed_ns: int = 0, stream=None,
-                   out: Result | None = None) -> Result:
+                   out: Result | None = None, timing: bool = False) -> Result:
     """Replay all traces at threshold T; ``out`` (a previous Result of the same
-    traces) is reused in place.  stream: torch.cuda.Stream / raw handle / None."""
+    traces) is reused in place.  stream: torch.cuda.Stream / raw handle / None.
+    timing: record CUDA events for scl_result_timing / scl_result_kernel_times."""
     o = _RunOpts()
     o.tick_ns, o.hwm_mode, o.formula = tick_ns, 0, formula
-    o.defer_finalize, o.elapsed_ns = int(defer_finalize), elapsed_ns
+    o.defer_finalize, o.elapsed_ns, o.timing = int(defer_finalize), elapsed_ns, int(timing)
     if stream is not None:
         o.cuda_stream = getattr(stream, "cuda_stream", stream)
     r = out if out is not None else Result(traces)
@@ -254,7 +255,7 @@ def scl_gate(r: Result):
 
 
 def scl_result_timing(r: Result):
-    """(replay_kernel_ms, run_ms, finalize_ms) of the last run (CUDA events)."""
+    """(replay_kernel_ms, run_ms, finalize_ms) of the last run (CUDA events; -1 without timing=True)."""
     a, b, c = ctypes.c_float(), ctypes.c_float(), ctypes.c_float()
     _check(lib.scl_result_timing(r.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
     return a.value, b.value, c.value

@@ -77,9 +77,10 @@ struct scl_result {
     // host
     std::vector<unsigned long long> h_sbase;
     std::vector<scl_trace_summary> h_summ;
-    unsigned long long* h_gate = nullptr;      // pinned: gate sums copied at the end of a6
+    unsigned long long* h_gate = nullptr;      // pinned, written by the a6 kernel (gate sums)
     bool summ_valid = false;
     bool finalized = false;
+    bool timed = false;                        // the last run recorded its phase events
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};   // run begin/end, finalize begin/end
     cudaEvent_t kev[2 * kRing] = {};           // replay kernel begin/end, one pair per run (ring)
     uint64_t nrun = 0, nread = 0;
@@ -450,7 +451,9 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
     if (tr->epoch >= (1u << 30)) { CU(cudaMemsetAsync(tr->d_uready, 0, tr->cap_segs * 4, st)); tr->epoch = 0; }
     tr->epoch += 1;
 
-    CU(cudaEventRecord(r->ev[0], st));
+    const bool tm = o.timing != 0;                 // phase / kernel events only when asked for
+    r->timed = tm;
+    if (tm) CU(cudaEventRecord(r->ev[0], st));
     PrepParams pp{};
     pp.table = r->d_table; pp.table_words = (size_t)tr->n_sites * SCL_NCOL + 3;
     pp.summ = reinterpret_cast<unsigned long long*>(r->d_summ); pp.summ_words = (size_t)NT * sizeof(scl_trace_summary) / 8;
@@ -482,12 +485,11 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
     p.prof = r->d_prof;
 #endif
     const int ks = (int)(r->nrun % kRing);
-    CU(cudaEventRecord(r->kev[2 * ks], st));
+    if (tm) CU(cudaEventRecord(r->kev[2 * ks], st));
     CU(launch_replay(&tr->tmap, p, r->grid, st));
-    CU(cudaEventRecord(r->kev[2 * ks + 1], st));
-    r->nrun += 1;
+    if (tm) { CU(cudaEventRecord(r->kev[2 * ks + 1], st)); r->nrun += 1; }
     CU(launch_post(p, st));
-    CU(cudaEventRecord(r->ev[1], st));
+    if (tm) CU(cudaEventRecord(r->ev[1], st));
     *out = r;
     if (!o.defer_finalize) {
         scl_status s3 = scl_finalize(r, 0);
@@ -510,11 +512,12 @@ extern "C" scl_status scl_finalize(scl_result* r, uint64_t elapsed_ns) {
     cudaStream_t st = r->stream;
     if (elapsed_ns) r->elapsed_ns = elapsed_ns;
     const unsigned S = tr->n_sites;
-    CU(cudaEventRecord(r->ev[2], st));
+    if (r->timed) CU(cudaEventRecord(r->ev[2], st));
     FinalParams f{};
     f.table = r->d_table; f.n_sites = S; f.formula = r->formula;
     f.elapsed_ns = (double)(r->elapsed_ns ? r->elapsed_ns : 1);
     f.prob = r->d_prob; f.rate = r->d_rate; f.flag = r->d_flag; f.key1 = r->d_key; f.val = r->d_val;
+    f.gate_out = r->h_gate;                    // pinned host memory, device-accessible (unified addressing)
     if (report_fused(S)) {
         CU(launch_report(f, r->d_rows, st));
     } else {
@@ -523,7 +526,6 @@ extern "C" scl_status scl_finalize(scl_result* r, uint64_t elapsed_ns) {
         CU(cub::DeviceRadixSort::SortPairs(r->d_cub, tb, r->d_key, r->d_key2, r->d_val, r->d_order, (int)S, 0, 64, st));
         CU(launch_rows(r->d_table, r->d_prob, r->d_rate, r->d_flag, r->d_order, S, r->d_rows, st));
     }
-    CU(cudaMemcpyAsync(r->h_gate, r->d_table + (size_t)S * SCL_NCOL, 24, cudaMemcpyDeviceToHost, st));
     CU(cudaEventRecord(r->ev[3], st));
     r->finalized = true;
     return SCL_OK;
@@ -597,14 +599,16 @@ extern "C" scl_status scl_gate(const scl_result* r, int64_t* num, int64_t* den, 
 
 extern "C" scl_status scl_result_timing(const scl_result* r, float* replay_kernel_ms, float* run_ms, float* finalize_ms) {
     if (!r) return fail(SCL_EINVAL, "NULL result");
-    CU(cudaEventSynchronize(r->finalized ? r->ev[3] : r->ev[1]));
-    float k = 0, a = 0, f = 0;
-    if (r->nrun) {
-        const int ks = (int)((r->nrun - 1) % kRing);
-        CU(cudaEventElapsedTime(&k, r->kev[2 * ks], r->kev[2 * ks + 1]));
+    float k = -1, a = -1, f = -1;
+    if (r->timed) {
+        CU(cudaEventSynchronize(r->finalized ? r->ev[3] : r->ev[1]));
+        if (r->nrun) {
+            const int ks = (int)((r->nrun - 1) % kRing);
+            CU(cudaEventElapsedTime(&k, r->kev[2 * ks], r->kev[2 * ks + 1]));
+        }
+        CU(cudaEventElapsedTime(&a, r->ev[0], r->ev[1]));
+        if (r->finalized) CU(cudaEventElapsedTime(&f, r->ev[2], r->ev[3]));
     }
-    CU(cudaEventElapsedTime(&a, r->ev[0], r->ev[1]));
-    if (r->finalized) CU(cudaEventElapsedTime(&f, r->ev[2], r->ev[3]));
     if (replay_kernel_ms) *replay_kernel_ms = k;
     if (run_ms) *run_ms = a;
     if (finalize_ms) *finalize_ms = f;

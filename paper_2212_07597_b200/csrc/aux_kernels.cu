@@ -118,9 +118,15 @@ __device__ __forceinline__ bool gate_open(const FinalParams& p) {
     return g[2] > 0 && (__int128)100 * (__int128)gnum >= (__int128)gden;
 }
 
+__device__ __forceinline__ void gate_copy(const FinalParams& p) {   // to the host-mapped buffer
+    const unsigned long long* g = p.table + (size_t)p.n_sites * SCL_NCOL;
+    p.gate_out[0] = g[0]; p.gate_out[1] = g[1]; p.gate_out[2] = g[2];
+}
+
 __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ FinalParams p)
 {
     const bool open = gate_open(p);
+    if (blockIdx.x == 0 && threadIdx.x == 0) gate_copy(p);
     for (unsigned sidx = blockIdx.x * blockDim.x + threadIdx.x; sidx < p.n_sites; sidx += gridDim.x * blockDim.x) {
         const SiteStat st = site_stat(p, sidx, open);
         p.prob[sidx] = st.prob; p.rate[sidx] = st.rate; p.flag[sidx] = st.flag ? 1 : 0;
@@ -154,7 +160,7 @@ __global__ void __launch_bounds__(1024) report_kernel(const __grid_constant__ Fi
     const unsigned tid = threadIdx.x, S = p.n_sites;
     const unsigned per = (S + 1023) / 1024, s0 = min(S, tid * per), s1 = min(S, s0 + per);
     const bool open = gate_open(p);
-    if (tid == 0) nflag = 0;
+    if (tid == 0) { nflag = 0; gate_copy(p); }
     __syncthreads();
     unsigned cf = 0;
     for (unsigned sidx = s0; sidx < s1; ++sidx) {

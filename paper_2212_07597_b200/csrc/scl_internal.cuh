@@ -110,6 +110,7 @@ struct FinalParams {
     double elapsed_ns;
     double* prob; double* rate; unsigned char* flag;
     unsigned long long* key1; unsigned int* val;   // sort inputs
+    unsigned long long* gate_out;     // [3] host-mapped pinned buffer: the gate sums (written by one thread)
 };
 
 // Per-run preparation (one launch instead of memsets + a host copy): zero the site table,

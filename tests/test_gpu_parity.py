@@ -210,11 +210,13 @@ def test_reload_grow_shrink_and_kernel_times():
         scl.scl_trace_reload(tr, ev, off, n_sites)
         assert (tr.n_traces, tr.n_sites) == (len(off) - 1, n_sites)
         for T in (97, 4001):
-            r = scl.scl_replay_run(T, tr, out=r)
+            r = scl.scl_replay_run(T, tr, out=r, timing=True)
             compare(ev, off, n_sites, T, r)
     assert len(scl.scl_result_kernel_times(r)) == 2 * (len(batches) + 1)
+    r = scl.scl_replay_run(97, tr, out=r)                  # untimed runs record no kernel events
+    assert scl.scl_result_timing(r) == (-1, -1, -1) and scl.scl_result_kernel_times(r) == []
     for _ in range(3):
-        r = scl.scl_replay_run(97, tr, out=r)
+        r = scl.scl_replay_run(97, tr, out=r, timing=True)
     ks = scl.scl_result_kernel_times(r)
     assert len(ks) == 3 and all(k > 0 for k in ks)
     assert scl.scl_result_kernel_times(r) == []

@@ -6,10 +6,10 @@ import paper_2212_07597_b200 as scl, tracegen
 
 def timeit(tr, T, reps=10):
     r = None
-    for _ in range(3): r = scl.scl_replay_run(T, tr, out=r)
+    for _ in range(3): r = scl.scl_replay_run(T, tr, out=r, timing=True)
     ks, rs = [], []
     for _ in range(reps):
-        r = scl.scl_replay_run(T, tr, out=r); tm = scl.scl_result_timing(r); ks.append(tm[0]); rs.append(tm[1])
+        r = scl.scl_replay_run(T, tr, out=r, timing=True); tm = scl.scl_result_timing(r); ks.append(tm[0]); rs.append(tm[1])
     s = scl.scl_trace_summaries(r)
     return statistics.median(ks), int(s["n_samples"].sum()), statistics.median(rs)
 

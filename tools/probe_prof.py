@@ -13,7 +13,7 @@ ev, off = tracegen.generate(cfg)
 tr = scl.scl_trace_load(ev, off, cfg.n_sites)
 r = None
 for _ in range(4):
-    r = scl.scl_replay_run(T, tr, out=r)
+    r = scl.scl_replay_run(T, tr, out=r, timing=True)
 ms = scl.scl_result_timing(r)[0]
 nunits_all = int(sum((cfg.events_per_trace + 8191) // 8192 for _ in range(nt)))
 bigbuf = np.zeros(48 + 4 * nunits_all, dtype=np.uint64)
