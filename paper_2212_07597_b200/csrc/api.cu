@@ -403,6 +403,15 @@ static scl_status alloc_result(scl_result* r, const scl_traces* tr) {
     return SCL_OK;
 }
 
+static FinalParams final_params(scl_result* r) {
+    FinalParams f{};
+    f.table = r->d_table; f.n_sites = r->tr->n_sites; f.formula = r->formula;
+    f.elapsed_ns = (double)(r->elapsed_ns ? r->elapsed_ns : 1);
+    f.prob = r->d_prob; f.rate = r->d_rate; f.flag = r->d_flag; f.key1 = r->d_key; f.val = r->d_val;
+    f.gate_out = r->h_gate;                    // pinned host memory, device-accessible (unified addressing)
+    return f;
+}
+
 extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, const scl_run_opts* opts, scl_result** out)
 {
     if (!tr || !out) return fail(SCL_EINVAL, "NULL argument");
@@ -488,8 +497,18 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
     if (tm) CU(cudaEventRecord(r->kev[2 * ks], st));
     CU(launch_replay(&tr->tmap, p, r->grid, st));
     if (tm) { CU(cudaEventRecord(r->kev[2 * ks + 1], st)); r->nrun += 1; }
+    // a6 fused into the post pass (its last block) when the run finalizes at once on a small table
+    const bool fuse = !o.defer_finalize && report_fused(tr->n_sites);
+    if (fuse) { p.fuse_report = 1; p.fin = final_params(r); p.rows = r->d_rows; }
     CU(launch_post(p, st));
     if (tm) CU(cudaEventRecord(r->ev[1], st));
+    if (fuse) {
+        if (tm) CU(cudaEventRecord(r->ev[2], st));
+        CU(cudaEventRecord(r->ev[3], st));
+        r->finalized = true;
+        *out = r;
+        return SCL_OK;
+    }
     *out = r;
     if (!o.defer_finalize) {
         scl_status s3 = scl_finalize(r, 0);
@@ -513,11 +532,7 @@ extern "C" scl_status scl_finalize(scl_result* r, uint64_t elapsed_ns) {
     if (elapsed_ns) r->elapsed_ns = elapsed_ns;
     const unsigned S = tr->n_sites;
     if (r->timed) CU(cudaEventRecord(r->ev[2], st));
-    FinalParams f{};
-    f.table = r->d_table; f.n_sites = S; f.formula = r->formula;
-    f.elapsed_ns = (double)(r->elapsed_ns ? r->elapsed_ns : 1);
-    f.prob = r->d_prob; f.rate = r->d_rate; f.flag = r->d_flag; f.key1 = r->d_key; f.val = r->d_val;
-    f.gate_out = r->h_gate;                    // pinned host memory, device-accessible (unified addressing)
+    const FinalParams f = final_params(r);
     if (report_fused(S)) {
         CU(launch_report(f, r->d_rows, st));
     } else {

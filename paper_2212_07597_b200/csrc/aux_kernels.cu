@@ -4,6 +4,7 @@
 //   rows_kernel        report rows in report order
 #include "scl_internal.cuh"
 #include "ptx.cuh"
+#include "report.cuh"
 #include <algorithm>
 
 namespace scl {
@@ -92,37 +93,6 @@ __global__ void __launch_bounds__(1024) prep_kernel(const __grid_constant__ Prep
 }
 
 // ============================================================================ a6
-// Probability, rate and flag of one site, from the summed table.
-struct SiteStat { double prob, rate; bool flag; };
-__device__ __forceinline__ SiteStat site_stat(const FinalParams& p, unsigned sidx, bool open)
-{
-    const unsigned long long* row = p.table + (size_t)sidx * SCL_NCOL;
-    const unsigned long long m = row[SCL_COL_LEAK_MALLOCS], f = row[SCL_COL_LEAK_FREES];
-    SiteStat r;
-    bool over;
-    if (p.formula == SCL_FORMULA_TEXTBOOK) {
-        r.prob = __dsub_rn(1.0, __ddiv_rn((double)(f + 1), (double)(m + 2)));
-        over = (unsigned __int128)m > (unsigned __int128)20 * f + 18;
-    } else {   // P:55-57, exactly as printed (reading Q8); flag p > 0.95 <=> m > 21 f + 18 (Q9)
-        r.prob = __dsub_rn(1.0, __ddiv_rn((double)(f + 1), (double)(m - f + 2)));
-        over = (unsigned __int128)m > (unsigned __int128)21 * f + 18;
-    }
-    r.rate = __ddiv_rn(__ddiv_rn((double)row[SCL_COL_MALLOC_BYTES], 1048576.0), __ddiv_rn(p.elapsed_ns, 1e9));
-    r.flag = open && over;
-    return r;
-}
-
-__device__ __forceinline__ bool gate_open(const FinalParams& p) {
-    const unsigned long long* g = p.table + (size_t)p.n_sites * SCL_NCOL;
-    const long long gnum = (long long)g[0], gden = (long long)g[1];
-    return g[2] > 0 && (__int128)100 * (__int128)gnum >= (__int128)gden;
-}
-
-__device__ __forceinline__ void gate_copy(const FinalParams& p) {   // to the host-mapped buffer
-    const unsigned long long* g = p.table + (size_t)p.n_sites * SCL_NCOL;
-    p.gate_out[0] = g[0]; p.gate_out[1] = g[1]; p.gate_out[2] = g[2];
-}
-
 __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ FinalParams p)
 {
     const bool open = gate_open(p);
@@ -137,70 +107,11 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ F
     }
 }
 
-__device__ __forceinline__ void write_row(const FinalParams& p, scl_site_row* rows, unsigned rank, unsigned sidx,
-                                          const SiteStat& st)
-{
-    scl_site_row r;
-    r.site = sidx; r.leak_flag = st.flag ? 1u : 0u;
-    #pragma unroll
-    for (int c = 0; c < SCL_NCOL; ++c) r.col[c] = p.table[(size_t)sidx * SCL_NCOL + c];
-    r.leak_prob = st.prob; r.leak_rate_mbps = st.rate;
-    rows[rank] = r;
-}
-
-// Whole a6 in one block (n_sites <= kReportSites): stats, report order, rows.  Rank of a flagged
-// site = flagged sites with a larger rate, or the same rate and a smaller site; rank of the
-// others = #flagged + unflagged sites before it (site order).
-constexpr unsigned kReportSites = 16384, kReportList = 2048;
+// Whole a6 in one block (n_sites <= kReportSites): report.cuh.
 __global__ void __launch_bounds__(1024) report_kernel(const __grid_constant__ FinalParams p, scl_site_row* rows)
 {
-    __shared__ double lrate[kReportList];
-    __shared__ unsigned lsite[kReportList];
-    __shared__ unsigned nflag, part[1024];
-    const unsigned tid = threadIdx.x, S = p.n_sites;
-    const unsigned per = (S + 1023) / 1024, s0 = min(S, tid * per), s1 = min(S, s0 + per);
-    const bool open = gate_open(p);
-    if (tid == 0) { nflag = 0; gate_copy(p); }
-    __syncthreads();
-    unsigned cf = 0;
-    for (unsigned sidx = s0; sidx < s1; ++sidx) {
-        const SiteStat st = site_stat(p, sidx, open);
-        if (st.flag) {
-            ++cf;
-            const unsigned k = atomicAdd(&nflag, 1u);
-            if (k < kReportList) { lrate[k] = st.rate; lsite[k] = sidx; }
-        }
-    }
-    part[tid] = cf;
-    __syncthreads();
-    for (unsigned d = 1; d < 1024; d <<= 1) {               // inclusive scan of the flag counts
-        const unsigned v = tid >= d ? part[tid - d] : 0;
-        __syncthreads();
-        part[tid] += v;
-        __syncthreads();
-    }
-    const unsigned F = nflag;
-    unsigned fb = part[tid] - cf;                           // flagged sites before s0
-    for (unsigned sidx = s0; sidx < s1; ++sidx) {
-        const SiteStat st = site_stat(p, sidx, open);
-        unsigned rank;
-        if (!st.flag) {
-            rank = F + (sidx - fb);
-        } else {
-            rank = 0;
-            if (F <= kReportList) {
-                for (unsigned k = 0; k < F; ++k)
-                    rank += (lrate[k] > st.rate || (lrate[k] == st.rate && lsite[k] < sidx)) ? 1u : 0u;
-            } else {                                        // many flagged sites: compare against all
-                for (unsigned j = 0; j < S; ++j) {
-                    const SiteStat o = site_stat(p, j, open);
-                    rank += (o.flag && (o.rate > st.rate || (o.rate == st.rate && j < sidx))) ? 1u : 0u;
-                }
-            }
-            ++fb;
-        }
-        write_row(p, rows, rank, sidx, st);
-    }
+    extern __shared__ __align__(16) unsigned char report_smem[];
+    report_block<1024>(p, rows, *reinterpret_cast<ReportSmem<1024>*>(report_smem));
 }
 
 __global__ void __launch_bounds__(256) rows_kernel(const unsigned long long* table, const double* prob, const double* rate,
@@ -243,7 +154,14 @@ bool report_fused(unsigned n_sites) { return n_sites <= kReportSites; }
 
 cudaError_t launch_report(const FinalParams& p, scl_site_row* rows, cudaStream_t st)
 {
-    report_kernel<<<1, 1024, 0, st>>>(p, rows);
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(report_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)report_smem_bytes<1024>());
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    report_kernel<<<1, 1024, report_smem_bytes<1024>(), st>>>(p, rows);
     return cudaGetLastError();
 }
 

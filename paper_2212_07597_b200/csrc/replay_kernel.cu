@@ -28,6 +28,7 @@
 #include <algorithm>
 #include "scl_internal.cuh"
 #include "ptx.cuh"
+#include "report.cuh"
 
 namespace scl {
 
@@ -619,16 +620,20 @@ __device__ void runner_role(const ReplayParams& p, unsigned ri, int lane)
     PROF_FLUSH(16)
 }
 
-// ============================================================================ post pass: reclaim (a4) + per-sample reduce
-// One persistent launch, every block resident (grid = blocks that fit), three phases:
-//  1. one warp per unit settles the leak tracker's free-pointer comparison for every
-//     episode segment inside the unit -- the episode entering it (UnitEntry) up to the first
-//     episode started in it, then each episode started in it up to the next (an episode is
-//     reclaimed iff its pointer is freed anywhere in its span, so units are independent):
-//     Bloom query per chunk (lane <-> chunk); each positive chunk becomes an exact re-check task;
-//  2. after all units: the re-check tasks, spread over all warps (one chunk each, through L2);
-//  3. after all re-checks: the per-sample reduce, one warp per trace.
-// ep_flag was zeroed by the runner at each episode's start; phases 1-2 only set it.
+// ============================================================================ post pass: reclaim (a4) + per-sample reduce (+ a6)
+// One persistent cooperative launch (every block resident):
+//  A. units (strided over the warps): a warp settles each unit that carries an episode or
+//     samples -- the leak tracker's free-pointer comparison for every episode segment
+//     inside the unit: the episode entering it up to the first episode started in it, then each
+//     episode started in it up to the next (an episode is reclaimed iff its pointer is freed
+//     anywhere in its span, so units are independent): Bloom query per chunk (lane <-> chunk),
+//     each positive chunk queued as an exact re-check task;
+//     traces: the per-sample reduce, one warp per trace;
+//  -- grid barrier --
+//  B. the re-check tasks, spread over all warps (one chunk each, through L2).  The first re-check
+//     that finds the free of an episode flips its ep_flag and counts the episode's frees;
+//  C. with fuse_report: the last block to finish runs a6 (report.cuh) on the complete table.
+// ep_flag was zeroed by the runner at each episode's start.
 __device__ __forceinline__ bool chunk_has_free(const ReplayParams& p, long long row0, long long off_t, long long n_t,
                                                unsigned pos0, unsigned long long ptr, unsigned sbeg, unsigned send, int lane)
 {
@@ -645,10 +650,17 @@ __device__ __forceinline__ bool chunk_has_free(const ReplayParams& p, long long 
     return __any_sync(kFull, hit);
 }
 
-__device__ void reclaim_unit(const ReplayParams& p, unsigned u, int lane)
+// The episode whose tracked object is freed: once, ep_flag 0 -> 1 and one free for its site.
+__device__ __forceinline__ void reclaimed(const ReplayParams& p, unsigned long long ep1) {
+    if (atomicExch(&p.ep_flag[ep1 - 1], 1u) == 0u) {
+        const unsigned site = p.samples[ep1 - 1].site;
+        atomicAdd(&p.table[(size_t)site * SCL_NCOL + SCL_COL_LEAK_FREES], 1ull);
+    }
+}
+
+__device__ void reclaim_unit(const ReplayParams& p, unsigned u, const UnitEntry& ent, int lane)
 {
     const Slot& S = reinterpret_cast<const Slot*>(p.urec)[u];
-    const UnitEntry ent = p.uent[u];
     const long long row_base = S.info.row_base, off_t = S.info.off_t, n_t = S.info.n_t;
     const long long g0 = row_base * kEpt;                    // global event index of unit position 0
     unsigned long long ep1 = ent.ep1, ptr = ent.eptr;        // current segment: episode (slot + 1), pointer, start
@@ -676,7 +688,7 @@ __device__ void reclaim_unit(const ReplayParams& p, unsigned u, int lane)
                 const int ch = __ffs(c) - 1;
                 found = chunk_has_free(p, row_base + (long long)ch * 32, off_t, n_t, (unsigned)ch * 32 * kEpt, ptr, sbeg, send, lane);
             }
-            if (found && lane == 0) p.ep_flag[ep1 - 1] = 1u;
+            if (found && lane == 0) reclaimed(p, ep1);
         }
     };
     for (unsigned long long s0 = ent.s_in; s0 < ent.s_out; s0 += 32) {     // samples taken in this unit
@@ -709,39 +721,57 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr) {
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) post_kernel(const __grid_constant__ ReplayParams p)
+__global__ void __launch_bounds__(256, 2) post_kernel(const __grid_constant__ ReplayParams p)
 {
+    extern __shared__ __align__(16) unsigned char post_smem[];            // a6 of the last block (fuse_report)
+    __shared__ unsigned last;
     const int lane = threadIdx.x & 31;
     const unsigned wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-    for (unsigned u = wid; u < p.n_segs; u += nw) reclaim_unit(p, u, lane);              // phase 1
+    for (unsigned u = wid; u < p.n_segs; u += nw) {                                       // phase A
+        const UnitEntry ent = p.uent[u];                     // units spread over the warps
+        if (ent.ep1 != 0 || ent.s_in != ent.s_out) reclaim_unit(p, u, ent, lane);
+    }
+    for (unsigned t = wid; t < p.n_traces; t += nw) samples_trace(p, t, lane);
     grid_barrier(&p.ticket[1]);
     const unsigned ntask = min(ld_acquire(&p.ticket[2]), p.rtask_cap);
-    for (unsigned h = wid; h < ntask; h += nw) {                                          // phase 2
+    for (unsigned h = wid; h < ntask; h += nw) {                                          // phase B
         const RTask tk = p.rtask[h];
         if (chunk_has_free(p, tk.row0, tk.off_t, tk.n_t, tk.pos0, tk.ptr, tk.sbeg, tk.send, lane) && lane == 0)
-            p.ep_flag[tk.ep1 - 1] = 1u;
+            reclaimed(p, tk.ep1);
     }
-    grid_barrier(&p.ticket[3]);
-    for (unsigned t = wid; t < p.n_traces; t += nw) samples_trace(p, t, lane);            // phase 3
+    if (!p.fuse_report) return;                                                           // phase C
+    __syncthreads();
+    if (threadIdx.x == 0) { __threadfence(); last = atomicAdd(&p.ticket[3], 1u) == gridDim.x - 1; }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    report_block<256>(p.fin, p.rows, *reinterpret_cast<ReportSmem<256>*>(post_smem));
 }
 
 cudaError_t launch_post(const ReplayParams& p, cudaStream_t st)
 {
     static int occ = 0, nsm = 0;
+    const size_t smem = p.fuse_report ? report_smem_bytes<256>() : 0;
+    static int occ_fused = 0;
     if (!occ) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, post_kernel, 256, 0);
+        cudaError_t e = cudaFuncSetAttribute(post_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)report_smem_bytes<256>());
         if (e != cudaSuccess) return e;
-        if (occ < 1) occ = 1;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, post_kernel, 256, 0);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_fused, post_kernel, 256, report_smem_bytes<256>());
+        if (e != cudaSuccess) return e;
+        occ = std::max(occ, 1); occ_fused = std::max(occ_fused, 1);
     }
     // every block resident (the phases wait for all warps): a cooperative launch of at most
     // occupancy x SMs blocks
     const unsigned need = std::max<unsigned>((std::max(p.n_segs, p.n_traces) + 7) / 8, 1u);
-    const unsigned grid = std::min<unsigned>(need, (unsigned)(occ * nsm));
+    const unsigned grid = std::min<unsigned>(need, (unsigned)((p.fuse_report ? occ_fused : occ) * nsm));
     void* args[] = {const_cast<ReplayParams*>(&p)};
-    return cudaLaunchCooperativeKernel((const void*)post_kernel, dim3(grid), dim3(256), args, 0, st);
+    return cudaLaunchCooperativeKernel((const void*)post_kernel, dim3(grid), dim3(256), args, smem, st);
 }
 
 // ============================================================================ kernel

@@ -1,0 +1,154 @@
+// report.cuh -- a6 for one block: per-site probability, rate and flag, the report order and the
+// rows (readings Q8-Q11 of DESIGN.md §3).  Used by report_kernel (1024 threads) and by
+// the last block of post_kernel (256 threads) when the run finalizes at once.
+#pragma once
+#include "scl_internal.cuh"
+
+namespace scl {
+
+// Probability, rate and flag of one site, from the summed table.
+// The flag is an integer decision (no division); bytes / 2^20 is an exact scaling.
+struct SiteStat { double prob, rate; bool flag; };
+__device__ __forceinline__ bool site_over(const FinalParams& p, unsigned long long m, unsigned long long f) {
+    return p.formula == SCL_FORMULA_TEXTBOOK ? (unsigned __int128)m > (unsigned __int128)20 * f + 18    // 1-(f+1)/(m+2) > 0.95
+                                             : (unsigned __int128)m > (unsigned __int128)21 * f + 18;   // reading Q9
+}
+__device__ __forceinline__ double site_prob(const FinalParams& p, unsigned long long m, unsigned long long f) {
+    return p.formula == SCL_FORMULA_TEXTBOOK ? __dsub_rn(1.0, __ddiv_rn((double)(f + 1), (double)(m + 2)))
+                                             : __dsub_rn(1.0, __ddiv_rn((double)(f + 1), (double)(m - f + 2)));   // Q8
+}
+__device__ __forceinline__ double site_rate(unsigned long long bytes, double elapsed_s) {
+    return __ddiv_rn(__dmul_rn((double)bytes, 1.0 / 1048576.0), elapsed_s);     // MB / s (Q11)
+}
+__device__ __forceinline__ double elapsed_s(const FinalParams& p) { return __ddiv_rn(p.elapsed_ns, 1e9); }
+__device__ __forceinline__ SiteStat site_stat(const FinalParams& p, unsigned sidx, bool open)
+{
+    const unsigned long long* row = p.table + (size_t)sidx * SCL_NCOL;
+    const unsigned long long m = __ldcg(&row[SCL_COL_LEAK_MALLOCS]), f = __ldcg(&row[SCL_COL_LEAK_FREES]);
+    SiteStat r;
+    r.prob = site_prob(p, m, f);
+    r.rate = site_rate(__ldcg(&row[SCL_COL_MALLOC_BYTES]), elapsed_s(p));
+    r.flag = open && site_over(p, m, f);
+    return r;
+}
+
+__device__ __forceinline__ bool gate_open(const FinalParams& p) {
+    const unsigned long long* g = p.table + (size_t)p.n_sites * SCL_NCOL;
+    const long long gnum = (long long)__ldcg(&g[0]), gden = (long long)__ldcg(&g[1]);
+    return __ldcg(&g[2]) > 0 && (__int128)100 * (__int128)gnum >= (__int128)gden;
+}
+
+__device__ __forceinline__ void gate_copy(const FinalParams& p) {   // to the host-mapped buffer
+    const unsigned long long* g = p.table + (size_t)p.n_sites * SCL_NCOL;
+    p.gate_out[0] = __ldcg(&g[0]); p.gate_out[1] = __ldcg(&g[1]); p.gate_out[2] = __ldcg(&g[2]);
+}
+
+
+constexpr unsigned kReportSites = 16384, kReportList = 2048, kRowWords = sizeof(scl_site_row) / 8;   // 13
+template <int NT> struct ReportSmem {
+    double lrate[kReportList]; unsigned lsite[kReportList];          // flagged sites (any order)
+    unsigned bits[kReportSites / 32], wpre[kReportSites / 32];        // flag bitmask, flags before each word
+    unsigned wsum[32], nflag;
+    unsigned long long stage[NT / 32][32 * kRowWords];                // per-warp row staging (coalesced writes)
+};
+template <int NT> constexpr size_t report_smem_bytes() { return sizeof(ReportSmem<NT>); }
+
+__device__ __forceinline__ void stat_row(const FinalParams& p, unsigned sidx, const SiteStat& st, unsigned long long* w) {
+    scl_site_row r;
+    r.site = sidx; r.leak_flag = st.flag ? 1u : 0u;
+    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(p.table + (size_t)sidx * SCL_NCOL);   // 80 B, 16-B aligned
+    #pragma unroll
+    for (int c = 0; c < SCL_NCOL / 2; ++c) { const ulonglong2 v = __ldcg(src + c); r.col[2 * c] = v.x; r.col[2 * c + 1] = v.y; }
+    r.leak_prob = st.prob; r.leak_rate_mbps = st.rate;
+    const unsigned long long* q = reinterpret_cast<const unsigned long long*>(&r);
+    #pragma unroll
+    for (int k = 0; k < (int)kRowWords; ++k) w[k] = q[k];
+}
+
+// Report order: flagged sites by (rate desc, site asc), then the others by site (a6).  Rank of a
+// flagged site = flagged sites with a larger rate, or the same rate and a smaller site; rank of an
+// unflagged site = #flagged + unflagged sites before it, so the unflagged sites of a warp's 32
+// consecutive sites take consecutive ranks: their rows are staged in shared memory and written
+// with lane-contiguous stores.  n_sites <= kReportSites; blockDim.x == NT.
+template <int NT>
+__device__ void report_block(const FinalParams& p, scl_site_row* rows, ReportSmem<NT>& sm)
+{
+    const unsigned tid = threadIdx.x, lane = tid & 31, wrp = tid >> 5, S = p.n_sites, nw = (S + 31) / 32;
+    const bool open = gate_open(p);
+    const double es = elapsed_s(p);
+    if (tid == 0) { sm.nflag = 0; gate_copy(p); }
+    __syncthreads();
+    for (unsigned base = 0; base < S; base += NT) {          // pass 1: flags (integer only), flagged list
+        const unsigned sidx = base + tid;
+        bool fl = false;
+        if (sidx < S) {
+            const unsigned long long* row = p.table + (size_t)sidx * SCL_NCOL;
+            const unsigned long long m = __ldcg(&row[SCL_COL_LEAK_MALLOCS]), f = __ldcg(&row[SCL_COL_LEAK_FREES]);
+            fl = open && site_over(p, m, f);
+            if (fl) {
+                const unsigned k = atomicAdd(&sm.nflag, 1u);
+                if (k < kReportList) { sm.lrate[k] = site_rate(__ldcg(&row[SCL_COL_MALLOC_BYTES]), es); sm.lsite[k] = sidx; }
+            }
+        }
+        const unsigned word = __ballot_sync(kFull, fl);
+        if (lane == 0 && (base >> 5) + wrp < nw) sm.bits[(base >> 5) + wrp] = word;
+    }
+    __syncthreads();
+    for (unsigned w0 = 0; w0 < nw; w0 += NT) {              // exclusive prefix of flags per word
+        const unsigned w = w0 + tid;
+        const unsigned c = w < nw ? __popc(sm.bits[w]) : 0u;
+        unsigned inc = c;
+        #pragma unroll
+        for (int d = 1; d < 32; d <<= 1) { const unsigned o = __shfl_up_sync(kFull, inc, d); if (lane >= (unsigned)d) inc += o; }
+        if (lane == 31) sm.wsum[wrp] = inc;
+        __syncthreads();
+        unsigned wb = w0 ? sm.wpre[w0 - 1] + __popc(sm.bits[w0 - 1]) : 0u;
+        for (unsigned q = 0; q < wrp; ++q) wb += sm.wsum[q];
+        if (w < nw) sm.wpre[w] = wb + inc - c;
+        __syncthreads();
+    }
+    const unsigned F = sm.nflag;
+    unsigned long long* stg = sm.stage[wrp];
+    for (unsigned base = 0; base < S; base += NT) {          // pass 2: stats, ranks, rows
+        const unsigned sidx = base + tid, wd = sidx >> 5;
+        const bool in = sidx < S;
+        const unsigned word = in ? sm.bits[wd] : 0u;
+        const bool fl = in && ((word >> lane) & 1u);
+        const unsigned um = __ballot_sync(kFull, in && !fl);  // unflagged lanes: consecutive ranks
+        unsigned long long w[kRowWords];
+        if (in) {
+            const SiteStat st = site_stat(p, sidx, open);
+            stat_row(p, sidx, st, w);
+            if (fl) {
+                unsigned rank = 0;
+                if (F <= kReportList) {
+                    for (unsigned k = 0; k < F; ++k)
+                        rank += (sm.lrate[k] > st.rate || (sm.lrate[k] == st.rate && sm.lsite[k] < sidx)) ? 1u : 0u;
+                } else {                                    // many flagged sites: compare against all
+                    for (unsigned j = 0; j < S; ++j) {
+                        const SiteStat o = site_stat(p, j, open);
+                        rank += (o.flag && (o.rate > st.rate || (o.rate == st.rate && j < sidx))) ? 1u : 0u;
+                    }
+                }
+                unsigned long long* dst = reinterpret_cast<unsigned long long*>(rows + rank);
+                #pragma unroll
+                for (int k = 0; k < (int)kRowWords; ++k) dst[k] = w[k];
+            } else {
+                const unsigned j = __popc(um & ((1u << lane) - 1u));          // slot among the warp's unflagged
+                #pragma unroll
+                for (int k = 0; k < (int)kRowWords; ++k) stg[j * kRowWords + k] = w[k];
+            }
+        }
+        __syncwarp();
+        if (um) {
+            const unsigned s_first = (base & ~31u) + (wrp << 5) + (unsigned)(__ffs(um) - 1);
+            const unsigned r0 = F + s_first - (sm.wpre[s_first >> 5] + __popc(sm.bits[s_first >> 5] & ((1u << (s_first & 31)) - 1u)));
+            unsigned long long* dst = reinterpret_cast<unsigned long long*>(rows + r0);
+            const unsigned nwds = (unsigned)__popc(um) * kRowWords;
+            for (unsigned k = lane; k < nwds; k += 32) dst[k] = stg[k];
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace scl

@@ -67,6 +67,16 @@ struct __align__(16) TicketInfo {
     unsigned t, kraw, slot, nbox;     // trace, unit index (| last << 31), state slot, boxes overlapping the trace
 };
 
+struct FinalParams {
+    const unsigned long long* table;  // [n_sites*SCL_NCOL + 3]
+    unsigned int n_sites;
+    int formula;
+    double elapsed_ns;
+    double* prob; double* rate; unsigned char* flag;
+    unsigned long long* key1; unsigned int* val;   // sort inputs
+    unsigned long long* gate_out;     // [3] host-mapped pinned buffer: the gate sums (written by one thread)
+};
+
 // One exact re-check of the reclaim pass: chunk rows [row0, row0 + 32) of a unit, unit positions
 // [sbeg, send), does any free of `ptr` occur?  (pos0: unit position of the chunk's first event.)
 struct __align__(16) RTask {
@@ -88,6 +98,9 @@ struct ReplayParams {
     unsigned int* ticket;             // [4]: unit tickets; post pass: units settled, task tail, warps done (zeroed per run)
     RTask* rtask;                     // [rtask_cap] exact re-checks queued by the reclaim pass
     unsigned int rtask_cap;
+    int fuse_report;                  // post_kernel's last block runs a6 (fin -> rows)
+    FinalParams fin;
+    scl_site_row* rows;
     unsigned int n_segs;
     unsigned int n_stream;            // CTAs [0, n_stream) stream units, the rest run traces
     unsigned int n_runners;           // embedded: gridDim.x * 2; dedicated: (gridDim.x - n_stream) * kRunnersPerCta
@@ -103,15 +116,6 @@ struct ReplayParams {
     unsigned long long* prof;         // debug build only (SCL_PROFILE): per-role cycle sums, else NULL
 };
 
-struct FinalParams {
-    const unsigned long long* table;  // [n_sites*SCL_NCOL + 3]
-    unsigned int n_sites;
-    int formula;
-    double elapsed_ns;
-    double* prob; double* rate; unsigned char* flag;
-    unsigned long long* key1; unsigned int* val;   // sort inputs
-    unsigned long long* gate_out;     // [3] host-mapped pinned buffer: the gate sums (written by one thread)
-};
 
 // Per-run preparation (one launch instead of memsets + a host copy): zero the site table,
 // the trace summaries, the runner states and the ticket counter; sample slot bases
@@ -129,8 +133,8 @@ struct PrepParams {
 };
 
 #ifdef __CUDACC__
-// Per-sample reduce of trace t by one warp: Tier-S columns, leak score (mallocs at episode start,
-// frees if the episode's object was reclaimed), footprint-trend endpoints and the gate
+// Per-sample reduce of trace t by one warp: Tier-S columns, leak mallocs (one per episode start,
+// P:31-39; the frees are counted by the reclaim pass), footprint-trend endpoints and the gate
 // sums (reading Q10).
 __device__ __forceinline__ void samples_trace(const ReplayParams& p, unsigned t, int lane)
 {
@@ -141,10 +145,7 @@ __device__ __forceinline__ void samples_trace(const ReplayParams& p, unsigned t,
         unsigned long long* row = p.table + (size_t)sm.site * SCL_NCOL;
         if (sm.kind == 0) { atomicAdd(&row[SCL_COL_N_GROWTH], 1ull); atomicAdd(&row[SCL_COL_GROWTH_BYTES], (unsigned long long)sm.net); }
         else              { atomicAdd(&row[SCL_COL_N_DECLINE], 1ull); atomicAdd(&row[SCL_COL_DECLINE_BYTES], (unsigned long long)(-sm.net)); }
-        if (sm.new_max) {
-            atomicAdd(&row[SCL_COL_LEAK_MALLOCS], 1ull);
-            if (p.ep_flag[sb + i]) atomicAdd(&row[SCL_COL_LEAK_FREES], 1ull);
-        }
+        if (sm.new_max) atomicAdd(&row[SCL_COL_LEAK_MALLOCS], 1ull);     // (frees: the reclaim pass)
     }
     if (lane == 0) {
         long long ff = 0, fl = 0;
