@@ -409,6 +409,7 @@ static FinalParams final_params(scl_result* r) {
     f.elapsed_ns = (double)(r->elapsed_ns ? r->elapsed_ns : 1);
     f.prob = r->d_prob; f.rate = r->d_rate; f.flag = r->d_flag; f.key1 = r->d_key; f.val = r->d_val;
     f.gate_out = r->h_gate;                    // pinned host memory, device-accessible (unified addressing)
+    f.prof = r->d_prof;
     return f;
 }
 
@@ -491,6 +492,7 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
 #ifdef SCL_PROFILE
     if (!r->d_prof) CU(cudaMalloc(&r->d_prof, (48 + 4 * (size_t)tr->cap_segs) * 8));
     CU(cudaMemsetAsync(r->d_prof, 0, (48 + 4 * (size_t)tr->n_segs) * 8, st));
+    CU(cudaMemsetAsync(r->d_prof + 40, 0xff, 8, st));          // post pass start: atomicMin
     p.prof = r->d_prof;
 #endif
     const int ks = (int)(r->nrun % kRing);

@@ -108,10 +108,10 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ F
 }
 
 // Whole a6 in one block (n_sites <= kReportSites): report.cuh.
-__global__ void __launch_bounds__(1024) report_kernel(const __grid_constant__ FinalParams p, scl_site_row* rows)
+__global__ void __launch_bounds__(512) report_kernel(const __grid_constant__ FinalParams p, scl_site_row* rows)
 {
     extern __shared__ __align__(16) unsigned char report_smem[];
-    report_block<1024>(p, rows, *reinterpret_cast<ReportSmem<1024>*>(report_smem));
+    report_block<512>(p, rows, *reinterpret_cast<ReportSmem<512>*>(report_smem));
 }
 
 __global__ void __launch_bounds__(256) rows_kernel(const unsigned long long* table, const double* prob, const double* rate,
@@ -157,11 +157,11 @@ cudaError_t launch_report(const FinalParams& p, scl_site_row* rows, cudaStream_t
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(report_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)report_smem_bytes<1024>());
+                                             (int)report_smem_bytes<512>());
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    report_kernel<<<1, 1024, report_smem_bytes<1024>(), st>>>(p, rows);
+    report_kernel<<<1, 512, report_smem_bytes<512>(), st>>>(p, rows);
     return cudaGetLastError();
 }
 

@@ -283,6 +283,9 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
 __device__ void producer_role(const ReplayParams& p, const CUtensorMap* tmap, Smem& s, unsigned char* stage, int lane)
 {
     if (lane != 0) return;
+    // the events are streamed once: evict them first, keeping the unit records, samples and the
+    // site table (which the runners and the post pass re-read) in L2
+    const uint64_t pol = l2_policy_evict_first();
     PROF_DECL
     auto resolve = [&](unsigned u) {
         SegInfo inf; inf.u = kInvalid; inf.nbox = 0;
@@ -313,8 +316,8 @@ __device__ void producer_role(const ReplayParams& p, const CUtensorMap* tmap, Sm
                 if (cur.u == kInvalid && g == 0) continue; // the sentinel goes to both compute groups
             } else {
                 mbar_expect_tx(&s.full[st], kSegBytes);
-                tma_load_2d(stage + (size_t)st * kSegBytes, tmap, 0, (int)(cur.row_base + (long long)g * kThreads),
-                            &s.full[st]);
+                tma_load_2d_hint(stage + (size_t)st * kSegBytes, tmap, 0, (int)(cur.row_base + (long long)g * kThreads),
+                                 &s.full[st], pol);
             }
             if (cur.u == kInvalid) { PROF_FLUSH(8) return; }
         }
@@ -651,20 +654,22 @@ __device__ __forceinline__ bool chunk_has_free(const ReplayParams& p, long long 
 }
 
 // The episode whose tracked object is freed: once, ep_flag 0 -> 1 and one free for its site.
-__device__ __forceinline__ void reclaimed(const ReplayParams& p, unsigned long long ep1) {
-    if (atomicExch(&p.ep_flag[ep1 - 1], 1u) == 0u) {
-        const unsigned site = p.samples[ep1 - 1].site;
+__device__ __forceinline__ void reclaimed(const ReplayParams& p, unsigned long long ep1, unsigned site) {
+    if (atomicExch(&p.ep_flag[ep1 - 1], 1u) == 0u)
         atomicAdd(&p.table[(size_t)site * SCL_NCOL + SCL_COL_LEAK_FREES], 1ull);
-    }
 }
 
-__device__ void reclaim_unit(const ReplayParams& p, unsigned u, const UnitEntry& ent, int lane)
+struct UnitCtx { long long row_base, off_t, n_t; unsigned long long ep1, eptr, s_in, s_out; };
+
+__device__ void reclaim_unit(const ReplayParams& p, unsigned u, const UnitCtx& x, int lane)
 {
     const Slot& S = reinterpret_cast<const Slot*>(p.urec)[u];
-    const long long row_base = S.info.row_base, off_t = S.info.off_t, n_t = S.info.n_t;
+    const long long row_base = x.row_base, off_t = x.off_t, n_t = x.n_t;
     const long long g0 = row_base * kEpt;                    // global event index of unit position 0
-    unsigned long long ep1 = ent.ep1, ptr = ent.eptr;        // current segment: episode (slot + 1), pointer, start
-    unsigned sbeg = 0;
+    unsigned long long ep1 = x.ep1, ptr = x.eptr;            // current segment: episode (slot + 1), pointer, start
+    unsigned sbeg = 0, site = 0;
+    const bool in_ep = ep1 != 0;
+    if (in_ep) site = __ldcg(&p.samples[ep1 - 1].site);      // (in flight with the Bloom words below)
     auto segment = [&](unsigned send) {                      // [sbeg, send) of the current episode
         if (!ep1 || send <= sbeg) return;
         const unsigned w = bloom_word(ptr), msk = bloom_mask(ptr);
@@ -679,7 +684,7 @@ __device__ void reclaim_unit(const ReplayParams& p, unsigned u, const UnitEntry&
             if (pos) {
                 RTask tk;
                 tk.ep1 = ep1; tk.ptr = ptr; tk.row0 = row_base + (long long)lane * 32; tk.off_t = off_t; tk.n_t = n_t;
-                tk.pos0 = cb; tk.sbeg = sbeg; tk.send = send; tk.pad = 0;
+                tk.pos0 = cb; tk.sbeg = sbeg; tk.send = send; tk.site = site;
                 p.rtask[base + __popc(cm & ((1u << lane) - 1u))] = tk;
             }
         } else {                                             // queue full: re-check here, in order
@@ -688,13 +693,13 @@ __device__ void reclaim_unit(const ReplayParams& p, unsigned u, const UnitEntry&
                 const int ch = __ffs(c) - 1;
                 found = chunk_has_free(p, row_base + (long long)ch * 32, off_t, n_t, (unsigned)ch * 32 * kEpt, ptr, sbeg, send, lane);
             }
-            if (found && lane == 0) reclaimed(p, ep1);
+            if (found && lane == 0) reclaimed(p, ep1, site);
         }
     };
-    for (unsigned long long s0 = ent.s_in; s0 < ent.s_out; s0 += 32) {     // samples taken in this unit
+    for (unsigned long long s0 = x.s_in; s0 < x.s_out; s0 += 32) {         // samples taken in this unit
         const unsigned long long si = s0 + (unsigned long long)lane;
-        bool nm = false; long long idx = 0;
-        if (si < ent.s_out) { const scl_sample smp = p.samples[si]; nm = smp.new_max != 0; idx = (long long)smp.idx; }
+        bool nm = false; long long idx = 0; unsigned st = 0;
+        if (si < x.s_out) { const scl_sample smp = p.samples[si]; nm = smp.new_max != 0; idx = (long long)smp.idx; st = smp.site; }
         unsigned em = __ballot_sync(kFull, nm);
         while (em) {
             const int e = __ffs(em) - 1;
@@ -704,6 +709,7 @@ __device__ void reclaim_unit(const ReplayParams& p, unsigned u, const UnitEntry&
             segment(pos);
             ep1 = s0 + (unsigned long long)e + 1;
             ptr = __ldcg(&p.ev[off_t + ie].ptr);
+            site = __shfl_sync(kFull, st, e);
             sbeg = pos;
         }
     }
@@ -721,31 +727,62 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr) {
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(256, 2) post_kernel(const __grid_constant__ ReplayParams p)
+__global__ void __launch_bounds__(256, 3) post_kernel(const __grid_constant__ ReplayParams p)
 {
     extern __shared__ __align__(16) unsigned char post_smem[];            // a6 of the last block (fuse_report)
     __shared__ unsigned last;
     const int lane = threadIdx.x & 31;
     const unsigned wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-    for (unsigned u = wid; u < p.n_segs; u += nw) {                                       // phase A
-        const UnitEntry ent = p.uent[u];                     // units spread over the warps
-        if (ent.ep1 != 0 || ent.s_in != ent.s_out) reclaim_unit(p, u, ent, lane);
+#ifdef SCL_PROFILE
+#define POST_T(i, op) if (p.prof && lane == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); op(&p.prof[40 + (i)], t_); }
+    POST_T(0, atomicMin)
+#else
+#define POST_T(i, op)
+#endif
+    for (unsigned k0 = 0; wid + k0 * nw < p.n_segs; k0 += 32) {                           // phase A
+        // this warp's units wid + k*nw: lane k loads unit k's entry and placement at once
+        const unsigned u = wid + (k0 + (unsigned)lane) * nw;
+        UnitCtx c{0, 0, 0, 0, 0, 0, 0};
+        if (u < p.n_segs) {
+            const UnitEntry e = p.uent[u];
+            const SegInfo& inf = reinterpret_cast<const Slot*>(p.urec)[u].info;
+            c.row_base = inf.row_base; c.off_t = inf.off_t; c.n_t = inf.n_t;
+            c.ep1 = e.ep1; c.eptr = e.eptr; c.s_in = e.s_in; c.s_out = e.s_out;
+        }
+        unsigned todo = __ballot_sync(kFull, u < p.n_segs && (c.ep1 != 0 || c.s_in != c.s_out));
+        while (todo) {
+            const int i = __ffs(todo) - 1;
+            todo &= todo - 1;
+            UnitCtx x;
+            x.row_base = shfl_ll(c.row_base, i); x.off_t = shfl_ll(c.off_t, i); x.n_t = shfl_ll(c.n_t, i);
+            x.ep1 = __shfl_sync(kFull, c.ep1, i); x.eptr = __shfl_sync(kFull, c.eptr, i);
+            x.s_in = __shfl_sync(kFull, c.s_in, i); x.s_out = __shfl_sync(kFull, c.s_out, i);
+            reclaim_unit(p, wid + (k0 + (unsigned)i) * nw, x, lane);
+        }
     }
     for (unsigned t = wid; t < p.n_traces; t += nw) samples_trace(p, t, lane);
+    POST_T(1, atomicMax)
     grid_barrier(&p.ticket[1]);
+    POST_T(2, atomicMax)
     const unsigned ntask = min(ld_acquire(&p.ticket[2]), p.rtask_cap);
+#ifdef SCL_PROFILE
+    if (p.prof && blockIdx.x == 0 && threadIdx.x == 0) p.prof[39] = ld_acquire(&p.ticket[2]);
+#endif
     for (unsigned h = wid; h < ntask; h += nw) {                                          // phase B
         const RTask tk = p.rtask[h];
         if (chunk_has_free(p, tk.row0, tk.off_t, tk.n_t, tk.pos0, tk.ptr, tk.sbeg, tk.send, lane) && lane == 0)
-            reclaimed(p, tk.ep1);
+            reclaimed(p, tk.ep1, tk.site);
     }
+    POST_T(3, atomicMax)
     if (!p.fuse_report) return;                                                           // phase C
     __syncthreads();
     if (threadIdx.x == 0) { __threadfence(); last = atomicAdd(&p.ticket[3], 1u) == gridDim.x - 1; }
     __syncthreads();
     if (!last) return;
     __threadfence();
+    POST_T(4, atomicMax)
     report_block<256>(p.fin, p.rows, *reinterpret_cast<ReportSmem<256>*>(post_smem));
+    POST_T(5, atomicMax)
 }
 
 cudaError_t launch_post(const ReplayParams& p, cudaStream_t st)

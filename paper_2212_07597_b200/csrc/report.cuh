@@ -2,6 +2,7 @@
 // rows (readings Q8-Q11 of DESIGN.md §3).  Used by report_kernel (1024 threads) and by
 // the last block of post_kernel (256 threads) when the run finalizes at once.
 #pragma once
+#include <cstddef>
 #include "scl_internal.cuh"
 
 namespace scl {
@@ -45,6 +46,9 @@ __device__ __forceinline__ void gate_copy(const FinalParams& p) {   // to the ho
 
 
 constexpr unsigned kReportSites = 16384, kReportList = 2048, kRowWords = sizeof(scl_site_row) / 8;   // 13
+static_assert(sizeof(scl_site_row) == 104 && offsetof(scl_site_row, leak_flag) == 4 && offsetof(scl_site_row, col) == 8 &&
+              offsetof(scl_site_row, leak_prob) == 88 && offsetof(scl_site_row, leak_rate_mbps) == 96,
+              "report_block writes scl_site_row as 13 words: {site, flag}, col[10], prob, rate");
 template <int NT> struct ReportSmem {
     double lrate[kReportList]; unsigned lsite[kReportList];          // flagged sites (any order)
     unsigned bits[kReportSites / 32], wpre[kReportSites / 32];        // flag bitmask, flags before each word
@@ -53,45 +57,53 @@ template <int NT> struct ReportSmem {
 };
 template <int NT> constexpr size_t report_smem_bytes() { return sizeof(ReportSmem<NT>); }
 
-__device__ __forceinline__ void stat_row(const FinalParams& p, unsigned sidx, const SiteStat& st, unsigned long long* w) {
-    scl_site_row r;
-    r.site = sidx; r.leak_flag = st.flag ? 1u : 0u;
-    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(p.table + (size_t)sidx * SCL_NCOL);   // 80 B, 16-B aligned
-    #pragma unroll
-    for (int c = 0; c < SCL_NCOL / 2; ++c) { const ulonglong2 v = __ldcg(src + c); r.col[2 * c] = v.x; r.col[2 * c + 1] = v.y; }
-    r.leak_prob = st.prob; r.leak_rate_mbps = st.rate;
-    const unsigned long long* q = reinterpret_cast<const unsigned long long*>(&r);
-    #pragma unroll
-    for (int k = 0; k < (int)kRowWords; ++k) w[k] = q[k];
-}
-
 // Report order: flagged sites by (rate desc, site asc), then the others by site (a6).  Rank of a
 // flagged site = flagged sites with a larger rate, or the same rate and a smaller site; rank of an
 // unflagged site = #flagged + unflagged sites before it, so the unflagged sites of a warp's 32
 // consecutive sites take consecutive ranks: their rows are staged in shared memory and written
-// with lane-contiguous stores.  n_sites <= kReportSites; blockDim.x == NT.
+// with lane-contiguous stores.  Four sites per thread and pass are in flight at once (the passes
+// are latency-bound).  n_sites <= kReportSites; blockDim.x == NT.
+constexpr int kRU = 1;
 template <int NT>
 __device__ void report_block(const FinalParams& p, scl_site_row* rows, ReportSmem<NT>& sm)
 {
     const unsigned tid = threadIdx.x, lane = tid & 31, wrp = tid >> 5, S = p.n_sites, nw = (S + 31) / 32;
+#ifdef SCL_PROFILE
+#define RPT_T(i) if (p.prof && tid == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); p.prof[46 + (i)] = t_; }
+#else
+#define RPT_T(i)
+#endif
     const bool open = gate_open(p);
     const double es = elapsed_s(p);
     if (tid == 0) { sm.nflag = 0; gate_copy(p); }
     __syncthreads();
-    for (unsigned base = 0; base < S; base += NT) {          // pass 1: flags (integer only), flagged list
-        const unsigned sidx = base + tid;
-        bool fl = false;
-        if (sidx < S) {
-            const unsigned long long* row = p.table + (size_t)sidx * SCL_NCOL;
-            const unsigned long long m = __ldcg(&row[SCL_COL_LEAK_MALLOCS]), f = __ldcg(&row[SCL_COL_LEAK_FREES]);
-            fl = open && site_over(p, m, f);
-            if (fl) {
-                const unsigned k = atomicAdd(&sm.nflag, 1u);
-                if (k < kReportList) { sm.lrate[k] = site_rate(__ldcg(&row[SCL_COL_MALLOC_BYTES]), es); sm.lsite[k] = sidx; }
+    RPT_T(0)
+    for (unsigned base = 0; base < S; base += kRU * NT) {    // pass 1: flags (integer only), flagged list
+        unsigned long long m[kRU], f[kRU];
+        #pragma unroll
+        for (int k = 0; k < kRU; ++k) {
+            const unsigned sidx = base + k * NT + tid;
+            m[k] = f[k] = 0;
+            if (sidx < S) {
+                const unsigned long long* row = p.table + (size_t)sidx * SCL_NCOL;
+                m[k] = __ldcg(&row[SCL_COL_LEAK_MALLOCS]); f[k] = __ldcg(&row[SCL_COL_LEAK_FREES]);
             }
         }
-        const unsigned word = __ballot_sync(kFull, fl);
-        if (lane == 0 && (base >> 5) + wrp < nw) sm.bits[(base >> 5) + wrp] = word;
+        #pragma unroll
+        for (int k = 0; k < kRU; ++k) {
+            const unsigned sidx = base + k * NT + tid;
+            const bool fl = sidx < S && open && site_over(p, m[k], f[k]);
+            if (fl) {
+                const unsigned q = atomicAdd(&sm.nflag, 1u);
+                if (q < kReportList) {
+                    sm.lrate[q] = site_rate(__ldcg(&p.table[(size_t)sidx * SCL_NCOL + SCL_COL_MALLOC_BYTES]), es);
+                    sm.lsite[q] = sidx;
+                }
+            }
+            const unsigned word = __ballot_sync(kFull, fl);
+            const unsigned wi = ((base + k * NT) >> 5) + wrp;
+            if (lane == 0 && wi < nw) sm.bits[wi] = word;
+        }
     }
     __syncthreads();
     for (unsigned w0 = 0; w0 < nw; w0 += NT) {              // exclusive prefix of flags per word
@@ -108,46 +120,66 @@ __device__ void report_block(const FinalParams& p, scl_site_row* rows, ReportSme
         __syncthreads();
     }
     const unsigned F = sm.nflag;
+    RPT_T(1)
     unsigned long long* stg = sm.stage[wrp];
-    for (unsigned base = 0; base < S; base += NT) {          // pass 2: stats, ranks, rows
-        const unsigned sidx = base + tid, wd = sidx >> 5;
-        const bool in = sidx < S;
-        const unsigned word = in ? sm.bits[wd] : 0u;
-        const bool fl = in && ((word >> lane) & 1u);
-        const unsigned um = __ballot_sync(kFull, in && !fl);  // unflagged lanes: consecutive ranks
-        unsigned long long w[kRowWords];
-        if (in) {
-            const SiteStat st = site_stat(p, sidx, open);
-            stat_row(p, sidx, st, w);
-            if (fl) {
-                unsigned rank = 0;
-                if (F <= kReportList) {
-                    for (unsigned k = 0; k < F; ++k)
-                        rank += (sm.lrate[k] > st.rate || (sm.lrate[k] == st.rate && sm.lsite[k] < sidx)) ? 1u : 0u;
-                } else {                                    // many flagged sites: compare against all
-                    for (unsigned j = 0; j < S; ++j) {
-                        const SiteStat o = site_stat(p, j, open);
-                        rank += (o.flag && (o.rate > st.rate || (o.rate == st.rate && j < sidx))) ? 1u : 0u;
+    for (unsigned base = 0; base < S; base += kRU * NT) {    // pass 2: stats, ranks, rows
+        ulonglong2 rv[kRU][SCL_NCOL / 2];                   // the table rows, one load each
+        #pragma unroll
+        for (int k = 0; k < kRU; ++k) {
+            const unsigned sidx = base + k * NT + tid;
+            const ulonglong2* src = reinterpret_cast<const ulonglong2*>(p.table + (size_t)min(sidx, S - 1) * SCL_NCOL);
+            #pragma unroll
+            for (int c = 0; c < SCL_NCOL / 2; ++c) rv[k][c] = __ldcg(src + c);
+        }
+        #pragma unroll
+        for (int k = 0; k < kRU; ++k) {
+            const unsigned sidx = base + k * NT + tid;
+            const bool in = sidx < S;
+            const unsigned word = in ? sm.bits[sidx >> 5] : 0u;
+            const bool fl = in && ((word >> lane) & 1u);
+            const unsigned um = __ballot_sync(kFull, in && !fl);  // unflagged lanes: consecutive ranks
+            if (in) {
+                const unsigned long long m = SCL_COL_LEAK_MALLOCS % 2 ? rv[k][SCL_COL_LEAK_MALLOCS / 2].y : rv[k][SCL_COL_LEAK_MALLOCS / 2].x;
+                const unsigned long long f = SCL_COL_LEAK_FREES % 2 ? rv[k][SCL_COL_LEAK_FREES / 2].y : rv[k][SCL_COL_LEAK_FREES / 2].x;
+                const unsigned long long by = SCL_COL_MALLOC_BYTES % 2 ? rv[k][SCL_COL_MALLOC_BYTES / 2].y : rv[k][SCL_COL_MALLOC_BYTES / 2].x;
+                const double prob = site_prob(p, m, f), rate = site_rate(by, es);
+                // the row's 13 words: {site, flag}, col[0..9], prob, rate  (scl_site_row layout)
+                auto word_at = [&](int q) -> unsigned long long {
+                    if (q == 0) return (unsigned long long)sidx | ((unsigned long long)(fl ? 1u : 0u) << 32);
+                    if (q == 11) return (unsigned long long)__double_as_longlong(prob);
+                    if (q == 12) return (unsigned long long)__double_as_longlong(rate);
+                    return (q - 1) % 2 ? rv[k][(q - 1) / 2].y : rv[k][(q - 1) / 2].x;
+                };
+                if (fl) {
+                    unsigned rank = 0;
+                    if (F <= kReportList) {
+                        for (unsigned q = 0; q < F; ++q)
+                            rank += (sm.lrate[q] > rate || (sm.lrate[q] == rate && sm.lsite[q] < sidx)) ? 1u : 0u;
+                    } else {                                // many flagged sites: compare against all
+                        for (unsigned j = 0; j < S; ++j) {
+                            const SiteStat o = site_stat(p, j, open);
+                            rank += (o.flag && (o.rate > rate || (o.rate == rate && j < sidx))) ? 1u : 0u;
+                        }
                     }
+                    unsigned long long* dst = reinterpret_cast<unsigned long long*>(rows + rank);
+                    #pragma unroll
+                    for (int q = 0; q < (int)kRowWords; ++q) dst[q] = word_at(q);
+                } else {
+                    const unsigned j = __popc(um & ((1u << lane) - 1u));      // slot among the warp's unflagged
+                    #pragma unroll
+                    for (int q = 0; q < (int)kRowWords; ++q) stg[j * kRowWords + q] = word_at(q);
                 }
-                unsigned long long* dst = reinterpret_cast<unsigned long long*>(rows + rank);
-                #pragma unroll
-                for (int k = 0; k < (int)kRowWords; ++k) dst[k] = w[k];
-            } else {
-                const unsigned j = __popc(um & ((1u << lane) - 1u));          // slot among the warp's unflagged
-                #pragma unroll
-                for (int k = 0; k < (int)kRowWords; ++k) stg[j * kRowWords + k] = w[k];
             }
+            __syncwarp();
+            if (um) {
+                const unsigned s_first = base + k * NT + (wrp << 5) + (unsigned)(__ffs(um) - 1);
+                const unsigned r0 = F + s_first - (sm.wpre[s_first >> 5] + __popc(sm.bits[s_first >> 5] & ((1u << (s_first & 31)) - 1u)));
+                unsigned long long* dst = reinterpret_cast<unsigned long long*>(rows + r0);
+                const unsigned nwds = (unsigned)__popc(um) * kRowWords;
+                for (unsigned q = lane; q < nwds; q += 32) dst[q] = stg[q];
+            }
+            __syncwarp();
         }
-        __syncwarp();
-        if (um) {
-            const unsigned s_first = (base & ~31u) + (wrp << 5) + (unsigned)(__ffs(um) - 1);
-            const unsigned r0 = F + s_first - (sm.wpre[s_first >> 5] + __popc(sm.bits[s_first >> 5] & ((1u << (s_first & 31)) - 1u)));
-            unsigned long long* dst = reinterpret_cast<unsigned long long*>(rows + r0);
-            const unsigned nwds = (unsigned)__popc(um) * kRowWords;
-            for (unsigned k = lane; k < nwds; k += 32) dst[k] = stg[k];
-        }
-        __syncwarp();
     }
 }
 

@@ -75,14 +75,16 @@ struct FinalParams {
     double* prob; double* rate; unsigned char* flag;
     unsigned long long* key1; unsigned int* val;   // sort inputs
     unsigned long long* gate_out;     // [3] host-mapped pinned buffer: the gate sums (written by one thread)
+    unsigned long long* prof;         // debug build only: phase timestamps of a6
 };
 
 // One exact re-check of the reclaim pass: chunk rows [row0, row0 + 32) of a unit, unit positions
-// [sbeg, send), does any free of `ptr` occur?  (pos0: unit position of the chunk's first event.)
+// [sbeg, send), does any free of `ptr` occur?  (pos0: unit position of the chunk's first event;
+// site: the episode's sample site, its leak-frees column.)
 struct __align__(16) RTask {
     unsigned long long ep1, ptr;
     long long row0, off_t, n_t;
-    unsigned pos0, sbeg, send, pad;
+    unsigned pos0, sbeg, send, site;
 };
 
 struct ReplayParams {

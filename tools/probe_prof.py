@@ -33,6 +33,10 @@ for base, (nm, nw, cats) in names.items():
         print("  walker per unit (cycles): " + "  ".join(f"{c}={float(buf[base+i])/max(units,1):.0f}" for i, c in enumerate(cats) if c not in ("units", "x")), f" units={units:.0f}")
 
 rc = bigbuf[24:40].astype(float)
+pt = bigbuf[40:48].astype(np.int64)
+if pt[0] > 0 and pt[1] > 0:
+    print(f"  post pass (us from its start): units+traces done {(pt[1]-pt[0])/1e3:.1f}  barrier {(pt[2]-pt[0])/1e3:.1f}  "
+          f"re-checks ({int(bigbuf[39])} tasks) done {(pt[3]-pt[0])/1e3:.1f}  report {(pt[4]-pt[0])/1e3:.1f} [gate+sync {(pt[6]-pt[0])/1e3:.1f} pass1+prefix {(pt[7]-pt[0])/1e3:.1f}] -> {(pt[5]-pt[0])/1e3:.1f}")
 print(f"  runner: invocations {rc[0]:.0f} batches {rc[1]:.0f} units {rc[2]:.0f} resolves {rc[3]:.0f} "
       f"resolve cyc/each {rc[4]/max(rc[3],1):.0f} ptr-exact {rc[5]:.0f} run cyc/invocation {rc[6]/max(rc[0],1):.0f} lock-fails {rc[7]:.0f}")
 nres = max(rc[3], 1)
