@@ -96,12 +96,14 @@ typedef struct {
     int64_t f_last_sample;    /*   the footprint trend endpoints used by the gate */
 } scl_trace_summary;
 
-enum { SCL_HWM_PREFIX = 0 };                          /* reading Q3 (prefix max) */
+enum { SCL_HWM_PREFIX = 0,                            /* reading Q3: new maximum = above the prefix max M_{i-1} */
+       SCL_HWM_SAMPLE = 1 };                          /* alternative: above every earlier sample footprint (NEXT-4) */
 enum { SCL_FORMULA_PAPER = 0, SCL_FORMULA_TEXTBOOK = 1 };
 
 typedef struct {
     uint64_t tick_ns;        /* synthetic time base: event i at (i+1)*tick_ns; 0 -> 1000 */
-    int hwm_mode;            /* SCL_HWM_PREFIX only */
+    int hwm_mode;            /* SCL_HWM_PREFIX (default) or SCL_HWM_SAMPLE: what a "new high-water
+                                mark" is compared against at a growth sample */
     int formula;             /* SCL_FORMULA_PAPER (default) or SCL_FORMULA_TEXTBOOK (Laplace) */
     int defer_finalize;      /* 1: stop after the site table (a1-a5); the caller may sum the
                                 device table across GPUs (scl_result_device_table) and then

@@ -183,14 +183,18 @@ def scl_trace_reload(traces: Traces, events, offsets, n_sites: int, validate: bo
     return traces
 
 
+HWM_PREFIX, HWM_SAMPLE = 0, 1
+FORMULA_PAPER, FORMULA_TEXTBOOK = 0, 1
+
+
 def scl_replay_run(threshold: int, traces: Traces, tick_ns: int = 0, formula: int = 0,
                    defer_finalize: bool = False, elapsed_ns: int = 0, stream=None,
-                   out: Result | None = None, timing: bool = False) -> Result:
+                   out: Result | None = None, timing: bool = False, hwm_mode: int = HWM_PREFIX) -> Result:
     """Replay all traces at threshold T; ``out`` (a previous Result of the same
     traces) is reused in place.  stream: torch.cuda.Stream / raw handle / None.
     timing: record CUDA events for scl_result_timing / scl_result_kernel_times."""
     o = _RunOpts()
-    o.tick_ns, o.hwm_mode, o.formula = tick_ns, 0, formula
+    o.tick_ns, o.hwm_mode, o.formula = tick_ns, hwm_mode, formula
     o.defer_finalize, o.elapsed_ns, o.timing = int(defer_finalize), elapsed_ns, int(timing)
     if stream is not None:
         o.cuda_stream = getattr(stream, "cuda_stream", stream)

@@ -420,7 +420,7 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
     if (threshold > (1ull << 62)) return fail(SCL_EINVAL, "threshold too large");
     scl_run_opts o{};
     if (opts) o = *opts;
-    if (o.hwm_mode != SCL_HWM_PREFIX) return fail(SCL_EINVAL, "only hwm_mode PREFIX is implemented on the GPU");
+    if (o.hwm_mode != SCL_HWM_PREFIX && o.hwm_mode != SCL_HWM_SAMPLE) return fail(SCL_EINVAL, "bad hwm_mode");
     if (o.formula != SCL_FORMULA_PAPER && o.formula != SCL_FORMULA_TEXTBOOK) return fail(SCL_EINVAL, "bad formula");
     CU(cudaSetDevice(tr->device));
     cudaStream_t st = (cudaStream_t)o.cuda_stream;
@@ -486,7 +486,7 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
             p.n_stream = (unsigned)r->grid; p.n_runners = (unsigned)r->grid * kEmbeddedRunners;
         }
     }
-    p.n_sites = tr->n_sites; p.n_traces = NT; p.T = (long long)threshold;
+    p.n_sites = tr->n_sites; p.n_traces = NT; p.T = (long long)threshold; p.hwm_sample = o.hwm_mode == SCL_HWM_SAMPLE;
     p.table = r->d_table; p.samples = r->d_samples; p.ep_flag = r->d_epflag; p.sbase = r->d_sbase;
     p.summ = r->d_summ; p.uent = tr->d_uent; p.rtask = r->d_rtask; p.rtask_cap = kRTaskCap;
 #ifdef SCL_PROFILE

@@ -333,22 +333,23 @@ __device__ void producer_role(const ReplayParams& p, const CUtensorMap* tmap, Sm
 // which a sample fires are resolved chunk by chunk.  The runner does no pointer matching: it
 // records the state entering each unit (UnitEntry) and the reclaim pass settles every episode
 // afterwards, all units in parallel -- the chain carries only what the sampler needs.
-struct RState { long long F, M, B; unsigned long long n, nep, ep1, eptr; unsigned next; };
+struct RState { long long F, M, B; unsigned long long n, nep, ep1, eptr; long long Ms; unsigned next; };
 
 __device__ __forceinline__ RState load_rstate(const RunState* rs, int lane) {
     const unsigned long long* w = reinterpret_cast<const unsigned long long*>(rs);
-    unsigned long long v = lane < 8 ? __ldcg(w + lane) : 0ull;      // F M B n nep ep1 eptr {next,pad}
+    unsigned long long v = lane < 9 ? __ldcg(w + lane) : 0ull;      // F M B n nep ep1 eptr Ms {next,pad}
     RState x;
     x.F = (long long)__shfl_sync(kFull, v, 0); x.M = (long long)__shfl_sync(kFull, v, 1);
     x.B = (long long)__shfl_sync(kFull, v, 2); x.n = __shfl_sync(kFull, v, 3);
     x.nep = __shfl_sync(kFull, v, 4); x.ep1 = __shfl_sync(kFull, v, 5); x.eptr = __shfl_sync(kFull, v, 6);
-    x.next = (unsigned)__shfl_sync(kFull, v, 7);      // low word: next
+    x.Ms = (long long)__shfl_sync(kFull, v, 7);
+    x.next = (unsigned)__shfl_sync(kFull, v, 8);      // low word: next
     return x;
 }
 __device__ __forceinline__ void store_rstate(RunState* rs, const RState& x, int lane) {
     if (lane == 0) {
         rs->F = x.F; rs->M = x.M; rs->B = x.B; rs->n = x.n; rs->nep = x.nep; rs->ep1 = x.ep1; rs->eptr = x.eptr;
-        rs->next = x.next;
+        rs->Ms = x.Ms; rs->next = x.next;
     }
 }
 
@@ -364,6 +365,7 @@ __device__ void resolve_unit(const ReplayParams& p, const Slot& S, RState& x, un
     const long long sPc = S.Pc[lane], sax = S.ax[lane], san = S.an[lane], susum = S.usum, sumx = S.umx;
     long long B = x.B;
     unsigned long long n = x.n, nep = x.nep, ep1 = x.ep1, eptr = x.eptr;
+    long long Ms = x.Ms;                                     // max sample footprint (hwm_mode SAMPLE)
     const long long hiL = F0 + sax, loL = F0 + san;          // F range of chunk `lane`
 #ifdef SCL_PROFILE
     const long long t_a = clock64();
@@ -444,19 +446,20 @@ __device__ void resolve_unit(const ReplayParams& p, const Slot& S, RState& x, un
                     }
                     const long long net = F - B;              // the |A - F| counter
                     const bool growth = net > 0;
-                    const bool nm = growth && F > Mp;         // new high-water mark (Q3, Q4)
+                    const bool nm = growth && F > (p.hwm_sample ? Ms : Mp);   // new high-water mark (Q3, Q4)
                     const unsigned long long slot_s = sb + n;
                     scl_sample smp;
                     smp.idx = (unsigned long long)(e0 + js); smp.net = net; smp.footprint = F;
                     smp.site = ev_site(ms); smp.kind = growth ? 0 : 1; smp.new_max = nm ? 1 : 0; smp.pad = 0;
                     p.samples[slot_s] = smp;
                     if (nm) { p.ep_flag[slot_s] = 0u; ep1 = slot_s + 1; eptr = ps; ++nep; }   // settled by the reclaim pass
-                    ++n; B = F;                               // "resets the counters"
+                    ++n; B = F; Ms = llmax(Ms, F);            // "resets the counters"
                     from = (unsigned)js + 1;
                 }
             }
             B = shfl_ll(B, l0); n = __shfl_sync(kFull, n, l0);
             nep = __shfl_sync(kFull, nep, l0); ep1 = __shfl_sync(kFull, ep1, l0); eptr = __shfl_sync(kFull, eptr, l0);
+            Ms = shfl_ll(Ms, l0);
             cur = l0 + 1;
         }
 #ifdef SCL_PROFILE
@@ -466,7 +469,7 @@ __device__ void resolve_unit(const ReplayParams& p, const Slot& S, RState& x, un
         cnext = c + 1;
     }
     x.F = F0 + susum; x.M = llmax(M0, F0 + sumx); x.B = B;
-    x.n = n; x.nep = nep; x.ep1 = ep1; x.eptr = eptr;
+    x.n = n; x.nep = nep; x.ep1 = ep1; x.eptr = eptr; x.Ms = Ms;
 #ifdef SCL_PROFILE
     RPROF_ADD(9, t_rows) RPROF_ADD(10, t_scan) RPROF_ADD(12, t_walk) RPROF_ADD(13, clock64() - t_b - t_rows - t_scan - t_walk)
 #endif

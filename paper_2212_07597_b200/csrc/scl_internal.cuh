@@ -53,6 +53,7 @@ struct __align__(16) RunState {
     long long F, M, B;                // footprint, high-water mark, footprint at the last sample
     unsigned long long n, nep, ep1;   // samples, episodes, current episode (sample slot + 1; 0 none)
     unsigned long long eptr;          // pointer of the current episode's allocation
+    long long Ms;                     // max footprint over the samples so far (hwm_mode SAMPLE)
     unsigned next, pad;               // next unit index to run
 };
 
@@ -109,6 +110,7 @@ struct ReplayParams {
     unsigned int epoch;               // run number on this traces handle (ready tag)
     unsigned int n_sites;
     unsigned int n_traces;
+    int hwm_sample;                   // 1: new maximum against earlier sample footprints (SCL_HWM_SAMPLE)
     long long T;
     unsigned long long* table;        // [n_sites*SCL_NCOL + 3]
     scl_sample* samples;              // [capacity]

@@ -10,16 +10,16 @@ import paper_2212_07597_b200 as scl
 REL_TOL = 1e-12
 
 
-def gpu_run(events, offsets, n_sites, T, formula=0, tick_ns=1000, traces=None, out=None, validate=False):
+def gpu_run(events, offsets, n_sites, T, formula=0, tick_ns=1000, traces=None, out=None, validate=False, hwm_mode=0):
     tr = traces if traces is not None else scl.scl_trace_load(events, offsets, n_sites, validate=validate)
-    r = scl.scl_replay_run(T, tr, formula=formula, tick_ns=tick_ns, out=out)
+    r = scl.scl_replay_run(T, tr, formula=formula, tick_ns=tick_ns, out=out, hwm_mode=hwm_mode)
     return tr, r
 
 
-def compare(events, offsets, n_sites, T, r, formula=0, tick_ns=1000, traces_to_check=None, ref=None):
+def compare(events, offsets, n_sites, T, r, formula=0, tick_ns=1000, traces_to_check=None, ref=None, hwm_mode=0):
     """Assert GPU result r == oracle on (events, offsets). Returns the oracle dict."""
     offsets = np.asarray(offsets, dtype=np.uint64)
-    ref = ref or oracle.full(events, offsets, n_sites, T, formula=formula, tick_ns=tick_ns, n_threads=8)
+    ref = ref or oracle.full(events, offsets, n_sites, T, hwm_mode=hwm_mode, formula=formula, tick_ns=tick_ns, n_threads=8)
     res = ref["result"]
     n_traces = len(offsets) - 1
     # per-trace summaries

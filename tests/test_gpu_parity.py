@@ -26,16 +26,15 @@ def _concat(traces):
 @pytest.mark.parametrize("name", _golden.all_names())
 def test_golden(name):
     g = _golden.load(name)
-    if g["hwm"] != "prefix":
-        pytest.skip("hwm_mode SAMPLE is oracle-only (NEXT-4)")
+    hwm = scl.HWM_PREFIX if g["hwm"] == "prefix" else scl.HWM_SAMPLE
     n_sites = max(max(e[3] for e in g["events"]) + 1, max(g["sites"], default=0) + 1)
     ev, off = _concat([g["events"]])
-    _, r = gpu_run(ev, off, n_sites, g["T"])
+    _, r = gpu_run(ev, off, n_sites, g["T"], hwm_mode=hwm)
     smp = scl.scl_samples(r, 0)
     got = [(int(s["idx"]), "G" if s["kind"] == 0 else "D", int(s["net"]), int(s["footprint"]), int(s["site"]),
             bool(s["new_max"])) for s in smp]
     assert got == g["samples"]
-    compare(ev, off, n_sites, g["T"], r)
+    compare(ev, off, n_sites, g["T"], r, hwm_mode=hwm)
 
 
 def test_random_small_ragged():
@@ -245,3 +244,24 @@ def test_report_many_flagged_sites():
     _, r = gpu_run(ev, off, n_sites, 1)
     ref = compare(ev, off, n_sites, 1, r)
     assert int(ref["flag"].sum()) == n_sites
+
+
+def test_hwm_mode_sample():
+    """NEXT-4: hwm_mode SAMPLE (a new maximum is above every earlier sample footprint, reading
+    Q3's alternative) on ragged random traces and a config-2 subset, against the oracle's SAMPLE
+    mode; the two readings give different episode sets on the same traces."""
+    rng = np.random.default_rng(21)
+    traces = [tracegen.random_small_trace(rng, int(rng.integers(0, 20000)), n_sites=23, max_size=int(rng.integers(1, 300)),
+                                          max_ptrs=int(rng.integers(2, 40))) for _ in range(120)]
+    ev, off = _concat(traces)
+    tr = scl.scl_trace_load(ev, off, 23)
+    r = None
+    for T in (3, 97, 4001):
+        r = scl.scl_replay_run(T, tr, out=r, hwm_mode=scl.HWM_SAMPLE)
+        compare(ev, off, 23, T, r, hwm_mode=scl.HWM_SAMPLE)
+    cfg = tracegen.CONFIGS[2].with_traces(6)
+    ev, off = tracegen.generate(cfg)
+    _, r = gpu_run(ev, off, cfg.n_sites, 1048583, hwm_mode=scl.HWM_SAMPLE)
+    a = compare(ev, off, cfg.n_sites, 1048583, r, hwm_mode=scl.HWM_SAMPLE)
+    b = oracle.full(ev, off, cfg.n_sites, 1048583, hwm_mode=oracle.HWM_PREFIX)
+    assert int(a["result"].summaries["n_episodes"].sum()) != int(b["result"].summaries["n_episodes"].sum())
