@@ -45,10 +45,11 @@ _lib = None
 def build(force: bool = False) -> str:
     """Compile oracle.c -> liboracle.so (plain C; no FMA contraction)."""
     src = os.path.join(_HERE, "oracle.c")
+    src2 = os.path.join(_HERE, "rate.c")
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < max(
-            os.path.getmtime(src), os.path.getmtime(os.path.join(_HERE, "oracle.h"))):
+            os.path.getmtime(src), os.path.getmtime(src2), os.path.getmtime(os.path.join(_HERE, "oracle.h"))):
         cmd = (f"gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fPIC -shared -pthread "
-               f"-o {_LIB_PATH}.tmp {src}")
+               f"-o {_LIB_PATH}.tmp {src} {src2} -lm")
         if os.system(cmd) != 0:
             raise RuntimeError("oracle build failed: " + cmd)
         os.replace(_LIB_PATH + ".tmp", _LIB_PATH)
@@ -70,6 +71,11 @@ def _load():
         lib.orc_next_prime.restype = U64
         lib.orc_validate_trace.argtypes = [P, U64, U32]
         lib.orc_validate_trace.restype = ctypes.c_int64
+        lib.orc_soft_log.argtypes = [ctypes.c_double]
+        lib.orc_soft_log.restype = ctypes.c_double
+        lib.orc_rate_draw.argtypes = [U64, U64, U32, U64]
+        lib.orc_rate_draw.restype = U64
+        lib.orc_rate_trace.argtypes = [P, U64, U64, U64, U32, U32, P, U64, P]
         _lib = lib
     return _lib
 
@@ -192,3 +198,43 @@ def full(events, offsets, n_sites, T, hwm_mode=HWM_PREFIX, formula=FORMULA_PAPER
     order = report_order(rate, flag)
     return dict(result=r, gate=(num, den, op), elapsed_ns=el, prob=prob, rate=rate,
                 flag=flag, order=order)
+
+
+# ---- rate-based byte sampler (NEXT-1 baseline, NEXT-3 copy volume; oracle/rate.c) ----
+RATE_SAMPLE_DTYPE = np.dtype([("idx", "<u8"), ("draw_sum", "<u8"), ("site", "<u4"), ("kind", "<u4")])
+KINDS_ALLOC_FREE, KINDS_COPY = 0b011, 0b100
+
+
+def soft_log(x: float) -> float:
+    return float(_load().orc_soft_log(x))
+
+
+def rate_draw(R: int, seed: int, trace: int, k: int) -> int:
+    return int(_load().orc_rate_draw(R, seed, trace, k))
+
+
+def rate_replay(events: np.ndarray, offsets, R: int, seed: int, kinds: int = KINDS_ALLOC_FREE):
+    """Per trace: the rate sampler's samples (RATE_SAMPLE_DTYPE) -> (samples, sample_off)."""
+    lib = _load()
+    offsets = np.asarray(offsets, dtype=np.uint64)
+    events = np.ascontiguousarray(events)
+    n_traces = len(offsets) - 1
+    per, counts = [], np.zeros(n_traces, dtype=np.uint64)
+    for t in range(n_traces):
+        b, e = int(offsets[t]), int(offsets[t + 1])
+        sub = events[b:e]
+        cap = 1024
+        while True:
+            out = np.zeros(cap, dtype=RATE_SAMPLE_DTYPE)
+            ns = ctypes.c_uint64()
+            rc = lib.orc_rate_trace(_ptr(sub) if e > b else None, e - b, R, seed, t, kinds, _ptr(out), cap,
+                                    ctypes.byref(ns))
+            if rc != 0:
+                raise ValueError(f"trace {t}: invalid event")
+            if ns.value <= cap:
+                break
+            cap = int(ns.value)
+        per.append(out[:ns.value]); counts[t] = ns.value
+    off = np.zeros(n_traces + 1, dtype=np.uint64)
+    off[1:] = np.cumsum(counts)
+    return (np.concatenate(per) if per else np.zeros(0, dtype=RATE_SAMPLE_DTYPE)), off

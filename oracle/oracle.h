@@ -102,6 +102,13 @@ uint64_t orc_next_prime(uint64_t base);
  * of the first bad event. */
 int64_t orc_validate_trace(const orc_event* ev, uint64_t n, uint32_t n_sites);
 
+/* ---- rate-based byte sampler (NEXT-1 baseline, NEXT-3 copy volume): oracle/rate.c ---- */
+typedef struct { uint64_t idx; uint64_t draw_sum; uint32_t site; uint32_t kind; } orc_rate_sample;   /* 24 B */
+double   orc_soft_log(double x);
+uint64_t orc_rate_draw(uint64_t R, uint64_t seed, uint32_t trace, uint64_t k);
+int      orc_rate_trace(const orc_event* ev, uint64_t n, uint64_t R, uint64_t seed, uint32_t trace,
+                        unsigned kinds, orc_rate_sample* out, uint64_t cap, uint64_t* n_samples);
+
 #ifdef __cplusplus
 }
 #endif
