@@ -191,6 +191,41 @@ scl_status scl_result_timing(const scl_result* r, float* replay_kernel_ms, float
  * without synchronising between them.  *n = number written (<= cap). */
 scl_status scl_result_kernel_times(const scl_result* r, float* ms, size_t cap, size_t* n);
 
+/* ---- Rate-based byte sampler: the paper's comparison baseline (Table
+ * tab:sampling-comparison) and copy-volume sampling (NEXT-3).
+ * Per trace a counter drawn from a geometric distribution with mean R is decremented by the
+ * bytes of every counted event; each time it drops below 0 a sample is taken and a new draw is
+ * added (one event may take several samples).  Draw k of trace t comes from a counter-based
+ * generator keyed by (seed, t, k) (Q17-Q19); seed 0 = deterministic mode (every
+ * draw = R).  Sample k fires at the first event whose cumulative counted bytes exceed
+ * S_k = G_1 + ... + G_k. */
+typedef struct {
+    uint64_t idx;        /* event index within the trace */
+    uint64_t draw_sum;   /* S_k */
+    uint32_t site;       /* the event's site */
+    uint32_t kind;       /* the event's kind (0 alloc, 1 free, 2 copy) */
+} scl_rate_sample;       /* 24 B */
+enum { SCL_RATE_ALLOC_FREE = 3, SCL_RATE_COPY = 4 };
+typedef struct scl_rate_result scl_rate_result;
+
+/* Run the rate sampler over every trace of the handle.  rate_bytes R >= 1; kinds: nonzero mask
+ * of {1 alloc, 2 free, 4 copy} (SCL_RATE_ALLOC_FREE: the baseline; SCL_RATE_COPY: copy volume).
+ * cuda_stream: cudaStream_t or NULL.  Synchronises once (the sample counts size the output).
+ * *out: NULL -> a new result; else a result of the same handle, reused.
+ * Errors: SCL_EINVAL (R = 0, bad kinds, NULL), SCL_EOVERFLOW (more than 2^32 samples), SCL_ENOMEM,
+ * SCL_ECUDA. */
+scl_status scl_rate_run(uint64_t rate_bytes, uint64_t seed, unsigned kinds, const scl_traces* traces,
+                        void* cuda_stream, scl_rate_result** out);
+/* Samples per trace (n_traces values). */
+scl_status scl_rate_counts(const scl_rate_result* r, uint64_t* counts, size_t cap, size_t* n);
+/* One trace's samples in order (k = 1, 2, ...). */
+scl_status scl_rate_samples(const scl_rate_result* r, uint32_t trace, scl_rate_sample* out, size_t cap, size_t* n);
+/* Samples per site (n_sites values); x R = the bytes credited to the site (copy volume). */
+scl_status scl_rate_site_counts(const scl_rate_result* r, uint64_t* counts, size_t cap, size_t* n);
+/* Device time of the run's kernels (ms), excluding the one host synchronisation. */
+scl_status scl_rate_timing(const scl_rate_result* r, float* ms);
+void scl_rate_free(scl_rate_result* r);
+
 void scl_traces_free(scl_traces* t);
 void scl_result_free(scl_result* r);
 const char* scl_last_error(void);

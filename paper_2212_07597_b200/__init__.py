@@ -20,13 +20,17 @@ from . import _build
 __all__ = ["SclError", "Traces", "Result", "scl_trace_load", "scl_trace_reload", "scl_replay_run", "scl_finalize",
            "scl_site_report", "scl_samples", "scl_trace_summaries", "scl_gate", "scl_result_device_table",
            "scl_result_timing", "scl_result_kernel_times", "scl_next_prime", "scl_traces_info", "EVENT_DTYPE", "SAMPLE_DTYPE",
-           "SUMMARY_DTYPE", "SITE_ROW_DTYPE", "COLS", "device_table_tensor", "write_trace_file"]
+           "SUMMARY_DTYPE", "SITE_ROW_DTYPE", "COLS", "device_table_tensor", "write_trace_file",
+           "RATE_SAMPLE_DTYPE", "RATE_ALLOC_FREE", "RATE_COPY", "RateResult", "scl_rate_run", "scl_rate_counts",
+           "scl_rate_samples", "scl_rate_site_counts", "scl_rate_timing"]
 
 EVENT_DTYPE = np.dtype([("ptr", "<u8"), ("meta", "<u8")])
 SAMPLE_DTYPE = np.dtype([("idx", "<u8"), ("net", "<i8"), ("footprint", "<i8"), ("site", "<u4"),
                          ("kind", "u1"), ("new_max", "u1"), ("pad", "<u2")])
 SUMMARY_DTYPE = np.dtype([("f_final", "<i8"), ("hwm", "<i8"), ("n_samples", "<u8"), ("n_episodes", "<u8"),
                           ("f_first_sample", "<i8"), ("f_last_sample", "<i8")])
+RATE_SAMPLE_DTYPE = np.dtype([("idx", "<u8"), ("draw_sum", "<u8"), ("site", "<u4"), ("kind", "<u4")])
+RATE_ALLOC_FREE, RATE_COPY = 3, 4
 SITE_ROW_DTYPE = np.dtype([("site", "<u4"), ("leak_flag", "<u4"), ("col", "<u8", (10,)),
                            ("leak_prob", "<f8"), ("leak_rate_mbps", "<f8")])
 COLS = ("n_malloc", "n_free", "malloc_bytes", "free_bytes", "n_growth", "n_decline",
@@ -58,6 +62,11 @@ def _load():
         "scl_trace_load": [ctypes.c_char_p, P, P, U32, U32, I32, I32, P],
         "scl_trace_reload": [P, P, P, U32, U32, I32, P],
         "scl_result_kernel_times": [P, P, SZ, P],
+        "scl_rate_run": [U64, U64, U32, P, P, P],
+        "scl_rate_counts": [P, P, SZ, P],
+        "scl_rate_samples": [P, U32, P, SZ, P],
+        "scl_rate_site_counts": [P, P, SZ, P],
+        "scl_rate_timing": [P, P],
         "scl_replay_run": [U64, P, P, P],
         "scl_result_device_table": [P, P, P],
         "scl_finalize": [P, U64],
@@ -76,6 +85,8 @@ def _load():
     lib.scl_traces_free.restype = None
     lib.scl_result_free.argtypes = [P]
     lib.scl_result_free.restype = None
+    lib.scl_rate_free.argtypes = [P]
+    lib.scl_rate_free.restype = None
     lib.scl_last_error.restype = ctypes.c_char_p
     lib.scl_next_prime.argtypes = [U64]
     lib.scl_next_prime.restype = U64
@@ -297,3 +308,71 @@ def write_trace_file(path: str, events: np.ndarray, offsets: np.ndarray, n_sites
         f.write(np.ascontiguousarray(events).tobytes())
         if site_names:
             f.write("".join(f"{a}\t{b}\n" for a, b in site_names).encode())
+
+
+class RateResult:
+    """Owning handle of scl_rate_result (the rate-based sampler, NEXT-1 / NEXT-3)."""
+
+    def __init__(self, traces: Traces):
+        self._h = ctypes.c_void_p(None)
+        self.traces = traces
+
+    @property
+    def handle(self):
+        return self._h
+
+    def free(self):
+        if self._h:
+            lib.scl_rate_free(self._h)
+            self._h = ctypes.c_void_p(None)
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def scl_rate_run(rate_bytes: int, traces: Traces, seed: int = 1, kinds: int = RATE_ALLOC_FREE, stream=None,
+                 out: RateResult | None = None) -> RateResult:
+    """Rate-based byte sampler over every trace: mean rate_bytes between samples, counted kinds
+    (RATE_ALLOC_FREE: the paper's baseline; RATE_COPY: copy volume); seed 0 = deterministic."""
+    st = getattr(stream, "cuda_stream", stream) if stream is not None else None
+    r = out if out is not None else RateResult(traces)
+    h = ctypes.c_void_p(r._h.value)
+    _check(lib.scl_rate_run(rate_bytes, seed, kinds, traces.handle, st, ctypes.byref(h)))
+    r._h = h
+    return r
+
+
+def scl_rate_counts(r: RateResult) -> np.ndarray:
+    n = ctypes.c_size_t()
+    _check(lib.scl_rate_counts(r.handle, None, 0, ctypes.byref(n)))
+    out = np.zeros(n.value, dtype=np.uint64)
+    if n.value:
+        _check(lib.scl_rate_counts(r.handle, out.ctypes.data, n.value, ctypes.byref(n)))
+    return out
+
+
+def scl_rate_samples(r: RateResult, trace: int) -> np.ndarray:
+    n = ctypes.c_size_t()
+    _check(lib.scl_rate_samples(r.handle, trace, None, 0, ctypes.byref(n)))
+    out = np.zeros(n.value, dtype=RATE_SAMPLE_DTYPE)
+    if n.value:
+        _check(lib.scl_rate_samples(r.handle, trace, out.ctypes.data, n.value, ctypes.byref(n)))
+    return out
+
+
+def scl_rate_site_counts(r: RateResult) -> np.ndarray:
+    n = ctypes.c_size_t()
+    _check(lib.scl_rate_site_counts(r.handle, None, 0, ctypes.byref(n)))
+    out = np.zeros(n.value, dtype=np.uint64)
+    if n.value:
+        _check(lib.scl_rate_site_counts(r.handle, out.ctypes.data, n.value, ctypes.byref(n)))
+    return out
+
+
+def scl_rate_timing(r: RateResult) -> float:
+    ms = ctypes.c_float()
+    _check(lib.scl_rate_timing(r.handle, ctypes.byref(ms)))
+    return ms.value

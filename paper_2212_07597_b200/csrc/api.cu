@@ -51,6 +51,10 @@ struct scl_traces {
     uint32_t n_segs = 0;
     mutable unsigned int epoch = 0;
     CUtensorMap tmap;
+    // rate sampler (lazy, per loaded traces): alloc / free / copy bytes per unit, before each unit, per trace
+    mutable unsigned long long *d_usum = nullptr, *d_ustart = nullptr, *d_ttot = nullptr;
+    mutable size_t cap_usum = 0, cap_ttot = 0;
+    mutable bool usum_valid = false;
 };
 
 constexpr int kRing = 128;
@@ -263,6 +267,7 @@ static scl_status upload(scl_traces* tr, const scl_event* src, bool src_dev, std
     if (n_traces) CU(cudaMemcpyAsync(tr->h_sabs.data(), tr->d_sabs, n_traces * 8, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     tr->n_traces = n_traces; tr->n_sites = n_sites; tr->n_events = n; tr->max_len = max_len; tr->n_segs = total;
+    tr->usum_valid = false;
     tr->h_off = std::move(h_off);
     if (err != ~0ull) {
         uint32_t t = (uint32_t)(std::upper_bound(tr->h_off.begin(), tr->h_off.end(), err) - tr->h_off.begin()) - 1;
@@ -341,7 +346,7 @@ extern "C" void scl_traces_free(scl_traces* t) {
     if (!t) return;
     cudaFree(t->d_ev); cudaFree(t->d_off); cudaFree(t->d_sabs); cudaFree(t->d_tk); cudaFree(t->d_urec); cudaFree(t->d_uready);
     cudaFree(t->d_tr_nseg); cudaFree(t->d_tr_base); cudaFree(t->d_run); cudaFree(t->d_uent); cudaFree(t->d_ticket);
-    cudaFree(t->d_err);
+    cudaFree(t->d_err); cudaFree(t->d_usum); cudaFree(t->d_ustart); cudaFree(t->d_ttot);
     delete t;
 }
 
@@ -658,6 +663,145 @@ extern "C" scl_status scl_debug_prof(const scl_result* r, unsigned long long* ou
     return SCL_OK;
 }
 #endif
+
+// ---------------------------------------------------------------- rate-based sampler (rate.cu)
+struct scl_rate_result {
+    const scl_traces* tr = nullptr;
+    cudaStream_t st = nullptr;
+    unsigned long long *d_count = nullptr, *d_sbase = nullptr, *d_S = nullptr, *d_site = nullptr;
+    scl_rate_sample* d_samples = nullptr;
+    size_t cap = 0, cap_sites = 0, cap_tr = 0;
+    std::vector<unsigned long long> h_count, h_sbase;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+
+extern "C" void scl_rate_free(scl_rate_result* r) {
+    if (!r) return;
+    cudaFree(r->d_count); cudaFree(r->d_sbase); cudaFree(r->d_S); cudaFree(r->d_site); cudaFree(r->d_samples);
+    for (auto& e : r->ev) if (e) cudaEventDestroy(e);
+    delete r;
+}
+
+extern "C" scl_status scl_rate_run(uint64_t R, uint64_t seed, unsigned kinds, const scl_traces* tr, void* cuda_stream,
+                                   scl_rate_result** out)
+{
+    if (!tr || !out) return fail(SCL_EINVAL, "NULL argument");
+    if (R == 0) return fail(SCL_EINVAL, "rate_bytes must be >= 1");
+    if (kinds == 0 || (kinds & ~7u)) return fail(SCL_EINVAL, "kinds: a nonzero mask of 1 alloc, 2 free, 4 copy");
+    CU(cudaSetDevice(tr->device));
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    const uint32_t NT = tr->n_traces;
+    const size_t nt1 = std::max<uint32_t>(NT, 1), ns1 = std::max<uint32_t>(tr->n_segs, 1);
+    if (!tr->usum_valid) {                             // per-unit byte sums, once per loaded traces
+        if (ns1 > tr->cap_usum) {
+            cudaFree(tr->d_usum); cudaFree(tr->d_ustart); tr->d_usum = tr->d_ustart = nullptr; tr->cap_usum = 0;
+            CU(cudaMalloc(&tr->d_usum, ns1 * 3 * 8)); CU(cudaMalloc(&tr->d_ustart, ns1 * 3 * 8));
+            tr->cap_usum = ns1;
+        }
+        if (nt1 > tr->cap_ttot) {
+            cudaFree(tr->d_ttot); tr->d_ttot = nullptr; tr->cap_ttot = 0;
+            CU(cudaMalloc(&tr->d_ttot, nt1 * 3 * 8));
+            tr->cap_ttot = nt1;
+        }
+        CU(cudaMemsetAsync(tr->d_ttot, 0, nt1 * 3 * 8, st));
+        CU(launch_unit_sums(tr->d_ev, tr->d_tk, tr->n_segs, tr->d_usum, tr->d_tr_base, tr->d_tr_nseg, NT,
+                            tr->d_ustart, tr->d_ttot, st));
+        tr->usum_valid = true;
+    }
+    scl_rate_result* r = *out;
+    const bool fresh = r == nullptr;
+    if (fresh) {
+        r = new scl_rate_result();
+        for (auto& e : r->ev) if (cudaEventCreate(&e) != cudaSuccess) { scl_rate_free(r); return fail(SCL_ECUDA, "event"); }
+    } else if (r->tr != tr) {
+        return fail(SCL_EINVAL, "*out is a result of another traces handle");
+    }
+    r->tr = tr; r->st = st;
+    auto fail_free = [&](scl_status s2, const std::string& m) { if (fresh) scl_rate_free(r); return fail(s2, m); };
+    if (nt1 > r->cap_tr) {
+        cudaFree(r->d_count); cudaFree(r->d_sbase); r->d_count = r->d_sbase = nullptr; r->cap_tr = 0;
+        if (cudaMalloc(&r->d_count, nt1 * 8) != cudaSuccess || cudaMalloc(&r->d_sbase, nt1 * 8) != cudaSuccess)
+            { cudaGetLastError(); return fail_free(SCL_ENOMEM, "rate counts"); }
+        r->cap_tr = nt1;
+    }
+    if (tr->n_sites > r->cap_sites) {
+        cudaFree(r->d_site); r->d_site = nullptr; r->cap_sites = 0;
+        if (cudaMalloc(&r->d_site, (size_t)tr->n_sites * 8) != cudaSuccess) { cudaGetLastError(); return fail_free(SCL_ENOMEM, "rate sites"); }
+        r->cap_sites = tr->n_sites;
+    }
+    RateParams p{};
+    p.ev = tr->d_ev; p.tk = tr->d_tk; p.n_segs = tr->n_segs; p.n_traces = NT; p.R = R; p.seed = seed; p.kinds = kinds;
+    p.ttot = tr->d_ttot; p.ustart = tr->d_ustart; p.count = r->d_count; p.sbase = r->d_sbase; p.site_count = r->d_site;
+    CU(cudaEventRecord(r->ev[0], st));
+    CU(launch_rate(p, 0, st));                         // samples per trace
+    CU(cudaEventRecord(r->ev[1], st));
+    r->h_count.resize(NT); r->h_sbase.resize((size_t)NT + 1);
+    if (NT) CU(cudaMemcpyAsync(r->h_count.data(), r->d_count, NT * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    unsigned long long tot = 0;
+    for (uint32_t t = 0; t < NT; ++t) { r->h_sbase[t] = tot; tot += r->h_count[t]; }
+    r->h_sbase[NT] = tot;
+    if (tot > (1ull << 32)) return fail_free(SCL_EOVERFLOW, "more than 2^32 rate samples: raise rate_bytes");
+    if (tot > r->cap || !r->d_S) {
+        cudaFree(r->d_S); cudaFree(r->d_samples); r->d_S = nullptr; r->d_samples = nullptr; r->cap = 0;
+        const size_t c = std::max<unsigned long long>(tot, 1);
+        if (cudaMalloc(&r->d_S, c * 8) != cudaSuccess || cudaMalloc(&r->d_samples, c * sizeof(scl_rate_sample)) != cudaSuccess)
+            { cudaGetLastError(); return fail_free(SCL_ENOMEM, "rate samples"); }
+        r->cap = c;
+    }
+    p.S = r->d_S; p.samples = r->d_samples;
+    if (NT) CU(cudaMemcpyAsync(r->d_sbase, r->h_sbase.data(), NT * 8, cudaMemcpyHostToDevice, st));
+    CU(cudaEventRecord(r->ev[2], st));
+    CU(cudaMemsetAsync(r->d_site, 0, (size_t)tr->n_sites * 8, st));
+    CU(launch_rate(p, 1, st));                         // S_k
+    CU(launch_rate(p, 2, st));                         // placement
+    CU(cudaEventRecord(r->ev[3], st));
+    *out = r;
+    return SCL_OK;
+}
+
+extern "C" scl_status scl_rate_counts(const scl_rate_result* r, uint64_t* counts, size_t cap, size_t* n) {
+    if (!r || !n) return fail(SCL_EINVAL, "NULL argument");
+    *n = r->h_count.size();
+    if (cap == 0) return SCL_OK;
+    if (!counts) return fail(SCL_EINVAL, "counts is NULL");
+    memcpy(counts, r->h_count.data(), std::min(cap, *n) * 8);
+    return SCL_OK;
+}
+
+extern "C" scl_status scl_rate_samples(const scl_rate_result* r, uint32_t trace, scl_rate_sample* out, size_t cap, size_t* n) {
+    if (!r || !n) return fail(SCL_EINVAL, "NULL argument");
+    if (trace >= r->h_count.size()) return fail(SCL_EINVAL, "trace out of range");
+    *n = r->h_count[trace];
+    if (cap == 0 || *n == 0) return SCL_OK;
+    if (!out) return fail(SCL_EINVAL, "out is NULL");
+    CU(cudaSetDevice(r->tr->device));
+    CU(cudaMemcpyAsync(out, r->d_samples + r->h_sbase[trace], std::min(cap, *n) * sizeof(scl_rate_sample),
+                       cudaMemcpyDeviceToHost, r->st));
+    CU(cudaStreamSynchronize(r->st));
+    return SCL_OK;
+}
+
+extern "C" scl_status scl_rate_site_counts(const scl_rate_result* r, uint64_t* counts, size_t cap, size_t* n) {
+    if (!r || !n) return fail(SCL_EINVAL, "NULL argument");
+    *n = r->tr->n_sites;
+    if (cap == 0) return SCL_OK;
+    if (!counts) return fail(SCL_EINVAL, "counts is NULL");
+    CU(cudaSetDevice(r->tr->device));
+    CU(cudaMemcpyAsync(counts, r->d_site, std::min(cap, *n) * 8, cudaMemcpyDeviceToHost, r->st));
+    CU(cudaStreamSynchronize(r->st));
+    return SCL_OK;
+}
+
+extern "C" scl_status scl_rate_timing(const scl_rate_result* r, float* ms) {
+    if (!r || !ms) return fail(SCL_EINVAL, "NULL argument");
+    CU(cudaEventSynchronize(r->ev[3]));
+    float a = 0, b = 0;
+    CU(cudaEventElapsedTime(&a, r->ev[0], r->ev[1]));
+    CU(cudaEventElapsedTime(&b, r->ev[2], r->ev[3]));
+    *ms = a + b;
+    return SCL_OK;
+}
 
 // "a prime number slightly above 10MB" -- smallest prime >= base (trial division)
 extern "C" uint64_t scl_next_prime(uint64_t base) {

@@ -164,6 +164,26 @@ __device__ __forceinline__ void samples_trace(const ReplayParams& p, unsigned t,
 }
 #endif
 
+// Rate-based byte sampler (rate.cu; NEXT-1 / NEXT-3).
+struct RateParams {
+    const scl_event* ev;
+    const TicketInfo* tk;              // [n_segs] unit placement (as the replay kernel's tickets)
+    unsigned n_segs, n_traces;
+    unsigned long long R, seed;
+    unsigned kinds;                    // counted event kinds: bit 0 alloc, 1 free, 2 copy
+    const unsigned long long* ttot;    // [n_traces][3] alloc / free / copy bytes per trace
+    const unsigned long long* ustart;  // [n_segs][3] the same before each unit (exclusive, within its trace)
+    unsigned long long* count;         // [n_traces] samples per trace
+    const unsigned long long* sbase;   // [n_traces] first sample slot
+    unsigned long long* S;             // [total] draw prefix sums S_k of the samples
+    scl_rate_sample* samples;          // [total]
+    unsigned long long* site_count;    // [n_sites] samples per site
+};
+cudaError_t launch_unit_sums(const scl_event* ev, const TicketInfo* tk, unsigned n_segs, unsigned long long* usum,
+                             const unsigned* tr_base, const unsigned* tr_nseg, unsigned n_traces,
+                             unsigned long long* ustart, unsigned long long* ttot, cudaStream_t st);
+cudaError_t launch_rate(const RateParams& p, int phase, cudaStream_t st);   // 0 count, 1 fill S, 2 place
+
 // launch wrappers (replay.cu)
 cudaError_t launch_load_stats(const scl_event* ev, const unsigned long long* off, unsigned n_traces,
                               unsigned long long n_events, unsigned n_sites, unsigned long long* sabs,

@@ -1,6 +1,8 @@
 """CPU-side checks of the C-ABI boundary: libscl.so loads, exports every
 function include/scl.h declares, and fails loudly (no CPU fallback) without a GPU."""
 import ctypes
+
+import oracle
 import os
 import re
 import subprocess
@@ -44,6 +46,7 @@ def test_next_prime_host_only():
 def test_struct_sizes():
     assert scl.SAMPLE_DTYPE.itemsize == 32 and scl.SITE_ROW_DTYPE.itemsize == 104
     assert scl.SUMMARY_DTYPE.itemsize == 48 and ctypes.sizeof(scl._RunOpts) == 40
+    assert scl.RATE_SAMPLE_DTYPE.itemsize == 24 and oracle.RATE_SAMPLE_DTYPE.itemsize == 24
 
 
 def test_no_cpu_fallback():
