@@ -272,6 +272,20 @@ def main():
 
     summ = scl.scl_trace_summaries(r)
     n_samples = int(summ["n_samples"].sum())
+
+    # NEXT-1: the paper's comparison (Table tab:sampling-comparison) on the same resident traces:
+    # the rate-based sampler at R = T (mean one sample per T bytes allocated or freed)
+    rr = scl.scl_rate_run(cfg.T, tr, seed=2022, stream=stream)
+    rate_ms = []
+    for _ in range(3):
+        rr = scl.scl_rate_run(cfg.T, tr, seed=2022, stream=stream, out=rr)
+        rate_ms.append(scl.scl_rate_timing(rr))
+    n_rate = int(scl.scl_rate_counts(rr).sum())
+    next1 = {"rate_samples": n_rate, "threshold_samples": n_samples,
+             "ratio": (n_rate / n_samples) if n_samples else None,
+             "sample_log_bytes": {"rate": n_rate * 24, "threshold": n_samples * 32},
+             "rate_kernels_ms": statistics.median(rate_ms),
+             "note": "rate-based byte sampler, R = T, seed 2022, same traces (per rank)"}
     kern_avg = statistics.mean(kern_ms)
     alg_bytes = n_ev * BYTES_PER_EVENT + n_samples * SAMPLE_BYTES + cfg.n_sites * ROW_BYTES_TABLE
     achieved = alg_bytes / (kern_avg / 1e3) / 1e9
@@ -339,6 +353,7 @@ def main():
                                  "(tables > 16384 sites: finalize + CUB radix sort + rows instead of report)",
             "kernel_timing": "replay_kernel durations from CUDA events in a second pass of K steps",
             "n_samples_per_step": n_samples,
+            "next1_rate_vs_threshold": next1,
             "cpu_baseline": cpu,
         }
         print(json.dumps(out))

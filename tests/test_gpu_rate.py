@@ -81,3 +81,29 @@ def test_rate_reload_and_errors():
     for bad in ((0, 1, 3), (10, 1, 0), (10, 1, 8)):
         with pytest.raises(scl.SclError):
             scl.scl_rate_run(bad[0], tr, seed=bad[1], kinds=bad[2])
+
+
+def test_copy_volume():
+    """NEXT-3: copy volume by rate sampling of the copied bytes at
+    R = 2 T (copy_rate_multiple 2); each sample credits R bytes to its site.  GPU = oracle
+    sample by sample; the credited bytes estimate every site's true copy bytes (binomial
+    tolerance); the threshold sampler ignores the copies (oracle parity on the same traces)."""
+    from parity import compare
+    cfg = tracegen.COPY_CFG.with_traces(6)
+    ev, off = tracegen.generate(cfg)
+    kind = ((ev["meta"] >> np.uint64(40)) & np.uint64(3)).astype(np.int64)
+    assert (kind == 2).sum() > 0.01 * len(ev)
+    tr = scl.scl_trace_load(ev, off, cfg.n_sites)
+    R = 2 * cfg.T
+    r = scl.scl_rate_run(R, tr, seed=31, kinds=scl.RATE_COPY)
+    _check(ev, off, cfg.n_sites, R, 31, scl.RATE_COPY, r)
+    site = (ev["meta"] >> np.uint64(43)).astype(np.int64)
+    size = (ev["meta"] & np.uint64((1 << 40) - 1)).astype(np.float64)
+    true = np.bincount(site[kind == 2], weights=size[kind == 2], minlength=cfg.n_sites)
+    est = scl.scl_rate_site_counts(r).astype(np.float64) * R
+    assert abs(est.sum() - true.sum()) < 4 * np.sqrt(true.sum() * R) + R
+    top = np.argsort(true)[-5:]                              # the heaviest copy sites
+    for s_ in top:
+        assert abs(est[s_] - true[s_]) < 5 * np.sqrt(true[s_] * R) + 2 * R
+    thr = scl.scl_replay_run(cfg.T, tr)
+    compare(ev, off, cfg.n_sites, cfg.T, thr)

@@ -27,7 +27,8 @@ class _Cfg(ctypes.Structure):
                 ("events_per_trace", ctypes.c_uint64), ("zipf_s", ctypes.c_double),
                 ("n_planted", ctypes.c_uint32), ("heavy_tailed", ctypes.c_uint32),
                 ("leak_T", ctypes.c_uint64), ("leak_lambda", ctypes.c_double),
-                ("leak_rate_spread", ctypes.c_double), ("seed", ctypes.c_uint64)]
+                ("leak_rate_spread", ctypes.c_double), ("seed", ctypes.c_uint64),
+                ("copy_lambda", ctypes.c_double)]
 
 
 @dataclass(frozen=True)
@@ -44,6 +45,7 @@ class Config:
     heavy_tailed: bool = False
     seed: int = 0
     t_sweep: tuple = ()          # config 5: thresholds of the sweep
+    copy_lambda: float = 0.0     # per-step probability of a copy event (NEXT-3 copy volume); 0: none
 
     @property
     def n_events(self) -> int:
@@ -55,7 +57,7 @@ class Config:
     def ctype(self) -> _Cfg:
         return _Cfg(self.n_traces, self.n_sites, self.events_per_trace, self.zipf_s,
                     self.n_planted, int(self.heavy_tailed), self.T, self.leak_lambda,
-                    self.leak_rate_spread, self.seed)
+                    self.leak_rate_spread, self.seed, self.copy_lambda)
 
 
 # smallest primes >= the bases (pinned against trial division
@@ -73,6 +75,10 @@ CONFIGS = {
     5: Config("cfg5", 256, 100_000_000, 10_000, 1.0, 8, 65537, 2.0e-6, heavy_tailed=True,
               seed=20221215 + 5, t_sweep=SWEEP),
 }
+
+# NEXT-3 (copy volume): config 2 with 2 % copy events (memcpy of an object-sized
+# buffer at the current line); copies leave the footprint, samples and leak tracker unchanged.
+COPY_CFG = replace(CONFIGS[2], name="cfg2-copy", copy_lambda=0.02, seed=20221215 + 26)
 
 _lib = None
 

@@ -73,6 +73,7 @@ struct tg_config {
     double   leak_lambda;      // per-step probability of a planted-leak allocation
     double   leak_rate_spread; // planted site k drawn with weight spread^(k/(n-1)) (config 3: 100)
     uint64_t seed;             // config seed, 20221215 + cfg
+    double   copy_lambda;      // per-step probability of a copy event (kind 2); 0: none
 };
 
 struct tg_event { uint64_t ptr; uint64_t meta; };
@@ -178,6 +179,12 @@ struct Model {
                 out[i].meta = pack(o.size, 1, zipf(g));                                // free site = current line
                 if (o.size <= 512) small_free[o.size >> 4].push_back(o.ptr);
                 else large_free[o.size].push_back(o.ptr);
+                continue;
+            }
+            if (c.copy_lambda > 0 && g.uniform() < c.copy_lambda) {                 // a memcpy at the current
+                const uint32_t cs = zipf(g);                                          // line, of an object-sized
+                out[i].ptr = 0;                                                       // buffer (no draw at all
+                out[i].meta = pack(size_for(cs, g), 2, cs);                           // when copy_lambda == 0)
                 continue;
             }
             uint32_t s;
