@@ -265,3 +265,31 @@ def test_hwm_mode_sample():
     a = compare(ev, off, cfg.n_sites, 1048583, r, hwm_mode=scl.HWM_SAMPLE)
     b = oracle.full(ev, off, cfg.n_sites, 1048583, hwm_mode=oracle.HWM_PREFIX)
     assert int(a["result"].summaries["n_episodes"].sum()) != int(b["result"].summaries["n_episodes"].sum())
+
+
+def test_edge_many_traces_max_sites_extreme_T():
+    """Edge cases: 4000 short traces (many runner lanes per warp), n_sites at the maximum 2^21
+    with sites spread over it (cold-site path), sizes up to 2^40 - 1, T = 1 (every event is a
+    sample) and T huge (no sample)."""
+    rng = np.random.default_rng(99)
+    traces = []
+    for i in range(4000):
+        n = int(rng.integers(0, 60))
+        tr_ = []
+        live = []
+        for _ in range(n):
+            if live and rng.random() < 0.4:
+                p, z, s_ = live.pop(int(rng.integers(len(live))))
+                tr_.append(("f", p, z, int(rng.integers(0, 1 << 21))))
+            else:
+                z = int(rng.choice([1, 16, (1 << 40) - 1, int(rng.integers(1, 1 << 30))]))
+                p = 0x1000 + 16 * len(tr_) + (i << 24)
+                live.append((p, z, 0))
+                tr_.append(("a", p, z, int(rng.integers(0, 1 << 21))))
+        traces.append(tr_)
+    ev, off = _concat(traces)
+    tr = scl.scl_trace_load(ev, off, 1 << 21)
+    r = None
+    for T in (1, 1 << 45):
+        r = scl.scl_replay_run(T, tr, out=r)
+        compare(ev, off, 1 << 21, T, r)
