@@ -28,6 +28,7 @@ _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 EVENT_DTYPE = np.dtype([("ptr", "<u8"), ("meta", "<u8")])
 SAMPLE_DTYPE = np.dtype([("idx", "<u8"), ("net", "<i8"), ("footprint", "<i8"),
                          ("site", "<u4"), ("kind", "u1"), ("new_max", "u1"), ("pad", "<u2")])
+DOMAIN_DTYPE = np.dtype([("alloc_bytes", "<u8"), ("managed_bytes", "<u8")])   # per sample (NEXT-2)
 SUMMARY_DTYPE = np.dtype([("f_final", "<i8"), ("hwm", "<i8"), ("n_samples", "<u8"),
                           ("n_episodes", "<u8"), ("f_first_sample", "<i8"), ("f_last_sample", "<i8")])
 assert EVENT_DTYPE.itemsize == 16 and SAMPLE_DTYPE.itemsize == 32 and SUMMARY_DTYPE.itemsize == 48
@@ -62,8 +63,8 @@ def _load():
         build()
         lib = ctypes.CDLL(_LIB_PATH)
         P, U64, U32, I32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int
-        lib.orc_replay_trace.argtypes = [P, U64, U64, I32, P, U64, P, P, U32]
-        lib.orc_replay_all.argtypes = [P, P, U32, U32, U64, I32, I32, P, P, P, P]
+        lib.orc_replay_trace.argtypes = [P, U64, U64, I32, P, U64, P, P, U32, P]
+        lib.orc_replay_all.argtypes = [P, P, U32, U32, U64, I32, I32, P, P, P, P, P]
         lib.orc_gate.argtypes = [P, U32, P, P, P]
         lib.orc_finalize.argtypes = [P, U32, I32, U64, I32, P, P, P]
         lib.orc_report_order.argtypes = [P, P, U32, P]
@@ -90,6 +91,7 @@ class OracleResult:
     sample_off: np.ndarray       # uint64 [n_traces+1] (offsets into samples after trimming)
     summaries: np.ndarray        # SUMMARY_DTYPE [n_traces]
     site_table: np.ndarray       # uint64 [n_sites, 10]
+    domains: np.ndarray = None   # DOMAIN_DTYPE parallel to samples (NEXT-2)
 
     def trace_samples(self, t: int) -> np.ndarray:
         return self.samples[int(self.sample_off[t]):int(self.sample_off[t + 1])]
@@ -122,8 +124,9 @@ def replay(events: np.ndarray, offsets, n_sites: int, T: int, hwm_mode: int = HW
     samples = np.zeros(max(int(soff[-1]), 1), dtype=SAMPLE_DTYPE)
     summ = np.zeros(n_traces, dtype=SUMMARY_DTYPE)
     table = np.zeros((n_sites, NCOL), dtype=np.uint64)
+    dom = np.zeros(len(samples), dtype=DOMAIN_DTYPE)
     rc = lib.orc_replay_all(_ptr(events), _ptr(offsets), n_traces, n_sites, T, hwm_mode,
-                            n_threads, _ptr(samples), _ptr(soff), _ptr(summ), _ptr(table))
+                            n_threads, _ptr(samples), _ptr(soff), _ptr(summ), _ptr(table), _ptr(dom))
     if rc != 0:
         raise ValueError("oracle: invalid event (site >= n_sites or kind 3)")
     ns = summ["n_samples"].astype(np.uint64)
@@ -132,7 +135,7 @@ def replay(events: np.ndarray, offsets, n_sites: int, T: int, hwm_mode: int = HW
         if n_traces else np.zeros(0, dtype=np.int64)
     out_off = np.zeros(n_traces + 1, dtype=np.uint64)
     out_off[1:] = np.cumsum(ns)
-    return OracleResult(samples[keep.astype(np.int64)], out_off, summ, table)
+    return OracleResult(samples[keep.astype(np.int64)], out_off, summ, table, dom[keep.astype(np.int64)])
 
 
 def gate(summaries: np.ndarray):

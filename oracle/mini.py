@@ -15,8 +15,12 @@ from __future__ import annotations
 from collections import defaultdict
 
 
-def replay_trace(events, T, hwm_mode="prefix"):
+def replay_trace(events, T, hwm_mode="prefix", with_domains=False):
+    """with_domains: also return, per sample, (A, managed part of A) -- the allocated bytes since
+    the last reset and those of managed-domain events (5th tuple element 1; NEXT-2)."""
     A = 0          # bytes allocated since the last sample (P:430)
+    Am = 0         # of which managed (Python) allocations
+    domains = []
     Fr = 0         # bytes freed since the last sample
     footprint = 0
     peak = 0
@@ -26,10 +30,13 @@ def replay_trace(events, T, hwm_mode="prefix"):
     samples = []
     cols = defaultdict(lambda: defaultdict(int))
     episodes = 0
-    for i, (kind, ptr, size, site) in enumerate(events):
+    for i, ev in enumerate(events):
+        kind, ptr, size, site = ev[:4]
         prev_peak = peak
         if kind == "a":
             A += size
+            if len(ev) > 4 and ev[4]:
+                Am += size
             footprint += size
             cols[site]["n_malloc"] += 1
             cols[site]["malloc_bytes"] += size
@@ -52,6 +59,7 @@ def replay_trace(events, T, hwm_mode="prefix"):
                 new_max = growth and footprint > peak_at_samples
             peak_at_samples = max(peak_at_samples, footprint)
             samples.append((i, "G" if growth else "D", net, footprint, site, new_max))
+            domains.append((A, Am))
             if growth:
                 cols[site]["n_growth"] += 1
                 cols[site]["growth_bytes"] += net
@@ -65,10 +73,12 @@ def replay_trace(events, T, hwm_mode="prefix"):
                 reclaimed = False
                 cols[site]["leak_mallocs"] += 1
                 episodes += 1
-            A = Fr = 0                      # "resets the counters"
+            A = Fr = Am = 0                 # "resets the counters"
     if tracked is not None and reclaimed:
         cols[tracked[1]]["leak_frees"] += 1
     summary = dict(f_final=footprint, hwm=peak, n_samples=len(samples), n_episodes=episodes,
                    f_first_sample=samples[0][3] if samples else 0,
                    f_last_sample=samples[-1][3] if samples else 0)
+    if with_domains:
+        return samples, summary, cols, domains
     return samples, summary, cols

@@ -51,7 +51,8 @@ static inline uint32_t ev_site(const orc_event* e) { return (uint32_t)(e->meta >
 int orc_replay_trace(const orc_event* ev, uint64_t n, uint64_t T, int hwm_mode,
                      orc_sample* samples, uint64_t cap,
                      orc_trace_summary* summary,
-                     uint64_t* site_table, uint32_t n_sites)
+                     uint64_t* site_table, uint32_t n_sites,
+                     orc_sample_domain* dom)
 {
     int64_t F = 0, M = 0, c = 0;
     int64_t Msample = 0;                 /* max over sample footprints (hwm_mode SAMPLE) */
@@ -59,6 +60,7 @@ int orc_replay_trace(const orc_event* ev, uint64_t n, uint64_t T, int hwm_mode,
     uint64_t ep_ptr = 0; uint32_t ep_site = 0;
     uint64_t ns = 0, n_ep = 0;
     int64_t f_first = 0, f_last = 0;
+    uint64_t a_since = 0, m_since = 0;   /* allocated / managed allocated bytes since the reset */
     const int64_t Ti = (int64_t)T;
 
     for (uint64_t i = 0; i < n; ++i) {
@@ -70,6 +72,7 @@ int orc_replay_trace(const orc_event* ev, uint64_t n, uint64_t T, int hwm_mode,
         if (kind == 2) continue;                     /* copies do not change footprint */
 
         int64_t d = (kind == 0) ? (int64_t)size : -(int64_t)size;
+        if (kind == 0) { a_since += size; if ((e->meta >> 42) & 1u) m_since += size; }
         int64_t Mprev = M;
         F += d;
         if (F > M) M = F;
@@ -87,7 +90,9 @@ int orc_replay_trace(const orc_event* ev, uint64_t n, uint64_t T, int hwm_mode,
                 orc_sample* s = &samples[ns];
                 s->idx = i; s->net = c; s->footprint = F; s->site = site;
                 s->kind = growth ? 0 : 1; s->new_max = (uint8_t)new_max; s->pad = 0;
+                if (dom) { dom[ns].alloc_bytes = a_since; dom[ns].managed_bytes = m_since; }
             }
+            a_since = 0; m_since = 0;
             if (ns == 0) f_first = F;
             f_last = F;
             ++ns;
@@ -119,7 +124,7 @@ int orc_replay_trace(const orc_event* ev, uint64_t n, uint64_t T, int hwm_mode,
 /* ---- many traces, one per task on a pthread pool (SURVEY §8(d) "Oracle timing") ---- */
 typedef struct {
     const orc_event* ev; const uint64_t* offsets; uint32_t n_traces; uint32_t n_sites;
-    uint64_t T; int hwm_mode; orc_sample* samples; const uint64_t* sample_off;
+    uint64_t T; int hwm_mode; orc_sample* samples; const uint64_t* sample_off; orc_sample_domain* dom;
     orc_trace_summary* summaries; uint64_t* table; int err; uint32_t* next;
 } orc_job;
 
@@ -132,7 +137,7 @@ static void* orc_worker(void* arg)
         uint64_t b = j->offsets[t], e = j->offsets[t + 1];
         uint64_t so = j->sample_off[t], cap = j->sample_off[t + 1] - so;
         if (orc_replay_trace(j->ev + b, e - b, j->T, j->hwm_mode, j->samples + so, cap,
-                             &j->summaries[t], j->table, j->n_sites) != 0) j->err = -1;
+                             &j->summaries[t], j->table, j->n_sites, j->dom ? j->dom + so : NULL) != 0) j->err = -1;
     }
     return NULL;
 }
@@ -140,7 +145,8 @@ static void* orc_worker(void* arg)
 int orc_replay_all(const orc_event* ev, const uint64_t* offsets, uint32_t n_traces,
                    uint32_t n_sites, uint64_t T, int hwm_mode, int n_threads,
                    orc_sample* samples, const uint64_t* sample_off,
-                   orc_trace_summary* summaries, uint64_t* site_table)
+                   orc_trace_summary* summaries, uint64_t* site_table,
+                   orc_sample_domain* dom)
 {
     if (n_threads < 1) n_threads = 1;
     size_t tab = (size_t)n_sites * ORC_NCOL;
@@ -152,7 +158,7 @@ int orc_replay_all(const orc_event* ev, const uint64_t* offsets, uint32_t n_trac
     for (int k = 0; k < n_threads; ++k) {
         orc_job* j = &jobs[k];
         j->ev = ev; j->offsets = offsets; j->n_traces = n_traces; j->n_sites = n_sites;
-        j->T = T; j->hwm_mode = hwm_mode; j->samples = samples; j->sample_off = sample_off;
+        j->T = T; j->hwm_mode = hwm_mode; j->samples = samples; j->sample_off = sample_off; j->dom = dom;
         j->summaries = summaries; j->err = 0; j->next = &next;
         j->table = (k == 0) ? site_table : (uint64_t*)calloc(tab ? tab : 1, sizeof(uint64_t));
         if (!j->table) err = -1;

@@ -61,10 +61,17 @@ enum { ORC_FORMULA_PAPER = 0, ORC_FORMULA_TEXTBOOK = 1 };
  * (n_sites x ORC_NCOL, row-major, caller-zeroed once).  Writes at most
  * `cap` samples; *summary->n_samples is the true count.
  * Returns 0, or -1 if an event's site >= n_sites or kind == 3. */
+/* Per sample (NEXT-2, SPEC S:121 / S:146): allocated bytes and managed-domain (meta bit 42)
+ * allocated bytes since the previous sample (the counters "reset" at P:434), the triggering
+ * event included; managed fraction = managed / max(alloc, 1) ("the fraction of Python (vs.
+ * native) allocations in the total sample"). */
+typedef struct { uint64_t alloc_bytes; uint64_t managed_bytes; } orc_sample_domain;
+
 int orc_replay_trace(const orc_event* ev, uint64_t n, uint64_t T, int hwm_mode,
                      orc_sample* samples, uint64_t cap,
                      orc_trace_summary* summary,
-                     uint64_t* site_table, uint32_t n_sites);
+                     uint64_t* site_table, uint32_t n_sites,
+                     orc_sample_domain* dom /* [cap] or NULL */);
 
 /* Replay all traces (offsets[n_traces+1]) on n_threads host threads (one
  * trace per task).  samples for trace t go to samples + sample_off[t],
@@ -73,7 +80,8 @@ int orc_replay_trace(const orc_event* ev, uint64_t n, uint64_t T, int hwm_mode,
 int orc_replay_all(const orc_event* ev, const uint64_t* offsets, uint32_t n_traces,
                    uint32_t n_sites, uint64_t T, int hwm_mode, int n_threads,
                    orc_sample* samples, const uint64_t* sample_off,
-                   orc_trace_summary* summaries, uint64_t* site_table);
+                   orc_trace_summary* summaries, uint64_t* site_table,
+                   orc_sample_domain* dom /* parallel to samples, or NULL */);
 
 /* Gate of P:62-65 ("slope of overall memory growth is at least 1%"), reading
  * Q10: num = sum_t (F_last - F_first), den = sum_t max(F_first, 1) over traces

@@ -139,11 +139,13 @@ def pack(kind: int, size: int, site: int, domain: int = 0) -> int:
 
 
 def from_tuples(events) -> np.ndarray:
-    """[(kind 'a'|'f'|'c', ptr, size, site), ...] -> EVENT_DTYPE array (hand-written traces)."""
+    """[(kind 'a'|'f'|'c', ptr, size, site[, domain]), ...] -> EVENT_DTYPE array (hand-written
+    traces; domain 1 = managed / Python, 0 = native, NEXT-2)."""
     k = {"a": 0, "f": 1, "c": 2}
     arr = np.zeros(len(events), dtype=EVENT_DTYPE)
-    for i, (kind, ptr, size, site) in enumerate(events):
-        arr[i] = (ptr, pack(k[kind], size, site))
+    for i, e in enumerate(events):
+        kind, ptr, size, site = e[:4]
+        arr[i] = (ptr, pack(k[kind], size, site, e[4] if len(e) > 4 else 0))
     return arr
 
 

@@ -208,7 +208,8 @@ struct Model {
                 else { p = large_bump; large_bump += (size + 4095) & ~4095ull; }
             }
             out[i].ptr = p;
-            out[i].meta = pack(size, 0, s);
+            out[i].meta = pack(size, 0, s) | (cls[s] == SMALL ? (1ull << 42) : 0ull);  // domain: small objects are
+                                                                                    // the interpreter's (managed)
             if (!leak) heap.push(Live{i + lifetime(s, g), p, size});
         }
     }
