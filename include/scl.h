@@ -191,6 +191,16 @@ scl_status scl_result_timing(const scl_result* r, float* replay_kernel_ms, float
  * without synchronising between them.  *n = number written (<= cap). */
 scl_status scl_result_kernel_times(const scl_result* r, float* ms, size_t cap, size_t* n);
 
+/* ---- Per-sample Python / native split ("the fraction of Python
+ * (vs. native) allocations in the total sample"): for each threshold sample,
+ * the bytes allocated since the previous sample (the triggering event included, frees
+ * excluded) and the part of them allocated in the managed domain (meta bit 42).  managed
+ * fraction = managed_bytes / max(alloc_bytes, 1). */
+typedef struct { uint64_t alloc_bytes; uint64_t managed_bytes; } scl_sample_domain;   /* 16 B */
+/* One trace's values, parallel to scl_samples (computed on the first call after a run; waits
+ * for it). */
+scl_status scl_sample_domains(const scl_result* r, uint32_t trace, scl_sample_domain* out, size_t cap, size_t* n);
+
 /* ---- Rate-based byte sampler: the paper's comparison baseline (Table
  * tab:sampling-comparison) and copy-volume sampling (NEXT-3).
  * Per trace a counter drawn from a geometric distribution with mean R is decremented by the

@@ -21,7 +21,7 @@ __all__ = ["SclError", "Traces", "Result", "scl_trace_load", "scl_trace_reload",
            "scl_site_report", "scl_samples", "scl_trace_summaries", "scl_gate", "scl_result_device_table",
            "scl_result_timing", "scl_result_kernel_times", "scl_next_prime", "scl_traces_info", "EVENT_DTYPE", "SAMPLE_DTYPE",
            "SUMMARY_DTYPE", "SITE_ROW_DTYPE", "COLS", "device_table_tensor", "write_trace_file",
-           "RATE_SAMPLE_DTYPE", "RATE_ALLOC_FREE", "RATE_COPY", "RateResult", "scl_rate_run", "scl_rate_counts",
+           "DOMAIN_DTYPE", "scl_sample_domains", "RATE_SAMPLE_DTYPE", "RATE_ALLOC_FREE", "RATE_COPY", "RateResult", "scl_rate_run", "scl_rate_counts",
            "scl_rate_samples", "scl_rate_site_counts", "scl_rate_timing"]
 
 EVENT_DTYPE = np.dtype([("ptr", "<u8"), ("meta", "<u8")])
@@ -30,6 +30,7 @@ SAMPLE_DTYPE = np.dtype([("idx", "<u8"), ("net", "<i8"), ("footprint", "<i8"), (
 SUMMARY_DTYPE = np.dtype([("f_final", "<i8"), ("hwm", "<i8"), ("n_samples", "<u8"), ("n_episodes", "<u8"),
                           ("f_first_sample", "<i8"), ("f_last_sample", "<i8")])
 RATE_SAMPLE_DTYPE = np.dtype([("idx", "<u8"), ("draw_sum", "<u8"), ("site", "<u4"), ("kind", "<u4")])
+DOMAIN_DTYPE = np.dtype([("alloc_bytes", "<u8"), ("managed_bytes", "<u8")])
 RATE_ALLOC_FREE, RATE_COPY = 3, 4
 SITE_ROW_DTYPE = np.dtype([("site", "<u4"), ("leak_flag", "<u4"), ("col", "<u8", (10,)),
                            ("leak_prob", "<f8"), ("leak_rate_mbps", "<f8")])
@@ -63,6 +64,7 @@ def _load():
         "scl_trace_reload": [P, P, P, U32, U32, I32, P],
         "scl_result_kernel_times": [P, P, SZ, P],
         "scl_rate_run": [U64, U64, U32, P, P, P],
+        "scl_sample_domains": [P, U32, P, SZ, P],
         "scl_rate_counts": [P, P, SZ, P],
         "scl_rate_samples": [P, U32, P, SZ, P],
         "scl_rate_site_counts": [P, P, SZ, P],
@@ -251,6 +253,17 @@ def scl_samples(r: Result, trace: int) -> np.ndarray:
     out = np.zeros(n.value, dtype=SAMPLE_DTYPE)
     if n.value:
         _check(lib.scl_samples(r.handle, trace, out.ctypes.data, n.value, ctypes.byref(n)))
+    return out
+
+
+def scl_sample_domains(r: Result, trace: int) -> np.ndarray:
+    """Per sample of the trace: bytes allocated since the previous sample and the managed-domain
+    part of them (NEXT-2); managed fraction = managed_bytes / max(alloc_bytes, 1)."""
+    n = ctypes.c_size_t()
+    _check(lib.scl_sample_domains(r.handle, trace, None, 0, ctypes.byref(n)))
+    out = np.zeros(n.value, dtype=DOMAIN_DTYPE)
+    if n.value:
+        _check(lib.scl_sample_domains(r.handle, trace, out.ctypes.data, n.value, ctypes.byref(n)))
     return out
 
 

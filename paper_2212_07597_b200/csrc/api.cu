@@ -78,6 +78,10 @@ struct scl_result {
     void* d_cub = nullptr; size_t cub_bytes = 0;
     scl_site_row* d_rows = nullptr;
     RTask* d_rtask = nullptr;                  // reclaim pass re-check queue
+    unsigned long long* d_P = nullptr;         // per-sample (alloc, managed) prefixes (NEXT-2, lazy)
+    scl_sample_domain* d_dom = nullptr;
+    size_t cap_dom = 0;
+    bool dom_valid = false;
     // host
     std::vector<unsigned long long> h_sbase;
     std::vector<scl_trace_summary> h_summ;
@@ -373,6 +377,7 @@ extern "C" void scl_result_free(scl_result* r) {
     if (!r) return;
     free_result_buffers(r);
     cudaFree(r->d_samples); cudaFree(r->d_epflag); cudaFree(r->d_prof); cudaFree(r->d_rtask);
+    cudaFree(r->d_P); cudaFree(r->d_dom);
     if (r->h_gate) cudaFreeHost(r->h_gate);
     for (auto& e : r->ev) if (e) cudaEventDestroy(e);
     for (auto& e : r->kev) if (e) cudaEventDestroy(e);
@@ -441,7 +446,7 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
     r->tr = tr; r->T = threshold; r->formula = o.formula; r->stream = st;
     const uint64_t tick = o.tick_ns ? o.tick_ns : tr->tick_ns;
     r->elapsed_ns = o.elapsed_ns ? o.elapsed_ns : tr->max_len * tick;
-    r->summ_valid = false; r->finalized = false;
+    r->summ_valid = false; r->finalized = false; r->dom_valid = false;
 
     // sample capacity per trace: min(n_t, floor(sum|d| / T)) -- every sample consumes |net| >= T
     // (prep_kernel computes the same bases on the device; the host copy serves scl_samples)
@@ -664,6 +669,61 @@ extern "C" scl_status scl_debug_prof(const scl_result* r, unsigned long long* ou
 }
 #endif
 
+// Per-unit alloc / free / copy / managed-alloc byte sums and their prefix within each trace (lazy,
+// once per loaded traces; the rate sampler and the per-sample domain split use them).
+static scl_status ensure_unit_sums(const scl_traces* tr, cudaStream_t st) {
+    if (tr->usum_valid) return SCL_OK;
+    const size_t nt1 = std::max<uint32_t>(tr->n_traces, 1), ns1 = std::max<uint32_t>(tr->n_segs, 1);
+    if (ns1 > tr->cap_usum) {
+        cudaFree(tr->d_usum); cudaFree(tr->d_ustart); tr->d_usum = tr->d_ustart = nullptr; tr->cap_usum = 0;
+        CU(cudaMalloc(&tr->d_usum, ns1 * kUCols * 8)); CU(cudaMalloc(&tr->d_ustart, ns1 * kUCols * 8));
+        tr->cap_usum = ns1;
+    }
+    if (nt1 > tr->cap_ttot) {
+        cudaFree(tr->d_ttot); tr->d_ttot = nullptr; tr->cap_ttot = 0;
+        CU(cudaMalloc(&tr->d_ttot, nt1 * kUCols * 8));
+        tr->cap_ttot = nt1;
+    }
+    CU(cudaMemsetAsync(tr->d_ttot, 0, nt1 * kUCols * 8, st));
+    CU(launch_unit_sums(tr->d_ev, tr->d_tk, tr->n_segs, tr->d_usum, tr->d_tr_base, tr->d_tr_nseg, tr->n_traces,
+                        tr->d_ustart, tr->d_ttot, st));
+    tr->usum_valid = true;
+    return SCL_OK;
+}
+
+extern "C" scl_status scl_sample_domains(const scl_result* rc, uint32_t trace, scl_sample_domain* out, size_t cap, size_t* n) {
+    if (!rc || !n) return fail(SCL_EINVAL, "NULL argument");
+    scl_result* r = const_cast<scl_result*>(rc);
+    const scl_traces* tr = r->tr;
+    if (trace >= tr->n_traces) return fail(SCL_EINVAL, "trace out of range");
+    CU(cudaSetDevice(tr->device));
+    scl_status s = ensure_summ(r);
+    if (s != SCL_OK) return s;
+    if (!r->dom_valid) {
+        s = ensure_unit_sums(tr, r->stream);
+        if (s != SCL_OK) return s;
+        if (r->cap_dom < r->cap || !r->d_dom) {
+            cudaFree(r->d_P); cudaFree(r->d_dom); r->d_P = nullptr; r->d_dom = nullptr; r->cap_dom = 0;
+            if (cudaMalloc(&r->d_P, r->cap * 16) != cudaSuccess || cudaMalloc(&r->d_dom, r->cap * sizeof(scl_sample_domain)) != cudaSuccess)
+                { cudaGetLastError(); return fail(SCL_ENOMEM, "sample domains"); }
+            r->cap_dom = r->cap;
+        }
+        DomainParams p{};
+        p.ev = tr->d_ev; p.tk = tr->d_tk; p.n_segs = tr->n_segs; p.n_traces = tr->n_traces; p.ustart = tr->d_ustart;
+        p.samples = r->d_samples; p.sbase = r->d_sbase; p.summ = r->d_summ; p.P = r->d_P; p.dom = r->d_dom;
+        CU(launch_domains(p, r->stream));
+        r->dom_valid = true;
+    }
+    const size_t cnt = r->h_summ[trace].n_samples;
+    *n = cnt;
+    if (cap == 0 || cnt == 0) return SCL_OK;
+    if (!out) return fail(SCL_EINVAL, "out is NULL");
+    CU(cudaMemcpyAsync(out, r->d_dom + r->h_sbase[trace], std::min(cap, cnt) * sizeof(scl_sample_domain),
+                       cudaMemcpyDeviceToHost, r->stream));
+    CU(cudaStreamSynchronize(r->stream));
+    return SCL_OK;
+}
+
 // ---------------------------------------------------------------- rate-based sampler (rate.cu)
 struct scl_rate_result {
     const scl_traces* tr = nullptr;
@@ -692,21 +752,9 @@ extern "C" scl_status scl_rate_run(uint64_t R, uint64_t seed, unsigned kinds, co
     cudaStream_t st = (cudaStream_t)cuda_stream;
     const uint32_t NT = tr->n_traces;
     const size_t nt1 = std::max<uint32_t>(NT, 1), ns1 = std::max<uint32_t>(tr->n_segs, 1);
-    if (!tr->usum_valid) {                             // per-unit byte sums, once per loaded traces
-        if (ns1 > tr->cap_usum) {
-            cudaFree(tr->d_usum); cudaFree(tr->d_ustart); tr->d_usum = tr->d_ustart = nullptr; tr->cap_usum = 0;
-            CU(cudaMalloc(&tr->d_usum, ns1 * 3 * 8)); CU(cudaMalloc(&tr->d_ustart, ns1 * 3 * 8));
-            tr->cap_usum = ns1;
-        }
-        if (nt1 > tr->cap_ttot) {
-            cudaFree(tr->d_ttot); tr->d_ttot = nullptr; tr->cap_ttot = 0;
-            CU(cudaMalloc(&tr->d_ttot, nt1 * 3 * 8));
-            tr->cap_ttot = nt1;
-        }
-        CU(cudaMemsetAsync(tr->d_ttot, 0, nt1 * 3 * 8, st));
-        CU(launch_unit_sums(tr->d_ev, tr->d_tk, tr->n_segs, tr->d_usum, tr->d_tr_base, tr->d_tr_nseg, NT,
-                            tr->d_ustart, tr->d_ttot, st));
-        tr->usum_valid = true;
+    {
+        scl_status s0 = ensure_unit_sums(tr, st);
+        if (s0 != SCL_OK) return s0;
     }
     scl_rate_result* r = *out;
     const bool fresh = r == nullptr;

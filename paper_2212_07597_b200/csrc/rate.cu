@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(1024) unit_sums_kernel(const scl_event* ev, co
 {
     const TicketInfo ti = tk[blockIdx.x];
     const long long row = (ti.off_t >> 3) + (long long)(ti.kraw & 0x7fffffffu) * kUnitRows + threadIdx.x;
-    unsigned long long s[3] = {0, 0, 0};                    // alloc, free, copy (registers: no dynamic index)
+    unsigned long long s[kUCols] = {0, 0, 0, 0};            // alloc, free, copy, managed alloc
     #pragma unroll
     for (int j = 0; j < kEpt; ++j) {
         const long long g = row * kEpt + j, ie = g - ti.off_t;
@@ -75,19 +75,20 @@ __global__ void __launch_bounds__(1024) unit_sums_kernel(const scl_event* ev, co
             const unsigned long long m = __ldcs(&ev[g].meta), z = ev_size(m);
             const unsigned kind = ev_kind(m);
             s[0] += kind == 0 ? z : 0ull; s[1] += kind == 1 ? z : 0ull; s[2] += kind == 2 ? z : 0ull;
+            s[3] += kind == 0 && ((m >> 42) & 1ull) ? z : 0ull;
         }
     }
-    __shared__ unsigned long long red[3][32];
+    __shared__ unsigned long long red[kUCols][32];
     #pragma unroll
-    for (int q = 0; q < 3; ++q) {
+    for (int q = 0; q < kUCols; ++q) {
         unsigned long long v = warp_sum((long long)s[q]);
         if ((threadIdx.x & 31) == 0) red[q][threadIdx.x >> 5] = v;
     }
     __syncthreads();
-    if (threadIdx.x < 3 * 32) {
+    if (threadIdx.x < kUCols * 32) {
         const int q = threadIdx.x >> 5, l = threadIdx.x & 31;
         const unsigned long long v = (unsigned long long)warp_sum((long long)red[q][l]);
-        if (l == 0) usum[(size_t)ti.slot * 3 + q] = v;
+        if (l == 0) usum[(size_t)ti.slot * kUCols + q] = v;
     }
 }
 
@@ -100,23 +101,24 @@ __global__ void __launch_bounds__(256) unit_scan_kernel(const unsigned long long
     const unsigned t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (t >= n_traces) return;
     const unsigned base = tr_base[t], ns = tr_nseg[t];
-    unsigned long long carry[3] = {0, 0, 0};
+    unsigned long long carry[kUCols] = {0, 0, 0, 0};
     for (unsigned k0 = 0; k0 < ns; k0 += 32) {
         const unsigned k = k0 + lane;
         #pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            const long long v = k < ns ? (long long)usum[(size_t)(base + k) * 3 + q] : 0;
+        for (int q = 0; q < kUCols; ++q) {
+            const long long v = k < ns ? (long long)usum[(size_t)(base + k) * kUCols + q] : 0;
             long long inc = v;
             #pragma unroll
             for (int d = 1; d < 32; d <<= 1) { const long long o = shfl_up_ll(inc, d); if (lane >= d) inc += o; }
-            if (k < ns) ustart[(size_t)(base + k) * 3 + q] = carry[q] + (unsigned long long)(inc - v);
+            if (k < ns) ustart[(size_t)(base + k) * kUCols + q] = carry[q] + (unsigned long long)(inc - v);
             carry[q] += (unsigned long long)shfl_ll(inc, 31);
         }
     }
-    if (lane < 3) ttot[(size_t)t * 3 + lane] = lane == 0 ? carry[0] : (lane == 1 ? carry[1] : carry[2]);
+    #pragma unroll
+    for (int q = 0; q < kUCols; ++q) if (lane == q) ttot[(size_t)t * kUCols + q] = carry[q];
 }
 
-__device__ __forceinline__ unsigned long long mask_sum(const unsigned long long* v3, unsigned kinds) {
+__device__ __forceinline__ unsigned long long mask_sum(const unsigned long long* v3, unsigned kinds) {   // columns 0-2
     return ((kinds & 1u) ? v3[0] : 0ull) + ((kinds & 2u) ? v3[1] : 0ull) + ((kinds & 4u) ? v3[2] : 0ull);
 }
 
@@ -128,7 +130,7 @@ __global__ void __launch_bounds__(256) rate_draws_kernel(const RateParams p, boo
     const int lane = threadIdx.x & 31;
     const unsigned t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (t >= p.n_traces) return;
-    const unsigned long long A = mask_sum(p.ttot + (size_t)t * 3, p.kinds);
+    const unsigned long long A = mask_sum(p.ttot + (size_t)t * kUCols, p.kinds);
     const double lq = (p.seed != 0 && p.R > 1) ? rate_log(__dsub_rn(1.0, __ddiv_rn(1.0, (double)p.R))) : -1.0;
     unsigned long long S0 = 0, k0 = 0, n = 0;
     const unsigned long long cap = fill ? p.count[t] : ~0ull;
@@ -174,7 +176,7 @@ __global__ void __launch_bounds__(1024) rate_place_kernel(const RateParams p)
     __syncthreads();
     unsigned long long wb = 0;
     for (unsigned q = 0; q < wrp; ++q) wb += wsum[q];
-    const unsigned long long a = mask_sum(p.ustart + (size_t)ti.slot * 3, p.kinds) + wb + (unsigned long long)inc - rs;
+    const unsigned long long a = mask_sum(p.ustart + (size_t)ti.slot * kUCols, p.kinds) + wb + (unsigned long long)inc - rs;
     const unsigned long long b = a + rs;
     if (rs == 0) return;
     // samples of this row: lower_bound(S, a) .. lower_bound(S, b) within the trace's samples
@@ -201,6 +203,89 @@ __global__ void __launch_bounds__(1024) rate_place_kernel(const RateParams p)
             ++k;
         }
     }
+}
+
+// ---------------------------------------------------------------- per-sample Python / native split (NEXT-2)
+// Allocated and managed-domain allocated bytes since the previous sample: inclusive
+// prefixes of both at every sample event (block per unit: its samples found by binary search in
+// the trace's sorted sample list, the unit's row sums scanned), then differences per trace.
+__global__ void __launch_bounds__(1024) domain_prefix_kernel(const DomainParams p)
+{
+    const TicketInfo ti = p.tk[blockIdx.x];
+    const unsigned t = ti.t;
+    const long long row_base = (ti.off_t >> 3) + (long long)(ti.kraw & 0x7fffffffu) * kUnitRows;
+    const long long lo = max(0ll, row_base * kEpt - ti.off_t), hi = min(ti.n_t, (row_base + kUnitRows) * kEpt - ti.off_t);
+    const scl_sample* smp = p.samples + p.sbase[t];
+    const unsigned long long K = p.summ[t].n_samples;
+    __shared__ unsigned long long k0s, k1s;
+    if (threadIdx.x < 2) {                                    // samples with lo <= idx < hi
+        const long long v = threadIdx.x == 0 ? lo : hi;
+        unsigned long long a = 0, b = K;
+        while (a < b) { const unsigned long long mid = (a + b) >> 1; if ((long long)smp[mid].idx < v) a = mid + 1; else b = mid; }
+        if (threadIdx.x == 0) k0s = a; else k1s = a;
+    }
+    __syncthreads();
+    const unsigned long long k0 = k0s, k1 = k1s;
+    if (k0 == k1) return;
+    // row sums of allocated / managed allocated bytes, block exclusive scan
+    const long long row = row_base + threadIdx.x;
+    unsigned long long ra = 0, rm = 0;
+    #pragma unroll
+    for (int j = 0; j < kEpt; ++j) {
+        const long long g = row * kEpt + j, ie = g - ti.off_t;
+        if (ie >= 0 && ie < ti.n_t) {
+            const unsigned long long m = __ldcg(&p.ev[g].meta);
+            if (ev_kind(m) == 0) { ra += ev_size(m); rm += ((m >> 42) & 1ull) ? ev_size(m) : 0ull; }
+        }
+    }
+    __shared__ unsigned long long wa[32], wm[32], pa[1024], pm[1024];
+    const int lane = threadIdx.x & 31, wrp = threadIdx.x >> 5;
+    long long ia = (long long)ra, im = (long long)rm;
+    #pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const long long oa = shfl_up_ll(ia, d), om = shfl_up_ll(im, d);
+        if (lane >= d) { ia += oa; im += om; }
+    }
+    if (lane == 31) { wa[wrp] = (unsigned long long)ia; wm[wrp] = (unsigned long long)im; }
+    __syncthreads();
+    unsigned long long ba = p.ustart[(size_t)ti.slot * kUCols + 0], bm = p.ustart[(size_t)ti.slot * kUCols + 3];
+    for (int q = 0; q < wrp; ++q) { ba += wa[q]; bm += wm[q]; }
+    pa[threadIdx.x] = ba + (unsigned long long)ia - ra;         // before the row
+    pm[threadIdx.x] = bm + (unsigned long long)im - rm;
+    __syncthreads();
+    for (unsigned long long k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+        const long long g = ti.off_t + (long long)smp[k].idx;      // the sample's event
+        const int r = (int)((g >> 3) - row_base);
+        unsigned long long A = pa[r], M = pm[r];
+        for (long long x = (g >> 3) << 3; x <= g; ++x) {
+            if (x - ti.off_t < 0) continue;
+            const unsigned long long m = __ldcg(&p.ev[x].meta);
+            if (ev_kind(m) == 0) { A += ev_size(m); M += ((m >> 42) & 1ull) ? ev_size(m) : 0ull; }
+        }
+        p.P[(p.sbase[t] + k) * 2 + 0] = A;
+        p.P[(p.sbase[t] + k) * 2 + 1] = M;
+    }
+}
+
+__global__ void __launch_bounds__(256) domain_diff_kernel(const DomainParams p)
+{
+    const int lane = threadIdx.x & 31;
+    const unsigned t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (t >= p.n_traces) return;
+    const unsigned long long K = p.summ[t].n_samples, b = p.sbase[t];
+    for (unsigned long long k = lane; k < K; k += 32) {
+        const unsigned long long a1 = p.P[(b + k) * 2], m1 = p.P[(b + k) * 2 + 1];
+        const unsigned long long a0 = k ? p.P[(b + k - 1) * 2] : 0ull, m0 = k ? p.P[(b + k - 1) * 2 + 1] : 0ull;
+        p.dom[b + k].alloc_bytes = a1 - a0;
+        p.dom[b + k].managed_bytes = m1 - m0;
+    }
+}
+
+cudaError_t launch_domains(const DomainParams& p, cudaStream_t st)
+{
+    if (p.n_segs) domain_prefix_kernel<<<p.n_segs, 1024, 0, st>>>(p);
+    if (p.n_traces) domain_diff_kernel<<<(p.n_traces + 7) / 8, 256, 0, st>>>(p);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_unit_sums(const scl_event* ev, const TicketInfo* tk, unsigned n_segs, unsigned long long* usum,

@@ -164,6 +164,22 @@ __device__ __forceinline__ void samples_trace(const ReplayParams& p, unsigned t,
 }
 #endif
 
+constexpr int kUCols = 4;               // per-unit byte sums: alloc, free, copy, managed alloc (rate.cu)
+
+// Per-sample Python / native split (rate.cu; NEXT-2).
+struct DomainParams {
+    const scl_event* ev;
+    const TicketInfo* tk;
+    unsigned n_segs, n_traces;
+    const unsigned long long* ustart;  // [n_segs][kUCols]
+    const scl_sample* samples;
+    const unsigned long long* sbase;
+    const scl_trace_summary* summ;
+    unsigned long long* P;             // [slots][2] inclusive (alloc, managed) prefix at each sample event
+    scl_sample_domain* dom;            // [slots]
+};
+cudaError_t launch_domains(const DomainParams& p, cudaStream_t st);
+
 // Rate-based byte sampler (rate.cu; NEXT-1 / NEXT-3).
 struct RateParams {
     const scl_event* ev;
@@ -171,8 +187,8 @@ struct RateParams {
     unsigned n_segs, n_traces;
     unsigned long long R, seed;
     unsigned kinds;                    // counted event kinds: bit 0 alloc, 1 free, 2 copy
-    const unsigned long long* ttot;    // [n_traces][3] alloc / free / copy bytes per trace
-    const unsigned long long* ustart;  // [n_segs][3] the same before each unit (exclusive, within its trace)
+    const unsigned long long* ttot;    // [n_traces][kUCols] alloc / free / copy / managed bytes per trace
+    const unsigned long long* ustart;  // [n_segs][kUCols] the same before each unit (exclusive, within its trace)
     unsigned long long* count;         // [n_traces] samples per trace
     const unsigned long long* sbase;   // [n_traces] first sample slot
     unsigned long long* S;             // [total] draw prefix sums S_k of the samples

@@ -293,3 +293,29 @@ def test_edge_many_traces_max_sites_extreme_T():
     for T in (1, 1 << 45):
         r = scl.scl_replay_run(T, tr, out=r)
         compare(ev, off, 1 << 21, T, r)
+
+
+def test_sample_domains():
+    """NEXT-2: per sample, allocated and managed-domain allocated bytes since the previous
+    sample, against the oracle, on ragged random traces with random domain bits and on config-2
+    traces (small objects managed), at several T."""
+    rng = np.random.default_rng(31)
+    traces = []
+    for i in range(150):
+        n = int(rng.choice([0, 1, 9, 255, 8191, 8193, 20000, int(rng.integers(1, 9000))]))
+        tr_ = tracegen.random_small_trace(rng, n, n_sites=13, max_size=int(rng.integers(1, 400)), max_ptrs=30)
+        traces.append([e + (int(rng.integers(0, 2)),) if e[0] == "a" else e for e in tr_])
+    cases = [(_concat(traces), 13, (5, 97, 4001))]
+    cfg = tracegen.CONFIGS[2].with_traces(4)
+    cases.append((tracegen.generate(cfg), cfg.n_sites, (1048583, cfg.T)))
+    for (ev, off), n_sites, Ts in cases:
+        tr = scl.scl_trace_load(ev, off, n_sites)
+        r = None
+        for T in Ts:
+            r = scl.scl_replay_run(T, tr, out=r)
+            ref = oracle.replay(ev, off, n_sites, T)
+            for t in range(len(off) - 1):
+                got = scl.scl_sample_domains(r, t)
+                exp = ref.domains[int(ref.sample_off[t]):int(ref.sample_off[t + 1])]
+                assert np.array_equal(got["alloc_bytes"], exp["alloc_bytes"]), (T, t)
+                assert np.array_equal(got["managed_bytes"], exp["managed_bytes"]), (T, t)
