@@ -201,6 +201,12 @@ typedef struct { uint64_t alloc_bytes; uint64_t managed_bytes; } scl_sample_doma
  * for it). */
 scl_status scl_sample_domains(const scl_result* r, uint32_t trace, scl_sample_domain* out, size_t cap, size_t* n);
 
+/* ---- Footprint trend: the samples' (idx, footprint) are
+ * the trend series.  Per trace, its exact maximum reconstruction error: max over events i of
+ * |F_i - footprint of the latest sample at or before i| (0 before the first sample); below T by
+ * the reset semantics.  n_traces values; computed on the first call after a run. */
+scl_status scl_trace_recon_error(const scl_result* r, uint64_t* err, size_t cap, size_t* n);
+
 /* ---- Rate-based byte sampler: the paper's comparison baseline (Table
  * tab:sampling-comparison) and copy-volume sampling (NEXT-3).
  * Per trace a counter drawn from a geometric distribution with mean R is decremented by the

@@ -21,7 +21,7 @@ __all__ = ["SclError", "Traces", "Result", "scl_trace_load", "scl_trace_reload",
            "scl_site_report", "scl_samples", "scl_trace_summaries", "scl_gate", "scl_result_device_table",
            "scl_result_timing", "scl_result_kernel_times", "scl_next_prime", "scl_traces_info", "EVENT_DTYPE", "SAMPLE_DTYPE",
            "SUMMARY_DTYPE", "SITE_ROW_DTYPE", "COLS", "device_table_tensor", "write_trace_file",
-           "DOMAIN_DTYPE", "scl_sample_domains", "RATE_SAMPLE_DTYPE", "RATE_ALLOC_FREE", "RATE_COPY", "RateResult", "scl_rate_run", "scl_rate_counts",
+           "DOMAIN_DTYPE", "scl_sample_domains", "scl_trace_recon_error", "RATE_SAMPLE_DTYPE", "RATE_ALLOC_FREE", "RATE_COPY", "RateResult", "scl_rate_run", "scl_rate_counts",
            "scl_rate_samples", "scl_rate_site_counts", "scl_rate_timing"]
 
 EVENT_DTYPE = np.dtype([("ptr", "<u8"), ("meta", "<u8")])
@@ -65,6 +65,7 @@ def _load():
         "scl_result_kernel_times": [P, P, SZ, P],
         "scl_rate_run": [U64, U64, U32, P, P, P],
         "scl_sample_domains": [P, U32, P, SZ, P],
+        "scl_trace_recon_error": [P, P, SZ, P],
         "scl_rate_counts": [P, P, SZ, P],
         "scl_rate_samples": [P, U32, P, SZ, P],
         "scl_rate_site_counts": [P, P, SZ, P],
@@ -264,6 +265,16 @@ def scl_sample_domains(r: Result, trace: int) -> np.ndarray:
     out = np.zeros(n.value, dtype=DOMAIN_DTYPE)
     if n.value:
         _check(lib.scl_sample_domains(r.handle, trace, out.ctypes.data, n.value, ctypes.byref(n)))
+    return out
+
+
+def scl_trace_recon_error(r: Result) -> np.ndarray:
+    """Per trace: max |F_i - latest sample footprint| over events (NEXT-4 trend; < T)."""
+    n = ctypes.c_size_t()
+    _check(lib.scl_trace_recon_error(r.handle, None, 0, ctypes.byref(n)))
+    out = np.zeros(n.value, dtype=np.uint64)
+    if n.value:
+        _check(lib.scl_trace_recon_error(r.handle, out.ctypes.data, n.value, ctypes.byref(n)))
     return out
 
 

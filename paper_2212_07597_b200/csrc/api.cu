@@ -82,6 +82,9 @@ struct scl_result {
     scl_sample_domain* d_dom = nullptr;
     size_t cap_dom = 0;
     bool dom_valid = false;
+    unsigned long long* d_recon = nullptr;     // per-trace max reconstruction error (NEXT-4, lazy)
+    size_t cap_recon = 0;
+    bool recon_valid = false;
     // host
     std::vector<unsigned long long> h_sbase;
     std::vector<scl_trace_summary> h_summ;
@@ -377,7 +380,7 @@ extern "C" void scl_result_free(scl_result* r) {
     if (!r) return;
     free_result_buffers(r);
     cudaFree(r->d_samples); cudaFree(r->d_epflag); cudaFree(r->d_prof); cudaFree(r->d_rtask);
-    cudaFree(r->d_P); cudaFree(r->d_dom);
+    cudaFree(r->d_P); cudaFree(r->d_dom); cudaFree(r->d_recon);
     if (r->h_gate) cudaFreeHost(r->h_gate);
     for (auto& e : r->ev) if (e) cudaEventDestroy(e);
     for (auto& e : r->kev) if (e) cudaEventDestroy(e);
@@ -446,7 +449,7 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
     r->tr = tr; r->T = threshold; r->formula = o.formula; r->stream = st;
     const uint64_t tick = o.tick_ns ? o.tick_ns : tr->tick_ns;
     r->elapsed_ns = o.elapsed_ns ? o.elapsed_ns : tr->max_len * tick;
-    r->summ_valid = false; r->finalized = false; r->dom_valid = false;
+    r->summ_valid = false; r->finalized = false; r->dom_valid = false; r->recon_valid = false;
 
     // sample capacity per trace: min(n_t, floor(sum|d| / T)) -- every sample consumes |net| >= T
     // (prep_kernel computes the same bases on the device; the host copy serves scl_samples)
@@ -703,7 +706,7 @@ extern "C" scl_status scl_sample_domains(const scl_result* rc, uint32_t trace, s
         s = ensure_unit_sums(tr, r->stream);
         if (s != SCL_OK) return s;
         if (r->cap_dom < r->cap || !r->d_dom) {
-            cudaFree(r->d_P); cudaFree(r->d_dom); r->d_P = nullptr; r->d_dom = nullptr; r->cap_dom = 0;
+            cudaFree(r->d_P); cudaFree(r->d_dom); cudaFree(r->d_recon); r->d_P = nullptr; r->d_dom = nullptr; r->cap_dom = 0;
             if (cudaMalloc(&r->d_P, r->cap * 16) != cudaSuccess || cudaMalloc(&r->d_dom, r->cap * sizeof(scl_sample_domain)) != cudaSuccess)
                 { cudaGetLastError(); return fail(SCL_ENOMEM, "sample domains"); }
             r->cap_dom = r->cap;
@@ -720,6 +723,35 @@ extern "C" scl_status scl_sample_domains(const scl_result* rc, uint32_t trace, s
     if (!out) return fail(SCL_EINVAL, "out is NULL");
     CU(cudaMemcpyAsync(out, r->d_dom + r->h_sbase[trace], std::min(cap, cnt) * sizeof(scl_sample_domain),
                        cudaMemcpyDeviceToHost, r->stream));
+    CU(cudaStreamSynchronize(r->stream));
+    return SCL_OK;
+}
+
+extern "C" scl_status scl_trace_recon_error(const scl_result* rc, uint64_t* err, size_t cap, size_t* n) {
+    if (!rc || !n) return fail(SCL_EINVAL, "NULL argument");
+    scl_result* r = const_cast<scl_result*>(rc);
+    const scl_traces* tr = r->tr;
+    *n = tr->n_traces;
+    if (cap == 0) return SCL_OK;
+    if (!err) return fail(SCL_EINVAL, "err is NULL");
+    CU(cudaSetDevice(tr->device));
+    if (!r->recon_valid) {
+        scl_status s = ensure_unit_sums(tr, r->stream);
+        if (s != SCL_OK) return s;
+        const size_t nt1 = std::max<uint32_t>(tr->n_traces, 1);
+        if (r->cap_recon < nt1) {
+            cudaFree(r->d_recon); r->d_recon = nullptr; r->cap_recon = 0;
+            if (cudaMalloc(&r->d_recon, nt1 * 8) != cudaSuccess) { cudaGetLastError(); return fail(SCL_ENOMEM, "recon"); }
+            r->cap_recon = nt1;
+        }
+        CU(cudaMemsetAsync(r->d_recon, 0, nt1 * 8, r->stream));
+        DomainParams p{};
+        p.ev = tr->d_ev; p.tk = tr->d_tk; p.n_segs = tr->n_segs; p.n_traces = tr->n_traces; p.ustart = tr->d_ustart;
+        p.samples = r->d_samples; p.sbase = r->d_sbase; p.summ = r->d_summ;
+        CU(launch_recon(p, r->d_recon, r->stream));
+        r->recon_valid = true;
+    }
+    CU(cudaMemcpyAsync(err, r->d_recon, std::min(cap, (size_t)*n) * 8, cudaMemcpyDeviceToHost, r->stream));
     CU(cudaStreamSynchronize(r->stream));
     return SCL_OK;
 }

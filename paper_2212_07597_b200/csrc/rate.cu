@@ -281,6 +281,68 @@ __global__ void __launch_bounds__(256) domain_diff_kernel(const DomainParams p)
     }
 }
 
+// ---------------------------------------------------------------- reconstruction error (NEXT-4 trend)
+// The samples' footprints are the footprint trend.  Per trace: max over events of
+// |F_i - footprint of the latest sample at or before i| (0 before the first sample) -- below T by
+// the reset semantics.  Block per unit (thread = row): F from the unit's alloc / free
+// prefix plus a block scan, the latest sample before each row by binary search.
+__global__ void __launch_bounds__(1024) recon_kernel(const DomainParams p, unsigned long long* err)
+{
+    const TicketInfo ti = p.tk[blockIdx.x];
+    const unsigned t = ti.t;
+    const long long row = (ti.off_t >> 3) + (long long)(ti.kraw & 0x7fffffffu) * kUnitRows + threadIdx.x;
+    long long d[kEpt], rs = 0;
+    unsigned live = 0;
+    #pragma unroll
+    for (int j = 0; j < kEpt; ++j) {
+        const long long g = row * kEpt + j, ie = g - ti.off_t;
+        d[j] = 0;
+        if (ie >= 0 && ie < ti.n_t) {
+            const unsigned long long m = __ldcs(&p.ev[g].meta);
+            const unsigned kind = ev_kind(m);
+            d[j] = kind == 0 ? (long long)ev_size(m) : (kind == 1 ? -(long long)ev_size(m) : 0);
+            live |= 1u << j;
+        }
+        rs += d[j];
+    }
+    __shared__ long long ws[32];
+    const int lane = threadIdx.x & 31, wrp = threadIdx.x >> 5;
+    long long inc = rs;
+    #pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) { const long long o = shfl_up_ll(inc, dd); if (lane >= dd) inc += o; }
+    if (lane == 31) ws[wrp] = inc;
+    __syncthreads();
+    long long F = (long long)(p.ustart[(size_t)ti.slot * kUCols + 0] - p.ustart[(size_t)ti.slot * kUCols + 1]);
+    for (int q = 0; q < wrp; ++q) F += ws[q];
+    F += inc - rs;                                           // footprint before the row
+    unsigned long long e = 0;
+    if (live) {
+        const scl_sample* smp = p.samples + p.sbase[t];
+        const unsigned long long K = p.summ[t].n_samples;
+        const long long r_lo = row * kEpt - ti.off_t;        // trace index of the row's first slot
+        unsigned long long a = 0, b = K;                     // first sample with idx >= r_lo
+        while (a < b) { const unsigned long long mid = (a + b) >> 1; if ((long long)smp[mid].idx < r_lo) a = mid + 1; else b = mid; }
+        long long B = a ? smp[a - 1].footprint : 0;
+        unsigned long long kn = a;
+        #pragma unroll
+        for (int j = 0; j < kEpt; ++j) {
+            if (!((live >> j) & 1u)) continue;
+            F += d[j];
+            if (kn < K && (long long)smp[kn].idx == r_lo + j) { B = F; ++kn; }
+            else { const long long x = F > B ? F - B : B - F; e = e > (unsigned long long)x ? e : (unsigned long long)x; }
+        }
+    }
+    #pragma unroll
+    for (int dd = 16; dd > 0; dd >>= 1) { const unsigned long long o = __shfl_xor_sync(kFull, e, dd); e = e > o ? e : o; }
+    if (lane == 0 && e) atomicMax(&err[t], e);
+}
+
+cudaError_t launch_recon(const DomainParams& p, unsigned long long* err, cudaStream_t st)
+{
+    if (p.n_segs) recon_kernel<<<p.n_segs, 1024, 0, st>>>(p, err);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_domains(const DomainParams& p, cudaStream_t st)
 {
     if (p.n_segs) domain_prefix_kernel<<<p.n_segs, 1024, 0, st>>>(p);

@@ -179,6 +179,7 @@ struct DomainParams {
     scl_sample_domain* dom;            // [slots]
 };
 cudaError_t launch_domains(const DomainParams& p, cudaStream_t st);
+cudaError_t launch_recon(const DomainParams& p, unsigned long long* err, cudaStream_t st);
 
 // Rate-based byte sampler (rate.cu; NEXT-1 / NEXT-3).
 struct RateParams {

@@ -319,3 +319,46 @@ def test_sample_domains():
                 exp = ref.domains[int(ref.sample_off[t]):int(ref.sample_off[t + 1])]
                 assert np.array_equal(got["alloc_bytes"], exp["alloc_bytes"]), (T, t)
                 assert np.array_equal(got["managed_bytes"], exp["managed_bytes"]), (T, t)
+
+
+def _recon_reference(ev, off, ref):
+    """Brute force from the definition on the oracle's samples: F_i by cumulative sum,
+    the step function of the latest sample footprint, max |difference| per trace."""
+    kind = ((ev["meta"] >> np.uint64(40)) & np.uint64(3)).astype(np.int64)
+    size = (ev["meta"] & np.uint64((1 << 40) - 1)).astype(np.int64)
+    d = np.where(kind == 0, size, np.where(kind == 1, -size, 0))
+    out = []
+    for t in range(len(off) - 1):
+        b, e = int(off[t]), int(off[t + 1])
+        if e == b:
+            out.append(0); continue
+        F = np.cumsum(d[b:e])
+        s = ref.trace_samples(t)
+        step = np.zeros(e - b, dtype=np.int64)
+        if len(s):
+            pos = np.searchsorted(s["idx"].astype(np.int64), np.arange(e - b), side="right") - 1
+            step = np.where(pos >= 0, s["footprint"][np.maximum(pos, 0)], 0)
+        live = kind[b:e] < 3
+        out.append(int(np.abs(F - step)[live].max()))
+    return np.array(out, dtype=np.uint64)
+
+
+def test_trace_recon_error():
+    """NEXT-4 trend: per-trace max reconstruction error equals the brute-force value on ragged
+    random traces, and is below T on every trace of the full bench workload (config 2)."""
+    rng = np.random.default_rng(41)
+    traces = [tracegen.random_small_trace(rng, int(rng.choice([0, 1, 9, 8193, int(rng.integers(1, 20000))])), n_sites=7,
+                                          max_size=int(rng.integers(1, 500)), max_ptrs=30) for _ in range(100)]
+    ev, off = _concat(traces)
+    tr = scl.scl_trace_load(ev, off, 7)
+    r = None
+    for T in (3, 211, 10**6):
+        r = scl.scl_replay_run(T, tr, out=r)
+        ref = oracle.replay(ev, off, 7, T)
+        assert np.array_equal(scl.scl_trace_recon_error(r), _recon_reference(ev, off, ref)), T
+    cfg = tracegen.CONFIGS[2]
+    ev, off = tracegen.generate(cfg)
+    tr = scl.scl_trace_load(ev, off, cfg.n_sites)
+    r = scl.scl_replay_run(cfg.T, tr)
+    err = scl.scl_trace_recon_error(r)
+    assert len(err) == cfg.n_traces and (err < cfg.T).all() and (err > cfg.T // 2).all()
