@@ -68,9 +68,10 @@ size_t replay_smem_bytes() { return 1024 + (size_t)kStages * kSegBytes + sizeof(
 
 // Blocked Bloom filter of freed pointers, 64 words (2048 bits) per 256-event chunk: one
 // word per pointer, two bits in it (one shared-memory OR per free; ~1.4 % false positives
-// at ~128 frees per chunk).  One multiply: word = bits 26..31, bits = 21..25 and 16..20.
+// at ~128 frees per chunk).  One multiply of the pointer's low word (16-B aligned pointers:
+// its low 4 bits are zero): word = bits 26..31, bits = 21..25 and 16..20.
 __device__ __forceinline__ unsigned bloom_hash(unsigned long long ptr) {
-    return (unsigned)(ptr >> 4) * 0x9E3779B1u;
+    return (unsigned)ptr * 0x9E3779B1u;
 }
 __device__ __forceinline__ unsigned bloom_word(unsigned long long ptr) { return bloom_hash(ptr) >> 26; }
 __device__ __forceinline__ unsigned bloom_mask(unsigned long long ptr) {
@@ -104,40 +105,41 @@ __device__ __forceinline__ void load_row_global(const scl_event* ev, long long r
 }
 
 // ============================================================================ compute warps
-// Fast path of one row (8 events) in a lane.  Every shared atomic is unconditional (no branch
-// around it): an event that does not count goes to the lane's sink slot (and adds 0 bytes, so
-// the sink never wraps); 32-bit byte-counter carries are gathered as a bitmask.  kAllHot: every
-// site is in the shared-memory table (n_sites <= kHot), no cold-site bookkeeping.
+// Fast path of one row (8 events) in a lane: sizes < 2^27 (size bits 32-39 zero).  Every shared
+// atomic is unconditional (no branch around it): an event that does not count goes to the lane's
+// sink slot (and adds 0 bytes, so the sink never wraps).  Tier-E slot of (site, kind) = site*2 +
+// (kind & 1): its byte offset site*8 + (kind&1)*4 is one bit-select of meta>>40 and meta>>38.
+// 32-bit byte-counter carries: one accumulated predicate, the rare wrap re-examined afterwards.
+// kAllHot: every site is in the shared-memory table (n_sites <= kHot), no cold-site bookkeeping.
 template <bool kAllHot>
 __device__ __forceinline__ void fast_row(const unsigned long long* ptr, const unsigned long long* meta, uint32_t cnt_s,
                                          uint32_t bl_s, uint32_t dslot, Smem& s, int& r32, int& mx32, int& mn32,
                                          unsigned& cold)
 {
-    unsigned old[kEpt], add[kEpt], carry = 0;
+    unsigned old[kEpt], add[kEpt];
+    bool anyc = false;
     #pragma unroll
     for (int j = 0; j < kEpt; ++j) {
         const unsigned hi = (unsigned)(meta[j] >> 32), lo = (unsigned)meta[j];
         const unsigned kind = (hi >> 8) & 3u, site = hi >> 11;
-        const int d = kind == 1 ? -(int)lo : (int)lo;
-        r32 += kind < 2 ? d : 0;                                              // a1: signed size
+        const bool isfree = kind == 1, af = kind < 2;
+        r32 += af ? (isfree ? -(int)lo : (int)lo) : 0;                        // a1: signed size
         mx32 = max(mx32, r32); mn32 = min(mn32, r32);
-        const bool h = kind < 2 && (kAllHot || site < (unsigned)kHot);
-        if (!kAllHot) cold |= (kind < 2 && !h ? 1u : 0u) << j;
-        const uint32_t a = cnt_s + (h ? ((kind & 1u) * kHot + site) * 4u : dslot);   // (kind, site) slot
+        const bool h = af && (kAllHot || site < (unsigned)kHot);
+        if (!kAllHot) cold |= (af && !h ? 1u : 0u) << j;
+        const uint32_t off = ((hi >> 8) & 0xfffffff8u) | ((hi >> 6) & 0x7u);  // site*8 + (kind&1)*4
+        const uint32_t a = cnt_s + (h ? off : dslot);
         add[j] = h ? lo : 0u;
         red_add(a, 1u);                                                       // a5 Tier E
         old[j] = atom_add(a + kBloOff, add[j]);
-        red_or(kind == 1 ? bl_s + bloom_word(ptr[j]) * 4u : cnt_s + dslot, bloom_mask(ptr[j]));   // freed ptr -> Bloom
+        red_or(isfree ? bl_s + bloom_word(ptr[j]) * 4u : cnt_s + dslot, bloom_mask(ptr[j]));   // freed ptr -> Bloom
     }
     #pragma unroll
-    for (int j = 0; j < kEpt; ++j) carry |= (old[j] + add[j] < old[j] ? 1u : 0u) << j;
-    while (carry) {                                   // rare: a 32-bit byte counter wrapped
-        const int j = __ffs(carry) - 1;
-        carry &= carry - 1;
-        unsigned long long mj = 0;
+    for (int j = 0; j < kEpt; ++j) anyc |= old[j] + add[j] < old[j];
+    if (anyc) {                                       // rare: a 32-bit byte counter wrapped
         #pragma unroll
-        for (int q = 0; q < kEpt; ++q) if (q == j) mj = meta[q];
-        atomicAdd(&s.bhi[ev_kind(mj) * kHot + ev_site(mj)], 1u);
+        for (int j = 0; j < kEpt; ++j)
+            if (old[j] + add[j] < old[j]) atomicAdd(&s.bhi[ev_site(meta[j]) * 2 + (ev_kind(meta[j]) & 1u)], 1u);
     }
 }
 
@@ -213,7 +215,7 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
                         tmx = llmax(tmx, run); tmn = llmin(tmn, run);
                         const unsigned site = ev_site(meta[j]);
                         if (site < (unsigned)kHot && size < (1ull << 32)) {
-                            const int x = kind * kHot + site;
+                            const int x = (int)site * 2 + (int)(kind & 1u);
                             atomicAdd(&s.cnt[x], 1u);
                             const unsigned old = atomicAdd(&s.blo[x], (unsigned)size);
                             if (old + (unsigned)size < old) atomicAdd(&s.bhi[x], 1u);
@@ -856,7 +858,7 @@ replay_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         for (int x = tid; x < 2 * kHot; x += kComputeWarps * 32) {   // flush Tier-E counters
             const unsigned c = s.cnt[x];
             if (c) {
-                const int kind = x / kHot, site = x % kHot;
+                const int kind = x & 1, site = x >> 1;
                 unsigned long long* row = p.table + (size_t)site * SCL_NCOL;
                 atomicAdd(&row[SCL_COL_N_MALLOC + kind], (unsigned long long)c);
                 atomicAdd(&row[SCL_COL_MALLOC_BYTES + kind], ((unsigned long long)s.bhi[x] << 32) | s.blo[x]);
