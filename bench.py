@@ -145,7 +145,7 @@ def cpu_oracle_baseline(ev, off, cfg, reps=3):
         for _ in range(reps if threads > 1 else 1):
             t0 = time.perf_counter()
             lib.orc_replay_all(oracle._ptr(ev), oracle._ptr(off), nt, cfg.n_sites, cfg.T, 0, threads,
-                               oracle._ptr(samples), oracle._ptr(soff), oracle._ptr(summ), oracle._ptr(table))
+                               oracle._ptr(samples), oracle._ptr(soff), oracle._ptr(summ), oracle._ptr(table), None)
             num, den, op = oracle.gate(summ)
             prob, rate, flag = oracle.finalize(table, op, oracle.elapsed_ns(off))
             oracle.report_order(rate, flag)
@@ -179,7 +179,7 @@ def run_reference(args):
 
     def step():
         lib.orc_replay_all(oracle._ptr(ev), oracle._ptr(off), nt, cfg.n_sites, cfg.T, 0, cores,
-                           oracle._ptr(samples), oracle._ptr(soff), oracle._ptr(summ), oracle._ptr(table))
+                           oracle._ptr(samples), oracle._ptr(soff), oracle._ptr(summ), oracle._ptr(table), None)
         num, den, op = oracle.gate(summ)
         prob, rate, flag = oracle.finalize(table, op, oracle.elapsed_ns(off))
         oracle.report_order(rate, flag)

@@ -760,9 +760,9 @@ extern "C" scl_status scl_trace_recon_error(const scl_result* rc, uint64_t* err,
 struct scl_rate_result {
     const scl_traces* tr = nullptr;
     cudaStream_t st = nullptr;
-    unsigned long long *d_count = nullptr, *d_sbase = nullptr, *d_S = nullptr, *d_site = nullptr;
+    unsigned long long *d_count = nullptr, *d_sbase = nullptr, *d_S = nullptr, *d_site = nullptr, *d_kfirst = nullptr;
     scl_rate_sample* d_samples = nullptr;
-    size_t cap = 0, cap_sites = 0, cap_tr = 0;
+    size_t cap = 0, cap_sites = 0, cap_tr = 0, cap_segs = 0;
     std::vector<unsigned long long> h_count, h_sbase;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
@@ -770,6 +770,7 @@ struct scl_rate_result {
 extern "C" void scl_rate_free(scl_rate_result* r) {
     if (!r) return;
     cudaFree(r->d_count); cudaFree(r->d_sbase); cudaFree(r->d_S); cudaFree(r->d_site); cudaFree(r->d_samples);
+    cudaFree(r->d_kfirst);
     for (auto& e : r->ev) if (e) cudaEventDestroy(e);
     delete r;
 }
@@ -804,6 +805,11 @@ extern "C" scl_status scl_rate_run(uint64_t R, uint64_t seed, unsigned kinds, co
             { cudaGetLastError(); return fail_free(SCL_ENOMEM, "rate counts"); }
         r->cap_tr = nt1;
     }
+    if (ns1 > r->cap_segs) {
+        cudaFree(r->d_kfirst); r->d_kfirst = nullptr; r->cap_segs = 0;
+        if (cudaMalloc(&r->d_kfirst, ns1 * 8) != cudaSuccess) { cudaGetLastError(); return fail_free(SCL_ENOMEM, "rate ranges"); }
+        r->cap_segs = ns1;
+    }
     if (tr->n_sites > r->cap_sites) {
         cudaFree(r->d_site); r->d_site = nullptr; r->cap_sites = 0;
         if (cudaMalloc(&r->d_site, (size_t)tr->n_sites * 8) != cudaSuccess) { cudaGetLastError(); return fail_free(SCL_ENOMEM, "rate sites"); }
@@ -812,6 +818,7 @@ extern "C" scl_status scl_rate_run(uint64_t R, uint64_t seed, unsigned kinds, co
     RateParams p{};
     p.ev = tr->d_ev; p.tk = tr->d_tk; p.n_segs = tr->n_segs; p.n_traces = NT; p.R = R; p.seed = seed; p.kinds = kinds;
     p.ttot = tr->d_ttot; p.ustart = tr->d_ustart; p.count = r->d_count; p.sbase = r->d_sbase; p.site_count = r->d_site;
+    p.kfirst = r->d_kfirst;
     CU(cudaEventRecord(r->ev[0], st));
     CU(launch_rate(p, 0, st));                         // samples per trace
     CU(cudaEventRecord(r->ev[1], st));

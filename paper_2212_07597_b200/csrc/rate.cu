@@ -9,6 +9,7 @@
 //   unit_scan_kernel   per trace: their exclusive prefix over the trace's units
 //   rate_count_kernel  per trace (warp): draws 32 at a time until S_k >= A_total -> sample count
 //   rate_fill_kernel   per trace (warp): the draw prefix sums S_k
+//   rate_ranges_kernel per unit (thread): the index of its first sample
 //   rate_place_kernel  per unit (block, lane = row of 8 events): the samples whose S_k falls in the
 //                      unit, each placed in its row by the row's counted-byte prefix; per-site counts
 // Draw k of trace t: splitmix64 keyed by (seed, t, k), u in (0, 1], G = 1 + floor(ln u / ln(1-1/R))
@@ -18,6 +19,12 @@
 #include "ptx.cuh"
 
 namespace scl {
+
+// meta word of event g through L1 (a row's 8 events share 4 sectors: the second access of each
+// sector hits L1; the streaming hint would re-fetch it from L2)
+__device__ __forceinline__ unsigned long long meta_l1(const scl_event* ev, long long g) {
+    return __ldca(reinterpret_cast<const unsigned long long*>(ev + g) + 1);
+}
 
 // ln x, x > 0: x = m 2^e, m in [sqrt(1/2), sqrt(2)), ln m = 2 atanh((m-1)/(m+1)) by its series
 // (terms up to f^23, Horner from the highest), every operation rounded separately.
@@ -72,7 +79,7 @@ __global__ void __launch_bounds__(1024) unit_sums_kernel(const scl_event* ev, co
     for (int j = 0; j < kEpt; ++j) {
         const long long g = row * kEpt + j, ie = g - ti.off_t;
         if (ie >= 0 && ie < ti.n_t) {
-            const unsigned long long m = __ldcs(&ev[g].meta), z = ev_size(m);
+            const unsigned long long m = meta_l1(ev, g), z = ev_size(m);
             const unsigned kind = ev_kind(m);
             s[0] += kind == 0 ? z : 0ull; s[1] += kind == 1 ? z : 0ull; s[2] += kind == 2 ? z : 0ull;
             s[3] += kind == 0 && ((m >> 42) & 1ull) ? z : 0ull;
@@ -164,7 +171,7 @@ __global__ void __launch_bounds__(1024) rate_place_kernel(const RateParams p)
     for (int j = 0; j < kEpt; ++j) {
         const long long g = row * kEpt + j, ie = g - ti.off_t;
         meta[j] = 0; sz[j] = 0;
-        if (ie >= 0 && ie < ti.n_t) { meta[j] = __ldcs(&p.ev[g].meta); sz[j] = counted(meta[j], p.kinds); }
+        if (ie >= 0 && ie < ti.n_t) { meta[j] = meta_l1(p.ev, g); sz[j] = counted(meta[j], p.kinds); }
         rs += sz[j];
     }
     // block exclusive scan of the row sums
@@ -178,12 +185,13 @@ __global__ void __launch_bounds__(1024) rate_place_kernel(const RateParams p)
     for (unsigned q = 0; q < wrp; ++q) wb += wsum[q];
     const unsigned long long a = mask_sum(p.ustart + (size_t)ti.slot * kUCols, p.kinds) + wb + (unsigned long long)inc - rs;
     const unsigned long long b = a + rs;
-    if (rs == 0) return;
-    // samples of this row: lower_bound(S, a) .. lower_bound(S, b) within the trace's samples
+    // the unit's samples [kfirst[u], kfirst[u+1]) (rate_ranges_kernel), then each row within them
     const unsigned long long* S = p.S + p.sbase[t];
-    const unsigned long long K = p.count[t];
+    const bool last = (ti.kraw >> 31) != 0;
+    const unsigned long long ukr[2] = {p.kfirst[ti.slot], last ? p.count[t] : p.kfirst[ti.slot + 1]};
+    if (rs == 0 || ukr[0] == ukr[1]) return;
     auto lower = [&](unsigned long long v) {
-        unsigned long long lo = 0, hi = K;
+        unsigned long long lo = ukr[0], hi = ukr[1];
         while (lo < hi) { const unsigned long long mid = (lo + hi) >> 1; if (__ldcg(S + mid) < v) lo = mid + 1; else hi = mid; }
         return lo;
     };
@@ -234,7 +242,7 @@ __global__ void __launch_bounds__(1024) domain_prefix_kernel(const DomainParams 
     for (int j = 0; j < kEpt; ++j) {
         const long long g = row * kEpt + j, ie = g - ti.off_t;
         if (ie >= 0 && ie < ti.n_t) {
-            const unsigned long long m = __ldcg(&p.ev[g].meta);
+            const unsigned long long m = meta_l1(p.ev, g);
             if (ev_kind(m) == 0) { ra += ev_size(m); rm += ((m >> 42) & 1ull) ? ev_size(m) : 0ull; }
         }
     }
@@ -298,7 +306,7 @@ __global__ void __launch_bounds__(1024) recon_kernel(const DomainParams p, unsig
         const long long g = row * kEpt + j, ie = g - ti.off_t;
         d[j] = 0;
         if (ie >= 0 && ie < ti.n_t) {
-            const unsigned long long m = __ldcs(&p.ev[g].meta);
+            const unsigned long long m = meta_l1(p.ev, g);
             const unsigned kind = ev_kind(m);
             d[j] = kind == 0 ? (long long)ev_size(m) : (kind == 1 ? -(long long)ev_size(m) : 0);
             live |= 1u << j;
@@ -350,6 +358,20 @@ cudaError_t launch_domains(const DomainParams& p, cudaStream_t st)
     return cudaGetLastError();
 }
 
+// Per unit: the index of its first sample, lower_bound(S_t, counted bytes before the unit)
+// (thread per unit; the placement blocks read their unit's range with one load).
+__global__ void __launch_bounds__(256) rate_ranges_kernel(const RateParams p)
+{
+    const unsigned q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= p.n_segs) return;
+    const TicketInfo ti = p.tk[q];
+    const unsigned long long v = mask_sum(p.ustart + (size_t)ti.slot * kUCols, p.kinds);
+    const unsigned long long* S = p.S + p.sbase[ti.t];
+    unsigned long long lo = 0, hi = p.count[ti.t];
+    while (lo < hi) { const unsigned long long mid = (lo + hi) >> 1; if (__ldcg(S + mid) < v) lo = mid + 1; else hi = mid; }
+    p.kfirst[ti.slot] = lo;
+}
+
 cudaError_t launch_unit_sums(const scl_event* ev, const TicketInfo* tk, unsigned n_segs, unsigned long long* usum,
                              const unsigned* tr_base, const unsigned* tr_nseg, unsigned n_traces,
                              unsigned long long* ustart, unsigned long long* ttot, cudaStream_t st)
@@ -364,6 +386,7 @@ cudaError_t launch_rate(const RateParams& p, int phase, cudaStream_t st)
     if (phase == 0 || phase == 1) {
         if (p.n_traces) rate_draws_kernel<<<(p.n_traces + 7) / 8, 256, 0, st>>>(p, phase == 1);
     } else if (p.n_segs) {
+        rate_ranges_kernel<<<(p.n_segs + 255) / 256, 256, 0, st>>>(p);
         rate_place_kernel<<<p.n_segs, 1024, 0, st>>>(p);
     }
     return cudaGetLastError();

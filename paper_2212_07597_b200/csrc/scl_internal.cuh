@@ -193,6 +193,7 @@ struct RateParams {
     unsigned long long* count;         // [n_traces] samples per trace
     const unsigned long long* sbase;   // [n_traces] first sample slot
     unsigned long long* S;             // [total] draw prefix sums S_k of the samples
+    unsigned long long* kfirst;        // [n_segs] index (within its trace) of each unit's first sample
     scl_rate_sample* samples;          // [total]
     unsigned long long* site_count;    // [n_sites] samples per site
 };
