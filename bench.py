@@ -348,8 +348,8 @@ def main():
                          "frac_of_8tbs_spec": achieved / 8000.0},
             "clocks": clk.summary(),
             "e2e": e2e,
-            "gpu_launches": 4 * args.steps,
-            "gpu_launches_note": "per step: prep_kernel, replay_kernel, post_kernel, report_kernel "
+            "gpu_launches": 2 * args.steps,
+            "gpu_launches_note": "per step: replay_kernel (its CTA 0 prepares the run), post_kernel (a6 in its last block) "
                                  "(tables > 16384 sites: finalize + CUB radix sort + rows instead of report)",
             "kernel_timing": "replay_kernel durations from CUDA events in a second pass of K steps",
             "n_samples_per_step": n_samples,

@@ -452,7 +452,7 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
     r->summ_valid = false; r->finalized = false; r->dom_valid = false; r->recon_valid = false;
 
     // sample capacity per trace: min(n_t, floor(sum|d| / T)) -- every sample consumes |net| >= T
-    // (prep_kernel computes the same bases on the device; the host copy serves scl_samples)
+    // (CTA 0 of the replay kernel computes the same bases on the device; the host copy serves scl_samples)
     const uint32_t NT = tr->n_traces;
     unsigned long long tot = 0;
     r->h_sbase.resize((size_t)NT + 1);
@@ -477,13 +477,6 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
     const bool tm = o.timing != 0;                 // phase / kernel events only when asked for
     r->timed = tm;
     if (tm) CU(cudaEventRecord(r->ev[0], st));
-    PrepParams pp{};
-    pp.table = r->d_table; pp.table_words = (size_t)tr->n_sites * SCL_NCOL + 3;
-    pp.summ = reinterpret_cast<unsigned long long*>(r->d_summ); pp.summ_words = (size_t)NT * sizeof(scl_trace_summary) / 8;
-    pp.run = reinterpret_cast<unsigned long long*>(tr->d_run); pp.run_words = (size_t)NT * sizeof(RunState) / 8;
-    pp.ticket = tr->d_ticket; pp.sbase = r->d_sbase; pp.off = tr->d_off; pp.sabs = tr->d_sabs;
-    pp.n_traces = NT; pp.T = threshold;
-    CU(launch_prep(pp, st));
 
     ReplayParams p{};
     p.ev = tr->d_ev; p.off = tr->d_off; p.tk = tr->d_tk;
@@ -501,7 +494,13 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
     }
     p.n_sites = tr->n_sites; p.n_traces = NT; p.T = (long long)threshold; p.hwm_sample = o.hwm_mode == SCL_HWM_SAMPLE;
     p.table = r->d_table; p.samples = r->d_samples; p.ep_flag = r->d_epflag; p.sbase = r->d_sbase;
-    p.summ = r->d_summ; p.uent = tr->d_uent; p.rtask = r->d_rtask; p.rtask_cap = kRTaskCap;
+    p.summ = r->d_summ; p.uent = tr->d_uent;
+    PrepParams& pp = p.prep;                   // done by CTA 0 of the replay kernel
+    pp.table = r->d_table; pp.table_words = (size_t)tr->n_sites * SCL_NCOL + 3;
+    pp.summ = reinterpret_cast<unsigned long long*>(r->d_summ); pp.summ_words = (size_t)NT * sizeof(scl_trace_summary) / 8;
+    pp.run = reinterpret_cast<unsigned long long*>(tr->d_run); pp.run_words = (size_t)NT * sizeof(RunState) / 8;
+    pp.ticket = tr->d_ticket; pp.sbase = r->d_sbase; pp.off = tr->d_off; pp.sabs = tr->d_sabs;
+    pp.n_traces = NT; pp.T = threshold; p.rtask = r->d_rtask; p.rtask_cap = kRTaskCap;
 #ifdef SCL_PROFILE
     if (!r->d_prof) CU(cudaMalloc(&r->d_prof, (48 + 4 * (size_t)tr->cap_segs) * 8));
     CU(cudaMemsetAsync(r->d_prof, 0, (48 + 4 * (size_t)tr->n_segs) * 8, st));

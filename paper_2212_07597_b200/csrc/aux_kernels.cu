@@ -61,37 +61,6 @@ __global__ void __launch_bounds__(256) load_stats_kernel(const scl_event* ev, co
     }
 }
 
-// ============================================================================ per-run preparation
-__global__ void __launch_bounds__(1024) prep_kernel(const __grid_constant__ PrepParams p)
-{
-    const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (size_t)gridDim.x * blockDim.x;
-    for (size_t i = tid; i < p.table_words; i += nth) p.table[i] = 0;
-    for (size_t i = tid; i < p.summ_words; i += nth) p.summ[i] = 0;
-    for (size_t i = tid; i < p.run_words; i += nth) p.run[i] = 0;
-    if (tid < 4) p.ticket[tid] = 0;
-    if (blockIdx.x != 0) return;
-    // block 0: exclusive scan of the per-trace sample capacities (thread j: a contiguous run of traces)
-    __shared__ unsigned long long part[1024];
-    const unsigned per = (p.n_traces + blockDim.x - 1) / blockDim.x;
-    const unsigned t0 = threadIdx.x * per, t1 = min(p.n_traces, t0 + per);
-    auto cap = [&](unsigned t) {
-        const unsigned long long n = p.off[t + 1] - p.off[t], b = p.sabs[t] / p.T;
-        return n < b ? n : b;
-    };
-    unsigned long long acc = 0;
-    for (unsigned t = t0; t < t1; ++t) acc += cap(t);
-    part[threadIdx.x] = acc;
-    __syncthreads();
-    for (unsigned d = 1; d < blockDim.x; d <<= 1) {          // Hillis-Steele inclusive scan
-        const unsigned long long v = threadIdx.x >= d ? part[threadIdx.x - d] : 0;
-        __syncthreads();
-        part[threadIdx.x] += v;
-        __syncthreads();
-    }
-    unsigned long long base = part[threadIdx.x] - acc;
-    for (unsigned t = t0; t < t1; ++t) { p.sbase[t] = base; base += cap(t); }
-}
-
 // ============================================================================ a6
 __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ FinalParams p)
 {
@@ -138,15 +107,6 @@ cudaError_t launch_load_stats(const scl_event* ev, const unsigned long long* off
     const unsigned long long warps = (n_events + 255) / 256;
     const unsigned blocks = (unsigned)std::min<unsigned long long>((warps + 7) / 8, 148ull * 8);
     load_stats_kernel<<<blocks, 256, 0, st>>>(ev, off, n_traces, n_events, n_sites, sabs, err);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_prep(const PrepParams& p, cudaStream_t st)
-{
-    size_t words = p.table_words > p.summ_words ? p.table_words : p.summ_words;
-    words = words > p.run_words ? words : p.run_words;
-    unsigned blocks = (unsigned)std::min<size_t>((words + 1023) / 1024, 148);
-    prep_kernel<<<blocks ? blocks : 1, 1024, 0, st>>>(p);
     return cudaGetLastError();
 }
 

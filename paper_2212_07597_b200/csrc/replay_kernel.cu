@@ -104,6 +104,42 @@ __device__ __forceinline__ void load_row_global(const scl_event* ev, long long r
     for (int j = 0; j < kEpt; ++j) { ulonglong2 v = __ldcg(q + j); ptr[j] = v.x; meta[j] = v.y; }
 }
 
+// ============================================================================ per-run preparation (CTA 0)
+__device__ void prepare_run(const ReplayParams& rp, unsigned long long* scratch)
+{
+    const PrepParams& p = rp.prep;
+    const unsigned tid = threadIdx.x, nth = blockDim.x;
+    for (size_t i = tid; i < p.table_words; i += nth) p.table[i] = 0;
+    for (size_t i = tid; i < p.summ_words; i += nth) p.summ[i] = 0;
+    for (size_t i = tid; i < p.run_words; i += nth) p.run[i] = 0;
+    if (tid < 7) p.ticket[tid] = 0;
+    // exclusive scan of the per-trace sample capacities (thread j: a contiguous run of traces)
+    const unsigned per = (p.n_traces + nth - 1) / nth;
+    const unsigned t0 = min(p.n_traces, tid * per), t1 = min(p.n_traces, t0 + per);
+    auto cap = [&](unsigned t) {
+        const unsigned long long n = p.off[t + 1] - p.off[t], b = p.sabs[t] / p.T;
+        return n < b ? n : b;
+    };
+    unsigned long long acc = 0;
+    for (unsigned t = t0; t < t1; ++t) acc += cap(t);
+    scratch[tid] = acc;
+    __syncthreads();
+    for (unsigned d = 1; d < nth; d <<= 1) {                 // Hillis-Steele inclusive scan
+        const unsigned long long v = tid >= d ? scratch[tid - d] : 0;
+        __syncthreads();
+        scratch[tid] += v;
+        __syncthreads();
+    }
+    unsigned long long base = scratch[tid] - acc;
+    for (unsigned t = t0; t < t1; ++t) { p.sbase[t] = base; base += cap(t); }
+    __syncthreads();
+    if (tid == 0) { __threadfence(); st_release(&rp.ticket[7], rp.epoch); }
+}
+
+__device__ __forceinline__ void wait_prepared(const ReplayParams& p) {
+    while (ld_acquire(&p.ticket[7]) != p.epoch) __nanosleep(32);
+}
+
 // ============================================================================ compute warps
 // Fast path of one row (8 events) in a lane: sizes < 2^27 (size bits 32-39 zero).  Every shared
 // atomic is unconditional (no branch around it): an event that does not count goes to the lane's
@@ -288,6 +324,7 @@ __device__ void producer_role(const ReplayParams& p, const CUtensorMap* tmap, Sm
     // the events are streamed once: evict them first, keeping the unit records, samples and the
     // site table (which the runners and the post pass re-read) in L2
     const uint64_t pol = l2_policy_evict_first();
+    wait_prepared(p);                                     // ticket counter zeroed by CTA 0
     PROF_DECL
     auto resolve = [&](unsigned u) {
         SegInfo inf; inf.u = kInvalid; inf.nbox = 0;
@@ -598,6 +635,7 @@ __device__ void runner_role(const ReplayParams& p, unsigned ri, int lane)
 {
     const unsigned ep_tag = p.epoch;
     const unsigned nr = p.n_runners;
+    wait_prepared(p);                                     // runner states, sample bases: CTA 0
     const unsigned cnt = ri < p.n_traces ? (p.n_traces - ri + nr - 1) / nr : 0u;
     const unsigned my_t = ri + (unsigned)lane * nr;
     unsigned my_base = 0, my_nseg = 0, my_next = 0;
@@ -838,6 +876,7 @@ replay_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         asm volatile("prefetch.tensormap [%0];" :: "l"((uint64_t)&tmap) : "memory");
     }
     __syncthreads();
+    if (blockIdx.x == 0) prepare_run(p, reinterpret_cast<unsigned long long*>(stage));   // stage: not in use yet
 
     // register rebalancing per warpgroup (launch: 96/thread): the four compute warpgroups
     // give 16 each, the producer + look-back warpgroup takes them (no spills in its resolver)

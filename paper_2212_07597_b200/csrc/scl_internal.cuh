@@ -79,6 +79,22 @@ struct FinalParams {
     unsigned long long* prof;         // debug build only: phase timestamps of a6
 };
 
+// Per-run preparation, done by CTA 0 of the replay kernel before the other CTAs' producers and
+// runners start: zero the site table, the trace summaries, the runner states and the counters;
+// sample slot bases sbase[t] = sum_{t'<t} min(n_t', floor(sum|d|_t' / T)) (the host computes the
+// same bound).
+struct PrepParams {
+    unsigned long long* table; size_t table_words;
+    unsigned long long* summ; size_t summ_words;
+    unsigned long long* run; size_t run_words;
+    unsigned int* ticket;             // [4]
+    unsigned long long* sbase;        // [n_traces]
+    const unsigned long long* off;    // [n_traces + 1]
+    const unsigned long long* sabs;   // [n_traces]
+    unsigned int n_traces;
+    unsigned long long T;
+};
+
 // One exact re-check of the reclaim pass: chunk rows [row0, row0 + 32) of a unit, unit positions
 // [sbeg, send), does any free of `ptr` occur?  (pos0: unit position of the chunk's first event;
 // site: the episode's sample site, its leak-frees column.)
@@ -98,9 +114,11 @@ struct ReplayParams {
     UnitEntry* uent;                  // [n_segs] state entering each unit (runner -> reclaim pass)
     const unsigned int* tr_nseg;      // [n_traces] units per trace
     const unsigned int* tr_base;      // [n_traces] first unit id of the trace
-    unsigned int* ticket;             // [4]: unit tickets; post pass: units settled, task tail, warps done (zeroed per run)
+    unsigned int* ticket;             // [8]: unit tickets; post pass: units settled, task tail, blocks done (zeroed
+                                      //      per run); [7] = epoch once the run is prepared (never zeroed)
     RTask* rtask;                     // [rtask_cap] exact re-checks queued by the reclaim pass
     unsigned int rtask_cap;
+    PrepParams prep;                  // CTA 0 prepares the run; ticket[7] = epoch once done
     int fuse_report;                  // post_kernel's last block runs a6 (fin -> rows)
     FinalParams fin;
     scl_site_row* rows;
@@ -121,20 +139,6 @@ struct ReplayParams {
 };
 
 
-// Per-run preparation (one launch instead of memsets + a host copy): zero the site table,
-// the trace summaries, the runner states and the ticket counter; sample slot bases
-// sbase[t] = sum_{t'<t} min(n_t', floor(sum|d|_t' / T)) (the host computes the same bound).
-struct PrepParams {
-    unsigned long long* table; size_t table_words;
-    unsigned long long* summ; size_t summ_words;
-    unsigned long long* run; size_t run_words;
-    unsigned int* ticket;             // [4]
-    unsigned long long* sbase;        // [n_traces]
-    const unsigned long long* off;    // [n_traces + 1]
-    const unsigned long long* sabs;   // [n_traces]
-    unsigned int n_traces;
-    unsigned long long T;
-};
 
 #ifdef __CUDACC__
 // Per-sample reduce of trace t by one warp: Tier-S columns, leak mallocs (one per episode start,
@@ -207,7 +211,6 @@ cudaError_t launch_load_stats(const scl_event* ev, const unsigned long long* off
                               unsigned long long n_events, unsigned n_sites, unsigned long long* sabs,
                               unsigned long long* err, cudaStream_t st);
 cudaError_t launch_replay(const CUtensorMap* tmap, const ReplayParams& p, int grid, cudaStream_t st);
-cudaError_t launch_prep(const PrepParams& p, cudaStream_t st);
 cudaError_t launch_post(const ReplayParams& p, cudaStream_t st);
 cudaError_t launch_finalize(const FinalParams& p, cudaStream_t st);
 bool report_fused(unsigned n_sites);   // a6 in one block (report_kernel) for tables this small
