@@ -186,6 +186,13 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
     const uint32_t cnt_s = smem_u32(s.cnt);
     const uint32_t dslot = (uint32_t)(2 * kHot + (grp * 8 + w8) * 32 + lane) * 4u;   // this lane's sink slot
     const bool all_hot = p.n_sites <= (unsigned)kHot;       // no cold site: no L2 path to track
+    // this lane's row r = 32*w8 + lane of every box: its 8 swizzled 16-B chunks (chunk j at j ^ (r & 7))
+    const int r = w8 * 32 + lane;
+    unsigned rofs[kEpt];
+    #pragma unroll
+    for (int j = 0; j < kEpt; ++j) rofs[j] = (unsigned)r * 128u + (unsigned)((j ^ (r & 7)) << 4);
+    int sl = kSlots - 1;                                    // unit slot (itu % kSlots) and its phase,
+    unsigned sph = 1u, cur_itu = ~0u;                       // advanced incrementally (no division)
     PROF_DECL
     for (unsigned it = grp;; it += 2) {
         const int st = it % kStages;
@@ -195,14 +202,14 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
         const SegInfo inf = s.info[st];
         const unsigned g = s.sub[st];
         const unsigned itu = it / kSub;                   // unit iteration of this CTA
-        const int sl = itu % kSlots;
+        if (itu != cur_itu) { cur_itu = itu; if (++sl == kSlots) { sl = 0; sph ^= 1u; } }
         if (inf.u == kInvalid) {
             // the look-back warps stop once all `itu` units of this CTA are published
             if (grp == 0 && w8 == 0 && lane == 0) atomicExch(&s.n_units, itu);
             PROF_FLUSH(0)
             return;
         }
-        if (g == (unsigned)grp) mbar_wait(&s.sempty[sl], ((itu / kSlots) & 1u) ^ 1u);   // group's first box of the unit
+        if (g == (unsigned)grp) mbar_wait(&s.sempty[sl], sph ^ 1u);   // group's first box of the unit
         PROF_MARK(1)
         Slot& S = s.slot[sl];
         const int c = g * 8 + w8;                         // chunk index within the unit
@@ -215,13 +222,12 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
         int r32 = 0, mx32 = INT_MIN, mn32 = INT_MAX;
         bool small = true;                                // 32-bit chunk summary is exact for this lane
         if (g < inf.nbox) {
-            // ---- the 8 events of row 32*w8+lane (16-B chunk j of row r sits at j ^ (r & 7))
-            const int r = w8 * 32 + lane;
-            const unsigned char* rowp = stage + (size_t)st * kSegBytes + (size_t)r * 128;
+            // ---- the 8 events of row r of the box
+            const unsigned char* boxp = stage + (size_t)st * kSegBytes;
             unsigned long long ptr[kEpt], meta[kEpt];
             #pragma unroll
             for (int j = 0; j < kEpt; ++j) {
-                ulonglong2 v = *reinterpret_cast<const ulonglong2*>(rowp + ((j ^ (r & 7)) << 4));
+                ulonglong2 v = *reinterpret_cast<const ulonglong2*>(boxp + rofs[j]);
                 ptr[j] = v.x; meta[j] = v.y;
             }
             const long long e0 = (inf.row_base + (long long)g * kThreads + r) * kEpt - inf.off_t;
