@@ -7,6 +7,7 @@
 // the per-run result buffers.  Every compute step runs in the kernels of
 // replay.cu; this file only plans, allocates, launches and copies.
 #include "scl_internal.cuh"
+#include "report.cuh"
 #include <cudaTypedefs.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cstdio>
@@ -78,6 +79,7 @@ struct scl_result {
     void* d_cub = nullptr; size_t cub_bytes = 0;
     scl_site_row* d_rows = nullptr;
     RTask* d_rtask = nullptr;                  // reclaim pass re-check queue
+    unsigned* d_rbits = nullptr; double* d_rlrate = nullptr; unsigned* d_rlsite = nullptr;   // a6 scratch
     unsigned long long* d_P = nullptr;         // per-sample (alloc, managed) prefixes (NEXT-2, lazy)
     scl_sample_domain* d_dom = nullptr;
     size_t cap_dom = 0;
@@ -380,6 +382,7 @@ extern "C" void scl_result_free(scl_result* r) {
     if (!r) return;
     free_result_buffers(r);
     cudaFree(r->d_samples); cudaFree(r->d_epflag); cudaFree(r->d_prof); cudaFree(r->d_rtask);
+    cudaFree(r->d_rbits); cudaFree(r->d_rlrate); cudaFree(r->d_rlsite);
     cudaFree(r->d_P); cudaFree(r->d_dom); cudaFree(r->d_recon);
     if (r->h_gate) cudaFreeHost(r->h_gate);
     for (auto& e : r->ev) if (e) cudaEventDestroy(e);
@@ -395,6 +398,8 @@ static scl_status alloc_result(scl_result* r, const scl_traces* tr) {
         for (auto& e : r->kev) CU(cudaEventCreate(&e));
         CU(cudaMallocHost(&r->h_gate, 32));
         CU(cudaMalloc(&r->d_rtask, (size_t)kRTaskCap * sizeof(RTask)));
+        CU(cudaMalloc(&r->d_rbits, kReportSites / 32 * 4));
+        CU(cudaMalloc(&r->d_rlrate, kReportList * 8)); CU(cudaMalloc(&r->d_rlsite, kReportList * 4));
         int grid = 0;
         replay_occupancy(&grid);
         r->grid = grid;
@@ -513,7 +518,10 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
     if (tm) { CU(cudaEventRecord(r->kev[2 * ks + 1], st)); r->nrun += 1; }
     // a6 fused into the post pass (its last block) when the run finalizes at once on a small table
     const bool fuse = !o.defer_finalize && report_fused(tr->n_sites);
-    if (fuse) { p.fuse_report = 1; p.fin = final_params(r); p.rows = r->d_rows; }
+    if (fuse) {
+        p.fuse_report = 1; p.fin = final_params(r); p.rows = r->d_rows;
+        p.rbits = r->d_rbits; p.rlrate = r->d_rlrate; p.rlsite = r->d_rlsite;
+    }
     CU(launch_post(p, st));
     if (tm) CU(cudaEventRecord(r->ev[1], st));
     if (fuse) {

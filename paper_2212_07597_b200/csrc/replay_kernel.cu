@@ -684,7 +684,8 @@ __device__ void runner_role(const ReplayParams& p, unsigned ri, int lane)
 //  -- grid barrier --
 //  B. the re-check tasks, spread over all warps (one chunk each, through L2).  The first re-check
 //     that finds the free of an episode flips its ep_flag and counts the episode's frees;
-//  C. with fuse_report: the last block to finish runs a6 (report.cuh) on the complete table.
+//  C. with fuse_report: a6 (report.cuh) over all blocks: flags per 32-site word, grid barrier,
+//     ranks and rows.
 // ep_flag was zeroed by the runner at each episode's start.
 __device__ __forceinline__ bool chunk_has_free(const ReplayParams& p, long long row0, long long off_t, long long n_t,
                                                unsigned pos0, unsigned long long ptr, unsigned sbeg, unsigned send, int lane)
@@ -778,8 +779,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr) {
 
 __global__ void __launch_bounds__(256, 3) post_kernel(const __grid_constant__ ReplayParams p)
 {
-    extern __shared__ __align__(16) unsigned char post_smem[];            // a6 of the last block (fuse_report)
-    __shared__ unsigned last;
+    extern __shared__ __align__(16) unsigned char post_smem[];            // a6 row staging (fuse_report)
     const int lane = threadIdx.x & 31;
     const unsigned wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
 #ifdef SCL_PROFILE
@@ -823,32 +823,34 @@ __global__ void __launch_bounds__(256, 3) post_kernel(const __grid_constant__ Re
             reclaimed(p, tk.ep1, tk.site);
     }
     POST_T(3, atomicMax)
-    if (!p.fuse_report) return;                                                           // phase C
-    __syncthreads();
-    if (threadIdx.x == 0) { __threadfence(); last = atomicAdd(&p.ticket[3], 1u) == gridDim.x - 1; }
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
+    if (!p.fuse_report) return;                                                           // phase C: a6
+    grid_barrier(&p.ticket[3]);                             // every re-check done: leak frees final
     POST_T(4, atomicMax)
-    report_block<256>(p.fin, p.rows, *reinterpret_cast<ReportSmem<256>*>(post_smem));
+    const ReportScratch rx{p.rbits, p.rlrate, p.rlsite, &p.ticket[5]};
+    report_grid_flags(p.fin, rx, wid, nw, lane);
+    grid_barrier(&p.ticket[4]);
+    report_grid_rows(p.fin, p.rows, rx, reinterpret_cast<unsigned long long*>(post_smem) + (threadIdx.x >> 5) * 32 * kRowWords,
+                     wid, nw, lane);
     POST_T(5, atomicMax)
 }
+
+constexpr size_t kPostStage = 8 * 32 * kRowWords * 8;          // a6 row staging: 8 warps x 32 rows
 
 cudaError_t launch_post(const ReplayParams& p, cudaStream_t st)
 {
     static int occ = 0, nsm = 0;
-    const size_t smem = p.fuse_report ? report_smem_bytes<256>() : 0;
+    const size_t smem = p.fuse_report ? kPostStage : 0;
     static int occ_fused = 0;
     if (!occ) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         cudaError_t e = cudaFuncSetAttribute(post_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)report_smem_bytes<256>());
+                                             (int)kPostStage);
         if (e != cudaSuccess) return e;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, post_kernel, 256, 0);
         if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_fused, post_kernel, 256, report_smem_bytes<256>());
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_fused, post_kernel, 256, kPostStage);
         if (e != cudaSuccess) return e;
         occ = std::max(occ, 1); occ_fused = std::max(occ_fused, 1);
     }

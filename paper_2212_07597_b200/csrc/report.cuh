@@ -1,9 +1,10 @@
-// report.cuh -- a6 for one block: per-site probability, rate and flag, the report order and the
-// rows (readings Q8-Q11 of DESIGN.md §3).  Used by report_kernel (1024 threads) and by
-// the last block of post_kernel (256 threads) when the run finalizes at once.
+// report.cuh -- a6: per-site probability, rate and flag, the report order and the rows (
+// readings Q8-Q11 of DESIGN.md §3).  report_block: one block (report_kernel, deferred runs);
+// report_grid_*: spread over post_kernel's blocks when the run finalizes at once.
 #pragma once
 #include <cstddef>
 #include "scl_internal.cuh"
+#include "ptx.cuh"
 
 namespace scl {
 
@@ -180,6 +181,97 @@ __device__ void report_block(const FinalParams& p, scl_site_row* rows, ReportSme
             }
             __syncwarp();
         }
+    }
+}
+
+// ---- a6 spread over a whole grid (post_kernel, fused): warp w owns the 32 sites of word w.
+struct ReportScratch { unsigned* bits; double* lrate; unsigned* lsite; unsigned* nflag; };
+
+// C1: integer flags (bitmask word per warp), flagged sites (rate, site) appended to a global list.
+static __device__ void report_grid_flags(const FinalParams& p, const ReportScratch& x, unsigned wid, unsigned nw, int lane)
+{
+    const unsigned S = p.n_sites, nwd = (S + 31) / 32;
+    const bool open = gate_open(p);
+    const double es = elapsed_s(p);
+    if (wid == 0 && lane == 0) gate_copy(p);
+    for (unsigned w = wid; w < nwd; w += nw) {
+        const unsigned sidx = w * 32 + (unsigned)lane;
+        bool fl = false;
+        if (sidx < S) {
+            const unsigned long long* row = p.table + (size_t)sidx * SCL_NCOL;
+            fl = open && site_over(p, __ldcg(&row[SCL_COL_LEAK_MALLOCS]), __ldcg(&row[SCL_COL_LEAK_FREES]));
+            if (fl) {
+                const unsigned q = atomicAdd(x.nflag, 1u);
+                if (q < kReportList) { x.lrate[q] = site_rate(__ldcg(&row[SCL_COL_MALLOC_BYTES]), es); x.lsite[q] = sidx; }
+            }
+        }
+        const unsigned word = __ballot_sync(kFull, fl);
+        if (lane == 0) x.bits[w] = word;
+    }
+}
+
+// C2: ranks and rows (after a grid barrier): flagged sites against the flagged list, unflagged
+// sites = #flagged + unflagged sites before them (staged, lane-contiguous stores).
+static __device__ void report_grid_rows(const FinalParams& p, scl_site_row* rows, const ReportScratch& x,
+                                 unsigned long long* stg, unsigned wid, unsigned nw, int lane)
+{
+    const unsigned S = p.n_sites, nwd = (S + 31) / 32;
+    const bool open = gate_open(p);
+    const double es = elapsed_s(p);
+    const unsigned F = __ldcg(x.nflag);
+    for (unsigned w = wid; w < nwd; w += nw) {
+        unsigned fbw = 0;                                      // flagged sites before word w
+        for (unsigned q = (unsigned)lane; q < w; q += 32) fbw += __popc(__ldcg(&x.bits[q]));
+        fbw = (unsigned)warp_sum((long long)fbw);
+        const unsigned word = __ldcg(&x.bits[w]);
+        const unsigned sidx = w * 32 + (unsigned)lane;
+        const bool in = sidx < S, fl = in && ((word >> lane) & 1u);
+        const unsigned um = __ballot_sync(kFull, in && !fl);
+        if (in) {
+            const ulonglong2* src = reinterpret_cast<const ulonglong2*>(p.table + (size_t)sidx * SCL_NCOL);
+            ulonglong2 rv[SCL_NCOL / 2];
+            #pragma unroll
+            for (int c = 0; c < SCL_NCOL / 2; ++c) rv[c] = __ldcg(src + c);
+            auto col = [&](int c) { return (c & 1) ? rv[c >> 1].y : rv[c >> 1].x; };
+            const double prob = site_prob(p, col(SCL_COL_LEAK_MALLOCS), col(SCL_COL_LEAK_FREES));
+            const double rate = site_rate(col(SCL_COL_MALLOC_BYTES), es);
+            auto word_at = [&](int q) -> unsigned long long {
+                if (q == 0) return (unsigned long long)sidx | ((unsigned long long)(fl ? 1u : 0u) << 32);
+                if (q == 11) return (unsigned long long)__double_as_longlong(prob);
+                if (q == 12) return (unsigned long long)__double_as_longlong(rate);
+                return col(q - 1);
+            };
+            if (fl) {
+                unsigned rank = 0;
+                if (F <= kReportList) {
+                    for (unsigned q = 0; q < F; ++q) {
+                        const double r2 = __ldcg(&x.lrate[q]);
+                        rank += (r2 > rate || (r2 == rate && __ldcg(&x.lsite[q]) < sidx)) ? 1u : 0u;
+                    }
+                } else {                                       // many flagged sites: compare against all
+                    for (unsigned j = 0; j < S; ++j) {
+                        const SiteStat o = site_stat(p, j, open);
+                        rank += (o.flag && (o.rate > rate || (o.rate == rate && j < sidx))) ? 1u : 0u;
+                    }
+                }
+                unsigned long long* dst = reinterpret_cast<unsigned long long*>(rows + rank);
+                #pragma unroll
+                for (int q = 0; q < (int)kRowWords; ++q) dst[q] = word_at(q);
+            } else {
+                const unsigned j = __popc(um & ((1u << lane) - 1u));
+                #pragma unroll
+                for (int q = 0; q < (int)kRowWords; ++q) stg[j * kRowWords + q] = word_at(q);
+            }
+        }
+        __syncwarp();
+        if (um) {
+            const int l1 = __ffs(um) - 1;                      // the first unflagged lane
+            const unsigned r0 = F + w * 32 + (unsigned)l1 - (fbw + __popc(word & ((1u << l1) - 1u)));
+            unsigned long long* dst = reinterpret_cast<unsigned long long*>(rows + r0);
+            const unsigned nwds = (unsigned)__popc(um) * kRowWords;
+            for (unsigned q = (unsigned)lane; q < nwds; q += 32) dst[q] = stg[q];
+        }
+        __syncwarp();
     }
 }
 

@@ -119,7 +119,9 @@ struct ReplayParams {
     RTask* rtask;                     // [rtask_cap] exact re-checks queued by the reclaim pass
     unsigned int rtask_cap;
     PrepParams prep;                  // CTA 0 prepares the run; ticket[7] = epoch once done
-    int fuse_report;                  // post_kernel's last block runs a6 (fin -> rows)
+    int fuse_report;                  // post_kernel runs a6 over all its blocks (fin -> rows)
+    unsigned* rbits;                  // [kReportSites/32] a6 scratch: flag bitmask words
+    double* rlrate; unsigned* rlsite; //   flagged sites' rates and ids (kReportList)
     FinalParams fin;
     scl_site_row* rows;
     unsigned int n_segs;
