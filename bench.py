@@ -349,7 +349,7 @@ def main():
             "clocks": clk.summary(),
             "e2e": e2e,
             "gpu_launches": 2 * args.steps,
-            "gpu_launches_note": "per step: replay_kernel (its CTA 0 prepares the run), post_kernel (a6 in its last block) "
+            "gpu_launches_note": "per step: replay_kernel (its CTA 0 prepares the run), post_kernel (a6 grid-wide after its reclaim phases) "
                                  "(tables > 16384 sites: finalize + CUB radix sort + rows instead of report)",
             "kernel_timing": "replay_kernel durations from CUDA events in a second pass of K steps",
             "n_samples_per_step": n_samples,

@@ -487,16 +487,7 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
     p.ev = tr->d_ev; p.off = tr->d_off; p.tk = tr->d_tk;
     p.urec = tr->d_urec; p.uready = tr->d_uready; p.run = tr->d_run; p.tr_nseg = tr->d_tr_nseg; p.tr_base = tr->d_tr_base;
     p.ticket = tr->d_ticket; p.n_segs = tr->n_segs; p.epoch = tr->epoch;
-    {   // runner layout: 2 runner warps in every streaming CTA (default), or dedicated runner CTAs
-        // (SCL_RUNNER_CTAS=1, experiments: measured slower on config 2)
-        static const bool dedicated = getenv("SCL_RUNNER_CTAS") && atoi(getenv("SCL_RUNNER_CTAS")) > 0;
-        if (dedicated && NT <= (unsigned)kMaxRunnerCtas * kRunnersPerCta * 32) {
-            const unsigned rc = std::min<unsigned>(replay_runner_ctas(NT), (unsigned)r->grid - 1);
-            p.n_stream = (unsigned)r->grid - rc; p.n_runners = rc * kRunnersPerCta;
-        } else {
-            p.n_stream = (unsigned)r->grid; p.n_runners = (unsigned)r->grid * kEmbeddedRunners;
-        }
-    }
+    p.n_runners = (unsigned)r->grid * kEmbeddedRunners;    // 2 runner warps in every CTA
     p.n_sites = tr->n_sites; p.n_traces = NT; p.T = (long long)threshold; p.hwm_sample = o.hwm_mode == SCL_HWM_SAMPLE;
     p.table = r->d_table; p.samples = r->d_samples; p.ep_flag = r->d_epflag; p.sbase = r->d_sbase;
     p.summ = r->d_summ; p.uent = tr->d_uent;

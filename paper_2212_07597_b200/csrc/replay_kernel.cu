@@ -886,17 +886,8 @@ replay_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     __syncthreads();
     if (blockIdx.x == 0) prepare_run(p, reinterpret_cast<unsigned long long*>(stage));   // stage: not in use yet
 
-    // register rebalancing per warpgroup (launch: 96/thread): the four compute warpgroups
-    // give 16 each, the producer + look-back warpgroup takes them (no spills in its resolver)
-    if (blockIdx.x >= p.n_stream) {
-        // runner CTA: warpgroups 0-1 hand their registers to warpgroups 2-4 (12 runner warps)
-        if (warp < 8) { asm volatile("setmaxnreg.dec.sync.aligned.u32 24;\n" ::: "memory"); return; }
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 144;\n" ::: "memory");   // 8x32x72 released = 12x32x48
-        runner_role(p, (blockIdx.x - p.n_stream) * kRunnersPerCta + (warp - 8), lane);
-        return;
-    }
-    // streaming CTA, per warpgroup (launch: 96/thread): the four compute warpgroups give 16
-    // each, the producer + publisher warpgroup takes them
+    // register rebalancing per warpgroup (launch: 96/thread): the four compute warpgroups give 16
+    // each, the producer + publisher + runners warpgroup takes them (no spills in the resolver)
     if (warp < kComputeWarps) asm volatile("setmaxnreg.dec.sync.aligned.u32 80;\n" ::: "memory");
     else                      asm volatile("setmaxnreg.inc.sync.aligned.u32 160;\n" ::: "memory");
     if (warp < kComputeWarps) {
@@ -915,15 +906,9 @@ replay_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         producer_role(p, &tmap, s, stage, lane);
     } else if (warp == kProducerWarp + 1) {
         publisher_role(p, s, lane);
-    } else if (p.n_stream == gridDim.x) {                             // embedded runners: 2 per CTA
+    } else {                                                          // 2 runner warps per CTA
         runner_role(p, blockIdx.x * kEmbeddedRunners + (warp - kProducerWarp - 2), lane);
     }
-}
-
-unsigned replay_runner_ctas(unsigned n_traces)
-{
-    const unsigned c = (n_traces + kRunnersPerCta - 1) / kRunnersPerCta;   // about one trace per runner warp
-    return c < 1 ? 1 : (c > (unsigned)kMaxRunnerCtas ? (unsigned)kMaxRunnerCtas : c);
 }
 
 int replay_occupancy(int* grid)

@@ -30,8 +30,6 @@ constexpr int kChunks = 32;                   // 256-event chunks per unit (one 
 constexpr int kComputeWarps = 16;                // two groups of 8, alternating boxes
 constexpr int kLBWarps = 3;                   // publisher + 2 runner warps (20 warps total, 96 registers)
 constexpr int kEmbeddedRunners = 2;           // default layout: warps 18-19 of every streaming CTA run traces
-constexpr int kRunnersPerCta = 12;            // runner CTA: warps 8..19 run traces (144 registers each)
-constexpr int kMaxRunnerCtas = 16;            // at most 16 of the SMs run traces instead of streaming
 constexpr int kProducerWarp = kComputeWarps;
 constexpr int kCtaThreads = (kComputeWarps + 1 + kLBWarps) * 32;
 constexpr int kStages = 4;                    // TMA ring depth
@@ -125,8 +123,7 @@ struct ReplayParams {
     FinalParams fin;
     scl_site_row* rows;
     unsigned int n_segs;
-    unsigned int n_stream;            // CTAs [0, n_stream) stream units, the rest run traces
-    unsigned int n_runners;           // embedded: gridDim.x * 2; dedicated: (gridDim.x - n_stream) * kRunnersPerCta
+    unsigned int n_runners;           // gridDim.x * kEmbeddedRunners
     unsigned int epoch;               // run number on this traces handle (ready tag)
     unsigned int n_sites;
     unsigned int n_traces;
@@ -223,6 +220,5 @@ cudaError_t launch_rows(const unsigned long long* table, const double* prob, con
 size_t replay_smem_bytes();
 size_t replay_urec_bytes();            // bytes of one unit record
 int replay_occupancy(int* grid);
-unsigned replay_runner_ctas(unsigned n_traces);   // CTAs of the grid that run traces
 
 }  // namespace scl
