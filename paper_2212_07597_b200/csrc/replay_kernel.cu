@@ -305,7 +305,7 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
         mbar_arrive(&s.empty[st]);                        // box consumed
         PROF_MARK(2)
         unsigned old = 0;
-        if (lane == 0) { __threadfence_block(); old = atomicAdd(&S.done, 1u); __threadfence_block(); }
+        if (lane == 0) old = atom_add_acq_rel_cta(&S.done, 1u);
         old = __shfl_sync(kFull, old, 0);
         if (old == kChunks - 1) {
             // last chunk of the unit: compose the 32 chunk summaries (lane = chunk) and publish
@@ -602,32 +602,39 @@ __device__ void publisher_role(const ReplayParams& p, Smem& s, int lane)
     Slot* urec = reinterpret_cast<Slot*>(p.urec);
     PROF_DECL
     for (;;) {
-        unsigned best = kInvalid;                        // the oldest full slot
-        if (lane < kSlots && ((volatile unsigned*)s.sstate)[lane] == 1) best = ((volatile unsigned*)s.situ)[lane];
-        #pragma unroll
-        for (int d = 16; d > 0; d >>= 1) best = min(best, __shfl_xor_sync(kFull, best, d));
-        if (best == kInvalid) {
+        // every full slot at once: copy each to its unit record and hand the shared-memory slot
+        // back right away (the copy is in flight from registers), then ONE device-scope fence
+        // before the ready flags of the whole batch
+        const unsigned fm = __ballot_sync(kFull, lane < kSlots && ((volatile unsigned*)s.sstate)[lane] == 1);
+        if (fm == 0) {
             const unsigned nu = ((volatile unsigned*)&s.n_units)[0], nd = ((volatile unsigned*)&s.n_done)[0];
             if (nu != kInvalid && nd >= nu) { PROF_FLUSH(16) return; }
             PROF_MARK(0)
             __nanosleep(32);
             continue;
         }
-        const unsigned cand = __ballot_sync(kFull, lane < kSlots && ((volatile unsigned*)s.sstate)[lane] == 1 &&
-                                                    ((volatile unsigned*)s.situ)[lane] == best);
-        const int q = __ffs(cand) - 1;
         __threadfence_block();
-        Slot& S = s.slot[q];
-        const unsigned u = S.info.slot;
-        const uint4* src = reinterpret_cast<const uint4*>(&S);
-        uint4* dst = reinterpret_cast<uint4*>(urec + u);
-        for (int o = lane; o < (int)(sizeof(Slot) / 16); o += 32) dst[o] = src[o];
-        __syncwarp();
+        const unsigned uq = ((fm >> lane) & 1u) ? ((volatile unsigned*)&s.slot[lane].info.slot)[0] : 0u;
+        for (unsigned m = fm; m; m &= m - 1) {
+            const int q = __ffs(m) - 1;
+            Slot& S = s.slot[q];
+            const uint4* src = reinterpret_cast<const uint4*>(&S);
+            uint4* dst = reinterpret_cast<uint4*>(urec + __shfl_sync(kFull, uq, q));
+            for (int o = lane; o < (int)(sizeof(Slot) / 16); o += 32) dst[o] = src[o];
+            __syncwarp();
+            if (lane == 0) {
+                S.done = 0; __threadfence_block();
+                atomicExch(&s.sstate[q], 0u); mbar_arrive(&s.sempty[q]);
+            }
+        }
+        unsigned uid[kSlots];
+        #pragma unroll
+        for (int q = 0; q < kSlots; ++q) uid[q] = __shfl_sync(kFull, uq, q);
         if (lane == 0) {
             __threadfence();
-            st_release(&p.uready[u], ep_tag);
-            S.done = 0; __threadfence_block();
-            atomicExch(&s.sstate[q], 0u); mbar_arrive(&s.sempty[q]); atomicAdd(&s.n_done, 1u);
+            #pragma unroll
+            for (int q = 0; q < kSlots; ++q) if ((fm >> q) & 1u) st_relaxed(&p.uready[uid[q]], ep_tag);
+            atomicAdd(&s.n_done, (unsigned)__popc(fm));
         }
         __syncwarp();
         PROF_MARK(1)
