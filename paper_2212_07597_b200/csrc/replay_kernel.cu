@@ -39,20 +39,21 @@ struct SegInfo {                     // one unit ticket, as the producer resolve
 };
 struct __align__(16) Slot {          // compute -> look-back summary of one unit
     SegInfo info;
-    long long csum[kChunks], cmx[kChunks], cmn[kChunks];   // per chunk, relative to the chunk start
     long long Pc[kChunks], ax[kChunks], an[kChunks];       // chunk prefix; max/min relative to the unit start
+                                                           // (before the compose: chunk sum, max, min
+                                                           // relative to the chunk start)
     long long usum, umx, umn;                              // unit aggregate
     unsigned done, itu;                                    // chunks finished; CTA unit iteration
     unsigned bloom[kChunks][kBloomWords];
 };
 
-constexpr int kESlots = 2 * kHot + kComputeWarps * 32;
+constexpr int kESlots = 4 * kHot + kComputeWarps * 32;
 constexpr uint32_t kBloOff = kESlots * 4;   // byte distance cnt -> blo
 
 struct __align__(16) Smem {
-    unsigned cnt[kESlots];           // Tier-E per (kind, hot site): event count   (slots >= 2*kHot:
-    unsigned blo[kESlots];           //   bytes, low 32 bits                        per-lane sinks of the
-    unsigned bhi[2 * kHot];          //   carries out of blo                         unconditional atomics)
+    unsigned cnt[kESlots];           // Tier-E per (kind, hot site): event count    (slot kind*kHot + site;
+    unsigned blo[kESlots];           //   bytes mod 2^32 (carries: straight to L2)  slots >= 4*kHot: per-lane
+                                     //   sinks of the unconditional atomics; copies counted, not reported)
     Slot slot[kSlots];
     SegInfo info[kStages];
     unsigned sub[kStages];           // box index within the unit
@@ -141,41 +142,51 @@ __device__ __forceinline__ void wait_prepared(const ReplayParams& p) {
 }
 
 // ============================================================================ compute warps
-// Fast path of one row (8 events) in a lane: sizes < 2^27 (size bits 32-39 zero).  Every shared
+// Fast path of one row (8 events) in a lane: sizes < 2^27 (size bits 27-39 zero).  Every shared
 // atomic is unconditional (no branch around it): an event that does not count goes to the lane's
-// sink slot (and adds 0 bytes, so the sink never wraps).  Tier-E slot of (site, kind) = site*2 +
-// (kind & 1): its byte offset site*8 + (kind&1)*4 is one bit-select of meta>>40 and meta>>38.
+// sink slot (and adds 0 bytes, so the sink never wraps).  Tier-E slot of (kind, site) = kind*kHot +
+// site (kind-major: a warp's random sites spread over all 32 banks), copies included -- with every
+// site hot, no event needs a select.  Kinds are
+// read as bits: bit 41 set = copy (no footprint change), else bit 40 = free (kind 3 is rejected
+// by the trace validation; unvalidated, it only widens the Bloom filter, which is re-checked).
 // 32-bit byte-counter carries: one accumulated predicate, the rare wrap re-examined afterwards.
 // kAllHot: every site is in the shared-memory table (n_sites <= kHot), no cold-site bookkeeping.
 template <bool kAllHot>
 __device__ __forceinline__ void fast_row(const unsigned long long* ptr, const unsigned long long* meta, uint32_t cnt_s,
-                                         uint32_t bl_s, uint32_t dslot, Smem& s, int& r32, int& mx32, int& mn32,
-                                         unsigned& cold)
+                                         uint32_t bl_s, uint32_t dslot, unsigned long long* table, int& r32,
+                                         int& mx32, int& mn32, unsigned& cold)
 {
     unsigned old[kEpt], add[kEpt];
     bool anyc = false;
     #pragma unroll
     for (int j = 0; j < kEpt; ++j) {
         const unsigned hi = (unsigned)(meta[j] >> 32), lo = (unsigned)meta[j];
-        const unsigned kind = (hi >> 8) & 3u, site = hi >> 11;
-        const bool isfree = kind == 1, af = kind < 2;
-        r32 += af ? (isfree ? -(int)lo : (int)lo) : 0;                        // a1: signed size
+        const bool isfree = (hi & 0x100u) != 0, af = (hi & 0x200u) == 0;
+        const int d = isfree ? -(int)lo : (int)lo;
+        if (af) r32 += d;                                                     // a1: signed size
         mx32 = max(mx32, r32); mn32 = min(mn32, r32);
-        const bool h = af && (kAllHot || site < (unsigned)kHot);
-        if (!kAllHot) cold |= (af && !h ? 1u : 0u) << j;
-        const uint32_t off = ((hi >> 8) & 0xfffffff8u) | ((hi >> 6) & 0x7u);  // site*8 + (kind&1)*4
-        const uint32_t a = cnt_s + (h ? off : dslot);
-        add[j] = h ? lo : 0u;
+        const uint32_t off = ((hi >> 9) & (uint32_t)(4 * kHot - 4)) | ((hi << 4) & (uint32_t)(3 * 4 * kHot));  // (kind*kHot + site)*4
+        uint32_t a;
+        if (kAllHot) {                                                        // site < kHot
+            a = cnt_s + off; add[j] = lo;
+        } else {
+            const bool h = (hi >> 11) < (unsigned)kHot;
+            cold |= (af && !h ? 1u : 0u) << j;
+            a = cnt_s + (h ? off : dslot); add[j] = h ? lo : 0u;
+        }
         red_add(a, 1u);                                                       // a5 Tier E
         old[j] = atom_add(a + kBloOff, add[j]);
         red_or(isfree ? bl_s + bloom_word(ptr[j]) * 4u : cnt_s + dslot, bloom_mask(ptr[j]));   // freed ptr -> Bloom
     }
     #pragma unroll
     for (int j = 0; j < kEpt; ++j) anyc |= old[j] + add[j] < old[j];
-    if (anyc) {                                       // rare: a 32-bit byte counter wrapped
+    if (anyc) {                                       // rare: a 32-bit byte counter wrapped: 2^32 to L2
         #pragma unroll
-        for (int j = 0; j < kEpt; ++j)
-            if (old[j] + add[j] < old[j]) atomicAdd(&s.bhi[ev_site(meta[j]) * 2 + (ev_kind(meta[j]) & 1u)], 1u);
+        for (int j = 0; j < kEpt; ++j) {
+            const unsigned kind = ev_kind(meta[j]);
+            if (old[j] + add[j] < old[j] && kind < 2)
+                atomicAdd(&table[(size_t)ev_site(meta[j]) * SCL_NCOL + SCL_COL_MALLOC_BYTES + kind], 1ull << 32);
+        }
     }
 }
 
@@ -184,7 +195,7 @@ __device__ __forceinline__ void fast_row(const unsigned long long* ptr, const un
 __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stage, int grp, int w8, int lane)
 {
     const uint32_t cnt_s = smem_u32(s.cnt);
-    const uint32_t dslot = (uint32_t)(2 * kHot + (grp * 8 + w8) * 32 + lane) * 4u;   // this lane's sink slot
+    const uint32_t dslot = (uint32_t)(4 * kHot + (grp * 8 + w8) * 32 + lane) * 4u;   // this lane's sink slot
     const bool all_hot = p.n_sites <= (unsigned)kHot;       // no cold site: no L2 path to track
     // this lane's row r = 32*w8 + lane of every box: its 8 swizzled 16-B chunks (chunk j at j ^ (r & 7))
     const int r = w8 * 32 + lane;
@@ -238,8 +249,8 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
             if (e0 >= 0 && e0 + kEpt <= inf.n_t && big == 0) {
                 // fast path: the whole row is in the trace and |partial sums| < 2^30: 32-bit running
                 // sum / max / min (a copy's d = 0 repeats an F already seen: harmless)
-                if (all_hot) fast_row<true>(ptr, meta, cnt_s, bl_s, dslot, s, r32, mx32, mn32, cold);
-                else         fast_row<false>(ptr, meta, cnt_s, bl_s, dslot, s, r32, mx32, mn32, cold);
+                if (all_hot) fast_row<true>(ptr, meta, cnt_s, bl_s, dslot, p.table, r32, mx32, mn32, cold);
+                else         fast_row<false>(ptr, meta, cnt_s, bl_s, dslot, p.table, r32, mx32, mn32, cold);
                 run = r32;
                 tmx = mx32; tmn = mn32;
                 small = r32 > -(1 << 25) && r32 < (1 << 25) && mx32 < (1 << 25) && mn32 > -(1 << 25);
@@ -257,10 +268,11 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
                         tmx = llmax(tmx, run); tmn = llmin(tmn, run);
                         const unsigned site = ev_site(meta[j]);
                         if (site < (unsigned)kHot && size < (1ull << 32)) {
-                            const int x = (int)site * 2 + (int)(kind & 1u);
+                            const int x = (int)kind * kHot + (int)site;
                             atomicAdd(&s.cnt[x], 1u);
                             const unsigned old = atomicAdd(&s.blo[x], (unsigned)size);
-                            if (old + (unsigned)size < old) atomicAdd(&s.bhi[x], 1u);
+                            if (old + (unsigned)size < old)
+                                atomicAdd(&p.table[(size_t)site * SCL_NCOL + SCL_COL_MALLOC_BYTES + kind], 1ull << 32);
                         } else {
                             cold |= 1u << j;
                         }
@@ -300,7 +312,7 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
             cmx = warp_max(Pl + tmx); cmn = warp_min(Pl + tmn);
             csum = shfl_ll(incl, 31);
         }
-        if (lane == 0) { S.csum[c] = csum; S.cmx[c] = cmx; S.cmn[c] = cmn; }
+        if (lane == 0) { S.Pc[c] = csum; S.ax[c] = cmx; S.an[c] = cmn; }   // composed in place below
         __syncwarp();
         mbar_arrive(&s.empty[st]);                        // box consumed
         PROF_MARK(2)
@@ -309,7 +321,7 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
         old = __shfl_sync(kFull, old, 0);
         if (old == kChunks - 1) {
             // last chunk of the unit: compose the 32 chunk summaries (lane = chunk) and publish
-            const long long cs = S.csum[lane], cx = S.cmx[lane], cn = S.cmn[lane];
+            const long long cs = S.Pc[lane], cx = S.ax[lane], cn = S.an[lane];
             long long ci = cs;
             #pragma unroll
             for (int d = 1; d < 32; d <<= 1) { long long o = shfl_up_ll(ci, d); if (lane >= d) ci += o; }
@@ -881,7 +893,7 @@ replay_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0 && (smem_u32(smem_raw) & 1023u) != 0) __trap();     // the 128-B swizzle needs 1024-B alignment
 
-    for (int x = tid; x < 2 * kHot; x += kCtaThreads) { s.cnt[x] = 0; s.blo[x] = 0; s.bhi[x] = 0; }
+    for (int x = tid; x < 4 * kHot; x += kCtaThreads) { s.cnt[x] = 0; s.blo[x] = 0; }
     for (int x = tid; x < kSlots; x += kCtaThreads) s.slot[x].done = 0;
     if (tid == 0) {
         for (int i = 0; i < kStages; ++i) { mbar_init(&s.full[i], 1); mbar_init(&s.empty[i], 8 * 32); }
@@ -900,13 +912,13 @@ replay_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     if (warp < kComputeWarps) {
         compute_role(p, s, stage, warp / 8, warp % 8, lane);
         named_bar(1, kComputeWarps * 32);                            // all compute warps done
-        for (int x = tid; x < 2 * kHot; x += kComputeWarps * 32) {   // flush Tier-E counters
-            const unsigned c = s.cnt[x];
+        for (int x = tid; x < 2 * kHot; x += kComputeWarps * 32) {   // flush Tier-E counters (allocs, frees)
+            const int kind = x & 1, site = x >> 1;
+            const unsigned c = s.cnt[kind * kHot + site];
             if (c) {
-                const int kind = x & 1, site = x >> 1;
                 unsigned long long* row = p.table + (size_t)site * SCL_NCOL;
                 atomicAdd(&row[SCL_COL_N_MALLOC + kind], (unsigned long long)c);
-                atomicAdd(&row[SCL_COL_MALLOC_BYTES + kind], ((unsigned long long)s.bhi[x] << 32) | s.blo[x]);
+                atomicAdd(&row[SCL_COL_MALLOC_BYTES + kind], (unsigned long long)s.blo[kind * kHot + site]);
             }
         }
     } else if (warp == kProducerWarp) {
