@@ -51,7 +51,8 @@ constexpr int kESlots = 4 * kHot + kComputeWarps * 32;
 constexpr uint32_t kBloOff = kESlots * 4;   // byte distance cnt -> blo
 
 struct __align__(16) Smem {
-    unsigned cnt[kESlots];           // Tier-E per (kind, hot site): event count    (slot kind*kHot + site;
+    unsigned cnt[kESlots];           // Tier-E per (kind, hot site): event count    (slot kind*kHot + site, or
+                                     //   (kind&1)*kWarm + site for the allocs and frees of n_sites > kHot;
     unsigned blo[kESlots];           //   bytes mod 2^32 (carries: straight to L2)  slots >= 4*kHot: per-lane
                                      //   sinks of the unconditional atomics; copies counted, not reported)
     Slot slot[kSlots];
@@ -150,7 +151,8 @@ __device__ __forceinline__ void wait_prepared(const ReplayParams& p) {
 // read as bits: bit 41 set = copy (no footprint change), else bit 40 = free (kind 3 is rejected
 // by the trace validation; unvalidated, it only widens the Bloom filter, which is re-checked).
 // 32-bit byte-counter carries: one accumulated predicate, the rare wrap re-examined afterwards.
-// kAllHot: every site is in the shared-memory table (n_sites <= kHot), no cold-site bookkeeping.
+// kAllHot: every site is in the shared-memory table (n_sites <= kHot), no cold-site bookkeeping;
+// otherwise the table holds the allocs and frees of the kWarm lowest site ids, the rest go to L2.
 template <bool kAllHot>
 __device__ __forceinline__ void fast_row(const unsigned long long* ptr, const unsigned long long* meta, uint32_t cnt_s,
                                          uint32_t bl_s, uint32_t dslot, unsigned long long* table, int& r32,
@@ -165,14 +167,15 @@ __device__ __forceinline__ void fast_row(const unsigned long long* ptr, const un
         const int d = isfree ? -(int)lo : (int)lo;
         if (af) r32 += d;                                                     // a1: signed size
         mx32 = max(mx32, r32); mn32 = min(mn32, r32);
-        const uint32_t off = ((hi >> 9) & (uint32_t)(4 * kHot - 4)) | ((hi << 4) & (uint32_t)(3 * 4 * kHot));  // (kind*kHot + site)*4
         uint32_t a;
         if (kAllHot) {                                                        // site < kHot
-            a = cnt_s + off; add[j] = lo;
+            const uint32_t off = ((hi >> 9) & (uint32_t)(4 * kHot - 4)) | ((hi << 4) & (uint32_t)(3 * 4 * kHot));
+            a = cnt_s + off; add[j] = lo;                                     // (kind*kHot + site)*4
         } else {
-            const bool h = (hi >> 11) < (unsigned)kHot;
+            const bool h = af && (hi >> 11) < (unsigned)kWarm;
             cold |= (af && !h ? 1u : 0u) << j;
-            a = cnt_s + (h ? off : dslot); add[j] = h ? lo : 0u;
+            const uint32_t offw = ((hi >> 9) & (uint32_t)(4 * kWarm - 4)) | ((hi << 5) & (uint32_t)(4 * kWarm));
+            a = cnt_s + (h ? offw : dslot); add[j] = h ? lo : 0u;                // ((kind&1)*kWarm + site)*4
         }
         red_add(a, 1u);                                                       // a5 Tier E
         old[j] = atom_add(a + kBloOff, add[j]);
@@ -267,8 +270,8 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
                     if (af) {
                         tmx = llmax(tmx, run); tmn = llmin(tmn, run);
                         const unsigned site = ev_site(meta[j]);
-                        if (site < (unsigned)kHot && size < (1ull << 32)) {
-                            const int x = (int)kind * kHot + (int)site;
+                        if (site < (unsigned)(all_hot ? kHot : kWarm) && size < (1ull << 32)) {
+                            const int x = (int)kind * (all_hot ? kHot : kWarm) + (int)site;
                             atomicAdd(&s.cnt[x], 1u);
                             const unsigned old = atomicAdd(&s.blo[x], (unsigned)size);
                             if (old + (unsigned)size < old)
@@ -912,13 +915,14 @@ replay_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     if (warp < kComputeWarps) {
         compute_role(p, s, stage, warp / 8, warp % 8, lane);
         named_bar(1, kComputeWarps * 32);                            // all compute warps done
-        for (int x = tid; x < 2 * kHot; x += kComputeWarps * 32) {   // flush Tier-E counters (allocs, frees)
-            const int kind = x & 1, site = x >> 1;
-            const unsigned c = s.cnt[kind * kHot + site];
+        const int cap = p.n_sites <= (unsigned)kHot ? kHot : kWarm;
+        for (int x = tid; x < 2 * cap; x += kComputeWarps * 32) {    // flush Tier-E counters (allocs, frees)
+            const int kind = x / cap, site = x % cap;
+            const unsigned c = s.cnt[x];
             if (c) {
                 unsigned long long* row = p.table + (size_t)site * SCL_NCOL;
                 atomicAdd(&row[SCL_COL_N_MALLOC + kind], (unsigned long long)c);
-                atomicAdd(&row[SCL_COL_MALLOC_BYTES + kind], (unsigned long long)s.blo[kind * kHot + site]);
+                atomicAdd(&row[SCL_COL_MALLOC_BYTES + kind], (unsigned long long)s.blo[x]);
             }
         }
     } else if (warp == kProducerWarp) {

@@ -35,7 +35,8 @@ constexpr int kCtaThreads = (kComputeWarps + 1 + kLBWarps) * 32;
 constexpr int kStages = 4;                    // TMA ring depth
 constexpr int kSlots = 6;                     // compute -> look-back unit summary ring (smem)
 constexpr int kBloomWords = 64;               // 2048-bit Bloom filter of freed pointers per chunk
-constexpr int kHot = 1024;                    // sites with shared-memory Tier-E counters
+constexpr int kHot = 1024;                    // sites with shared-memory Tier-E counters (all 4 kinds)
+constexpr int kWarm = 2 * kHot;               // the same storage when n_sites > kHot: allocs and frees only
 constexpr long long kNeg = -(1ll << 62);      // "no event" sentinels for max / min
 constexpr long long kPos = (1ll << 62);
 constexpr unsigned long long kNoEp = ~0ull;
