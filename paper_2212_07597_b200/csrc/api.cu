@@ -222,7 +222,7 @@ static scl_status upload(scl_traces* tr, const scl_event* src, bool src_dev, std
             return fail(SCL_ENOMEM, "per-trace buffers");
         tr->cap_tr = nt1;
     }
-    if (!tr->d_err && (!grow(tr->d_err, 1) || !grow(tr->d_ticket, 4))) return fail(SCL_ENOMEM, "counters");
+    if (!tr->d_err && (!grow(tr->d_err, 1) || !grow(tr->d_ticket, 8))) return fail(SCL_ENOMEM, "counters");
     if (n > 0) CU(cudaMemcpyAsync(tr->d_ev, src, n * sizeof(scl_event), src_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
     if (rows_alloc * 8 > n) CU(cudaMemsetAsync(tr->d_ev + n, 0, (rows_alloc * 8 - n) * sizeof(scl_event), st));
     CU(cudaMemcpyAsync(tr->d_off, h_off.data(), h_off.size() * 8, cudaMemcpyHostToDevice, st));

@@ -86,7 +86,7 @@ struct PrepParams {
     unsigned long long* table; size_t table_words;
     unsigned long long* summ; size_t summ_words;
     unsigned long long* run; size_t run_words;
-    unsigned int* ticket;             // [4]
+    unsigned int* ticket;             // [8] (the replay kernel's counters; [0..6] zeroed here)
     unsigned long long* sbase;        // [n_traces]
     const unsigned long long* off;    // [n_traces + 1]
     const unsigned long long* sabs;   // [n_traces]
