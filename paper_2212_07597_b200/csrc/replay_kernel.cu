@@ -139,7 +139,8 @@ __device__ void prepare_run(const ReplayParams& rp, unsigned long long* scratch)
 }
 
 __device__ __forceinline__ void wait_prepared(const ReplayParams& p) {
-    while (ld_acquire(&p.ticket[7]) != p.epoch) __nanosleep(32);
+    while (ld_relaxed(&p.ticket[7]) != p.epoch) __nanosleep(32);
+    fence_acquire();
 }
 
 // ============================================================================ compute warps
@@ -545,10 +546,11 @@ __device__ void run_trace(const ReplayParams& p, RState& x, unsigned t, unsigned
     while (x.next < nseg) {
         // ready prefix of the next 32 units (lane i <-> unit next+i)
         const unsigned ui = x.next + (unsigned)lane;
-        const bool rdy = ui < nseg && ld_acquire(&p.uready[base + ui]) == ep_tag;
+        const bool rdy = ui < nseg && ld_relaxed(&p.uready[base + ui]) == ep_tag;
         const unsigned nr = ~__ballot_sync(kFull, rdy);
         const int m = nr ? __ffs(nr) - 1 : 32;               // units next .. next+m-1 are ready
         if (m == 0) return;
+        fence_acquire();
         RPROF_ADD(1, 1) RPROF_ADD(2, m)
 #ifdef SCL_PROFILE
         if (lane < m) PROF_UNIT_T(base + x.next + lane, 2)
@@ -673,9 +675,10 @@ __device__ void runner_role(const ReplayParams& p, unsigned ri, int lane)
     for (;;) {
         const bool alive = (unsigned)lane < cnt && my_next < my_nseg;
         if (!__any_sync(kFull, alive)) break;
-        const bool ready = alive && ld_acquire(&p.uready[my_base + my_next]) == ep_tag;
+        const bool ready = alive && ld_relaxed(&p.uready[my_base + my_next]) == ep_tag;
         unsigned rm = __ballot_sync(kFull, ready);
         if (!rm) { PROF_MARK(0) __nanosleep(64); continue; }
+        fence_acquire();
         PROF_MARK(0)
         while (rm) {
             const int i = __ffs(rm) - 1;
@@ -794,7 +797,8 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr) {
     if (threadIdx.x == 0) {
         __threadfence();
         atomicAdd(ctr, 1u);
-        while (ld_acquire(ctr) < gridDim.x) __nanosleep(32);
+        while (ld_relaxed(ctr) < gridDim.x) __nanosleep(32);
+        fence_acquire();
     }
     __syncthreads();
 }
