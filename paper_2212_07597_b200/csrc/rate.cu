@@ -20,10 +20,18 @@
 
 namespace scl {
 
-// meta word of event g through L1 (a row's 8 events share 4 sectors: the second access of each
-// sector hits L1; the streaming hint would re-fetch it from L2)
-__device__ __forceinline__ unsigned long long meta_l1(const scl_event* ev, long long g) {
-    return __ldca(reinterpret_cast<const unsigned long long*>(ev + g) + 1);
+// The 8 meta words of row `row` (128 B, 32-B aligned) with four 256-bit loads: a lane reading its own
+// row issues 4 requests instead of 8 (measured -11 % on the rate sampler).  The caller guarantees
+// the row overlaps its trace (the device copy is padded to whole rows).
+__device__ __forceinline__ void row_meta(const scl_event* ev, long long row, unsigned long long* meta) {
+    const unsigned long long* q = reinterpret_cast<const unsigned long long*>(ev + row * kEpt);
+    #pragma unroll
+    for (int i = 0; i < kEpt / 2; ++i) {
+        unsigned long long m0, m1;                             // (the pointers are not needed)
+        asm volatile("{\n\t.reg .b64 p0, p1;\n\tld.global.nc.v4.u64 {p0,%0,p1,%1}, [%2];\n}"
+                     : "=l"(m0), "=l"(m1) : "l"(q + 4 * i));
+        meta[2 * i] = m0; meta[2 * i + 1] = m1;
+    }
 }
 
 // ln x, x > 0: x = m 2^e, m in [sqrt(1/2), sqrt(2)), ln m = 2 atanh((m-1)/(m+1)) by its series
@@ -75,11 +83,14 @@ __global__ void __launch_bounds__(1024) unit_sums_kernel(const scl_event* ev, co
     const TicketInfo ti = tk[blockIdx.x];
     const long long row = (ti.off_t >> 3) + (long long)(ti.kraw & 0x7fffffffu) * kUnitRows + threadIdx.x;
     unsigned long long s[kUCols] = {0, 0, 0, 0};            // alloc, free, copy, managed alloc
+    unsigned long long mr[kEpt];
+    const long long r0 = row * kEpt - ti.off_t;
+    if (r0 + kEpt > 0 && r0 < ti.n_t) row_meta(ev, row, mr);
     #pragma unroll
     for (int j = 0; j < kEpt; ++j) {
-        const long long g = row * kEpt + j, ie = g - ti.off_t;
+        const long long ie = r0 + j;
         if (ie >= 0 && ie < ti.n_t) {
-            const unsigned long long m = meta_l1(ev, g), z = ev_size(m);
+            const unsigned long long m = mr[j], z = ev_size(m);
             const unsigned kind = ev_kind(m);
             s[0] += kind == 0 ? z : 0ull; s[1] += kind == 1 ? z : 0ull; s[2] += kind == 2 ? z : 0ull;
             s[3] += kind == 0 && ((m >> 42) & 1ull) ? z : 0ull;
@@ -167,11 +178,14 @@ __global__ void __launch_bounds__(1024) rate_place_kernel(const RateParams p)
     const unsigned t = ti.t, lane = threadIdx.x & 31, wrp = threadIdx.x >> 5;
     const long long row = (ti.off_t >> 3) + (long long)(ti.kraw & 0x7fffffffu) * kUnitRows + threadIdx.x;
     unsigned long long sz[kEpt], meta[kEpt], rs = 0;
+    const long long r0 = row * kEpt - ti.off_t;               // trace index of the row's first event
+    if (r0 + kEpt > 0 && r0 < ti.n_t) row_meta(p.ev, row, meta);
     #pragma unroll
     for (int j = 0; j < kEpt; ++j) {
-        const long long g = row * kEpt + j, ie = g - ti.off_t;
-        meta[j] = 0; sz[j] = 0;
-        if (ie >= 0 && ie < ti.n_t) { meta[j] = meta_l1(p.ev, g); sz[j] = counted(meta[j], p.kinds); }
+        const long long ie = r0 + j;
+        const bool in = ie >= 0 && ie < ti.n_t;
+        if (!in) meta[j] = 0;
+        sz[j] = in ? counted(meta[j], p.kinds) : 0ull;
         rs += sz[j];
     }
     // block exclusive scan of the row sums
@@ -237,12 +251,14 @@ __global__ void __launch_bounds__(1024) domain_prefix_kernel(const DomainParams 
     if (k0 == k1) return;
     // row sums of allocated / managed allocated bytes, block exclusive scan
     const long long row = row_base + threadIdx.x;
-    unsigned long long ra = 0, rm = 0;
+    unsigned long long ra = 0, rm = 0, mr[kEpt];
+    const long long r0 = row * kEpt - ti.off_t;
+    if (r0 + kEpt > 0 && r0 < ti.n_t) row_meta(p.ev, row, mr);
     #pragma unroll
     for (int j = 0; j < kEpt; ++j) {
-        const long long g = row * kEpt + j, ie = g - ti.off_t;
+        const long long ie = r0 + j;
         if (ie >= 0 && ie < ti.n_t) {
-            const unsigned long long m = meta_l1(p.ev, g);
+            const unsigned long long m = mr[j];
             if (ev_kind(m) == 0) { ra += ev_size(m); rm += ((m >> 42) & 1ull) ? ev_size(m) : 0ull; }
         }
     }
@@ -301,12 +317,15 @@ __global__ void __launch_bounds__(1024) recon_kernel(const DomainParams p, unsig
     const long long row = (ti.off_t >> 3) + (long long)(ti.kraw & 0x7fffffffu) * kUnitRows + threadIdx.x;
     long long d[kEpt], rs = 0;
     unsigned live = 0;
+    unsigned long long mr[kEpt];
+    const long long r0 = row * kEpt - ti.off_t;
+    if (r0 + kEpt > 0 && r0 < ti.n_t) row_meta(p.ev, row, mr);
     #pragma unroll
     for (int j = 0; j < kEpt; ++j) {
-        const long long g = row * kEpt + j, ie = g - ti.off_t;
+        const long long ie = r0 + j;
         d[j] = 0;
         if (ie >= 0 && ie < ti.n_t) {
-            const unsigned long long m = meta_l1(p.ev, g);
+            const unsigned long long m = mr[j];
             const unsigned kind = ev_kind(m);
             d[j] = kind == 0 ? (long long)ev_size(m) : (kind == 1 ? -(long long)ev_size(m) : 0);
             live |= 1u << j;
