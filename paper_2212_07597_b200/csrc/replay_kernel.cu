@@ -835,7 +835,8 @@ __global__ void __launch_bounds__(256, 3) post_kernel(const __grid_constant__ Re
             reclaim_unit(p, wid + (k0 + (unsigned)i) * nw, x, lane);
         }
     }
-    for (unsigned t = wid; t < p.n_traces; t += nw) samples_trace(p, t, lane);
+    // per-trace reduce on the last warps (they settle one unit fewer than the first ones)
+    for (unsigned t = nw - 1 - wid; t < p.n_traces; t += nw) samples_trace(p, t, lane);
     POST_T(1, atomicMax)
     grid_barrier(&p.ticket[1]);
     POST_T(2, atomicMax)
