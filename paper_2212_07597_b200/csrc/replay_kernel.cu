@@ -419,6 +419,86 @@ __device__ __forceinline__ void store_rstate(RunState* rs, const RState& x, int 
 // 32c+l, 8 events); one combined warp scan gives each lane the footprint and the running
 // high-water mark before its first event, and the lane holding the first exit of the band
 // walks its own events sequentially (successive samples included), then broadcasts the state.
+// One candidate chunk of resolve_unit in 32-bit arithmetic: every prefix of the chunk (relative to
+// its start Fc) is within +-2^29, so event sizes, lane sums and their combined scan fit in int32.  A
+// lane's running max / min include its start value (the F of an earlier event, inside the band and
+// <= Mc), so no sentinel is needed; the band limits are taken relative to Fc and clamped to int32.
+__device__ __forceinline__ int clamp_i32(long long v) {
+    return (int)llmax(llmin(v, (long long)INT_MAX), (long long)INT_MIN);
+}
+__device__ __forceinline__ void resolve_chunk32(const ReplayParams& p, const unsigned long long* rp,
+                                             const unsigned long long* rm, long long e0, long long n_t, long long Fc,
+                                             long long Mc, long long& B, unsigned long long& n, unsigned long long& nep,
+                                             unsigned long long& ep1, unsigned long long& eptr, long long& Ms,
+                                             unsigned long long sb, int lane)
+{
+    int fe[kEpt], run = 0, lmx = 0, lmn = 0;                 // relative to the lane's start
+    unsigned live = 0;
+    #pragma unroll
+    for (int jj = 0; jj < kEpt; ++jj) {
+        const long long ie = e0 + jj;
+        const unsigned kind = ev_kind(rm[jj]);
+        const bool af = ie >= 0 && ie < n_t && kind < 2;
+        const int sz = (int)(unsigned)rm[jj];                 // < 2^30 for a counted event here
+        run += af ? (kind == 0 ? sz : -sz) : 0;
+        fe[jj] = run;
+        lmx = max(lmx, run); lmn = min(lmn, run);
+        live |= (af ? 1u : 0u) << jj;
+    }
+    int ssum = run, smax = lmx;                               // combined inclusive scan, relative to Fc
+    #pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {
+        const int os = __shfl_up_sync(kFull, ssum, dd), om = __shfl_up_sync(kFull, smax, dd);
+        if (lane >= dd) { smax = max(om, os + smax); ssum = os + ssum; }
+    }
+    const int xl = ssum - run;                                // F before the lane, relative to Fc
+    const int mprev = __shfl_up_sync(kFull, smax, 1);
+    const long long Ml = lane == 0 ? Mc : llmax(Mc, Fc + mprev);   // max F before the lane's events
+    int cur = 0;
+    for (;;) {
+        const int hi = clamp_i32(B + p.T - Fc), lo = clamp_i32(B - p.T - Fc);
+        const unsigned cm = __ballot_sync(kFull, lane >= cur && (xl + lmx >= hi || xl + lmn <= lo));
+        if (!cm) break;
+        const int l0 = __ffs(cm) - 1;
+        if (lane == l0) {                                     // this lane's exits, in order
+            unsigned from = 0;
+            int h2 = hi, l2 = lo;
+            for (;;) {
+                unsigned ex = 0;
+                #pragma unroll
+                for (int jj = 0; jj < kEpt; ++jj) { const int v = xl + fe[jj]; ex |= (v >= h2 || v <= l2 ? 1u : 0u) << jj; }
+                ex &= live & ~((1u << from) - 1u);
+                if (!ex) break;
+                const int js = __ffs(ex) - 1;
+                int vf = 0, mp = INT_MIN;
+                unsigned long long ms = 0, ps = 0;
+                #pragma unroll
+                for (int jj = 0; jj < kEpt; ++jj) {
+                    if (jj < js) mp = max(mp, xl + fe[jj]);
+                    if (jj == js) { vf = xl + fe[jj]; ms = rm[jj]; ps = rp[jj]; }
+                }
+                const long long F = Fc + vf, Mp = mp == INT_MIN ? Ml : llmax(Ml, Fc + mp);
+                const long long net = F - B;                  // the |A - F| counter
+                const bool growth = net > 0;
+                const bool nm = growth && F > (p.hwm_sample ? Ms : Mp);   // new high-water mark (Q3, Q4)
+                const unsigned long long slot_s = sb + n;
+                scl_sample smp;
+                smp.idx = (unsigned long long)(e0 + js); smp.net = net; smp.footprint = F;
+                smp.site = ev_site(ms); smp.kind = growth ? 0 : 1; smp.new_max = nm ? 1 : 0; smp.pad = 0;
+                p.samples[slot_s] = smp;
+                if (nm) { p.ep_flag[slot_s] = 0u; ep1 = slot_s + 1; eptr = ps; ++nep; }   // settled by the reclaim pass
+                ++n; B = F; Ms = llmax(Ms, F);            // "resets the counters"
+                h2 = clamp_i32(B + p.T - Fc); l2 = clamp_i32(B - p.T - Fc);
+                from = (unsigned)js + 1;
+            }
+        }
+        B = shfl_ll(B, l0); n = __shfl_sync(kFull, n, l0);
+        nep = __shfl_sync(kFull, nep, l0); ep1 = __shfl_sync(kFull, ep1, l0); eptr = __shfl_sync(kFull, eptr, l0);
+        Ms = shfl_ll(Ms, l0);
+        cur = l0 + 1;
+    }
+}
+
 __device__ void resolve_unit(const ReplayParams& p, const Slot& S, RState& x, unsigned long long sb, int lane)
 {
     const SegInfo inf = S.info;
@@ -434,6 +514,9 @@ __device__ void resolve_unit(const ReplayParams& p, const Slot& S, RState& x, un
     const long long t_b = clock64(); RPROF_ADD(8, t_b - t_a)          /* record wait */
     long long t_rows = 0, t_scan = 0, t_walk = 0;
 #endif
+    // chunks whose footprint stays within +-2^29 of their start: resolved in 32-bit arithmetic
+    const unsigned small = __ballot_sync(kFull, sax - sPc < (1ll << 29) && sax - sPc > -(1ll << 29) &&
+                                                san - sPc < (1ll << 29) && san - sPc > -(1ll << 29));
     int cnext = 0;                                           // chunks < cnext are resolved
     for (;;) {
         const unsigned ccm = __ballot_sync(kFull, lane >= cnext && (hiL >= B + p.T || loL <= B - p.T));
@@ -455,6 +538,11 @@ __device__ void resolve_unit(const ReplayParams& p, const Slot& S, RState& x, un
         const long long t_r = clock64(); t_rows += t_r - t_l;
 #endif
         const long long e0 = row * kEpt - inf.off_t;           // trace index of the lane's first event
+        if ((small >> c) & 1u) {
+            resolve_chunk32(p, rp, rm, e0, inf.n_t, Fc, Mc, B, n, nep, ep1, eptr, Ms, sb, lane);
+            cnext = c + 1;
+            continue;
+        }
         long long fe[kEpt], run = 0, lmx = kNeg, lmn = kPos;   // fe[jj]: F after event jj - F before the lane
         unsigned live = 0;                                      // events that move F (alloc/free in the trace)
         #pragma unroll
