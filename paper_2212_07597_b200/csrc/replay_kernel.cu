@@ -434,11 +434,13 @@ __device__ __forceinline__ void resolve_chunk32(const ReplayParams& p, const uns
 {
     int fe[kEpt], run = 0, lmx = 0, lmn = 0;                 // relative to the lane's start
     unsigned live = 0;
+    // events of the row inside the trace: [jlo, jhi)
+    const int jlo = (int)llmin(llmax(-e0, 0ll), (long long)kEpt), jhi = (int)llmax(llmin(n_t - e0, (long long)kEpt), 0ll);
+    const unsigned inr = ((1u << jhi) - 1u) & ~((1u << jlo) - 1u);
     #pragma unroll
     for (int jj = 0; jj < kEpt; ++jj) {
-        const long long ie = e0 + jj;
         const unsigned kind = ev_kind(rm[jj]);
-        const bool af = ie >= 0 && ie < n_t && kind < 2;
+        const bool af = ((inr >> jj) & 1u) && kind < 2;
         const int sz = (int)(unsigned)rm[jj];                 // < 2^30 for a counted event here
         run += af ? (kind == 0 ? sz : -sz) : 0;
         fe[jj] = run;
@@ -517,6 +519,7 @@ __device__ void resolve_unit(const ReplayParams& p, const Slot& S, RState& x, un
     // chunks whose footprint stays within +-2^29 of their start: resolved in 32-bit arithmetic
     const unsigned small = __ballot_sync(kFull, sax - sPc < (1ll << 29) && sax - sPc > -(1ll << 29) &&
                                                 san - sPc < (1ll << 29) && san - sPc > -(1ll << 29));
+    const bool ufit = __all_sync(kFull, sax < (1ll << 31) && sax > -(1ll << 31));   // chunk maxima fit int32
     int cnext = 0;                                           // chunks < cnext are resolved
     for (;;) {
         const unsigned ccm = __ballot_sync(kFull, lane >= cnext && (hiL >= B + p.T || loL <= B - p.T));
@@ -531,7 +534,9 @@ __device__ void resolve_unit(const ReplayParams& p, const Slot& S, RState& x, un
         load_row_global(p.ev, row, rp, rm);
         // while the rows are in flight: F and the high-water mark before chunk c
         const long long Fc = F0 + shfl_ll(sPc, c);
-        const long long Mc = llmax(M0, warp_max(lane < c ? hiL : kNeg));
+        long long Mc;                                           // max F before chunk c
+        if (ufit) { const int m = __reduce_max_sync(kFull, lane < c ? (int)sax : INT_MIN); Mc = c ? llmax(M0, F0 + m) : M0; }
+        else      Mc = llmax(M0, warp_max(lane < c ? hiL : kNeg));
 #ifdef SCL_PROFILE
         #pragma unroll
         for (int jj = 0; jj < kEpt; ++jj) { long long v = (long long)rm[jj]; PROF_TOUCH(v) rm[jj] = (unsigned long long)v; }
@@ -651,11 +656,24 @@ __device__ void run_trace(const ReplayParams& p, RState& x, unsigned t, unsigned
         if (lane < m) { us = R[lane].usum; ux = R[lane].umx; un = R[lane].umn; }
         // footprint and high-water mark do not depend on the samples: one combined scan gives F and
         // M at the start of every unit of the batch ((s1,m1).(s2,m2) = (s1+s2, max(m1, s1+m2)))
-        long long ps = us, pm = ux;                           // inclusive, relative to the batch start
-        #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const long long os = shfl_up_ll(ps, d), om = shfl_up_ll(pm, d);
-            if (lane >= d) { pm = llmax(om, os + pm); ps = os + ps; }
+        long long ps, pm;                                     // inclusive, relative to the batch start
+        const bool bfit = __all_sync(kFull, lane >= m || (us < (1ll << 25) && us > -(1ll << 25) &&
+                                                            ux < (1ll << 25) && un > -(1ll << 25)));
+        if (bfit) {                                           // 32-bit scan; a unit's max includes its start
+            int ps32 = lane < m ? (int)us : 0, pm32 = lane < m ? (int)llmax(ux, 0ll) : 0;
+            #pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int os = __shfl_up_sync(kFull, ps32, d), om = __shfl_up_sync(kFull, pm32, d);
+                if (lane >= d) { pm32 = max(om, os + pm32); ps32 = os + ps32; }
+            }
+            ps = ps32; pm = pm32;
+        } else {
+            ps = us; pm = ux;
+            #pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const long long os = shfl_up_ll(ps, d), om = shfl_up_ll(pm, d);
+                if (lane >= d) { pm = llmax(om, os + pm); ps = os + ps; }
+            }
         }
         const long long Pe = ps - us;                         // F at the unit start - F at the batch start
         long long Me = shfl_up_ll(pm, 1);                      // max F (rel.) over the units before
