@@ -43,7 +43,7 @@ struct scl_traces {
     size_t cap_tr = 0;
     TicketInfo* d_tk = nullptr;
     void* d_urec = nullptr;                    // per unit: published summary record
-    unsigned int* d_uready = nullptr;          // per unit: run epoch when published
+    unsigned long long* d_uagg = nullptr;      // per unit: tagged aggregate words (published flag)
     UnitEntry* d_uent = nullptr;               // per unit: state entering it (runner -> reclaim pass)
     size_t cap_segs = 0;
     unsigned long long* d_err = nullptr;       // first invalid event (load check)
@@ -259,10 +259,10 @@ static scl_status upload(scl_traces* tr, const scl_event* src, bool src_dev, std
     if (nn > tr->cap_segs) {
         tr->cap_segs = 0;
         cudaFree(tr->d_urec); tr->d_urec = nullptr;
-        if (!grow(tr->d_tk, nn) || !grow(tr->d_uready, nn) || !grow(tr->d_uent, nn) ||
+        if (!grow(tr->d_tk, nn) || !grow(tr->d_uagg, nn * 4) || !grow(tr->d_uent, nn) ||
             cudaMalloc(&tr->d_urec, nn * replay_urec_bytes()) != cudaSuccess)
             { cudaGetLastError(); return fail(SCL_ENOMEM, "unit plan"); }
-        CU(cudaMemsetAsync(tr->d_uready, 0, nn * 4, st));      // epoch tags start at 1
+        CU(cudaMemsetAsync(tr->d_uagg, 0, nn * 32, st));       // epoch tags start at 1
         tr->cap_segs = nn;
     }
     if (total) CU(cudaMemcpyAsync(tr->d_tk, tk.data(), total * sizeof(TicketInfo), cudaMemcpyHostToDevice, st));
@@ -353,7 +353,7 @@ extern "C" scl_status scl_trace_reload(scl_traces* tr, const scl_event* events, 
 
 extern "C" void scl_traces_free(scl_traces* t) {
     if (!t) return;
-    cudaFree(t->d_ev); cudaFree(t->d_off); cudaFree(t->d_sabs); cudaFree(t->d_tk); cudaFree(t->d_urec); cudaFree(t->d_uready);
+    cudaFree(t->d_ev); cudaFree(t->d_off); cudaFree(t->d_sabs); cudaFree(t->d_tk); cudaFree(t->d_urec); cudaFree(t->d_uagg);
     cudaFree(t->d_tr_nseg); cudaFree(t->d_tr_base); cudaFree(t->d_run); cudaFree(t->d_uent); cudaFree(t->d_ticket);
     cudaFree(t->d_err); cudaFree(t->d_usum); cudaFree(t->d_ustart); cudaFree(t->d_ttot);
     delete t;
@@ -476,7 +476,10 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
     }
 
     // epoch-tagged look-back flags: no per-run clear of the state array
-    if (tr->epoch >= (1u << 30)) { CU(cudaMemsetAsync(tr->d_uready, 0, tr->cap_segs * 4, st)); tr->epoch = 0; }
+    // (the aggregate words carry the low 16 bits: cleared, and tag 0 skipped, once per 2^16 runs)
+    if (tr->epoch >= (1u << 30)) { tr->epoch = 0; CU(cudaMemsetAsync(tr->d_ticket, 0, 8 * 4, st)); }   // no stale "prepared"
+    if (((tr->epoch + 1) & 0xffffu) == 0) { CU(cudaMemsetAsync(tr->d_uagg, 0, tr->cap_segs * 32, st)); tr->epoch += 1; }
+    if (tr->epoch == 0) CU(cudaMemsetAsync(tr->d_uagg, 0, tr->cap_segs * 32, st));
     tr->epoch += 1;
 
     const bool tm = o.timing != 0;                 // phase / kernel events only when asked for
@@ -485,7 +488,7 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
 
     ReplayParams p{};
     p.ev = tr->d_ev; p.off = tr->d_off; p.tk = tr->d_tk;
-    p.urec = tr->d_urec; p.uready = tr->d_uready; p.run = tr->d_run; p.tr_nseg = tr->d_tr_nseg; p.tr_base = tr->d_tr_base;
+    p.urec = tr->d_urec; p.uagg = tr->d_uagg; p.run = tr->d_run; p.tr_nseg = tr->d_tr_nseg; p.tr_base = tr->d_tr_base;
     p.ticket = tr->d_ticket; p.n_segs = tr->n_segs; p.epoch = tr->epoch;
     p.n_runners = (unsigned)r->grid * kEmbeddedRunners;    // 2 runner warps in every CTA
     p.n_sites = tr->n_sites; p.n_traces = NT; p.T = (long long)threshold; p.hwm_sample = o.hwm_mode == SCL_HWM_SAMPLE;

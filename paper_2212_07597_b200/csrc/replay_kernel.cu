@@ -638,8 +638,19 @@ __device__ void run_trace(const ReplayParams& p, RState& x, unsigned t, unsigned
     RPROF_ADD(0, 1)
     while (x.next < nseg) {
         // ready prefix of the next 32 units (lane i <-> unit next+i)
+        // the unit's tagged aggregate words are its ready flag: one load gives both
         const unsigned ui = x.next + (unsigned)lane;
-        const bool rdy = ui < nseg && ld_relaxed(&p.uready[base + ui]) == ep_tag;
+        long long us = 0, ux = kNeg, un = kPos;
+        bool rdy = false;
+        if (ui < nseg) {
+            const unsigned long long* w = p.uagg + (size_t)(base + ui) * 4;
+            unsigned long long w0, w1, w2;
+            ld_relaxed_v2(w, w0, w1);
+            w2 = ld_relaxed_u64(w + 2);
+            const unsigned long long tag = ep_tag & 0xffffu;
+            rdy = (w0 & 0xffffu) == tag && (w1 & 0xffffu) == tag && (w2 & 0xffffu) == tag;
+            us = (long long)w0 >> 16; ux = (long long)w1 >> 16; un = (long long)w2 >> 16;
+        }
         const unsigned nr = ~__ballot_sync(kFull, rdy);
         const int m = nr ? __ffs(nr) - 1 : 32;               // units next .. next+m-1 are ready
         if (m == 0) return;
@@ -652,8 +663,10 @@ __device__ void run_trace(const ReplayParams& p, RState& x, unsigned t, unsigned
 #endif
         const Slot* R = rec + base + x.next;
         UnitEntry* ue = p.uent + base + x.next;
-        long long us = 0, ux = kNeg, un = kPos;
-        if (lane < m) { us = R[lane].usum; ux = R[lane].umx; un = R[lane].umn; }
+        if (lane >= m) { us = 0; ux = kNeg; un = kPos; }
+        if (__any_sync(kFull, lane < m && us == kAggBig)) {   // a value beyond 48 bits: from the records
+            if (lane < m) { us = R[lane].usum; ux = R[lane].umx; un = R[lane].umn; }
+        }
         // footprint and high-water mark do not depend on the samples: one combined scan gives F and
         // M at the start of every unit of the batch ((s1,m1).(s2,m2) = (s1+s2, max(m1, s1+m2)))
         long long ps, pm;                                     // inclusive, relative to the batch start
@@ -737,7 +750,10 @@ __device__ void publisher_role(const ReplayParams& p, Smem& s, int lane)
             continue;
         }
         __threadfence_block();
-        const unsigned uq = ((fm >> lane) & 1u) ? ((volatile unsigned*)&s.slot[lane].info.slot)[0] : 0u;
+        const bool mine = (fm >> lane) & 1u;                 // lane q <-> slot q: its unit id and aggregate
+        const unsigned uq = mine ? ((volatile unsigned*)&s.slot[lane].info.slot)[0] : 0u;
+        long long a3[3] = {0, 0, 0};
+        if (mine) { a3[0] = s.slot[lane].usum; a3[1] = s.slot[lane].umx; a3[2] = s.slot[lane].umn; }
         for (unsigned m = fm; m; m &= m - 1) {
             const int q = __ffs(m) - 1;
             Slot& S = s.slot[q];
@@ -750,15 +766,17 @@ __device__ void publisher_role(const ReplayParams& p, Smem& s, int lane)
                 atomicExch(&s.sstate[q], 0u); mbar_arrive(&s.sempty[q]);
             }
         }
-        unsigned uid[kSlots];
-        #pragma unroll
-        for (int q = 0; q < kSlots; ++q) uid[q] = __shfl_sync(kFull, uq, q);
-        if (lane == 0) {
-            __threadfence();
+        __syncwarp();
+        __threadfence();                                     // the records before their aggregate words
+        if (mine) {
+            const unsigned long long tag = ep_tag & 0xffffu;
+            const bool fit = a3[0] > kAggBig && a3[0] < -kAggBig && a3[1] > kAggBig && a3[1] < -kAggBig &&
+                             a3[2] > kAggBig && a3[2] < -kAggBig;
+            unsigned long long* w = p.uagg + (size_t)uq * 4;
             #pragma unroll
-            for (int q = 0; q < kSlots; ++q) if ((fm >> q) & 1u) st_relaxed(&p.uready[uid[q]], ep_tag);
-            atomicAdd(&s.n_done, (unsigned)__popc(fm));
+            for (int i = 0; i < 3; ++i) st_relaxed_u64(w + i, ((unsigned long long)(fit ? a3[i] : kAggBig) << 16) | tag);
         }
+        if (lane == 0) atomicAdd(&s.n_done, (unsigned)__popc(fm));
         __syncwarp();
         PROF_MARK(1)
     }
@@ -781,7 +799,7 @@ __device__ void runner_role(const ReplayParams& p, unsigned ri, int lane)
     for (;;) {
         const bool alive = (unsigned)lane < cnt && my_next < my_nseg;
         if (!__any_sync(kFull, alive)) break;
-        const bool ready = alive && ld_relaxed(&p.uready[my_base + my_next]) == ep_tag;
+        const bool ready = alive && (ld_relaxed_u64(p.uagg + (size_t)(my_base + my_next) * 4 + 2) & 0xffffu) == (ep_tag & 0xffffu);
         unsigned rm = __ballot_sync(kFull, ready);
         if (!rm) { PROF_MARK(0) __nanosleep(64); continue; }
         fence_acquire();

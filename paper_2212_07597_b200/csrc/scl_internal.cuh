@@ -41,6 +41,7 @@ constexpr long long kNeg = -(1ll << 62);      // "no event" sentinels for max / 
 constexpr long long kPos = (1ll << 62);
 constexpr unsigned long long kNoEp = ~0ull;
 constexpr unsigned kInvalid = 0xffffffffu;
+constexpr long long kAggBig = -(1ll << 47);   // tagged aggregate word: the value does not fit in 48 bits
 
 // ---- event decoding (include/scl.h) ----------------------------------------
 __host__ __device__ inline uint64_t ev_size(uint64_t meta) { return meta & 0xFFFFFFFFFFull; }
@@ -108,7 +109,8 @@ struct ReplayParams {
     const unsigned long long* off;    // [n_traces+1]
     const TicketInfo* tk;             // [n_segs] in ticket order (unit index, trace)
     void* urec;                       // [n_segs] unit records (summaries published by the look-back warps)
-    unsigned int* uready;             // [n_segs] = epoch when the unit's record is published
+    unsigned long long* uagg;         // [n_segs][4] unit sum, max, min as (value << 16 | epoch tag), published
+                                      // after the unit record (value kAggBig: read it from the record)
     RunState* run;                    // [n_traces] per-trace runner state (zeroed per run)
     UnitEntry* uent;                  // [n_segs] state entering each unit (runner -> reclaim pass)
     const unsigned int* tr_nseg;      // [n_traces] units per trace
