@@ -432,6 +432,11 @@ __device__ __forceinline__ void resolve_chunk32(const ReplayParams& p, const uns
                                              unsigned long long& ep1, unsigned long long& eptr, long long& Ms,
                                              unsigned long long sb, int lane)
 {
+#ifdef SCL_PROFILE
+    const long long t_0 = clock64();
+    { unsigned long long v = rm[0] ^ rm[7]; PROF_TOUCH(v) }
+    const long long t_1 = clock64(); RPROF_ADD(9, t_1 - t_0)
+#endif
     int fe[kEpt], run = 0, lmx = 0, lmn = 0;                 // relative to the lane's start
     unsigned live = 0;
     // events of the row inside the trace: [jlo, jhi)
@@ -456,6 +461,10 @@ __device__ __forceinline__ void resolve_chunk32(const ReplayParams& p, const uns
     const int xl = ssum - run;                                // F before the lane, relative to Fc
     const int mprev = __shfl_up_sync(kFull, smax, 1);
     const long long Ml = lane == 0 ? Mc : llmax(Mc, Fc + mprev);   // max F before the lane's events
+#ifdef SCL_PROFILE
+    { long long v = Ml; PROF_TOUCH(v) }
+    const long long t_2 = clock64(); RPROF_ADD(10, t_2 - t_1)
+#endif
     int cur = 0;
     for (;;) {
         const int hi = clamp_i32(B + p.T - Fc), lo = clamp_i32(B - p.T - Fc);
@@ -499,6 +508,10 @@ __device__ __forceinline__ void resolve_chunk32(const ReplayParams& p, const uns
         Ms = shfl_ll(Ms, l0);
         cur = l0 + 1;
     }
+#ifdef SCL_PROFILE
+    { long long v = B; PROF_TOUCH(v) }
+    RPROF_ADD(12, clock64() - t_2)
+#endif
 }
 
 __device__ void resolve_unit(const ReplayParams& p, const Slot& S, RState& x, unsigned long long sb, int lane)
