@@ -219,7 +219,8 @@ void orc_finalize(const uint64_t* site_table, uint32_t n_sites, int gate_open,
             over = (unsigned __int128)m > (unsigned __int128)21 * f + 18;
         }
         prob[s] = p;
-        rate[s] = ((double)row[ORC_MALLOC_BYTES] / 1048576.0) / ((double)elapsed_ns / 1e9);
+        /* reading Q20: an elapsed time of 0 (every trace empty, so no site has bytes) counts as 1 ns */
+        rate[s] = ((double)row[ORC_MALLOC_BYTES] / 1048576.0) / ((double)(elapsed_ns ? elapsed_ns : 1) / 1e9);
         flag[s] = (uint8_t)(gate_open && over);
     }
 }

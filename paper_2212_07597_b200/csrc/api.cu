@@ -508,6 +508,12 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
 #endif
     const int ks = (int)(r->nrun % kRing);
     if (tm) CU(cudaEventRecord(r->kev[2 * ks], st));
+    if (tr->n_segs == 0) {                     // no event at all: no replay launch, prepare here
+        CU(cudaMemsetAsync(pp.table, 0, pp.table_words * 8, st));
+        CU(cudaMemsetAsync(pp.summ, 0, pp.summ_words * 8, st));
+        CU(cudaMemsetAsync(tr->d_ticket, 0, 7 * 4, st));
+        if (NT) CU(cudaMemsetAsync(r->d_sbase, 0, (size_t)NT * 8, st));
+    }
     CU(launch_replay(&tr->tmap, p, r->grid, st));
     if (tm) { CU(cudaEventRecord(r->kev[2 * ks + 1], st)); r->nrun += 1; }
     // a6 fused into the post pass (its last block) when the run finalizes at once on a small table

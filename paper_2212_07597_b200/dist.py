@@ -67,3 +67,63 @@ def replay_distributed(events, offsets, n_sites: int, T: int, rank: int, world: 
     reduce_table(device_table_tensor(r), group)
     scl_finalize(r, el)
     return tr, r, rng
+
+
+# ---------------------------------------------------------------- resident waves
+# A rank whose shard does not fit in HBM (configs 4/5 at 1/2/4 GPUs) replays it in waves of whole
+# traces: traces are independent (every trace starts from F = 0 with its own sampler and tracker),
+# so a wave needs no carry; the summable tables of the waves add up (integer sums), and a6 runs
+# once on the total.  Per-trace outputs (summaries, samples) are collected per wave.
+
+def plan_waves(offsets, wave_events: int):
+    """Consecutive trace ranges [t0, t1) with at most ``wave_events`` events each (a single trace
+    longer than that is a wave of its own)."""
+    off = np.asarray(offsets, dtype=np.uint64)
+    n = len(off) - 1
+    waves, t0 = [], 0
+    while t0 < n:
+        limit = np.uint64(int(off[t0]) + max(int(wave_events), 1))
+        t1 = int(np.searchsorted(off, limit, side="right")) - 1      # last boundary <= limit
+        t1 = min(max(t1, t0 + 1), n)
+        waves.append((t0, t1))
+        t0 = t1
+    return waves
+
+
+def replay_waves(events, offsets, n_sites: int, T: int, wave_events: int, device: int = 0,
+                 tick_ns: int = 1000, formula: int = 0, rank: int = 0, world: int = 1, group=None,
+                 keep_samples: bool = True):
+    """Replay this rank's shard in resident waves of at most ``wave_events`` events (one device
+    trace buffer, refilled per wave), sum the waves' tables on the device, all-reduce across ranks
+    when world > 1, and run a6 once.  Returns (result of the last wave holding the global table and
+    report, per-trace summaries of the shard, per-trace sample arrays or None, shard trace range)."""
+    import torch
+    from . import (device_table_tensor, scl_finalize, scl_replay_run, scl_samples, scl_trace_load,
+                   scl_trace_reload, scl_trace_summaries)
+    if world > 1:
+        ev, off, rng = shard(events, offsets, rank, world)
+    else:
+        ev, off, rng = events, np.asarray(offsets, dtype=np.uint64), (0, len(offsets) - 1)
+    tr, r, acc = None, None, None
+    summaries, samples = [], [] if keep_samples else None
+    for t0, t1 in plan_waves(off, wave_events):
+        a, b = int(off[t0]), int(off[t1])
+        wev, woff = ev[a:b], (off[t0:t1 + 1] - off[t0]).astype(np.uint64)
+        tr = scl_trace_load(wev, woff, n_sites, device=device) if tr is None else \
+            scl_trace_reload(tr, wev, woff, n_sites)
+        r = scl_replay_run(T, tr, tick_ns=tick_ns, formula=formula, defer_finalize=True, out=r)
+        tab = device_table_tensor(r)
+        acc = tab.clone() if acc is None else acc.add_(tab)
+        summaries.append(scl_trace_summaries(r).copy())
+        if keep_samples:
+            samples.extend(scl_samples(r, t) for t in range(t1 - t0))
+    if r is None:
+        raise ValueError("no traces to replay")
+    device_table_tensor(r).copy_(acc)
+    lens = off[1:] - off[:-1]
+    el = global_elapsed_ns(int(lens.max()) if len(lens) else 0, tick_ns, group, device=f"cuda:{device}") \
+        if world > 1 else (int(lens.max()) if len(lens) else 0) * tick_ns
+    if world > 1:
+        reduce_table(device_table_tensor(r), group)
+    scl_finalize(r, el)
+    return r, np.concatenate(summaries), samples, rng

@@ -80,3 +80,24 @@ def test_gloo_world2_table_reduce_matches_single_process():
     num, den, cnt = (int(x) for x in ref[-3:])
     op = cnt > 0 and 100 * num >= den
     assert (num, den, op) == oracle.gate(full.summaries)
+
+
+def test_plan_waves_cover_in_order_within_limit():
+    """Resident waves: consecutive whole-trace ranges covering every trace once, each within the
+    event budget unless it is a single longer trace."""
+    rng = np.random.default_rng(3)
+    for _ in range(50):
+        lens = rng.integers(0, 50, size=int(rng.integers(1, 40)))
+        off = np.zeros(len(lens) + 1, dtype=np.uint64)
+        off[1:] = np.cumsum(lens)
+        budget = int(rng.integers(1, 120))
+        waves = sdist.plan_waves(off, budget)
+        assert waves[0][0] == 0 and waves[-1][1] == len(lens)
+        for (a0, a1), (b0, b1) in zip(waves, waves[1:]):
+            assert a1 == b0
+        for t0, t1 in waves:
+            assert t1 > t0
+            n = int(off[t1] - off[t0])
+            assert n <= budget or t1 == t0 + 1
+            if t1 < len(lens):                               # greedy: the next trace would not fit
+                assert int(off[t1 + 1] - off[t0]) > budget

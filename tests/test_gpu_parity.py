@@ -362,3 +362,17 @@ def test_trace_recon_error():
     r = scl.scl_replay_run(cfg.T, tr)
     err = scl.scl_trace_recon_error(r)
     assert len(err) == cfg.n_traces and (err < cfg.T).all() and (err > cfg.T // 2).all()
+
+
+def test_all_empty_traces_after_reuse():
+    """Degenerate input: every trace empty (no unit, no replay launch), on a result reused from a
+    non-empty run -- the summaries, table, report and gate must be those of the empty traces."""
+    rng = np.random.default_rng(5)
+    full = [tracegen.random_small_trace(rng, 5000, n_sites=9, max_size=300, max_ptrs=20) for _ in range(3)]
+    ev, off = _concat(full)
+    tr, r = gpu_run(ev, off, 9, 257)
+    compare(ev, off, 9, 257, r)
+    ev0, off0 = _concat([[], [], []])
+    scl.scl_trace_reload(tr, ev0, off0, 9)
+    r = scl.scl_replay_run(257, tr, out=r)
+    compare(ev0, off0, 9, 257, r)

@@ -344,6 +344,17 @@ def test_formula_closed_form():
     assert not flag_closed.any()                                    # gate closed -> nothing reported
 
 
+def test_rate_closed_form_and_zero_elapsed():
+    """Rate (Q11): malloc bytes in MB over elapsed seconds; 3 MiB over 2 s = 1.5 MB/s.
+    Elapsed 0 only happens with every trace empty (no bytes anywhere): rate 0 (reading Q20)."""
+    tab = np.zeros((2, 10), dtype=np.uint64)
+    tab[0, 2] = 3 << 20
+    _, rate, _ = oracle.finalize(tab, True, 2 * 10**9)
+    assert rate[0] == 1.5 and rate[1] == 0.0
+    _, rate0, _ = oracle.finalize(np.zeros((2, 10), dtype=np.uint64), True, 0)
+    assert np.array_equal(rate0, [0.0, 0.0])
+
+
 def test_formula_grid_exact():
     pairs = [(m, f) for m in range(0, 101) for f in range(0, m + 1)]
     tab = np.zeros((len(pairs), 10), dtype=np.uint64)
