@@ -323,18 +323,8 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
         unsigned old = 0;
         if (lane == 0) old = atom_add_acq_rel_cta(&S.done, 1u);
         old = __shfl_sync(kFull, old, 0);
-        if (old == kChunks - 1) {
-            // last chunk of the unit: compose the 32 chunk summaries (lane = chunk) and publish
-            const long long cs = S.Pc[lane], cx = S.ax[lane], cn = S.an[lane];
-            long long ci = cs;
-            #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) { long long o = shfl_up_ll(ci, d); if (lane >= d) ci += o; }
-            const long long Pc = ci - cs, ax = Pc + cx, an = Pc + cn;
-            S.Pc[lane] = Pc; S.ax[lane] = ax; S.an[lane] = an;
-            const long long usum = shfl_ll(ci, 31), umx = warp_max(ax), umn = warp_min(an);
-            if (lane == 0) { S.usum = usum; S.umx = umx; S.umn = umn; PROF_UNIT_T(S.info.slot, 0) }
-            __syncwarp();
-            if (lane == 0) { S.itu = itu; ((volatile unsigned*)s.situ)[sl] = itu; __threadfence_block(); atomicExch(&s.sstate[sl], 1u); }
+        if (old == kChunks - 1 && lane == 0) {              // last chunk of the unit: hand it to the publisher
+            S.itu = itu; ((volatile unsigned*)s.situ)[sl] = itu; __threadfence_block(); atomicExch(&s.sstate[sl], 1u);
         }
     }
 }
@@ -765,11 +755,22 @@ __device__ void publisher_role(const ReplayParams& p, Smem& s, int lane)
         __threadfence_block();
         const bool mine = (fm >> lane) & 1u;                 // lane q <-> slot q: its unit id and aggregate
         const unsigned uq = mine ? ((volatile unsigned*)&s.slot[lane].info.slot)[0] : 0u;
-        long long a3[3] = {0, 0, 0};
-        if (mine) { a3[0] = s.slot[lane].usum; a3[1] = s.slot[lane].umx; a3[2] = s.slot[lane].umn; }
+        long long a3[3] = {0, 0, 0};                         // the aggregate of slot `lane` (composed below)
         for (unsigned m = fm; m; m &= m - 1) {
             const int q = __ffs(m) - 1;
             Slot& S = s.slot[q];
+            {   // compose the unit's 32 chunk summaries (lane = chunk): prefixes, max / min, aggregate
+                const long long cs = S.Pc[lane], cx = S.ax[lane], cn = S.an[lane];
+                long long ci = cs;
+                #pragma unroll
+                for (int d = 1; d < 32; d <<= 1) { long long o = shfl_up_ll(ci, d); if (lane >= d) ci += o; }
+                const long long Pc = ci - cs, ax = Pc + cx, an = Pc + cn;
+                S.Pc[lane] = Pc; S.ax[lane] = ax; S.an[lane] = an;
+                const long long usum = shfl_ll(ci, 31), umx = warp_max(ax), umn = warp_min(an);
+                if (lane == 0) { S.usum = usum; S.umx = umx; S.umn = umn; PROF_UNIT_T(S.info.slot, 0) }
+                if (lane == q) { a3[0] = usum; a3[1] = umx; a3[2] = umn; }
+                __syncwarp();
+            }
             const uint4* src = reinterpret_cast<const uint4*>(&S);
             uint4* dst = reinterpret_cast<uint4*>(urec + __shfl_sync(kFull, uq, q));
             for (int o = lane; o < (int)(sizeof(Slot) / 16); o += 32) dst[o] = src[o];
