@@ -43,7 +43,7 @@ struct __align__(16) Slot {          // compute -> look-back summary of one unit
                                                            // (before the compose: chunk sum, max, min
                                                            // relative to the chunk start)
     long long usum, umx, umn;                              // unit aggregate
-    unsigned done, itu;                                    // chunks finished; CTA unit iteration
+    unsigned pad0, pad1;
     unsigned bloom[kChunks][kBloomWords];
 };
 
@@ -58,11 +58,10 @@ struct __align__(16) Smem {
     Slot slot[kSlots];
     SegInfo info[kStages];
     unsigned sub[kStages];           // box index within the unit
-    uint64_t full[kStages], empty[kStages], sempty[kSlots];
-    unsigned sstate[kSlots];         // 0 compute-owned, 1 full (ready for look-back), 2 claimed
-    unsigned situ[kSlots];           // priority of a full slot (unit iteration; + 10^6 after a failed try)
+    uint64_t full[kStages], empty[kStages];
+    uint64_t sempty[kSlots];         // slot free again (publisher -> compute)
+    uint64_t sdone[kSlots];          // the slot's unit is complete: one arrival per chunk (compute -> publisher)
     unsigned n_units;                // units handed to this CTA (known at the end of the tickets)
-    unsigned n_done;                 // units finished by the look-back warps
 };
 
 size_t replay_urec_bytes() { return sizeof(Slot); }
@@ -320,12 +319,7 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
         __syncwarp();
         mbar_arrive(&s.empty[st]);                        // box consumed
         PROF_MARK(2)
-        unsigned old = 0;
-        if (lane == 0) old = atom_add_acq_rel_cta(&S.done, 1u);
-        old = __shfl_sync(kFull, old, 0);
-        if (old == kChunks - 1 && lane == 0) {              // last chunk of the unit: hand it to the publisher
-            S.itu = itu; ((volatile unsigned*)s.situ)[sl] = itu; __threadfence_block(); atomicExch(&s.sstate[sl], 1u);
-        }
+        if (lane == 0) mbar_arrive(&s.sdone[sl]);         // chunk summarised: the 32nd arrival completes the unit
     }
 }
 
@@ -740,19 +734,22 @@ __device__ void publisher_role(const ReplayParams& p, Smem& s, int lane)
     const unsigned ep_tag = p.epoch;
     Slot* urec = reinterpret_cast<Slot*>(p.urec);
     PROF_DECL
+    unsigned j = 0;                                      // this CTA's next unit (slot j % kSlots)
     for (;;) {
-        // every full slot at once: copy each to its unit record and hand the shared-memory slot
-        // back right away (the copy is in flight from registers), then ONE device-scope fence
-        // before the ready flags of the whole batch
-        const unsigned fm = __ballot_sync(kFull, lane < kSlots && ((volatile unsigned*)s.sstate)[lane] == 1);
-        if (fm == 0) {
-            const unsigned nu = ((volatile unsigned*)&s.n_units)[0], nd = ((volatile unsigned*)&s.n_done)[0];
-            if (nu != kInvalid && nd >= nu) { PROF_FLUSH(16) return; }
+        // units complete in order (almost): wait for unit j, take every complete unit after it,
+        // copy each to its unit record and hand the shared-memory slot back right away (the copy
+        // is in flight from registers), then ONE device-scope fence before the aggregate words
+        if (!mbar_try(&s.sdone[j % kSlots], (j / kSlots) & 1u)) {
+            const unsigned nu = ((volatile unsigned*)&s.n_units)[0];
+            if (nu != kInvalid && j >= nu) { PROF_FLUSH(16) return; }
             PROF_MARK(0)
-            __nanosleep(32);
             continue;
         }
-        __threadfence_block();
+        unsigned nb = 1;
+        while (nb < (unsigned)kSlots && mbar_test(&s.sdone[(j + nb) % kSlots], ((j + nb) / kSlots) & 1u)) ++nb;
+        unsigned fm = 0;
+        for (unsigned b = 0; b < nb; ++b) fm |= 1u << ((j + b) % kSlots);
+        j += nb;
         const bool mine = (fm >> lane) & 1u;                 // lane q <-> slot q: its unit id and aggregate
         const unsigned uq = mine ? ((volatile unsigned*)&s.slot[lane].info.slot)[0] : 0u;
         long long a3[3] = {0, 0, 0};                         // the aggregate of slot `lane` (composed below)
@@ -775,10 +772,7 @@ __device__ void publisher_role(const ReplayParams& p, Smem& s, int lane)
             uint4* dst = reinterpret_cast<uint4*>(urec + __shfl_sync(kFull, uq, q));
             for (int o = lane; o < (int)(sizeof(Slot) / 16); o += 32) dst[o] = src[o];
             __syncwarp();
-            if (lane == 0) {
-                S.done = 0; __threadfence_block();
-                atomicExch(&s.sstate[q], 0u); mbar_arrive(&s.sempty[q]);
-            }
+            if (lane == 0) mbar_arrive(&s.sempty[q]);
         }
         __syncwarp();
         __threadfence();                                     // the records before their aggregate words
@@ -790,7 +784,6 @@ __device__ void publisher_role(const ReplayParams& p, Smem& s, int lane)
             #pragma unroll
             for (int i = 0; i < 3; ++i) st_relaxed_u64(w + i, ((unsigned long long)(fit ? a3[i] : kAggBig) << 16) | tag);
         }
-        if (lane == 0) atomicAdd(&s.n_done, (unsigned)__popc(fm));
         __syncwarp();
         PROF_MARK(1)
     }
@@ -1040,11 +1033,10 @@ replay_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     if (tid == 0 && (smem_u32(smem_raw) & 1023u) != 0) __trap();     // the 128-B swizzle needs 1024-B alignment
 
     for (int x = tid; x < 4 * kHot; x += kCtaThreads) { s.cnt[x] = 0; s.blo[x] = 0; }
-    for (int x = tid; x < kSlots; x += kCtaThreads) s.slot[x].done = 0;
     if (tid == 0) {
         for (int i = 0; i < kStages; ++i) { mbar_init(&s.full[i], 1); mbar_init(&s.empty[i], 8 * 32); }
-        for (int i = 0; i < kSlots; ++i) { mbar_init(&s.sempty[i], 1); s.sstate[i] = 0; s.situ[i] = 0; }
-        s.n_units = kInvalid; s.n_done = 0;
+        for (int i = 0; i < kSlots; ++i) { mbar_init(&s.sempty[i], 1); mbar_init(&s.sdone[i], kChunks); }
+        s.n_units = kInvalid;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" :: "l"((uint64_t)&tmap) : "memory");
     }
