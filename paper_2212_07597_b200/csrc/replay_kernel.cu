@@ -64,6 +64,7 @@ struct __align__(16) Smem {
     unsigned n_units;                // units handed to this CTA (known at the end of the tickets)
 };
 
+static_assert(sizeof(Slot) % 16 == 0, "unit records are copied by the TMA engine in 16-B units");
 size_t replay_urec_bytes() { return sizeof(Slot); }
 size_t replay_smem_bytes() { return 1024 + (size_t)kStages * kSegBytes + sizeof(Smem); }
 
@@ -766,13 +767,19 @@ __device__ void publisher_role(const ReplayParams& p, Smem& s, int lane)
                 const long long usum = shfl_ll(ci, 31), umx = warp_max(ax), umn = warp_min(an);
                 if (lane == 0) { S.usum = usum; S.umx = umx; S.umn = umn; PROF_UNIT_T(S.info.slot, 0) }
                 if (lane == q) { a3[0] = usum; a3[1] = umx; a3[2] = umn; }
-                __syncwarp();
             }
-            const uint4* src = reinterpret_cast<const uint4*>(&S);
-            uint4* dst = reinterpret_cast<uint4*>(urec + __shfl_sync(kFull, uq, q));
-            for (int o = lane; o < (int)(sizeof(Slot) / 16); o += 32) dst[o] = src[o];
+            // the record goes out through the TMA engine (one bulk copy of the slot)
+            fence_proxy_async_shared();                      // the compose's writes before the async-proxy read
             __syncwarp();
-            if (lane == 0) mbar_arrive(&s.sempty[q]);
+            const unsigned u = __shfl_sync(kFull, uq, q);
+            if (lane == 0) bulk_s2g(urec + u, &S, (uint32_t)sizeof(Slot));
+        }
+        if (lane == 0) {
+            bulk_commit();
+            bulk_wait_read();                                // every slot of the batch read: hand them back
+            for (unsigned m = fm; m; m &= m - 1) mbar_arrive(&s.sempty[__ffs(m) - 1]);
+            bulk_wait_all();                                 // the records written
+            fence_proxy_async_global();
         }
         __syncwarp();
         __threadfence();                                     // the records before their aggregate words
