@@ -238,7 +238,8 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
         const uint32_t bl_s = smem_u32(&S.bloom[c][0]);
 
         long long run = 0, tmx = kNeg, tmn = kPos;
-        int r32 = 0, mx32 = INT_MIN, mn32 = INT_MAX;
+        int r32 = 0, mx32 = 0, mn32 = 0;                  // the lane's max / min include its start value
+                                                          // (an earlier F: harmless for M and the band)
         bool small = true;                                // 32-bit chunk summary is exact for this lane
         if (!(br.w & 0x100u)) {
             // ---- the 8 events of row r of the box
@@ -304,14 +305,12 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
         // ---- chunk summary: sum, max / min prefix relative to the chunk start
         long long csum, cmx, cmn;
         if (__all_sync(kFull, small)) {                       // 32-bit scan + REDUX
+            const int tot = __reduce_add_sync(kFull, r32);      // (off the scan's dependency chain)
             int incl = r32;
             #pragma unroll
             for (int d = 1; d < 32; d <<= 1) { int o = __shfl_up_sync(kFull, incl, d); if (lane >= d) incl += o; }
-            const int a = mx32 == INT_MIN ? INT_MIN : incl - r32 + mx32;
-            const int b = mn32 == INT_MAX ? INT_MAX : incl - r32 + mn32;
-            const int am = __reduce_max_sync(kFull, a), bm = __reduce_min_sync(kFull, b);
-            csum = __shfl_sync(kFull, incl, 31);
-            cmx = am == INT_MIN ? kNeg : am; cmn = bm == INT_MAX ? kPos : bm;
+            const int am = __reduce_max_sync(kFull, incl - r32 + mx32), bm = __reduce_min_sync(kFull, incl - r32 + mn32);
+            csum = tot; cmx = am; cmn = bm;
         } else {
             long long incl = run;
             #pragma unroll
