@@ -62,7 +62,7 @@ class ClockSampler:
     """NVML polling of SM clock and throttle reasons during the timed region."""
 
     def __init__(self, index):
-        self.samples, self.reasons, self.stop = [], set(), threading.Event()
+        self.samples, self.reasons, self.stop, self.first = [], set(), threading.Event(), threading.Event()
         try:
             import pynvml
             pynvml.nvmlInit()
@@ -89,12 +89,14 @@ class ClockSampler:
                         self.reasons.add(name.replace("nvmlClocksEventReason", "").lower())
             except Exception:
                 pass
-            time.sleep(0.002)
+            self.first.set()
+            time.sleep(0.0005)
 
     def __enter__(self):
         if self.nv:
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
+            self.first.wait(1.0)                      # polling before the timed work is enqueued
         return self
 
     def __exit__(self, *a):
@@ -105,7 +107,7 @@ class ClockSampler:
     def summary(self):
         med = statistics.median(self.samples) if self.samples else None
         return {"sm_mhz": med, "sm_max_mhz": self.max, "reasons": sorted(self.reasons - {"gpuidle"}),
-                "n_samples": len(self.samples), "source": "nvml, 2 ms polling during the timed region"}
+                "n_samples": len(self.samples), "source": "nvml, 0.5 ms polling during the timed regions"}
 
 
 def measured_peak():
@@ -260,6 +262,7 @@ def main():
             r = step(r, timing=True)
         torch.cuda.synchronize()
     kern_ms = scl.scl_result_kernel_times(r)
+    clk.samples += clk2.samples; clk.reasons |= clk2.reasons
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
