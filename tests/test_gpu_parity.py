@@ -376,3 +376,27 @@ def test_all_empty_traces_after_reuse():
     scl.scl_trace_reload(tr, ev0, off0, 9)
     r = scl.scl_replay_run(257, tr, out=r)
     compare(ev0, off0, 9, 257, r)
+
+
+def test_unit_aggregates_beyond_48_bits():
+    """A unit whose footprint range exceeds 2^47 bytes (its published aggregate words cannot carry
+    it, so the runner reads the unit record), among ordinary units of the same traces."""
+    rng = np.random.default_rng(11)
+    traces = []
+    for t in range(3):
+        tr_, live = [], []
+        for i in range(30000):
+            if 9000 <= i < 9400:                               # unit 1: 400 allocs of ~2^40 bytes
+                s, p = (1 << 40) - 1 - i, 0x7000000000 + 16 * i
+                live.append((p, s)); tr_.append(("a", p, s, 1))
+            elif live and (i >= 20000 or rng.random() < 0.45):
+                p, s = live.pop(int(rng.integers(len(live))))
+                tr_.append(("f", p, s, 2))
+            else:
+                s, p = int(rng.integers(1, 5000)), 0x1000 + 16 * i
+                live.append((p, s)); tr_.append(("a", p, s, 0))
+        traces.append(tr_)
+    ev, off = _concat(traces)
+    for T in (1 << 20, (1 << 45) + 3):
+        _, r = gpu_run(ev, off, 3, T)
+        compare(ev, off, 3, T, r)
