@@ -5,25 +5,24 @@
 // leak tracker with the free-pointer comparison P:20-39, per-line statistics
 // P:488-494.  Readings Q1-Q16: DESIGN.md §3.
 //
-// One persistent CTA per SM, warp-specialised:
-//   producer warp   one ticket per 8192-event unit (tickets ordered (unit index,
-//                   trace), so the units of one trace are spread over time);
-//                   issues the unit's 2-D TMA boxes (32 KiB, 128-B swizzle)
-//                   into a kStages-deep shared-memory ring;
-//   8 compute warps one 256-event chunk per box each: signed sizes, chunk sum
-//                   and max/min prefix, Tier-E site counters (32-bit shared
-//                   atomics + carry word), a 2048-bit Bloom filter of freed
-//                   pointers; the last warp to finish a unit composes the 32
-//                   chunk summaries and publishes the unit aggregate at once;
-//   3 look-back warps take whole units round-robin: find the incoming state by
-//                   a decoupled look-back over the trace's earlier units
-//                   (aggregates are composed while the sampler band provably
-//                   stays closed; the warp waits only at the first unit where
-//                   a sample could fire), resolve the samples (re-reading only
-//                   the chunks whose range leaves the band, through L2),
-//                   publish the inclusive state, then check the frees against
-//                   the tracked pointer (Bloom query per chunk, exact re-check
-//                   of positives).
+// replay_kernel: one persistent CTA per SM, warp-specialised:
+//   producer warp   CTA 0 first prepares the run (zeroes tables / states, scans the sample
+//                   bases); then one ticket per 8192-event unit (tickets ordered (unit index,
+//                   trace), so the units of one trace are spread over time), the unit's four
+//                   2-D TMA boxes (32 KiB, 128-B swizzle, L2 evict_first) into a 4-stage ring;
+//   16 compute warps in two groups alternating boxes, one 256-event chunk per warp per box:
+//                   signed sizes, the chunk's sum and max/min prefix, Tier-E site counters
+//                   (unconditional 32-bit shared atomics), a 2048-bit Bloom filter of freed
+//                   pointers; one mbarrier arrival per chunk completes the unit's slot;
+//   publisher warp  per complete unit (in order): composes the 32 chunk summaries, copies the
+//                   unit record to global through the TMA engine, hands the slot back, and after
+//                   one fence per batch publishes the unit's tagged aggregate words;
+//   2 runner warps  each trace has one runner lane that advances it strictly in order over its
+//                   published units: batches of units without a sample composed from their
+//                   aggregates, units where a sample fires resolved chunk by chunk (32-bit when
+//                   the chunk allows), entry states recorded for the reclaim pass.
+// post_kernel (cooperative): the free-pointer comparison of every episode segment (Bloom query
+// per chunk, exact re-checks of positives), the per-sample reduce, and a6 when fused.
 #include <climits>
 #include <algorithm>
 #include "scl_internal.cuh"

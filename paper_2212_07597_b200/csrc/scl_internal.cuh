@@ -15,10 +15,10 @@ namespace scl {
 // (the look-back granule) is kSub = 4 boxes = 8192 events = 32 chunks of 256
 // events (one chunk per compute warp per box).  One persistent CTA per SM:
 //   warps 0..15  compute: two groups of 8 alternate boxes (one chunk per warp), no CTA barriers;
-//                the last warp to finish a unit publishes its aggregate
+//                one arrival per chunk on the unit slot's completion mbarrier
 //   warp  16     producer: tickets (one per unit) + TMA issue into a kStages ring
-//   warps 17..19 look-back: chain the units of a trace, resolve samples,
-//                match frees against the tracked pointer, publish
+//   warp  17     publisher: composes and publishes each complete unit
+//   warps 18..19 runners: advance their traces over the published units, resolve samples
 constexpr int kThreads = 256;                 // rows per box = compute threads
 constexpr int kEpt = 8;                       // events per row
 constexpr int kSeg = kThreads * kEpt;         // events per box
@@ -29,7 +29,7 @@ constexpr int kUnit = kSeg * kSub;            // events per unit (8192)
 constexpr int kChunks = 32;                   // 256-event chunks per unit (one per look-back lane)
 constexpr int kComputeWarps = 16;                // two groups of 8, alternating boxes
 constexpr int kLBWarps = 3;                   // publisher + 2 runner warps (20 warps total, 96 registers)
-constexpr int kEmbeddedRunners = 2;           // default layout: warps 18-19 of every streaming CTA run traces
+constexpr int kEmbeddedRunners = 2;           // warps 18-19 of every CTA run traces
 constexpr int kProducerWarp = kComputeWarps;
 constexpr int kCtaThreads = (kComputeWarps + 1 + kLBWarps) * 32;
 constexpr int kStages = 4;                    // TMA ring depth
