@@ -475,7 +475,7 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
         r->cap = c;
     }
 
-    // epoch-tagged look-back flags: no per-run clear of the state array
+    // epoch-tagged unit aggregate words: no per-run clear
     // (the aggregate words carry the low 16 bits: cleared, and tag 0 skipped, once per 2^16 runs)
     if (tr->epoch >= (1u << 30)) { tr->epoch = 0; CU(cudaMemsetAsync(tr->d_ticket, 0, 8 * 4, st)); }   // no stale "prepared"
     if (((tr->epoch + 1) & 0xffffu) == 0) { CU(cudaMemsetAsync(tr->d_uagg, 0, tr->cap_segs * 32, st)); tr->epoch += 1; }
@@ -671,7 +671,7 @@ extern "C" scl_status scl_result_kernel_times(const scl_result* rc, float* ms, s
 }
 
 #ifdef SCL_PROFILE
-// Debug build only: per-role cycle sums of the last run (compute 0..7, producer 8..15, look-back 16..23).
+// Debug build only: per-role cycle sums of the last run (compute 0..7, producer 8..15, publisher + runners 16..23).
 extern "C" scl_status scl_debug_prof(const scl_result* r, unsigned long long* out) {
     if (!r || !r->d_prof) return fail(SCL_EINVAL, "no profile");
     CU(cudaMemcpy(out, r->d_prof, (48 + 4 * (size_t)r->tr->n_segs) * 8, cudaMemcpyDeviceToHost));

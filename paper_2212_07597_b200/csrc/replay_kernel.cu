@@ -36,7 +36,7 @@ struct SegInfo {                     // one unit ticket, as the producer resolve
     long long off_t, n_t, row_base;  // trace start, trace length, first global row of the unit
     unsigned nbox, pad;              // boxes of this unit that overlap the trace
 };
-struct __align__(16) Slot {          // compute -> look-back summary of one unit
+struct __align__(16) Slot {          // compute -> publisher -> runners / post pass: one unit
     SegInfo info;
     long long Pc[kChunks], ax[kChunks], an[kChunks];       // chunk prefix; max/min relative to the unit start
                                                            // (before the compose: chunk sum, max, min
@@ -222,7 +222,7 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
         const unsigned itu = it / kSub;                   // unit iteration of this CTA
         if (itu != cur_itu) { cur_itu = itu; if (++sl == kSlots) { sl = 0; sph ^= 1u; } }
         if (br.w & 0x200u) {
-            // the look-back warps stop once all `itu` units of this CTA are published
+            // the publisher stops once all `itu` units of this CTA are published
             if (grp == 0 && w8 == 0 && lane == 0) atomicExch(&s.n_units, itu);
             PROF_FLUSH(0)
             return;
@@ -737,7 +737,7 @@ __device__ void run_trace(const ReplayParams& p, RState& x, unsigned t, unsigned
 }
 
 // Publisher warp (one per CTA): copies each finished unit's summary from its shared-memory
-// slot to the unit's global record, marks it ready and frees the slot at once.
+// slot to the unit's global record, frees the slot, publishes the tagged aggregate words.
 __device__ void publisher_role(const ReplayParams& p, Smem& s, int lane)
 {
     const unsigned ep_tag = p.epoch;

@@ -12,7 +12,7 @@ namespace scl {
 // Events are viewed as 128-B rows of 8.  A TMA box is 256 rows (2048 events,
 // 32 KiB), staged in shared memory with the 128-byte swizzle so that each
 // compute lane reads its own row with conflict-free LDS.128.  A chain UNIT
-// (the look-back granule) is kSub = 4 boxes = 8192 events = 32 chunks of 256
+// (the runners' granule) is kSub = 4 boxes = 8192 events = 32 chunks of 256
 // events (one chunk per compute warp per box).  One persistent CTA per SM:
 //   warps 0..15  compute: two groups of 8 alternate boxes (one chunk per warp), no CTA barriers;
 //                one arrival per chunk on the unit slot's completion mbarrier
@@ -26,14 +26,14 @@ constexpr int kSegBytes = kSeg * 16;
 constexpr int kSub = 4;                       // boxes per unit
 constexpr int kUnitRows = kThreads * kSub;
 constexpr int kUnit = kSeg * kSub;            // events per unit (8192)
-constexpr int kChunks = 32;                   // 256-event chunks per unit (one per look-back lane)
+constexpr int kChunks = 32;                   // 256-event chunks per unit (one per runner lane)
 constexpr int kComputeWarps = 16;                // two groups of 8, alternating boxes
 constexpr int kLBWarps = 3;                   // publisher + 2 runner warps (20 warps total, 96 registers)
 constexpr int kEmbeddedRunners = 2;           // warps 18-19 of every CTA run traces
 constexpr int kProducerWarp = kComputeWarps;
 constexpr int kCtaThreads = (kComputeWarps + 1 + kLBWarps) * 32;
 constexpr int kStages = 4;                    // TMA ring depth
-constexpr int kSlots = 6;                     // compute -> look-back unit summary ring (smem)
+constexpr int kSlots = 6;                     // compute -> publisher unit summary ring (smem)
 constexpr int kBloomWords = 64;               // 2048-bit Bloom filter of freed pointers per chunk
 constexpr int kHot = 1024;                    // sites with shared-memory Tier-E counters (all 4 kinds)
 constexpr int kWarm = 2 * kHot;               // the same storage when n_sites > kHot: allocs and frees only
@@ -108,7 +108,7 @@ struct ReplayParams {
     const scl_event* ev;              // padded device copy (multiple of 8 events)
     const unsigned long long* off;    // [n_traces+1]
     const TicketInfo* tk;             // [n_segs] in ticket order (unit index, trace)
-    void* urec;                       // [n_segs] unit records (summaries published by the look-back warps)
+    void* urec;                       // [n_segs] unit records (copied out by the publisher warps)
     unsigned long long* uagg;         // [n_segs][4] unit sum, max, min as (value << 16 | epoch tag), published
                                       // after the unit record (value kAggBig: read it from the record)
     RunState* run;                    // [n_traces] per-trace runner state (zeroed per run)
