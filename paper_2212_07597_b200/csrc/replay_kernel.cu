@@ -55,10 +55,8 @@ struct __align__(16) Smem {
     unsigned blo[kESlots];           //   bytes mod 2^32 (carries: straight to L2)  slots >= 4*kHot: per-lane
                                      //   sinks of the unconditional atomics; copies counted, not reported)
     Slot slot[kSlots];
-    SegInfo info[kStages];           // the box's unit (read by one lane, for the unit record)
-    uint4 brec[kStages];             // what every compute lane needs, one 16-B load: trace index of the
-                                     //   box's first event (2 words), events of the trace from there
-                                     //   (clamped to [-1, 2^31)), box index | outside << 8 | sentinel << 9
+    SegInfo info[kStages];
+    unsigned sub[kStages];           // box index within the unit
     uint64_t full[kStages], empty[kStages];
     uint64_t sempty[kSlots];         // slot free again (publisher -> compute)
     uint64_t sdone[kSlots];          // the slot's unit is complete: one arrival per chunk (compute -> publisher)
@@ -215,13 +213,11 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
         PROF_MARK(3)
         mbar_wait(&s.full[st], (it / kStages) & 1u);
         PROF_MARK(0)
-        const uint4 br = s.brec[st];
-        const long long e0b = (long long)(((unsigned long long)br.y << 32) | br.x);
-        const int rem = (int)br.z;
-        const unsigned g = br.w & 0xffu;
+        const SegInfo inf = s.info[st];
+        const unsigned g = s.sub[st];
         const unsigned itu = it / kSub;                   // unit iteration of this CTA
         if (itu != cur_itu) { cur_itu = itu; if (++sl == kSlots) { sl = 0; sph ^= 1u; } }
-        if (br.w & 0x200u) {
+        if (inf.u == kInvalid) {
             // the publisher stops once all `itu` units of this CTA are published
             if (grp == 0 && w8 == 0 && lane == 0) atomicExch(&s.n_units, itu);
             PROF_FLUSH(0)
@@ -232,7 +228,7 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
         Slot& S = s.slot[sl];
         const int c = g * 8 + w8;                         // chunk index within the unit
         S.bloom[c][lane] = 0u; S.bloom[c][lane + 32] = 0u;
-        if (g == 0 && w8 == 0 && lane == 0) S.info = s.info[st];
+        if (g == 0 && w8 == 0 && lane == 0) S.info = inf;
         __syncwarp();
         const uint32_t bl_s = smem_u32(&S.bloom[c][0]);
 
@@ -240,7 +236,7 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
         int r32 = 0, mx32 = 0, mn32 = 0;                  // the lane's max / min include its start value
                                                           // (an earlier F: harmless for M and the band)
         bool small = true;                                // 32-bit chunk summary is exact for this lane
-        if (!(br.w & 0x100u)) {
+        if (g < inf.nbox) {
             // ---- the 8 events of row r of the box
             const unsigned char* boxp = stage + (size_t)st * kSegBytes;
             unsigned long long ptr[kEpt], meta[kEpt];
@@ -249,12 +245,12 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
                 ulonglong2 v = *reinterpret_cast<const ulonglong2*>(boxp + rofs[j]);
                 ptr[j] = v.x; meta[j] = v.y;
             }
-            const long long e0 = e0b + (long long)r * kEpt;
+            const long long e0 = (inf.row_base + (long long)g * kThreads + r) * kEpt - inf.off_t;
             unsigned big = 0;                                 // any size >= 2^27 in the row?
             #pragma unroll
             for (int j = 0; j < kEpt; ++j) big |= ((unsigned)meta[j] >> 27) | ((unsigned)(meta[j] >> 32) & 0xffu);
             unsigned cold = 0;                                // events for the L2 (cold site) path
-            if (e0 >= 0 && r * kEpt + kEpt <= rem && big == 0) {
+            if (e0 >= 0 && e0 + kEpt <= inf.n_t && big == 0) {
                 // fast path: the whole row is in the trace and |partial sums| < 2^30: 32-bit running
                 // sum / max / min (a copy's d = 0 repeats an F already seen: harmless)
                 if (all_hot) fast_row<true>(ptr, meta, cnt_s, bl_s, dslot, p.table, r32, mx32, mn32, cold);
@@ -269,7 +265,7 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
                 for (int j = 0; j < kEpt; ++j) {
                     const long long ie = e0 + j;
                     const unsigned kind = ev_kind(meta[j]);
-                    const bool af = ie >= 0 && r * kEpt + j < rem && kind < 2;
+                    const bool af = ie >= 0 && ie < inf.n_t && kind < 2;
                     const unsigned long long size = ev_size(meta[j]);
                     run += af ? (kind == 0 ? (long long)size : -(long long)size) : 0;     // a1: signed size
                     if (af) {
@@ -358,13 +354,7 @@ __device__ void producer_role(const ReplayParams& p, const CUtensorMap* tmap, Sm
             PROF_MARK(1)
             mbar_wait(&s.empty[st], ((it / kStages) & 1u) ^ 1u);
             PROF_MARK(0)
-            s.info[st] = cur;
-            {
-                const long long e0b = (cur.row_base + (long long)g * kThreads) * kEpt - cur.off_t;
-                const long long rm = llmin(llmax(cur.n_t - e0b, -1ll), (long long)INT_MAX);
-                const unsigned fl = g | (g >= cur.nbox ? 0x100u : 0u) | (cur.u == kInvalid ? 0x200u : 0u);
-                s.brec[st] = make_uint4((unsigned)e0b, (unsigned)((unsigned long long)e0b >> 32), (unsigned)(int)rm, fl);
-            }
+            s.info[st] = cur; s.sub[st] = g;
             if (cur.u == kInvalid || g >= cur.nbox) {
                 mbar_arrive(&s.full[st]);                  // sentinel / box outside the trace
                 if (cur.u == kInvalid && g == 0) continue; // the sentinel goes to both compute groups
