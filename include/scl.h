@@ -155,6 +155,18 @@ scl_status scl_trace_reload(scl_traces* traces, const scl_event* events, const u
 scl_status scl_replay_run(uint64_t threshold, const scl_traces* traces,
                           const scl_run_opts* opts, scl_result** out);
 
+/* The same replay at another threshold over the handle's LAST stream pass (the scl_replay_run
+ * that produced `base`): the per-unit summaries, Bloom filters and per-event (Tier E) site
+ * counters of that pass are reused, so the events are not streamed again -- only the runners
+ * re-chain every trace (re-reading the rows where a sample fires) and the reclaim pass, the
+ * per-sample reduce and a6 run for the new threshold (several thresholds, one
+ * read of the events).  Output contract, options and errors as scl_replay_run; in addition
+ * SCL_EINVAL when base is NULL, belongs to another handle, is not of the handle's last stream
+ * pass (another scl_replay_run or a reload came after it) or is *out.  Ordered on
+ * opts->cuda_stream after the base run when both use the same stream. */
+scl_status scl_replay_rethreshold(uint64_t threshold, const scl_traces* traces, const scl_result* base,
+                                  const scl_run_opts* opts, scl_result** out);
+
 /* Device pointer to the result's summable int64 table: n_sites*SCL_NCOL site-table
  * values followed by 3 gate values (sum of F_last-F_first, sum of max(F_first,1),
  * number of traces with >= 2 samples).  Summing it element-wise across GPUs (an

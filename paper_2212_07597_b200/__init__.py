@@ -17,7 +17,7 @@ import numpy as np
 
 from . import _build
 
-__all__ = ["SclError", "Traces", "Result", "scl_trace_load", "scl_trace_reload", "scl_replay_run", "scl_finalize",
+__all__ = ["SclError", "Traces", "Result", "scl_trace_load", "scl_trace_reload", "scl_replay_run", "scl_replay_rethreshold", "scl_replay_sweep", "scl_finalize",
            "scl_site_report", "scl_samples", "scl_trace_summaries", "scl_gate", "scl_result_device_table",
            "scl_result_timing", "scl_result_kernel_times", "scl_next_prime", "scl_traces_info", "EVENT_DTYPE", "SAMPLE_DTYPE",
            "SUMMARY_DTYPE", "SITE_ROW_DTYPE", "COLS", "device_table_tensor", "write_trace_file",
@@ -71,6 +71,7 @@ def _load():
         "scl_rate_site_counts": [P, P, SZ, P],
         "scl_rate_timing": [P, P],
         "scl_replay_run": [U64, P, P, P],
+        "scl_replay_rethreshold": [U64, P, P, P, P],
         "scl_result_device_table": [P, P, P],
         "scl_finalize": [P, U64],
         "scl_site_report": [P, P, SZ, P],
@@ -217,6 +218,31 @@ def scl_replay_run(threshold: int, traces: Traces, tick_ns: int = 0, formula: in
     _check(lib.scl_replay_run(threshold, traces.handle, ctypes.byref(o), ctypes.byref(h)))
     r._h = h
     return r
+
+
+def scl_replay_rethreshold(threshold: int, traces: Traces, base: Result, tick_ns: int = 0, formula: int = 0,
+                           defer_finalize: bool = False, elapsed_ns: int = 0, stream=None,
+                           out: Result | None = None, timing: bool = False, hwm_mode: int = HWM_PREFIX) -> Result:
+    """The replay at another threshold over the handle's last stream pass (the run that gave
+    ``base``): the events are not streamed again (K5, several thresholds in one read)."""
+    o = _RunOpts()
+    o.tick_ns, o.hwm_mode, o.formula = tick_ns, hwm_mode, formula
+    o.defer_finalize, o.elapsed_ns, o.timing = int(defer_finalize), elapsed_ns, int(timing)
+    if stream is not None:
+        o.cuda_stream = getattr(stream, "cuda_stream", stream)
+    r = out if out is not None else Result(traces)
+    h = ctypes.c_void_p(r._h.value)
+    _check(lib.scl_replay_rethreshold(threshold, traces.handle, base.handle, ctypes.byref(o), ctypes.byref(h)))
+    r._h = h
+    return r
+
+
+def scl_replay_sweep(thresholds, traces: Traces, **kw) -> list:
+    """One stream pass at thresholds[0], every other threshold re-chained over it."""
+    rs = [scl_replay_run(int(thresholds[0]), traces, **kw)]
+    for T in thresholds[1:]:
+        rs.append(scl_replay_rethreshold(int(T), traces, rs[0], **kw))
+    return rs
 
 
 def scl_result_device_table(r: Result):

@@ -64,6 +64,7 @@ constexpr unsigned kRTaskCap = 1u << 16;      // reclaim re-check queue (overflo
 struct scl_result {
     const scl_traces* tr = nullptr;
     uint64_t T = 0;
+    unsigned epoch = 0;                        // the handle's stream pass this result belongs to
     int formula = 0;
     uint64_t elapsed_ns = 0;
     cudaStream_t stream = nullptr;
@@ -348,6 +349,7 @@ extern "C" scl_status scl_trace_reload(scl_traces* tr, const scl_event* events, 
     const uint64_t n = h_off[n_traces];
     const bool src_dev = n > 0 && is_device_ptr(events);
     if (validate) { st = validate_host(events, src_dev, h_off, n_traces); if (st != SCL_OK) return st; }
+    tr->epoch += 1;                            // no earlier result is of this handle's stream pass any more
     return upload(tr, events, src_dev, std::move(h_off), n_traces, n_sites, (cudaStream_t)cuda_stream);
 }
 
@@ -431,9 +433,13 @@ static FinalParams final_params(scl_result* r) {
     return f;
 }
 
-extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, const scl_run_opts* opts, scl_result** out)
+static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const scl_run_opts* opts, scl_result** out,
+                              const scl_result* base)
 {
     if (!tr || !out) return fail(SCL_EINVAL, "NULL argument");
+    if (base && (base->tr != tr || base->epoch != tr->epoch || !base->epoch))
+        return fail(SCL_EINVAL, "base is not a result of the handle's last stream pass");
+    if (base && *out == base) return fail(SCL_EINVAL, "*out must not be the base result");
     if (threshold == 0) return fail(SCL_EINVAL, "threshold must be >= 1");
     if (threshold > (1ull << 62)) return fail(SCL_EINVAL, "threshold too large");
     scl_run_opts o{};
@@ -477,10 +483,13 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
 
     // epoch-tagged unit aggregate words: no per-run clear
     // (the aggregate words carry the low 16 bits: cleared, and tag 0 skipped, once per 2^16 runs)
-    if (tr->epoch >= (1u << 30)) { tr->epoch = 0; CU(cudaMemsetAsync(tr->d_ticket, 0, 8 * 4, st)); }   // no stale "prepared"
-    if (((tr->epoch + 1) & 0xffffu) == 0) { CU(cudaMemsetAsync(tr->d_uagg, 0, tr->cap_segs * 32, st)); tr->epoch += 1; }
-    if (tr->epoch == 0) CU(cudaMemsetAsync(tr->d_uagg, 0, tr->cap_segs * 32, st));
-    tr->epoch += 1;
+    if (!base) {                               // a new stream pass (a re-threshold reads the last one)
+        if (tr->epoch >= (1u << 30)) { tr->epoch = 0; CU(cudaMemsetAsync(tr->d_ticket, 0, 8 * 4, st)); }   // no stale "prepared"
+        if (((tr->epoch + 1) & 0xffffu) == 0) { CU(cudaMemsetAsync(tr->d_uagg, 0, tr->cap_segs * 32, st)); tr->epoch += 1; }
+        if (tr->epoch == 0) CU(cudaMemsetAsync(tr->d_uagg, 0, tr->cap_segs * 32, st));
+        tr->epoch += 1;
+    }
+    r->epoch = tr->epoch;
 
     const bool tm = o.timing != 0;                 // phase / kernel events only when asked for
     r->timed = tm;
@@ -508,13 +517,23 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
 #endif
     const int ks = (int)(r->nrun % kRing);
     if (tm) CU(cudaEventRecord(r->kev[2 * ks], st));
-    if (tr->n_segs == 0) {                     // no event at all: no replay launch, prepare here
+    if (tr->n_segs == 0 || base) {             // no replay launch: prepare here
         CU(cudaMemsetAsync(pp.table, 0, pp.table_words * 8, st));
         CU(cudaMemsetAsync(pp.summ, 0, pp.summ_words * 8, st));
         CU(cudaMemsetAsync(tr->d_ticket, 0, 7 * 4, st));
-        if (NT) CU(cudaMemsetAsync(r->d_sbase, 0, (size_t)NT * 8, st));
+        if (NT) CU(cudaMemcpyAsync(r->d_sbase, r->h_sbase.data(), (size_t)NT * 8, cudaMemcpyHostToDevice, st));
     }
-    CU(launch_replay(&tr->tmap, p, r->grid, st));
+    if (base) {                                // the per-event columns (Tier E) of the stream pass
+        CU(cudaMemsetAsync(pp.run, 0, pp.run_words * 8, st));
+        if (tr->n_sites)
+            CU(cudaMemcpy2DAsync(r->d_table, SCL_NCOL * 8, base->d_table, SCL_NCOL * 8, 4 * 8, tr->n_sites,
+                                 cudaMemcpyDeviceToDevice, st));
+        p.rechain = 1;
+        p.n_runners = std::min<unsigned>(NT, (unsigned)r->grid * 8);
+        CU(launch_rechain(p, st));
+    } else {
+        CU(launch_replay(&tr->tmap, p, r->grid, st));
+    }
     if (tm) { CU(cudaEventRecord(r->kev[2 * ks + 1], st)); r->nrun += 1; }
     // a6 fused into the post pass (its last block) when the run finalizes at once on a small table
     const bool fuse = !o.defer_finalize && report_fused(tr->n_sites);
@@ -537,6 +556,18 @@ extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, c
         if (s3 != SCL_OK) return s3;
     }
     return SCL_OK;
+}
+
+extern "C" scl_status scl_replay_run(uint64_t threshold, const scl_traces* tr, const scl_run_opts* opts, scl_result** out)
+{
+    return replay_impl(threshold, tr, opts, out, nullptr);
+}
+
+extern "C" scl_status scl_replay_rethreshold(uint64_t threshold, const scl_traces* tr, const scl_result* base,
+                                             const scl_run_opts* opts, scl_result** out)
+{
+    if (!base) return fail(SCL_EINVAL, "NULL base");
+    return replay_impl(threshold, tr, opts, out, base);
 }
 
 extern "C" scl_status scl_result_device_table(scl_result* r, int64_t** dev_ptr, size_t* n_int64) {

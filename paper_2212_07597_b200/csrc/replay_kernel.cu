@@ -801,7 +801,7 @@ __device__ void runner_role(const ReplayParams& p, unsigned ri, int lane)
 {
     const unsigned ep_tag = p.epoch;
     const unsigned nr = p.n_runners;
-    wait_prepared(p);                                     // runner states, sample bases: CTA 0
+    if (!p.rechain) wait_prepared(p);                     // runner states, sample bases: CTA 0
     const unsigned cnt = ri < p.n_traces ? (p.n_traces - ri + nr - 1) / nr : 0u;
     const unsigned my_t = ri + (unsigned)lane * nr;
     unsigned my_base = 0, my_nseg = 0, my_next = 0;
@@ -1072,6 +1072,21 @@ replay_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     } else {                                                          // 2 runner warps per CTA
         runner_role(p, blockIdx.x * kEmbeddedRunners + (warp - kProducerWarp - 2), lane);
     }
+}
+
+// Another threshold over the handle's last stream pass: the runners alone, reading the published
+// unit records and aggregate words (tagged with that pass's epoch) and re-reading only the rows
+// where a sample fires.
+__global__ void __launch_bounds__(128) rechain_kernel(const __grid_constant__ ReplayParams p)
+{
+    runner_role(p, blockIdx.x * 4 + (threadIdx.x >> 5), threadIdx.x & 31);
+}
+
+cudaError_t launch_rechain(const ReplayParams& p, cudaStream_t st)
+{
+    if (p.n_segs == 0) return cudaSuccess;
+    rechain_kernel<<<(p.n_runners + 3) / 4, 128, 0, st>>>(p);
+    return cudaGetLastError();
 }
 
 int replay_occupancy(int* grid)

@@ -119,6 +119,7 @@ struct ReplayParams {
                                       //      per run); [7] = epoch once the run is prepared (never zeroed)
     RTask* rtask;                     // [rtask_cap] exact re-checks queued by the reclaim pass
     unsigned int rtask_cap;
+    int rechain;                      // runners only, over the handle's last stream pass (prepared by the host)
     PrepParams prep;                  // CTA 0 prepares the run; ticket[7] = epoch once done
     int fuse_report;                  // post_kernel runs a6 over all its blocks (fin -> rows)
     unsigned* rbits;                  // [kReportSites/32] a6 scratch: flag bitmask words
@@ -214,6 +215,7 @@ cudaError_t launch_load_stats(const scl_event* ev, const unsigned long long* off
                               unsigned long long* err, cudaStream_t st);
 cudaError_t launch_replay(const CUtensorMap* tmap, const ReplayParams& p, int grid, cudaStream_t st);
 cudaError_t launch_post(const ReplayParams& p, cudaStream_t st);
+cudaError_t launch_rechain(const ReplayParams& p, cudaStream_t st);   // runner warps alone
 cudaError_t launch_finalize(const FinalParams& p, cudaStream_t st);
 bool report_fused(unsigned n_sites);   // a6 in one block (report_kernel) for tables this small
 cudaError_t launch_report(const FinalParams& p, scl_site_row* rows, cudaStream_t st);
