@@ -54,3 +54,19 @@ def test_rethreshold_stale_base_errors():
     scl.scl_trace_reload(tr, ev, off, cfg.n_sites)                   # a reload: b2 is stale
     with pytest.raises(scl.SclError):
         scl.scl_replay_rethreshold(7, tr, b2)
+
+
+def test_rethreshold_all_empty_and_deferred_finalize():
+    ev = tracegen.from_tuples([])
+    off = np.zeros(4, dtype=np.uint64)
+    tr = scl.scl_trace_load(ev, off, 5)
+    base = scl.scl_replay_run(101, tr)
+    r = scl.scl_replay_rethreshold(7, tr, base)
+    compare(ev, off, 5, 7, r)
+    cfg = tracegen.CONFIGS[1]
+    ev, off = tracegen.generate(cfg)
+    tr = scl.scl_trace_load(ev, off, cfg.n_sites)
+    base = scl.scl_replay_run(cfg.T, tr)
+    r = scl.scl_replay_rethreshold(65537, tr, base, defer_finalize=True, tick_ns=1000)
+    scl.scl_finalize(r, oracle.elapsed_ns(off, 1000))
+    compare(ev, off, cfg.n_sites, 65537, r)
