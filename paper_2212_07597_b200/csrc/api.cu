@@ -263,9 +263,11 @@ static scl_status upload(scl_traces* tr, const scl_event* src, bool src_dev, std
         if (!grow(tr->d_tk, nn) || !grow(tr->d_uagg, nn * 4) || !grow(tr->d_uent, nn) ||
             cudaMalloc(&tr->d_urec, nn * replay_urec_bytes()) != cudaSuccess)
             { cudaGetLastError(); return fail(SCL_ENOMEM, "unit plan"); }
-        CU(cudaMemsetAsync(tr->d_uagg, 0, nn * 32, st));       // epoch tags start at 1
         tr->cap_segs = nn;
     }
+    // no aggregate word of an earlier trace set survives a (re)load: a unit index unused for a
+    // while could otherwise hold a tag that a later run reuses (tags are the epoch's low 16 bits)
+    CU(cudaMemsetAsync(tr->d_uagg, 0, tr->cap_segs * 32, st));
     if (total) CU(cudaMemcpyAsync(tr->d_tk, tk.data(), total * sizeof(TicketInfo), cudaMemcpyHostToDevice, st));
     if (n_traces) {
         CU(cudaMemcpyAsync(tr->d_tr_nseg, nseg.data(), n_traces * 4, cudaMemcpyHostToDevice, st));
