@@ -400,3 +400,19 @@ def test_unit_aggregates_beyond_48_bits():
     for T in (1 << 20, (1 << 45) + 3):
         _, r = gpu_run(ev, off, 3, T)
         compare(ev, off, 3, T, r)
+
+
+def test_hot_sites_with_high_ids():
+    """n_sites > 1024 with the hot sites spread over high, colliding ids: the warm table's slots
+    (site mod 2048, first claimer) and the L2 path both in play."""
+    cfg = tracegen.CONFIGS[3].with_traces(12)
+    ev, off = tracegen.generate(cfg)
+    rng = np.random.default_rng(8)
+    perm = rng.permutation(1 << 20)[:cfg.n_sites].astype(np.uint64)      # rank r -> a high random id
+    site = ev["meta"] >> np.uint64(43)
+    ev = ev.copy()
+    ev["meta"] = (ev["meta"] & np.uint64((1 << 43) - 1)) | (perm[site.astype(np.int64)] << np.uint64(43))
+    n_sites = 1 << 20
+    for T in (cfg.T, 1048583):
+        _, r = gpu_run(ev, off, n_sites, T)
+        compare(ev, off, n_sites, T, r, traces_to_check=range(0, 12, 3))
