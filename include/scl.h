@@ -44,7 +44,7 @@ typedef enum {
     SCL_ETRACE = -4,     /* invalid trace (validate = 1): message names trace and first bad event */
     SCL_EOVERFLOW = -5,  /* a result does not fit (e.g. > 2^21 sites) */
     SCL_EIO = -6,        /* trace file unreadable or malformed */
-    SCL_ENCCL = -7       /* reserved: collective failure */
+    SCL_ENCCL = -7       /* NCCL unavailable or a collective failed (scl_run_opts.nccl_comm) */
 } scl_status;
 
 /* One trace event, 16 bytes, 16-byte aligned, array-of-structs.
@@ -111,8 +111,17 @@ typedef struct {
     int timing;              /* 1: record CUDA events around the phases and the replay kernel
                                 (scl_result_timing, scl_result_kernel_times); 0: one completion
                                 event only (each event record costs ~2.5 us of stream time) */
-    uint64_t elapsed_ns;     /* 0: max_t n_t * tick_ns over this handle's traces */
+    uint64_t elapsed_ns;     /* 0: max_t n_t * tick_ns over this handle's traces (over every rank's
+                                traces when nccl_comm is set) */
     void* cuda_stream;       /* cudaStream_t, NULL = default stream */
+    void* nccl_comm;         /* ncclComm_t of the ranks that hold the other trace shards, or NULL
+                                (single GPU).  Set: after a1-a5 the summable table is SUM
+                                all-reduced and the elapsed time MAX all-reduced over the ranks on
+                                cuda_stream, then a6 runs (unless defer_finalize) -- every rank
+                                ends with the global report; samples stay rank-local.  Every rank
+                                must make the matching call.  The library loads libnccl.so.2
+                                (already in the process, or from the system) on first use;
+                                SCL_ENCCL if it cannot or a collective fails. */
 } scl_run_opts;
 
 typedef struct scl_traces scl_traces;  /* opaque: device copy of events + offsets + segment plan */
@@ -186,6 +195,11 @@ scl_status scl_samples(const scl_result* r, uint32_t trace, scl_sample* out, siz
 
 /* All traces' summaries (host buffer of n_traces). */
 scl_status scl_trace_summaries(const scl_result* r, scl_trace_summary* out, size_t cap, size_t* n);
+/* One trace's summary (SURVEY §8(b)'s scl_trace_summary; that name is the struct here): any output
+ * pointer may be NULL.  Errors: SCL_EINVAL
+ * for a NULL result or trace >= n_traces. */
+scl_status scl_trace_summary_of(const scl_result* r, uint32_t trace, int64_t* f_final, int64_t* hwm,
+                                uint64_t* n_samples, uint64_t* n_episodes);
 
 /* Gate of P:62-65 (reading Q10): num = sum(F_last - F_first), den = sum max(F_first,1)
  * over traces with >= 2 samples; open iff some trace qualifies and 100*num >= den. */

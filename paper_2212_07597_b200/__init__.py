@@ -50,7 +50,7 @@ class SclError(RuntimeError):
 class _RunOpts(ctypes.Structure):
     _fields_ = [("tick_ns", ctypes.c_uint64), ("hwm_mode", ctypes.c_int), ("formula", ctypes.c_int),
                 ("defer_finalize", ctypes.c_int), ("timing", ctypes.c_int), ("elapsed_ns", ctypes.c_uint64),
-                ("cuda_stream", ctypes.c_void_p)]
+                ("cuda_stream", ctypes.c_void_p), ("nccl_comm", ctypes.c_void_p)]
 
 
 def _load():
@@ -72,6 +72,7 @@ def _load():
         "scl_rate_timing": [P, P],
         "scl_replay_run": [U64, P, P, P],
         "scl_replay_rethreshold": [U64, P, P, P, P],
+        "scl_trace_summary_of": [P, U32, P, P, P, P],
         "scl_result_device_table": [P, P, P],
         "scl_finalize": [P, U64],
         "scl_site_report": [P, P, SZ, P],
@@ -204,7 +205,8 @@ FORMULA_PAPER, FORMULA_TEXTBOOK = 0, 1
 
 def scl_replay_run(threshold: int, traces: Traces, tick_ns: int = 0, formula: int = 0,
                    defer_finalize: bool = False, elapsed_ns: int = 0, stream=None,
-                   out: Result | None = None, timing: bool = False, hwm_mode: int = HWM_PREFIX) -> Result:
+                   out: Result | None = None, timing: bool = False, hwm_mode: int = HWM_PREFIX,
+                   nccl_comm: int | None = None) -> Result:
     """Replay all traces at threshold T; ``out`` (a previous Result of the same
     traces) is reused in place.  stream: torch.cuda.Stream / raw handle / None.
     timing: record CUDA events for scl_result_timing / scl_result_kernel_times."""
@@ -213,6 +215,8 @@ def scl_replay_run(threshold: int, traces: Traces, tick_ns: int = 0, formula: in
     o.defer_finalize, o.elapsed_ns, o.timing = int(defer_finalize), elapsed_ns, int(timing)
     if stream is not None:
         o.cuda_stream = getattr(stream, "cuda_stream", stream)
+    if nccl_comm is not None:
+        o.nccl_comm = nccl_comm                     # raw ncclComm_t: table SUM / elapsed MAX in the library
     r = out if out is not None else Result(traces)
     h = ctypes.c_void_p(r._h.value)
     _check(lib.scl_replay_run(threshold, traces.handle, ctypes.byref(o), ctypes.byref(h)))
@@ -311,6 +315,13 @@ def scl_trace_summaries(r: Result) -> np.ndarray:
     if n.value:
         _check(lib.scl_trace_summaries(r.handle, out.ctypes.data, n.value, ctypes.byref(n)))
     return out
+
+
+def scl_trace_summary_of(r: Result, trace: int):
+    """(f_final, hwm, n_samples, n_episodes) of one trace."""
+    f, h, n, e = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_uint64(), ctypes.c_uint64()
+    _check(lib.scl_trace_summary_of(r.handle, trace, ctypes.byref(f), ctypes.byref(h), ctypes.byref(n), ctypes.byref(e)))
+    return f.value, h.value, n.value, e.value
 
 
 def scl_gate(r: Result):

@@ -16,6 +16,8 @@
 #include <string>
 #include <vector>
 #include <unordered_map>
+#include <dlfcn.h>
+#include <nccl.h>                              // types only: the functions come from dlsym
 #include <algorithm>
 
 using namespace scl;
@@ -63,6 +65,8 @@ constexpr unsigned kRTaskCap = 1u << 16;      // reclaim re-check queue (overflo
 
 struct scl_result {
     const scl_traces* tr = nullptr;
+    unsigned long long* d_el = nullptr;        // nccl_comm runs: the elapsed time being MAX-reduced
+    unsigned long long h_el = 0;
     uint64_t T = 0;
     unsigned epoch = 0;                        // the handle's stream pass this result belongs to
     int formula = 0;
@@ -387,7 +391,7 @@ extern "C" void scl_result_free(scl_result* r) {
     free_result_buffers(r);
     cudaFree(r->d_samples); cudaFree(r->d_epflag); cudaFree(r->d_prof); cudaFree(r->d_rtask);
     cudaFree(r->d_rbits); cudaFree(r->d_rlrate); cudaFree(r->d_rlsite);
-    cudaFree(r->d_P); cudaFree(r->d_dom); cudaFree(r->d_recon);
+    cudaFree(r->d_P); cudaFree(r->d_dom); cudaFree(r->d_recon); cudaFree(r->d_el);
     if (r->h_gate) cudaFreeHost(r->h_gate);
     for (auto& e : r->ev) if (e) cudaEventDestroy(e);
     for (auto& e : r->kev) if (e) cudaEventDestroy(e);
@@ -433,6 +437,16 @@ static FinalParams final_params(scl_result* r) {
     f.gate_out = r->h_gate;                    // pinned host memory, device-accessible (unified addressing)
     f.prof = r->d_prof;
     return f;
+}
+
+// NCCL through the process's libnccl.so.2 (torch's, when loaded) or the system's, resolved once.
+using AllReduceFn = ncclResult_t (*)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+static AllReduceFn nccl_allreduce() {
+    static AllReduceFn fn = []() -> AllReduceFn {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        return h ? (AllReduceFn)dlsym(h, "ncclAllReduce") : nullptr;
+    }();
+    return fn;
 }
 
 static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const scl_run_opts* opts, scl_result** out,
@@ -537,8 +551,10 @@ static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const sc
         CU(launch_replay(&tr->tmap, p, r->grid, st));
     }
     if (tm) { CU(cudaEventRecord(r->kev[2 * ks + 1], st)); r->nrun += 1; }
-    // a6 fused into the post pass (its last block) when the run finalizes at once on a small table
-    const bool fuse = !o.defer_finalize && report_fused(tr->n_sites);
+    // a6 fused into the post pass when the run finalizes at once on a small table (not when the
+    // table is first reduced across ranks)
+    const bool reduce = o.nccl_comm != nullptr;
+    const bool fuse = !o.defer_finalize && !reduce && report_fused(tr->n_sites);
     if (fuse) {
         p.fuse_report = 1; p.fin = final_params(r); p.rows = r->d_rows;
         p.rbits = r->d_rbits; p.rlrate = r->d_rlrate; p.rlsite = r->d_rlsite;
@@ -553,6 +569,23 @@ static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const sc
         return SCL_OK;
     }
     *out = r;
+    if (reduce) {                              // one int64 SUM all-reduce of the table
+        AllReduceFn ar = nccl_allreduce();
+        if (!ar) return fail(SCL_ENCCL, "libnccl.so.2 not found");
+        ncclComm_t comm = (ncclComm_t)o.nccl_comm;
+        if (ar(r->d_table, r->d_table, (size_t)tr->n_sites * SCL_NCOL + 3, ncclInt64, ncclSum, comm, st) != ncclSuccess)
+            return fail(SCL_ENCCL, "ncclAllReduce (site table) failed");
+        if (!o.elapsed_ns) {                   // Q11 over every rank's traces: MAX of max_t n_t * tick
+            if (!r->d_el) CU(cudaMalloc(&r->d_el, 8));
+            r->h_el = r->elapsed_ns;
+            CU(cudaMemcpyAsync(r->d_el, &r->h_el, 8, cudaMemcpyHostToDevice, st));
+            if (ar(r->d_el, r->d_el, 1, ncclUint64, ncclMax, comm, st) != ncclSuccess)
+                return fail(SCL_ENCCL, "ncclAllReduce (elapsed) failed");
+            CU(cudaMemcpyAsync(&r->h_el, r->d_el, 8, cudaMemcpyDeviceToHost, st));
+            CU(cudaStreamSynchronize(st));
+            r->elapsed_ns = r->h_el;
+        }
+    }
     if (!o.defer_finalize) {
         scl_status s3 = scl_finalize(r, 0);
         if (s3 != SCL_OK) return s3;
@@ -653,6 +686,21 @@ extern "C" scl_status scl_trace_summaries(const scl_result* r, scl_trace_summary
     if (cap == 0) return SCL_OK;
     if (!out) return fail(SCL_EINVAL, "out is NULL");
     memcpy(out, r->h_summ.data(), std::min(cap, (size_t)*n) * sizeof(scl_trace_summary));
+    return SCL_OK;
+}
+
+extern "C" scl_status scl_trace_summary_of(const scl_result* r, uint32_t trace, int64_t* f_final, int64_t* hwm,
+                                        uint64_t* n_samples, uint64_t* n_episodes) {
+    if (!r) return fail(SCL_EINVAL, "NULL result");
+    if (trace >= r->tr->n_traces) return fail(SCL_EINVAL, "trace out of range");
+    CU(cudaSetDevice(r->tr->device));
+    scl_status s = ensure_summ(r);
+    if (s != SCL_OK) return s;
+    const scl_trace_summary& m = r->h_summ[trace];
+    if (f_final) *f_final = m.f_final;
+    if (hwm) *hwm = m.hwm;
+    if (n_samples) *n_samples = m.n_samples;
+    if (n_episodes) *n_episodes = m.n_episodes;
     return SCL_OK;
 }
 
