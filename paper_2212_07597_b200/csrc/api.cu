@@ -227,7 +227,12 @@ static scl_status upload(scl_traces* tr, const scl_event* src, bool src_dev, std
             return fail(SCL_ENOMEM, "per-trace buffers");
         tr->cap_tr = nt1;
     }
-    if (!tr->d_err && (!grow(tr->d_err, 1) || !grow(tr->d_ticket, 8))) return fail(SCL_ENOMEM, "counters");
+    if (!tr->d_err) {
+        if (!grow(tr->d_err, 1) || !grow(tr->d_ticket, 8)) return fail(SCL_ENOMEM, "counters");
+        // ticket[7] is the "run prepared" flag compared with the run's epoch: a fresh block may hold
+        // a freed handle's epoch (fuzzing found producers starting before CTA 0 had prepared)
+        CU(cudaMemsetAsync(tr->d_ticket, 0, 8 * sizeof(unsigned), st));
+    }
     if (n > 0) CU(cudaMemcpyAsync(tr->d_ev, src, n * sizeof(scl_event), src_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
     if (rows_alloc * 8 > n) CU(cudaMemsetAsync(tr->d_ev + n, 0, (rows_alloc * 8 - n) * sizeof(scl_event), st));
     CU(cudaMemcpyAsync(tr->d_off, h_off.data(), h_off.size() * 8, cudaMemcpyHostToDevice, st));

@@ -416,3 +416,17 @@ def test_hot_sites_with_high_ids():
     for T in (cfg.T, 1048583):
         _, r = gpu_run(ev, off, n_sites, T)
         compare(ev, off, n_sites, T, r, traces_to_check=range(0, 12, 3))
+
+
+def test_handles_created_and_freed_repeatedly():
+    """Regression (found by tools/fuzz.py): a new handle's counter block may be a freed handle's
+    memory, whose "run prepared" word held the same epoch; the block is now zeroed at creation.
+    Create / run / check / free in a loop, one unit per trace so that every CTA races CTA 0."""
+    rng = np.random.default_rng(12)
+    for it in range(20):
+        traces = [tracegen.random_small_trace(rng, 8191, n_sites=5000, max_size=1 << 20, max_ptrs=50), []]
+        ev, off = _concat(traces)
+        tr = scl.scl_trace_load(ev, off, 5000)
+        r = scl.scl_replay_run(1000 + it, tr, tick_ns=1000)
+        compare(ev, off, 5000, 1000 + it, r)
+        r.free(); tr.free()
