@@ -214,9 +214,12 @@ static scl_status upload(scl_traces* tr, const scl_event* src, bool src_dev, std
                                        "): load them in waves");
     }
     const uint64_t rows_alloc = std::max<uint64_t>((n + 7) / 8, 1);
+    // + kPadRows zeroed rows: a candidate chunk's lanes past the last event of the last trace
+    // re-read up to 31 rows beyond it (load_row_global); they land here, not past the mapping.
+    constexpr uint64_t kPadRows = 32;
     if (rows_alloc > tr->cap_rows) {
         cudaFree(tr->d_ev); tr->d_ev = nullptr; tr->cap_rows = 0;
-        if (cudaMalloc(&tr->d_ev, rows_alloc * 128) != cudaSuccess) { cudaGetLastError(); tr->d_ev = nullptr; return fail(SCL_ENOMEM, "events"); }
+        if (cudaMalloc(&tr->d_ev, (rows_alloc + kPadRows) * 128) != cudaSuccess) { cudaGetLastError(); tr->d_ev = nullptr; return fail(SCL_ENOMEM, "events"); }
         tr->cap_rows = rows_alloc;
     }
     const size_t nt1 = std::max<uint32_t>(n_traces, 1);
@@ -234,7 +237,7 @@ static scl_status upload(scl_traces* tr, const scl_event* src, bool src_dev, std
         CU(cudaMemsetAsync(tr->d_ticket, 0, 8 * sizeof(unsigned), st));
     }
     if (n > 0) CU(cudaMemcpyAsync(tr->d_ev, src, n * sizeof(scl_event), src_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
-    if (rows_alloc * 8 > n) CU(cudaMemsetAsync(tr->d_ev + n, 0, (rows_alloc * 8 - n) * sizeof(scl_event), st));
+    CU(cudaMemsetAsync(tr->d_ev + n, 0, ((rows_alloc + kPadRows) * 8 - n) * sizeof(scl_event), st));
     CU(cudaMemcpyAsync(tr->d_off, h_off.data(), h_off.size() * 8, cudaMemcpyHostToDevice, st));
     CU(cudaMemsetAsync(tr->d_sabs, 0, nt1 * 8, st));
     CU(cudaMemsetAsync(tr->d_err, 0xff, 8, st));

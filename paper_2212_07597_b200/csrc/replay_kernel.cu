@@ -98,15 +98,10 @@ __device__ __forceinline__ unsigned bloom_mask(unsigned long long ptr) {
 #endif
 
 // The 8 events of one global row, through L2 (re-read path).  A row past the end of its trace
-// (a chunk's lanes beyond the last event) may lie past the end of the event buffer: it is not
-// read (its events are outside the trace and masked anyway).  end = off_t + n_t of the trace.
-__device__ __forceinline__ void load_row_global(const scl_event* ev, long long row, long long end,
+// (a chunk's lanes beyond the last event, masked by the caller) is still read: the event buffer
+// carries 32 zeroed rows past its last row for exactly these lanes (scl_trace_load).
+__device__ __forceinline__ void load_row_global(const scl_event* ev, long long row,
                                                 unsigned long long* ptr, unsigned long long* meta) {
-    if (row * kEpt >= end) {
-        #pragma unroll
-        for (int j = 0; j < kEpt; ++j) { ptr[j] = 0; meta[j] = 0; }
-        return;
-    }
     const ulonglong2* q = reinterpret_cast<const ulonglong2*>(ev + row * kEpt);
     #pragma unroll
     for (int j = 0; j < kEpt; ++j) { ulonglong2 v = __ldcg(q + j); ptr[j] = v.x; meta[j] = v.y; }
@@ -534,7 +529,7 @@ __device__ void resolve_unit(const ReplayParams& p, const Slot& S, RState& x, un
 #ifdef SCL_PROFILE
         long long t_l = clock64();
 #endif
-        load_row_global(p.ev, row, inf.off_t + inf.n_t, rp, rm);
+        load_row_global(p.ev, row, rp, rm);
         // while the rows are in flight: F and the high-water mark before chunk c
         const long long Fc = F0 + shfl_ll(sPc, c);
         long long Mc;                                           // max F before chunk c
@@ -860,7 +855,7 @@ __device__ __forceinline__ bool chunk_has_free(const ReplayParams& p, long long 
 {
     const long long row = row0 + lane;
     unsigned long long rp[kEpt], rm[kEpt];
-    load_row_global(p.ev, row, off_t + n_t, rp, rm);
+    load_row_global(p.ev, row, rp, rm);
     bool hit = false;
     #pragma unroll
     for (int jj = 0; jj < kEpt; ++jj) {
