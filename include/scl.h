@@ -127,7 +127,8 @@ typedef struct {
 typedef struct scl_traces scl_traces;  /* opaque: device copy of events + offsets + segment plan */
 typedef struct scl_result scl_result;  /* opaque: samples, summaries, site table, report */
 
-/* Load traces into library-owned device memory.
+/* Load traces into library-owned device memory (a copy: 16 B per event, rounded up to
+ * 8-event rows, plus 32 zeroed rows the kernels may read past the last trace).
  *   path      binary trace file ("SCLTRC01" format) or NULL to use the arrays
  *   events    n = offsets[n_traces] events (host or device pointer)
  *   offsets   n_traces+1 uint64 event offsets, offsets[0] = 0, non-decreasing (host or device)
