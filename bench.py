@@ -4,13 +4,17 @@
 Contract (driver): ``python bench.py --gpus N --steps K --warmup W [--impl reference]``
 prints ONE JSON line on rank 0.  A step is one pass of the whole hot path
 a1..a6 over the resident workload: scl_replay_run (streaming
-replay kernel + per-sample reduce) -> [N>1: NCCL all-reduce of the int64 site
-table] -> scl_finalize (probabilities, flags, report order, rows).
+replay kernel [+ the Tier-E reduce of its cold-record stream] + reclaim /
+per-sample pass) -> [N>1: NCCL all-reduce of the int64 site table] ->
+scl_finalize (probabilities, flags, report order, rows).
 
-Workload (N=1): BASELINE configs[1] = config 2, 64 traces x 1M events, 1000
-sites, 4 planted leaks, T = next_prime(10 MiB).  N>1: weak scaling -- every
-rank replays its own 64-trace batch (trace ids rank*64 ...), and the per-site
-tables are summed with one all-reduce (the method's only exchange step).
+Workload: BASELINE configs[2] = config 3, the largest configuration that fits
+one B200: 1024 traces x 10^6 events (16.4 GB), 50,000 sites (Zipf 1.0), 16
+planted leaks with mixed rates, T = next_prime(10 MiB).  N>1 (launched by
+torchrun, or spawned here when --gpus N > 1 and WORLD_SIZE is unset): strong
+scaling -- the same 1024 traces split into contiguous shards of 1024/N traces,
+and the per-site tables summed with one all-reduce (the method's only exchange
+step); --scaling weak gives every rank a full config-sized batch instead.
 
 --impl reference: the CPU oracle (oracle/oracle.c) as it stands, on the host
 cores, on the same workload (rank 0 only).
@@ -39,21 +43,25 @@ ROW_BYTES_TABLE = 80
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--traces", type=int, default=0, help="override traces per rank (testing)")
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--traces", type=int, default=0,
+                    help="override the total traces (strong) / traces per rank (weak)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the K5 threshold-sweep field")
     return ap.parse_args()
 
 
-def workload(cfg, n_traces_rank, world):
-    return {"workload": f"{cfg.name}: {n_traces_rank} traces/GPU x {cfg.events_per_trace} events, "
+def workload(cfg, n_traces_rank, world, n_traces_total=None, scaling="strong"):
+    tot = n_traces_total if n_traces_total is not None else n_traces_rank * world
+    return {"workload": f"{cfg.name}: {tot} traces x {cfg.events_per_trace} events ({n_traces_rank} traces/GPU), "
                         f"{cfg.n_sites} sites (Zipf {cfg.zipf_s}), {cfg.n_planted} planted leaks, T={cfg.T}",
-            "traces_per_gpu": n_traces_rank, "events_per_trace": cfg.events_per_trace,
+            "traces_total": tot, "traces_per_gpu": n_traces_rank, "events_per_trace": cfg.events_per_trace,
+            "scaling": scaling,
             "n_sites": cfg.n_sites, "threshold": cfg.T, "event_bytes": BYTES_PER_EVENT,
             "l2": f"inputs larger than L2 ({n_traces_rank * cfg.events_per_trace * 16 / 1e9:.2f} GB > 0.126 GB); no flush needed",
             "parallelism": f"dp{world} (trace shards, int64 all-reduce of the site table)"}
@@ -129,11 +137,18 @@ def ncu_traffic(config_id):
         return None
 
 
-def cpu_oracle_baseline(ev, off, cfg, reps=3):
-    """The oracle as it stands, on all host cores and on 1 core, on the full
-    rank-0 workload (a few core-seconds, bounded)."""
-    import oracle
-    lib = oracle._load()
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def _oracle_pass(lib, oracle, ev, off, cfg, threads):
     nt = len(off) - 1
     cap = oracle.sample_bound(ev, off, cfg.T)
     soff = np.zeros(nt + 1, dtype=np.uint64)
@@ -141,27 +156,34 @@ def cpu_oracle_baseline(ev, off, cfg, reps=3):
     samples = np.zeros(max(int(soff[-1]), 1), dtype=oracle.SAMPLE_DTYPE)
     summ = np.zeros(nt, dtype=oracle.SUMMARY_DTYPE)
     table = np.zeros((cfg.n_sites, oracle.NCOL), dtype=np.uint64)
+    t0 = time.perf_counter()
+    lib.orc_replay_all(oracle._ptr(ev), oracle._ptr(off), nt, cfg.n_sites, cfg.T, 0, threads,
+                       oracle._ptr(samples), oracle._ptr(soff), oracle._ptr(summ), oracle._ptr(table), None)
+    num, den, op = oracle.gate(summ)
+    prob, rate, flag = oracle.finalize(table, op, oracle.elapsed_ns(off))
+    oracle.report_order(rate, flag)
+    return time.perf_counter() - t0
+
+
+def cpu_oracle_baseline(ev, off, cfg, reps=3, one_core_traces=64):
+    """The oracle as it stands, on all host cores (the full rank-0 workload) and on 1 core (a
+    bounded sample: its first ``one_core_traces`` traces), a1..a6 -- a few core-seconds."""
+    import oracle
+    lib = oracle._load()
+    nt = len(off) - 1
     cores = os.cpu_count() or 1
-    res = {}
-    for threads in (cores, 1):
-        best = None
-        for _ in range(reps if threads > 1 else 1):
-            t0 = time.perf_counter()
-            lib.orc_replay_all(oracle._ptr(ev), oracle._ptr(off), nt, cfg.n_sites, cfg.T, 0, threads,
-                               oracle._ptr(samples), oracle._ptr(soff), oracle._ptr(summ), oracle._ptr(table), None)
-            num, den, op = oracle.gate(summ)
-            prob, rate, flag = oracle.finalize(table, op, oracle.elapsed_ns(off))
-            oracle.report_order(rate, flag)
-            dt = time.perf_counter() - t0
-            best = dt if best is None else min(best, dt)
-        res[threads] = len(ev) / best
-    return {"value": res[cores], "unit": "events/s", "cores": cores, "kind": "oracle",
-            "value_1core": res[1],
-            "sample": f"the full rank-0 workload ({len(ev)} events, {nt} traces), a1..a6, best of {reps}"}
+    best = min(_oracle_pass(lib, oracle, ev, off, cfg, cores) for _ in range(reps))
+    n1 = min(nt, one_core_traces)
+    ev1, off1 = ev[:int(off[n1])], off[:n1 + 1]
+    t1 = _oracle_pass(lib, oracle, ev1, off1, cfg, 1)
+    return {"value": len(ev) / best, "unit": "events/s", "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(), "value_1core": len(ev1) / t1,
+            "sample": f"all cores: the full rank-0 workload ({len(ev)} events, {nt} traces), a1..a6, best of {reps}; "
+                      f"1 core: its first {n1} traces ({len(ev1)} events)"}
 
 
 def run_reference(args):
-    """--impl reference: the oracle on the host cores (rank 0 only)."""
+    """--impl reference: the oracle on the host cores (rank 0 only; the other ranks exit)."""
     import tracegen
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -171,41 +193,68 @@ def run_reference(args):
     ev, off = tracegen.generate(cfg.with_traces(ntr))
     import oracle
     lib = oracle._load()
-    nt = len(off) - 1
-    cap = oracle.sample_bound(ev, off, cfg.T)
-    soff = np.zeros(nt + 1, dtype=np.uint64)
-    soff[1:] = np.cumsum(cap)
-    samples = np.zeros(max(int(soff[-1]), 1), dtype=oracle.SAMPLE_DTYPE)
-    summ = np.zeros(nt, dtype=oracle.SUMMARY_DTYPE)
-    table = np.zeros((cfg.n_sites, oracle.NCOL), dtype=np.uint64)
     cores = os.cpu_count() or 1
-
-    def step():
-        lib.orc_replay_all(oracle._ptr(ev), oracle._ptr(off), nt, cfg.n_sites, cfg.T, 0, cores,
-                           oracle._ptr(samples), oracle._ptr(soff), oracle._ptr(summ), oracle._ptr(table), None)
-        num, den, op = oracle.gate(summ)
-        prob, rate, flag = oracle.finalize(table, op, oracle.elapsed_ns(off))
-        oracle.report_order(rate, flag)
-
     for _ in range(args.warmup):
-        step()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        step()
-    dt = time.perf_counter() - t0
+        _oracle_pass(lib, oracle, ev, off, cfg, cores)
+    dt = sum(_oracle_pass(lib, oracle, ev, off, cfg, cores) for _ in range(args.steps))
     v = len(ev) * args.steps / dt
     print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": "events/s",
                       "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-                      "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+                      "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": args.scaling,
                       "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-                      "config": workload(cfg, ntr, 1),
+                      "config": workload(cfg, ntr, 1, ntr, args.scaling),
                       "cpu_baseline": {"value": v, "unit": "events/s", "cores": cores, "kind": "oracle",
+                                       "cpu_model": cpu_model(),
                                        "sample": f"full workload ({len(ev)} events) per step"},
                       "e2e": {"value": v, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
 
 
+def plan_launch(gpus: int, world_env, n_devices: int, impl: str = "native"):
+    """How this process runs (pure; tested on CPU): ("run", None) -- this process is the
+    rank (torchrun set WORLD_SIZE, or N = 1); ("spawn", None) -- start N NCCL ranks here with
+    torch.distributed.run; ("error", msg) -- the request cannot be honoured."""
+    if gpus < 1:
+        return "error", f"--gpus {gpus}: must be >= 1"
+    if world_env is not None:
+        if int(world_env) != gpus:
+            return "error", f"--gpus {gpus} but WORLD_SIZE={world_env}: launch one rank per GPU"
+        return "run", None
+    if gpus == 1 or impl == "reference":
+        return "run", None
+    if n_devices < gpus:
+        return "error", f"--gpus {gpus} needs {gpus} CUDA devices on this node, {n_devices} visible"
+    return "spawn", None
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def rank_traces(n_total: int, rank: int, world: int):
+    """Strong scaling: contiguous trace shard [t0, t1) of ``rank`` (sizes differ by at most 1)."""
+    q, r = divmod(n_total, world)
+    t0 = rank * q + min(rank, r)
+    return t0, t0 + q + (1 if rank < r else 0)
+
+
 def main():
     args = parse()
+    world_env = os.environ.get("WORLD_SIZE")
+    n_dev = 0
+    if world_env is None and args.gpus > 1 and args.impl != "reference":
+        import torch
+        n_dev = torch.cuda.device_count()
+    how, msg = plan_launch(args.gpus, world_env, n_dev, args.impl)
+    if how == "error":
+        print(f"bench.py: {msg}", file=sys.stderr)
+        sys.exit(2)
+    if how == "spawn":                               # one NCCL rank per GPU, started here
+        os.execv(sys.executable, [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                                  f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+                                  "--master-port", str(_free_port()), os.path.abspath(__file__), *sys.argv[1:]])
     if args.impl == "reference":
         return run_reference(args)
     import torch
@@ -214,28 +263,37 @@ def main():
     import paper_2212_07597_b200 as scl
     import tracegen
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = int(world_env or "1")
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = tracegen.CONFIGS[args.config]
-    ntr = args.traces or cfg.n_traces
-    gcfg = cfg.with_traces(ntr * world)
+    if args.scaling == "strong":                    # the config's traces, split across the ranks
+        n_total = args.traces or cfg.n_traces
+        t0, t1 = rank_traces(n_total, rank, world)
+    else:                                           # every rank a config-sized batch of its own
+        per = args.traces or cfg.n_traces
+        n_total = per * world
+        t0, t1 = rank * per, (rank + 1) * per
+    ntr = t1 - t0
+    gcfg = cfg.with_traces(n_total)
     # pinned host copy of this rank's traces (inputs of the e2e leg)
     n_ev = ntr * cfg.events_per_trace
-    pinned = torch.empty(n_ev * 2, dtype=torch.int64, pin_memory=True)
+    pinned = torch.empty(max(n_ev, 1) * 2, dtype=torch.int64, pin_memory=True)
     host_ev = pinned.numpy().view(tracegen.EVENT_DTYPE)
-    _, off_local = tracegen.generate(gcfg, rank * ntr, (rank + 1) * ntr, out=host_ev)
+    _, off_local = tracegen.generate(gcfg, t0, t1, out=host_ev)
+    host_ev = host_ev[:n_ev]
     stream = torch.cuda.current_stream()
     elapsed_ns = cfg.events_per_trace * 1000          # global max n_t * tick (all traces equal)
+    total_events_step = n_total * cfg.events_per_trace
 
     tr = scl.scl_trace_load(host_ev, off_local, cfg.n_sites, device=local)
     r = None
 
-    def step(r, timing=False):
-        r = scl.scl_replay_run(cfg.T, tr, stream=stream, out=r, defer_finalize=world > 1, elapsed_ns=elapsed_ns,
+    def step(r, timing=False, t=tr):
+        r = scl.scl_replay_run(cfg.T, t, stream=stream, out=r, defer_finalize=world > 1, elapsed_ns=elapsed_ns,
                                timing=timing)
         if world > 1:
             dist.all_reduce(scl.device_table_tensor(r))
@@ -244,7 +302,6 @@ def main():
 
     for _ in range(max(args.warmup, 3)):
         r = step(r)
-    kern_ms, n_samples = [], 0
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -255,8 +312,10 @@ def main():
             r = step(r)
         e1.record(stream)
         torch.cuda.synchronize()
-    # the replay kernel's own duration (roofline): the same K steps again with the library's
-    # CUDA events around the kernel (kept out of the timed loop above: ~2.5 us per event record)
+    if world > 1:
+        dist.barrier()
+    # the stream pass's own duration (roofline): the same K steps again with the library's CUDA
+    # events around its kernels (kept out of the timed loop above: ~2.5 us per event record)
     scl.scl_result_kernel_times(r)
     with ClockSampler(local) as clk2:
         for _ in range(args.steps):
@@ -264,15 +323,12 @@ def main():
         torch.cuda.synchronize()
     kern_ms = scl.scl_result_kernel_times(r)
     clk.samples += clk2.samples; clk.reasons |= clk2.reasons
-    if world > 1:
-        dist.barrier()
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    total_events = n_ev * world * args.steps
-    value = total_events / (ms_max / 1e3)
+    value = total_events_step * args.steps / (ms_max / 1e3)
 
     summ = scl.scl_trace_summaries(r)
     n_samples = int(summ["n_samples"].sum())
@@ -290,6 +346,7 @@ def main():
              "sample_log_bytes": {"rate": n_rate * 24, "threshold": n_samples * 32},
              "rate_kernels_ms": statistics.median(rate_ms),
              "note": "rate-based byte sampler, R = T, seed 2022, same traces (per rank)"}
+    del rr
     # K5: a threshold sweep (11 primes above 2^20 .. 2^30) as 11 full replays vs one stream pass
     # + 10 re-thresholds over it (per rank, results reused; device time on the bench stream)
     sweep = None
@@ -309,48 +366,56 @@ def main():
                                          for T_, r_ in zip(Ts[1:], sw[1:])])) for _ in range(2))
         sweep = {"thresholds": len(Ts), "full_replays_ms": ms_full, "one_pass_plus_rethreshold_ms": ms_sweep,
                  "note": "K5: scl_replay_sweep (one stream pass, the other thresholds re-chained over it)"}
+        for x in full + sw:
+            x.free()
         del full, sw
     kern_avg = statistics.mean(kern_ms)
     alg_bytes = n_ev * BYTES_PER_EVENT + n_samples * SAMPLE_BYTES + cfg.n_sites * ROW_BYTES_TABLE
     achieved = alg_bytes / (kern_avg / 1e3) / 1e9
     peak, peak_src = measured_peak()
     traffic = ncu_traffic(args.config)
+    launches = scl.scl_result_launches(r)           # kernels of one step (the library's count)
+    cold = launches > 2 + (0 if world == 1 else (1 if cfg.n_sites <= 16384 else 2))
 
     # e2e through the public API: H2D of this step's events from pinned memory, replay, report D2H
     e2e = None
     if not args.no_e2e:
         # the user's batch loop: refill a handle with the next batch of traces from pinned host
-        # memory (H2D inside the timed region), replay it, read the report back (D2H)
+        # memory (H2D inside the timed region), replay it, [all-reduce], read the report back (D2H)
+        tr.free()
+        r.free()
         torch.cuda.synchronize()
-        reps = max(3, min(10, args.steps))
+        reps = max(3, min(5, args.steps))
         trx = scl.scl_trace_load(host_ev, off_local, cfg.n_sites, device=local)
         rx = None
-        for _ in range(2):                             # warm: buffers sized, result allocated
-            scl.scl_trace_reload(trx, host_ev, off_local, cfg.n_sites, stream=stream)
-            rx = scl.scl_replay_run(cfg.T, trx, stream=stream, out=rx, defer_finalize=world > 1,
-                                    elapsed_ns=elapsed_ns)
-            rows = scl.scl_site_report(rx)
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(reps):
+
+        def e2e_step(rx):
             scl.scl_trace_reload(trx, host_ev, off_local, cfg.n_sites, stream=stream)
             rx = scl.scl_replay_run(cfg.T, trx, stream=stream, out=rx, defer_finalize=world > 1,
                                     elapsed_ns=elapsed_ns)
             if world > 1:
                 dist.all_reduce(scl.device_table_tensor(rx))
                 scl.scl_finalize(rx, elapsed_ns)
-            rows = scl.scl_site_report(rx)
+            return rx, scl.scl_site_report(rx)
+
+        for _ in range(2):                             # warm: buffers sized, result allocated
+            rx, rows = e2e_step(rx)
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
-        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        t0_ = time.perf_counter()
+        for _ in range(reps):
+            rx, rows = e2e_step(rx)
+        torch.cuda.synchronize()
+        dt = torch.tensor([time.perf_counter() - t0_], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-        e2e = {"value": n_ev * world * reps / float(dt.item()), "unit": "events/s",
+        e2e = {"value": total_events_step * reps / float(dt.item()), "unit": "events/s",
                "h2d_bytes_per_step": int(n_ev * 16 + off_local.nbytes),
                "d2h_bytes_per_step": int(rows.nbytes + 24),
-               "note": "per step: scl_trace_reload(pinned host events -> the handle's device buffers) + "
-                       "scl_replay_run + scl_site_report (wall clock, max over ranks)"}
+               "note": "per step and rank: scl_trace_reload(pinned host events -> the handle's device buffers) + "
+                       "scl_replay_run [+ all-reduce + scl_finalize] + scl_site_report (wall clock, max over ranks); "
+                       "bytes are rank 0's"}
         rx.free()
         trx.free()
 
@@ -361,21 +426,27 @@ def main():
         out = {
             "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic (tracegen, seeded)",
-            "config": workload(cfg, ntr, world),
-            "hbm_gbs_step": total_events * BYTES_PER_EVENT / (ms_max / 1e3) / 1e9,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "int64", "data": "synthetic (tracegen, seeded)",
+            "config": workload(cfg, ntr, world, n_total, args.scaling),
+            "hbm_gbs_step": total_events_step * BYTES_PER_EVENT / (ms_max / 1e3) / 1e9 / world,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "scl::replay_kernel",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "scl::replay_kernel" + (" + scl::cold_hist_kernel (Tier E of its cold-record "
+                                                           "stream; the stream pass a1-a5)" if cold else ""),
                          "kernel_ms": kern_avg, "peak_source": peak_src,
                          "alg_bytes_per_launch": alg_bytes,
                          "alg_bytes_rule": "16 B/event read + 32 B/sample written + 80 B/site table flush",
-                         "frac_of_8tbs_spec": achieved / 8000.0},
+                         "frac_of_8tbs_spec": achieved / 8000.0,
+                         "step_frac": total_events_step * BYTES_PER_EVENT / world / (ms_max / args.steps / 1e3) / 1e9 / peak},
             "clocks": clk.summary(),
             "e2e": e2e,
-            "gpu_launches": 2 * args.steps,
-            "gpu_launches_note": "per step: replay_kernel (its CTA 0 prepares the run), post_kernel (a6 grid-wide after its reclaim phases) "
-                                 "(tables > 16384 sites: finalize + CUB radix sort + rows instead of report)",
-            "kernel_timing": "replay_kernel durations from CUDA events in a second pass of K steps",
+            "gpu_launches": launches * args.steps,
+            "gpu_launches_note": "per step: replay_kernel (its CTA 0 prepares the run)" +
+                                 (", cold_hist_kernel" if cold else "") +
+                                 ", post_kernel (reclaim + per-sample reduce + a6 grid-wide)" if world == 1 else
+                                 ", post_kernel (reclaim + per-sample reduce), then after the all-reduce the a6 "
+                                 "kernel(s): report_kernel, or report_flags + report_rows above 16,384 sites",
+            "kernel_timing": "stream-pass kernel durations from the library's CUDA events in a second pass of K steps",
             "n_samples_per_step": n_samples,
             "next1_rate_vs_threshold": next1,
             "k5_threshold_sweep": sweep,

@@ -149,8 +149,9 @@ scl_status scl_trace_load(const char* path, const scl_event* events, const uint6
  * call returns after one synchronisation of that stream (the per-trace sample bounds come
  * back to the host).  Runs of this handle still in flight on ANOTHER stream must have
  * finished.  Results of the handle stay valid handles (re-sized on their next run); their
- * earlier contents are stale.  On SCL_EINVAL from the event check the handle holds no
- * traces until the next successful reload.
+ * earlier contents are stale.  On SCL_EINVAL from the event check, and on SCL_ENOMEM (a
+ * buffer could not grow: the old traces may already be overwritten), the handle holds no
+ * traces until the next successful reload (a run of it replays nothing).
  * Errors: as scl_trace_load. */
 scl_status scl_trace_reload(scl_traces* traces, const scl_event* events, const uint64_t* offsets,
                             uint32_t n_traces, uint32_t n_sites, int validate, void* cuda_stream);
@@ -167,7 +168,9 @@ scl_status scl_replay_run(uint64_t threshold, const scl_traces* traces,
 
 /* The same replay at another threshold over the handle's LAST stream pass (the scl_replay_run
  * that produced `base`): the per-unit summaries, Bloom filters and per-event (Tier E) site
- * counters of that pass are reused, so the events are not streamed again -- only the runners
+ * counters of that pass are reused (the handle keeps this rank's Tier E as the pass computed
+ * it, so a base whose table was since all-reduced, in the library or by the caller, does not
+ * count the other ranks twice), so the events are not streamed again -- only the runners
  * re-chain every trace (re-reading the rows where a sample fires) and the reclaim pass, the
  * per-sample reduce and a6 run for the new threshold (several thresholds, one
  * read of the events).  Output contract, options and errors as scl_replay_run; in addition
@@ -217,6 +220,12 @@ scl_status scl_result_timing(const scl_result* r, float* replay_kernel_ms, float
  * most the latest 128), oldest first; waits for them.  Lets a caller time many back-to-back runs
  * without synchronising between them.  *n = number written (<= cap). */
 scl_status scl_result_kernel_times(const scl_result* r, float* ms, size_t cap, size_t* n);
+
+/* Number of kernels the library launched for the result's last run and finalize (replay or
+ * re-chain kernel, the cold-site Tier-E reduce when n_sites > 4096, the post pass, and the a6
+ * kernels of a deferred finalize).  Host bookkeeping only: does not wait.
+ * Errors: SCL_EINVAL (NULL). */
+scl_status scl_result_launches(const scl_result* r, uint32_t* n);
 
 /* ---- Per-sample Python / native split ("the fraction of Python
  * (vs. native) allocations in the total sample"): for each threshold sample,

@@ -19,7 +19,7 @@ from . import _build
 
 __all__ = ["SclError", "Traces", "Result", "scl_trace_load", "scl_trace_reload", "scl_replay_run", "scl_replay_rethreshold", "scl_replay_sweep", "scl_finalize",
            "scl_site_report", "scl_samples", "scl_trace_summaries", "scl_gate", "scl_result_device_table",
-           "scl_result_timing", "scl_result_kernel_times", "scl_next_prime", "scl_traces_info", "EVENT_DTYPE", "SAMPLE_DTYPE",
+           "scl_result_timing", "scl_result_kernel_times", "scl_result_launches", "scl_next_prime", "scl_traces_info", "EVENT_DTYPE", "SAMPLE_DTYPE",
            "SUMMARY_DTYPE", "SITE_ROW_DTYPE", "COLS", "device_table_tensor", "write_trace_file",
            "DOMAIN_DTYPE", "scl_sample_domains", "scl_trace_recon_error", "RATE_SAMPLE_DTYPE", "RATE_ALLOC_FREE", "RATE_COPY", "RateResult", "scl_rate_run", "scl_rate_counts",
            "scl_rate_samples", "scl_rate_site_counts", "scl_rate_timing"]
@@ -63,6 +63,7 @@ def _load():
         "scl_trace_load": [ctypes.c_char_p, P, P, U32, U32, I32, I32, P],
         "scl_trace_reload": [P, P, P, U32, U32, I32, P],
         "scl_result_kernel_times": [P, P, SZ, P],
+        "scl_result_launches": [P, P],
         "scl_rate_run": [U64, U64, U32, P, P, P],
         "scl_sample_domains": [P, U32, P, SZ, P],
         "scl_trace_recon_error": [P, P, SZ, P],
@@ -263,7 +264,11 @@ def device_table_tensor(r: Result):
 
     class _Iface:
         __cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (ptr, False), "version": 2}
-    return torch.as_tensor(_Iface(), device="cuda")
+    # no device argument: the tensor stays on the pointer's own device (never a copy on the
+    # current device, which an all-reduce would update instead of the library's table)
+    t = torch.as_tensor(_Iface())
+    assert t.data_ptr() == ptr, "device_table_tensor must alias the library's table"
+    return t
 
 
 def scl_finalize(r: Result, elapsed_ns: int = 0):
@@ -343,6 +348,13 @@ def scl_result_kernel_times(r: Result) -> list:
     n = ctypes.c_size_t()
     _check(lib.scl_result_kernel_times(r.handle, buf, 128, ctypes.byref(n)))
     return [buf[i] for i in range(n.value)]
+
+
+def scl_result_launches(r: Result) -> int:
+    """Kernels the library launched for the result's last run (+ its finalize)."""
+    n = ctypes.c_uint32()
+    _check(lib.scl_result_launches(r.handle, ctypes.byref(n)))
+    return n.value
 
 
 def scl_next_prime(base: int) -> int:

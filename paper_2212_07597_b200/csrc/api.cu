@@ -9,7 +9,6 @@
 #include "scl_internal.cuh"
 #include "report.cuh"
 #include <cudaTypedefs.h>
-#include <cub/device/device_radix_sort.cuh>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -58,6 +57,15 @@ struct scl_traces {
     mutable unsigned long long *d_usum = nullptr, *d_ustart = nullptr, *d_ttot = nullptr;
     mutable size_t cap_usum = 0, cap_ttot = 0;
     mutable bool usum_valid = false;
+    // cold-record stream of the sites beyond the shared-memory table (n_sites > kWarm), per stream pass
+    mutable unsigned long long* d_crec = nullptr;
+    mutable unsigned* d_crec_fill = nullptr;
+    mutable unsigned long long* d_cctr = nullptr;       // [2] records allocated, exhausted
+    mutable unsigned long long crec_cap = 0;
+    mutable unsigned long long* h_covf = nullptr;       // pinned: the last exhausted pool (grow it)
+    // Tier-E columns of the last stream pass (written by its post pass; a re-threshold copies them)
+    mutable unsigned long long* d_tierE = nullptr;
+    mutable size_t cap_tierE = 0;
 };
 
 constexpr int kRing = 128;
@@ -79,12 +87,12 @@ struct scl_result {
     scl_trace_summary* d_summ = nullptr;
     size_t cap_sites = 0, cap_tr = 0;
     int grid = 0;
-    double* d_prob = nullptr; double* d_rate = nullptr; unsigned char* d_flag = nullptr;
-    unsigned long long *d_key = nullptr, *d_key2 = nullptr; unsigned int *d_val = nullptr, *d_order = nullptr;
-    void* d_cub = nullptr; size_t cub_bytes = 0;
     scl_site_row* d_rows = nullptr;
     RTask* d_rtask = nullptr;                  // reclaim pass re-check queue
     unsigned* d_rbits = nullptr; double* d_rlrate = nullptr; unsigned* d_rlsite = nullptr;   // a6 scratch
+    unsigned* d_rsb = nullptr;                 // [n_sb + 1]: a6 superblock flag counts, then the flagged count
+    unsigned n_sb = 0;
+    unsigned nlaunch = 0;                      // kernels launched by the last run (+ its finalize)
     unsigned long long* d_P = nullptr;         // per-sample (alloc, managed) prefixes (NEXT-2, lazy)
     scl_sample_domain* d_dom = nullptr;
     size_t cap_dom = 0;
@@ -110,6 +118,14 @@ static bool is_device_ptr(const void* p) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// The device's view of pinned host memory (cudaHostAlloc / cudaHostRegister, mapped under UVA), or
+// NULL for pageable memory (which only the DMA path of cudaMemcpy can read).
+static const scl_event* mapped_host(const scl_event* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    return a.type == cudaMemoryTypeHost && a.devicePointer ? (const scl_event*)a.devicePointer : nullptr;
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -214,12 +230,18 @@ static scl_status upload(scl_traces* tr, const scl_event* src, bool src_dev, std
                                        "): load them in waves");
     }
     const uint64_t rows_alloc = std::max<uint64_t>((n + 7) / 8, 1);
+    // After a failed allocation the handle holds no traces (its buffers may already be replaced):
+    // every count is 0 and earlier results are stale, so no later run reads freed memory.
+    auto nomem = [&](const char* what) {
+        tr->n_traces = 0; tr->n_events = 0; tr->n_segs = 0; tr->max_len = 0; tr->epoch += 1;
+        return fail(SCL_ENOMEM, std::string("out of device memory: ") + what + " (the handle now holds no traces)");
+    };
     // + kPadRows zeroed rows: a candidate chunk's lanes past the last event of the last trace
     // re-read up to 31 rows beyond it (load_row_global); they land here, not past the mapping.
     constexpr uint64_t kPadRows = 32;
     if (rows_alloc > tr->cap_rows) {
         cudaFree(tr->d_ev); tr->d_ev = nullptr; tr->cap_rows = 0;
-        if (cudaMalloc(&tr->d_ev, (rows_alloc + kPadRows) * 128) != cudaSuccess) { cudaGetLastError(); tr->d_ev = nullptr; return fail(SCL_ENOMEM, "events"); }
+        if (cudaMalloc(&tr->d_ev, (rows_alloc + kPadRows) * 128) != cudaSuccess) { cudaGetLastError(); tr->d_ev = nullptr; return nomem("events"); }
         tr->cap_rows = rows_alloc;
     }
     const size_t nt1 = std::max<uint32_t>(n_traces, 1);
@@ -227,21 +249,26 @@ static scl_status upload(scl_traces* tr, const scl_event* src, bool src_dev, std
         tr->cap_tr = 0;
         if (!grow(tr->d_off, nt1 + 1) || !grow(tr->d_sabs, nt1) || !grow(tr->d_tr_nseg, nt1) ||
             !grow(tr->d_tr_base, nt1) || !grow(tr->d_run, nt1))
-            return fail(SCL_ENOMEM, "per-trace buffers");
+            return nomem("per-trace buffers");
         tr->cap_tr = nt1;
     }
     if (!tr->d_err) {
-        if (!grow(tr->d_err, 1) || !grow(tr->d_ticket, 8)) return fail(SCL_ENOMEM, "counters");
+        if (!grow(tr->d_err, 1) || !grow(tr->d_ticket, 8)) { cudaFree(tr->d_err); tr->d_err = nullptr; return nomem("counters"); }
         // ticket[7] is the "run prepared" flag compared with the run's epoch: a fresh block may hold
         // a freed handle's epoch (fuzzing found producers starting before CTA 0 had prepared)
         CU(cudaMemsetAsync(tr->d_ticket, 0, 8 * sizeof(unsigned), st));
     }
-    if (n > 0) CU(cudaMemcpyAsync(tr->d_ev, src, n * sizeof(scl_event), src_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    // A device source or pinned host memory is copied by the statistics pass itself (one read of the
+    // source, one write to HBM -- the events are not read back); pageable memory takes the DMA copy.
+    const scl_event* csrc = n == 0 ? nullptr : src_dev ? src : mapped_host(src);
+    if (csrc && (reinterpret_cast<uintptr_t>(csrc) & 15u)) csrc = nullptr;
+    if (n > 0 && !csrc) CU(cudaMemcpyAsync(tr->d_ev, src, n * sizeof(scl_event), src_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
     CU(cudaMemsetAsync(tr->d_ev + n, 0, ((rows_alloc + kPadRows) * 8 - n) * sizeof(scl_event), st));
     CU(cudaMemcpyAsync(tr->d_off, h_off.data(), h_off.size() * 8, cudaMemcpyHostToDevice, st));
     CU(cudaMemsetAsync(tr->d_sabs, 0, nt1 * 8, st));
     CU(cudaMemsetAsync(tr->d_err, 0xff, 8, st));
-    CU(launch_load_stats(tr->d_ev, tr->d_off, n_traces, n, n_sites, tr->d_sabs, tr->d_err, st));
+    CU(launch_load_stats(csrc ? csrc : tr->d_ev, tr->d_off, n_traces, n, n_sites, tr->d_sabs, tr->d_err,
+                         csrc ? tr->d_ev : nullptr, st));
 
     // unit plan (while the copy runs): unit k of trace t covers rows (off_t/8) + 1024k ...;
     // tickets ordered (k, t) so that one trace's units are spread over the run
@@ -274,7 +301,7 @@ static scl_status upload(scl_traces* tr, const scl_event* src, bool src_dev, std
         cudaFree(tr->d_urec); tr->d_urec = nullptr;
         if (!grow(tr->d_tk, nn) || !grow(tr->d_uagg, nn * 4) || !grow(tr->d_uent, nn) ||
             cudaMalloc(&tr->d_urec, nn * replay_urec_bytes()) != cudaSuccess)
-            { cudaGetLastError(); return fail(SCL_ENOMEM, "unit plan"); }
+            { cudaGetLastError(); tr->d_urec = nullptr; return nomem("unit plan"); }
         tr->cap_segs = nn;
     }
     // no aggregate word of an earlier trace set survives a (re)load: a unit index unused for a
@@ -372,6 +399,8 @@ extern "C" void scl_traces_free(scl_traces* t) {
     cudaFree(t->d_ev); cudaFree(t->d_off); cudaFree(t->d_sabs); cudaFree(t->d_tk); cudaFree(t->d_urec); cudaFree(t->d_uagg);
     cudaFree(t->d_tr_nseg); cudaFree(t->d_tr_base); cudaFree(t->d_run); cudaFree(t->d_uent); cudaFree(t->d_ticket);
     cudaFree(t->d_err); cudaFree(t->d_usum); cudaFree(t->d_ustart); cudaFree(t->d_ttot);
+    cudaFree(t->d_crec); cudaFree(t->d_crec_fill); cudaFree(t->d_cctr); cudaFree(t->d_tierE);
+    if (t->h_covf) cudaFreeHost(t->h_covf);
     delete t;
 }
 
@@ -385,12 +414,10 @@ extern "C" scl_status scl_traces_info(const scl_traces* t, uint64_t* n_events, u
 
 // ---------------------------------------------------------------- run
 static void free_result_buffers(scl_result* r) {
-    cudaFree(r->d_table); cudaFree(r->d_sbase); cudaFree(r->d_summ); cudaFree(r->d_prob); cudaFree(r->d_rate);
-    cudaFree(r->d_flag); cudaFree(r->d_key); cudaFree(r->d_key2); cudaFree(r->d_val); cudaFree(r->d_order);
-    cudaFree(r->d_cub); cudaFree(r->d_rows);
-    r->d_table = nullptr; r->d_sbase = nullptr; r->d_summ = nullptr; r->d_prob = nullptr; r->d_rate = nullptr;
-    r->d_flag = nullptr; r->d_key = nullptr; r->d_key2 = nullptr; r->d_val = nullptr; r->d_order = nullptr;
-    r->d_cub = nullptr; r->d_rows = nullptr;
+    cudaFree(r->d_table); cudaFree(r->d_sbase); cudaFree(r->d_summ); cudaFree(r->d_rows);
+    cudaFree(r->d_rbits); cudaFree(r->d_rsb);
+    r->d_table = nullptr; r->d_sbase = nullptr; r->d_summ = nullptr; r->d_rows = nullptr;
+    r->d_rbits = nullptr; r->d_rsb = nullptr;
     r->cap_sites = 0; r->cap_tr = 0;
 }
 
@@ -398,7 +425,7 @@ extern "C" void scl_result_free(scl_result* r) {
     if (!r) return;
     free_result_buffers(r);
     cudaFree(r->d_samples); cudaFree(r->d_epflag); cudaFree(r->d_prof); cudaFree(r->d_rtask);
-    cudaFree(r->d_rbits); cudaFree(r->d_rlrate); cudaFree(r->d_rlsite);
+    cudaFree(r->d_rlrate); cudaFree(r->d_rlsite);
     cudaFree(r->d_P); cudaFree(r->d_dom); cudaFree(r->d_recon); cudaFree(r->d_el);
     if (r->h_gate) cudaFreeHost(r->h_gate);
     for (auto& e : r->ev) if (e) cudaEventDestroy(e);
@@ -414,7 +441,6 @@ static scl_status alloc_result(scl_result* r, const scl_traces* tr) {
         for (auto& e : r->kev) CU(cudaEventCreate(&e));
         CU(cudaMallocHost(&r->h_gate, 32));
         CU(cudaMalloc(&r->d_rtask, (size_t)kRTaskCap * sizeof(RTask)));
-        CU(cudaMalloc(&r->d_rbits, kReportSites / 32 * 4));
         CU(cudaMalloc(&r->d_rlrate, kReportList * 8)); CU(cudaMalloc(&r->d_rlsite, kReportList * 4));
         int grid = 0;
         replay_occupancy(&grid);
@@ -425,14 +451,11 @@ static scl_status alloc_result(scl_result* r, const scl_traces* tr) {
     CU(cudaMalloc(&r->d_table, (S * SCL_NCOL + 3) * 8));
     CU(cudaMalloc(&r->d_sbase, nt * 8));
     CU(cudaMalloc(&r->d_summ, nt * sizeof(scl_trace_summary)));
-    CU(cudaMalloc(&r->d_prob, S * 8)); CU(cudaMalloc(&r->d_rate, S * 8)); CU(cudaMalloc(&r->d_flag, S));
-    CU(cudaMalloc(&r->d_key, S * 8)); CU(cudaMalloc(&r->d_key2, S * 8));
-    CU(cudaMalloc(&r->d_val, S * 4)); CU(cudaMalloc(&r->d_order, S * 4));
+    const size_t nwd = (std::max<size_t>(S, kReportSites) + 31) / 32;
+    CU(cudaMalloc(&r->d_rbits, nwd * 4));
+    r->n_sb = (unsigned)((nwd + kSuper - 1) / kSuper);
+    CU(cudaMalloc(&r->d_rsb, (r->n_sb + 1) * 4));
     CU(cudaMalloc(&r->d_rows, S * sizeof(scl_site_row)));
-    size_t tb = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, r->d_key, r->d_key2, r->d_val, r->d_order, (int)S);
-    r->cub_bytes = std::max<size_t>(tb, 1);
-    CU(cudaMalloc(&r->d_cub, r->cub_bytes));
     r->cap_sites = S; r->cap_tr = nt;
     return SCL_OK;
 }
@@ -441,7 +464,6 @@ static FinalParams final_params(scl_result* r) {
     FinalParams f{};
     f.table = r->d_table; f.n_sites = r->tr->n_sites; f.formula = r->formula;
     f.elapsed_ns = (double)(r->elapsed_ns ? r->elapsed_ns : 1);
-    f.prob = r->d_prob; f.rate = r->d_rate; f.flag = r->d_flag; f.key1 = r->d_key; f.val = r->d_val;
     f.gate_out = r->h_gate;                    // pinned host memory, device-accessible (unified addressing)
     f.prof = r->d_prof;
     return f;
@@ -455,6 +477,30 @@ static AllReduceFn nccl_allreduce() {
         return h ? (AllReduceFn)dlsym(h, "ncclAllReduce") : nullptr;
     }();
     return fn;
+}
+
+// Cold-record pool of a stream pass (n_sites > kWarm): room for 5/16 of the events plus one partial
+// chunk per compute warp; a pass that exhausts it is still exact (the rest of its cold events take
+// the direct L2 path) and the next pass gets twice the room.  Best effort: no pool = all L2.
+static void ensure_cold_pool(const scl_traces* tr) {
+    if (tr->n_sites <= (uint32_t)kWarm) return;
+    if (!tr->d_cctr) {
+        if (cudaMalloc(&tr->d_cctr, 16) != cudaSuccess) { cudaGetLastError(); tr->d_cctr = nullptr; return; }
+        cudaMemset(tr->d_cctr, 0, 16);
+        if (cudaHostAlloc(&tr->h_covf, 8, cudaHostAllocMapped) != cudaSuccess) { cudaGetLastError(); tr->h_covf = nullptr; }
+        else *tr->h_covf = 0;
+    }
+    unsigned long long want = tr->n_events / 16 * 5 + 4096ull * kRecChunk;
+    if (tr->h_covf && *tr->h_covf) { want = std::max(want, 2 * tr->crec_cap); *tr->h_covf = 0; }
+    want = std::min<unsigned long long>(want, tr->n_events + 4096ull * kRecChunk);
+    want = (want + kRecChunk - 1) / kRecChunk * kRecChunk;
+    if (want <= tr->crec_cap) return;
+    cudaFree(tr->d_crec); cudaFree(tr->d_crec_fill); tr->d_crec = nullptr; tr->d_crec_fill = nullptr; tr->crec_cap = 0;
+    if (cudaMalloc(&tr->d_crec, want * 8) != cudaSuccess ||
+        cudaMalloc(&tr->d_crec_fill, want / kRecChunk * 4) != cudaSuccess) {
+        cudaGetLastError(); cudaFree(tr->d_crec); tr->d_crec = nullptr; tr->d_crec_fill = nullptr; return;
+    }
+    tr->crec_cap = want;
 }
 
 static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const scl_run_opts* opts, scl_result** out,
@@ -485,6 +531,7 @@ static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const sc
     const uint64_t tick = o.tick_ns ? o.tick_ns : tr->tick_ns;
     r->elapsed_ns = o.elapsed_ns ? o.elapsed_ns : tr->max_len * tick;
     r->summ_valid = false; r->finalized = false; r->dom_valid = false; r->recon_valid = false;
+    r->nlaunch = 0;
 
     // sample capacity per trace: min(n_t, floor(sum|d| / T)) -- every sample consumes |net| >= T
     // (CTA 0 of the replay kernel computes the same bases on the device; the host copy serves scl_samples)
@@ -527,11 +574,21 @@ static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const sc
     p.n_sites = tr->n_sites; p.n_traces = NT; p.T = (long long)threshold; p.hwm_sample = o.hwm_mode == SCL_HWM_SAMPLE;
     p.table = r->d_table; p.samples = r->d_samples; p.ep_flag = r->d_epflag; p.sbase = r->d_sbase;
     p.summ = r->d_summ; p.uent = tr->d_uent;
+    if (!base) ensure_cold_pool(tr);
+    p.crec = tr->d_crec; p.crec_cap = tr->crec_cap; p.cctr = tr->d_cctr; p.crec_fill = tr->d_crec_fill;
+    p.covf = tr->h_covf;
+    if (tr->n_sites > tr->cap_tierE) {
+        cudaFree(tr->d_tierE); tr->d_tierE = nullptr; tr->cap_tierE = 0;
+        if (cudaMalloc(&tr->d_tierE, (size_t)tr->n_sites * 32) != cudaSuccess) { cudaGetLastError(); if (fresh) scl_result_free(r); return fail(SCL_ENOMEM, "tier E"); }
+        tr->cap_tierE = tr->n_sites;
+    }
+    p.tierE = tr->d_tierE;
     PrepParams& pp = p.prep;                   // done by CTA 0 of the replay kernel
     pp.table = r->d_table; pp.table_words = (size_t)tr->n_sites * SCL_NCOL + 3;
     pp.summ = reinterpret_cast<unsigned long long*>(r->d_summ); pp.summ_words = (size_t)NT * sizeof(scl_trace_summary) / 8;
     pp.run = reinterpret_cast<unsigned long long*>(tr->d_run); pp.run_words = (size_t)NT * sizeof(RunState) / 8;
     pp.ticket = tr->d_ticket; pp.sbase = r->d_sbase; pp.off = tr->d_off; pp.sabs = tr->d_sabs;
+    pp.rsbcnt = r->d_rsb; pp.n_sb = r->n_sb;
     pp.n_traces = NT; pp.T = threshold; p.rtask = r->d_rtask; p.rtask_cap = kRTaskCap;
 #ifdef SCL_PROFILE
     if (!r->d_prof) CU(cudaMalloc(&r->d_prof, (48 + 4 * (size_t)tr->cap_segs) * 8));
@@ -545,29 +602,35 @@ static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const sc
         CU(cudaMemsetAsync(pp.table, 0, pp.table_words * 8, st));
         CU(cudaMemsetAsync(pp.summ, 0, pp.summ_words * 8, st));
         CU(cudaMemsetAsync(tr->d_ticket, 0, 7 * 4, st));
+        CU(cudaMemsetAsync(r->d_rsb, 0, r->n_sb * 4, st));
         if (NT) CU(cudaMemcpyAsync(r->d_sbase, r->h_sbase.data(), (size_t)NT * 8, cudaMemcpyHostToDevice, st));
     }
-    if (base) {                                // the per-event columns (Tier E) of the stream pass
+    if (base) {                                // the per-event columns (Tier E) of the stream pass, as its
+                                               // post pass kept them (base's own table may be reduced since)
         CU(cudaMemsetAsync(pp.run, 0, pp.run_words * 8, st));
         if (tr->n_sites)
-            CU(cudaMemcpy2DAsync(r->d_table, SCL_NCOL * 8, base->d_table, SCL_NCOL * 8, 4 * 8, tr->n_sites,
+            CU(cudaMemcpy2DAsync(r->d_table, SCL_NCOL * 8, tr->d_tierE, 4 * 8, 4 * 8, tr->n_sites,
                                  cudaMemcpyDeviceToDevice, st));
         p.rechain = 1;
         p.n_runners = std::min<unsigned>(NT, (unsigned)r->grid * 8);
         CU(launch_rechain(p, st));
+        r->nlaunch += tr->n_segs ? 1 : 0;
     } else {
         CU(launch_replay(&tr->tmap, p, r->grid, st));
+        CU(launch_cold_hist(p, st));           // Tier E of the sites beyond the shared-memory table
+        r->nlaunch += (tr->n_segs ? 1 : 0) + (cold_hist_launched(p) ? 1 : 0);
     }
     if (tm) { CU(cudaEventRecord(r->kev[2 * ks + 1], st)); r->nrun += 1; }
     // a6 fused into the post pass when the run finalizes at once on a small table (not when the
     // table is first reduced across ranks)
     const bool reduce = o.nccl_comm != nullptr;
-    const bool fuse = !o.defer_finalize && !reduce && report_fused(tr->n_sites);
+    const bool fuse = !o.defer_finalize && !reduce;
     if (fuse) {
         p.fuse_report = 1; p.fin = final_params(r); p.rows = r->d_rows;
-        p.rbits = r->d_rbits; p.rlrate = r->d_rlrate; p.rlsite = r->d_rlsite;
+        p.rbits = r->d_rbits; p.rlrate = r->d_rlrate; p.rlsite = r->d_rlsite; p.rsbcnt = r->d_rsb;
     }
     CU(launch_post(p, st));
+    r->nlaunch += 1;
     if (tm) CU(cudaEventRecord(r->ev[1], st));
     if (fuse) {
         if (tm) CU(cudaEventRecord(r->ev[2], st));
@@ -631,11 +694,12 @@ extern "C" scl_status scl_finalize(scl_result* r, uint64_t elapsed_ns) {
     const FinalParams f = final_params(r);
     if (report_fused(S)) {
         CU(launch_report(f, r->d_rows, st));
-    } else {
-        CU(launch_finalize(f, st));
-        size_t tb = r->cub_bytes;
-        CU(cub::DeviceRadixSort::SortPairs(r->d_cub, tb, r->d_key, r->d_key2, r->d_val, r->d_order, (int)S, 0, 64, st));
-        CU(launch_rows(r->d_table, r->d_prob, r->d_rate, r->d_flag, r->d_order, S, r->d_rows, st));
+        r->nlaunch += 1;
+    } else {                                   // larger tables: the grid a6 of report.cuh in two kernels
+        CU(cudaMemsetAsync(r->d_rsb, 0, (r->n_sb + 1) * 4, st));
+        const ReportScratch x{r->d_rbits, r->d_rlrate, r->d_rlsite, r->d_rsb + r->n_sb, r->d_rsb};
+        CU(launch_report_grid(f, x, r->d_rows, st));
+        r->nlaunch += 2;
     }
     CU(cudaEventRecord(r->ev[3], st));
     r->finalized = true;
@@ -738,6 +802,12 @@ extern "C" scl_status scl_result_timing(const scl_result* r, float* replay_kerne
     if (replay_kernel_ms) *replay_kernel_ms = k;
     if (run_ms) *run_ms = a;
     if (finalize_ms) *finalize_ms = f;
+    return SCL_OK;
+}
+
+extern "C" scl_status scl_result_launches(const scl_result* r, uint32_t* n) {
+    if (!r || !n) return fail(SCL_EINVAL, "NULL argument");
+    *n = r->nlaunch;
     return SCL_OK;
 }
 

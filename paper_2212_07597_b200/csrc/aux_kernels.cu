@@ -1,7 +1,8 @@
 // aux_kernels.cu -- small sm_100a kernels around the streaming replay kernel:
 //   load_stats_kernel  per-trace sum|d| (sample-capacity bound) + argument check, at load time
-//   finalize_kernel    a6: leak probability, rate, flag, sort key
-//   rows_kernel        report rows in report order
+//   report_kernel      a6 in one block (tables <= kReportSites): probability, rate
+//                      (P:65-69), flag, report order and rows
+//   report_flags_kernel / report_rows_kernel   the same over a grid, for larger tables
 #include "scl_internal.cuh"
 #include "ptx.cuh"
 #include "report.cuh"
@@ -13,11 +14,13 @@ namespace scl {
 // Per trace: sum |d| over alloc/free events (the sample-capacity bound floor(sum|d|/T)), and
 // the first invalid event (size 0, kind 3, site >= n_sites).  One warp per 256-event chunk
 // (grid-stride, 8 events = one 128-B row per lane); a chunk inside one trace is reduced in the
-// warp before its single atomic.
+// warp before its single atomic.  dst != NULL: the same pass is the load's copy (ev: the caller's
+// device buffer or pinned host memory mapped into the device's address space; dst: the handle's
+// device copy), so the events reach HBM once and are not read back for the statistics.
 __global__ void __launch_bounds__(256) load_stats_kernel(const scl_event* ev, const unsigned long long* off,
                                                          unsigned n_traces, unsigned long long n_events,
                                                          unsigned n_sites, unsigned long long* sabs,
-                                                         unsigned long long* err)
+                                                         unsigned long long* err, scl_event* dst)
 {
     const int lane = threadIdx.x & 31;
     const unsigned long long wid = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -33,6 +36,11 @@ __global__ void __launch_bounds__(256) load_stats_kernel(const scl_event* ev, co
         ulonglong2 v[8];
         #pragma unroll
         for (int j = 0; j < 8; ++j) v[j] = i0 + j < n_events ? __ldcs(q + j) : make_ulonglong2(0, 0);
+        if (dst) {
+            ulonglong2* o = reinterpret_cast<ulonglong2*>(dst + i0);
+            #pragma unroll
+            for (int j = 0; j < 8; ++j) if (i0 + j < n_events) o[j] = v[j];
+        }
         unsigned long long acc = 0;
         bool split = false;
         #pragma unroll
@@ -61,19 +69,21 @@ __global__ void __launch_bounds__(256) load_stats_kernel(const scl_event* ev, co
     }
 }
 
-// ============================================================================ a6
-__global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ FinalParams p)
+// ============================================================================ a6 (report.cuh)
+// Tables above kReportSites after a deferred finalize: C1 (flags, flagged list) and C2 (ranks, rows)
+// as two stream-ordered grid kernels (the launch boundary is the grid barrier of the fused path).
+constexpr int kRptThreads = 256;
+__global__ void __launch_bounds__(kRptThreads) report_flags_kernel(const __grid_constant__ FinalParams p, ReportScratch x)
 {
-    const bool open = gate_open(p);
-    if (blockIdx.x == 0 && threadIdx.x == 0) gate_copy(p);
-    for (unsigned sidx = blockIdx.x * blockDim.x + threadIdx.x; sidx < p.n_sites; sidx += gridDim.x * blockDim.x) {
-        const SiteStat st = site_stat(p, sidx, open);
-        p.prob[sidx] = st.prob; p.rate[sidx] = st.rate; p.flag[sidx] = st.flag ? 1 : 0;
-        // report order key: flagged by rate desc (rate >= 0, so ~bits is descending), others last;
-        // a stable radix sort over site-ordered input breaks ties by site asc.
-        p.key1[sidx] = st.flag ? ~(unsigned long long)__double_as_longlong(st.rate) : ~0ull;
-        p.val[sidx] = sidx;
-    }
+    const unsigned wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    report_grid_flags(p, x, wid, nw, threadIdx.x & 31);
+}
+__global__ void __launch_bounds__(kRptThreads) report_rows_kernel(const __grid_constant__ FinalParams p, ReportScratch x,
+                                                                 scl_site_row* rows)
+{
+    __shared__ unsigned long long stg[kRptThreads / 32][32 * kRowWords];
+    const unsigned wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    report_grid_rows(p, rows, x, stg[threadIdx.x >> 5], wid, nw, threadIdx.x & 31);
 }
 
 // Whole a6 in one block (n_sites <= kReportSites): report.cuh.
@@ -83,30 +93,15 @@ __global__ void __launch_bounds__(512) report_kernel(const __grid_constant__ Fin
     report_block<512>(p, rows, *reinterpret_cast<ReportSmem<512>*>(report_smem));
 }
 
-__global__ void __launch_bounds__(256) rows_kernel(const unsigned long long* table, const double* prob, const double* rate,
-                                                   const unsigned char* flag, const unsigned int* order, unsigned n_sites,
-                                                   scl_site_row* rows)
-{
-    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n_sites; i += gridDim.x * blockDim.x) {
-        const unsigned sidx = order[i];
-        scl_site_row r;
-        r.site = sidx; r.leak_flag = flag[sidx];
-        #pragma unroll
-        for (int c = 0; c < SCL_NCOL; ++c) r.col[c] = table[(size_t)sidx * SCL_NCOL + c];
-        r.leak_prob = prob[sidx]; r.leak_rate_mbps = rate[sidx];
-        rows[i] = r;
-    }
-}
-
 // ============================================================================ launch wrappers
 cudaError_t launch_load_stats(const scl_event* ev, const unsigned long long* off, unsigned n_traces,
                               unsigned long long n_events, unsigned n_sites, unsigned long long* sabs,
-                              unsigned long long* err, cudaStream_t st)
+                              unsigned long long* err, scl_event* dst, cudaStream_t st)
 {
     if (n_traces == 0 || n_events == 0) return cudaSuccess;
     const unsigned long long warps = (n_events + 255) / 256;
     const unsigned blocks = (unsigned)std::min<unsigned long long>((warps + 7) / 8, 148ull * 8);
-    load_stats_kernel<<<blocks, 256, 0, st>>>(ev, off, n_traces, n_events, n_sites, sabs, err);
+    load_stats_kernel<<<blocks, 256, 0, st>>>(ev, off, n_traces, n_events, n_sites, sabs, err, dst);
     return cudaGetLastError();
 }
 
@@ -125,23 +120,14 @@ cudaError_t launch_report(const FinalParams& p, scl_site_row* rows, cudaStream_t
     return cudaGetLastError();
 }
 
-cudaError_t launch_finalize(const FinalParams& p, cudaStream_t st)
+cudaError_t launch_report_grid(const FinalParams& p, const ReportScratch& x, scl_site_row* rows, cudaStream_t st)
 {
-    unsigned blocks = (p.n_sites + 255) / 256;
-    if (blocks > 4096) blocks = 4096;
-    if (blocks == 0) blocks = 1;
-    finalize_kernel<<<blocks, 256, 0, st>>>(p);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_rows(const unsigned long long* table, const double* prob, const double* rate,
-                        const unsigned char* flag, const unsigned int* order, unsigned n_sites,
-                        scl_site_row* rows, cudaStream_t st)
-{
-    unsigned blocks = (n_sites + 255) / 256;
-    if (blocks > 4096) blocks = 4096;
-    if (blocks == 0) blocks = 1;
-    rows_kernel<<<blocks, 256, 0, st>>>(table, prob, rate, flag, order, n_sites, rows);
+    const unsigned words = (p.n_sites + 31) / 32;
+    const unsigned blocks = std::max(1u, std::min((words + kRptThreads / 32 - 1) / (kRptThreads / 32), 148u * 8));
+    report_flags_kernel<<<blocks, kRptThreads, 0, st>>>(p, x);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    report_rows_kernel<<<blocks, kRptThreads, 0, st>>>(p, x, rows);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,105 @@
+// cold_hist.cu -- Tier E (a5: per-site malloc / free counts and bytes) of the sites that
+// do not fit the replay kernel's shared-memory table (site >= kWarm when n_sites > kHot).
+//
+// The stream pass writes the meta word of every such alloc / free to the cold-record stream
+// (chunks of kRecChunk records, one compute warp's at a time); this kernel reduces the stream per
+// (site, kind) in shared memory and adds the sums to the site table.  The cold sites are split into
+// ranges of kColdSites sites (2 kinds x 4 B packed count:8 | bytes:24 per site = 224 KiB); CTA b
+// takes range b % R of the chunks of group b / R, so the R CTAs that read the same chunks are
+// adjacent and run together (the second read of a chunk hits L2).  Carries out of a packed field
+// are corrected exactly in the L2 table (as in replay_kernel); a size >= 2^24 goes to L2 directly.
+#include "scl_internal.cuh"
+#include "ptx.cuh"
+#include <algorithm>
+
+namespace scl {
+
+__global__ void __launch_bounds__(1024, 1) cold_hist_kernel(const __grid_constant__ ReplayParams p, unsigned R)
+{
+    extern __shared__ __align__(16) unsigned ctab[];          // [2][kColdSites]
+    const unsigned r = blockIdx.x % R, G = gridDim.x / R, g = blockIdx.x / R;
+    if (g >= G) return;
+    const unsigned lo = (unsigned)kWarm + r * (unsigned)kColdSites;
+    const unsigned ns = min((unsigned)kColdSites, p.n_sites - lo);   // sites of this range
+    for (unsigned i = threadIdx.x; i < 2 * (unsigned)kColdSites; i += blockDim.x) ctab[i] = 0;
+    __syncthreads();
+    const unsigned long long used = min(ld_relaxed_u64(p.cctr), p.crec_cap);
+    const unsigned long long nchunks = used / kRecChunk;
+    auto one = [&](unsigned long long m) {
+        const unsigned site = ev_site(m) - lo, kind = ev_kind(m) & 1u;
+        if (site >= ns) return;                                   // another range (or an invalid id)
+        const unsigned long long size = ev_size(m);
+        unsigned long long* row = p.table + (size_t)(site + lo) * SCL_NCOL;
+        if (size < (1ull << 24)) {
+            const unsigned ad = (1u << 24) + (unsigned)size;
+            const unsigned o = atomicAdd(&ctab[kind * kColdSites + site], ad);
+            const unsigned c1 = ((o & 0xFFFFFFu) + (unsigned)size) >> 24;
+            const unsigned w = (unsigned)(((unsigned long long)o + ad) >> 32);
+            if (c1 | w) {
+                atomicAdd(&row[SCL_COL_N_MALLOC + kind], ((unsigned long long)w << 8) - c1);
+                if (c1) atomicAdd(&row[SCL_COL_MALLOC_BYTES + kind], 1ull << 24);
+            }
+        } else {
+            atomicAdd(&row[SCL_COL_N_MALLOC + kind], 1ull);
+            atomicAdd(&row[SCL_COL_MALLOC_BYTES + kind], size);
+        }
+    };
+    // two chunks per pass, each thread 2 x 16 B of each (8 records in flight per thread)
+    constexpr unsigned kPer = kRecChunk / 2 / 1024;              // 16-B loads per thread per chunk (2)
+    for (unsigned long long c0 = g; c0 < nchunks; c0 += 2ull * G) {
+        ulonglong2 v[2 * kPer];
+        unsigned fill[2];
+        #pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const unsigned long long c = c0 + (unsigned long long)q * G;
+            fill[q] = c < nchunks ? min(__ldcg(p.crec_fill + c), (unsigned)kRecChunk) : 0u;
+            const ulonglong2* src = reinterpret_cast<const ulonglong2*>(p.crec + c * kRecChunk);
+            #pragma unroll
+            for (unsigned k = 0; k < kPer; ++k) {
+                const unsigned i = (threadIdx.x + k * 1024u) * 2u;
+                v[q * kPer + k] = i < fill[q] ? __ldcg(src + i / 2) : make_ulonglong2(0, 0);
+            }
+        }
+        #pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            #pragma unroll
+            for (unsigned k = 0; k < kPer; ++k) {
+                const unsigned i = (threadIdx.x + k * 1024u) * 2u;
+                if (i < fill[q]) one(v[q * kPer + k].x);
+                if (i + 1 < fill[q]) one(v[q * kPer + k].y);
+            }
+        }
+    }
+    __syncthreads();
+    for (unsigned i = threadIdx.x; i < 2 * ns; i += blockDim.x) {
+        const unsigned kind = i / ns, site = i % ns;
+        const unsigned w = ctab[kind * kColdSites + site];
+        if (w) {
+            unsigned long long* row = p.table + (size_t)(site + lo) * SCL_NCOL;
+            atomicAdd(&row[SCL_COL_N_MALLOC + kind], (unsigned long long)(w >> 24));
+            atomicAdd(&row[SCL_COL_MALLOC_BYTES + kind], (unsigned long long)(w & 0xFFFFFFu));
+        }
+    }
+}
+
+bool cold_hist_launched(const ReplayParams& p) { return p.n_sites > (unsigned)kWarm && p.n_segs > 0; }
+
+cudaError_t launch_cold_hist(const ReplayParams& p, cudaStream_t st)
+{
+    if (!cold_hist_launched(p)) return cudaSuccess;
+    static int nsm = 0;
+    constexpr size_t smem = 2 * (size_t)kColdSites * 4;
+    if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaError_t e = cudaFuncSetAttribute(cold_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) { nsm = 0; return e; }
+    }
+    const unsigned R = (p.n_sites - kWarm + kColdSites - 1) / kColdSites;
+    const unsigned G = std::max(1u, (unsigned)nsm / R);
+    cold_hist_kernel<<<R * G, 1024, smem, st>>>(p, R);
+    return cudaGetLastError();
+}
+
+}  // namespace scl

@@ -47,6 +47,7 @@ struct __align__(16) Slot {          // compute -> publisher -> runners / post p
 };
 
 constexpr int kESlots = 4 * kHot + kComputeWarps * 32;
+
 constexpr uint32_t kBloOff = kESlots * 4;   // byte distance cnt -> blo
 
 struct __align__(16) Smem {
@@ -116,6 +117,8 @@ __device__ void prepare_run(const ReplayParams& rp, unsigned long long* scratch)
     for (size_t i = tid; i < p.summ_words; i += nth) p.summ[i] = 0;
     for (size_t i = tid; i < p.run_words; i += nth) p.run[i] = 0;
     if (tid < 7) p.ticket[tid] = 0;
+    if (tid < 2 && rp.cctr) rp.cctr[tid] = 0;              // cold-record pool: allocated, exhausted
+    for (unsigned i = tid; i < p.n_sb; i += nth) p.rsbcnt[i] = 0;
     // exclusive scan of the per-trace sample capacities (thread j: a contiguous run of traces)
     const unsigned per = (p.n_traces + nth - 1) / nth;
     const unsigned t0 = min(p.n_traces, tid * per), t1 = min(p.n_traces, t0 + per);
@@ -149,12 +152,15 @@ __device__ __forceinline__ void wait_prepared(const ReplayParams& p) {
 // atomic is unconditional (no branch around it): an event that does not count goes to the lane's
 // sink slot (and adds 0 bytes, so the sink never wraps).  Tier-E slot of (kind, site) = kind*kHot +
 // site (kind-major: a warp's random sites spread over all 32 banks), copies included -- with every
-// site hot, no event needs a select.  Kinds are
-// read as bits: bit 41 set = copy (no footprint change), else bit 40 = free (kind 3 is rejected
-// by the trace validation; unvalidated, it only widens the Bloom filter, which is re-checked).
-// 32-bit byte-counter carries: one accumulated predicate, the rare wrap re-examined afterwards.
+// site hot, no event needs a select.  Two counters per slot: the event count (a u32 that cannot wrap
+// within one CTA) and the bytes mod 2^32, whose rare wrap is re-examined after the row (a packed
+// count | bytes word was measured slower: its carries are frequent enough that nearly every warp
+// takes the correction branch).  Kinds are read as bits: bit 41 set = copy (no footprint change),
+// else bit 40 = free (kind 3 is rejected by the trace validation; unvalidated, it only widens the
+// Bloom filter, which is re-checked).
 // kAllHot: every site is in the shared-memory table (n_sites <= kHot), no cold-site bookkeeping;
-// otherwise the table holds the allocs and frees of the kWarm lowest site ids, the rest go to L2.
+// otherwise the table holds the allocs and frees of the kWarm lowest site ids, the others are
+// returned in `cold` (bit j: event j) for the cold-record stream.
 template <bool kAllHot>
 __device__ __forceinline__ void fast_row(const unsigned long long* ptr, const unsigned long long* meta, uint32_t cnt_s,
                                          uint32_t bl_s, uint32_t dslot, unsigned long long* table, int& r32,
@@ -195,13 +201,60 @@ __device__ __forceinline__ void fast_row(const unsigned long long* ptr, const un
     }
 }
 
+// Cold events of the row (bit j of rec: event j) -> the warp's chunk of the cold-record stream:
+// one warp scan of the per-lane counts gives each lane its run of slots, the records are staged in
+// the warp's own 4-KiB slice of the TMA box it just read (its rows are in registers now; at most 256
+// records) and copied out with lane-contiguous stores (whole sectors).  A new chunk is taken from the
+// pool when the current one cannot hold the row's records (the rest of it is left unused; its fill
+// is written when the warp leaves it).  When the pool is exhausted the records are returned for the
+// direct L2 path.  Returns whether the slice was written (the async proxy's next TMA write must be
+// ordered after it: fence.proxy.async before the box is released).
+struct ColdCursor { unsigned long long base; unsigned fill; };   // base ~0: no chunk (pool exhausted)
+
+__device__ __forceinline__ unsigned cold_records(const ReplayParams& p, ColdCursor& cc, const unsigned long long* meta,
+                                                 unsigned rec, uint32_t slice_s, int lane, bool& staged)
+{
+    const unsigned nc = __popc(rec);
+    unsigned incl = nc;
+    #pragma unroll
+    for (int d = 1; d < 32; d <<= 1) { const unsigned o = __shfl_up_sync(kFull, incl, d); if (lane >= d) incl += o; }
+    const unsigned tot = __shfl_sync(kFull, incl, 31);
+    if (tot == 0) return 0u;
+    if (cc.fill + tot > (unsigned)kRecChunk) {
+        unsigned long long nb = 0;
+        if (lane == 0) {
+            if (cc.base != ~0ull) p.crec_fill[cc.base / kRecChunk] = cc.fill;
+            nb = atomicAdd(p.cctr, (unsigned long long)kRecChunk);
+            if (nb + kRecChunk > p.crec_cap) { nb = ~0ull; if (p.covf) *p.covf = 1ull; }   // pool exhausted
+        }
+        cc.base = __shfl_sync(kFull, nb, 0); cc.fill = 0;
+    }
+    if (cc.base == ~0ull) return rec;                 // -> direct L2 reductions
+    __syncwarp();                                     // every lane's row is in registers
+    uint32_t a = slice_s + 8u * (incl - nc);
+    #pragma unroll
+    for (int j = 0; j < kEpt; ++j)
+        if ((rec >> j) & 1u) { asm volatile("st.shared.u64 [%0], %1;" :: "r"(a), "l"(meta[j]) : "memory"); a += 8u; }
+    __syncwarp();
+    unsigned long long* dst = p.crec + cc.base + cc.fill;
+    for (unsigned k = (unsigned)lane; k < tot; k += 32) {
+        unsigned long long v;
+        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(slice_s + 8u * k) : "memory");
+        dst[k] = v;
+    }
+    cc.fill += tot;
+    staged = true;
+    return 0u;
+}
+
 // Two groups of 8 warps alternate boxes (group 0: boxes 0 and 2 of a unit, group 1: 1 and 3);
 // warp w8 of a group takes rows 32*w8 .. 32*w8+31 of its box = chunk g*8 + w8 of the unit.
 __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stage, int grp, int w8, int lane)
 {
     const uint32_t cnt_s = smem_u32(s.cnt);
     const uint32_t dslot = (uint32_t)(4 * kHot + (grp * 8 + w8) * 32 + lane) * 4u;   // this lane's sink slot
-    const bool all_hot = p.n_sites <= (unsigned)kHot;       // no cold site: no L2 path to track
+    const bool all_hot = p.n_sites <= (unsigned)kHot;       // no cold site: no record stream
+    ColdCursor cc{~0ull, (unsigned)kRecChunk};              // no chunk yet (taken at the first cold record)
     // this lane's row r = 32*w8 + lane of every box: its 8 swizzled 16-B chunks (chunk j at j ^ (r & 7))
     const int r = w8 * 32 + lane;
     unsigned rofs[kEpt];
@@ -220,6 +273,7 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
         const unsigned itu = it / kSub;                   // unit iteration of this CTA
         if (itu != cur_itu) { cur_itu = itu; if (++sl == kSlots) { sl = 0; sph ^= 1u; } }
         if (inf.u == kInvalid) {
+            if (lane == 0 && cc.base != ~0ull) p.crec_fill[cc.base / kRecChunk] = cc.fill;   // the last chunk's fill
             // the publisher stops once all `itu` units of this CTA are published
             if (grp == 0 && w8 == 0 && lane == 0) atomicExch(&s.n_units, itu);
             PROF_FLUSH(0)
@@ -238,6 +292,7 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
         int r32 = 0, mx32 = 0, mn32 = 0;                  // the lane's max / min include its start value
                                                           // (an earlier F: harmless for M and the band)
         bool small = true;                                // 32-bit chunk summary is exact for this lane
+        bool staged = false;                              // cold records staged in this warp's slice of the box
         if (g < inf.nbox) {
             // ---- the 8 events of row r of the box
             const unsigned char* boxp = stage + (size_t)st * kSegBytes;
@@ -251,12 +306,12 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
             unsigned big = 0;                                 // any size >= 2^27 in the row?
             #pragma unroll
             for (int j = 0; j < kEpt; ++j) big |= ((unsigned)meta[j] >> 27) | ((unsigned)(meta[j] >> 32) & 0xffu);
-            unsigned cold = 0;                                // events for the L2 (cold site) path
+            unsigned cold = 0, rec = 0;                       // events for the L2 path / the record stream
             if (e0 >= 0 && e0 + kEpt <= inf.n_t && big == 0) {
                 // fast path: the whole row is in the trace and |partial sums| < 2^30: 32-bit running
                 // sum / max / min (a copy's d = 0 repeats an F already seen: harmless)
-                if (all_hot) fast_row<true>(ptr, meta, cnt_s, bl_s, dslot, p.table, r32, mx32, mn32, cold);
-                else         fast_row<false>(ptr, meta, cnt_s, bl_s, dslot, p.table, r32, mx32, mn32, cold);
+                if (all_hot) fast_row<true>(ptr, meta, cnt_s, bl_s, dslot, p.table, r32, mx32, mn32, rec);
+                else         fast_row<false>(ptr, meta, cnt_s, bl_s, dslot, p.table, r32, mx32, mn32, rec);
                 run = r32;
                 tmx = mx32; tmn = mn32;
                 small = r32 > -(1 << 25) && r32 < (1 << 25) && mx32 < (1 << 25) && mn32 > -(1 << 25);
@@ -286,6 +341,8 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
                     }
                 }
             }
+            if (!all_hot)                                     // (warp-collective; fallback -> L2)
+                cold |= cold_records(p, cc, meta, rec, smem_u32(boxp) + (uint32_t)w8 * 32u * 128u, lane, staged);
             while (cold) {                                    // cold site / huge size: L2 reductions
                 const int j = __ffs(cold) - 1;
                 cold &= cold - 1;
@@ -317,6 +374,7 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
             csum = shfl_ll(incl, 31);
         }
         if (lane == 0) { S.Pc[c] = csum; S.ax[c] = cmx; S.an[c] = cmn; }   // composed in place below
+        if (staged) fence_proxy_async_shared();            // generic writes before the next TMA write of the box
         __syncwarp();
         mbar_arrive(&s.empty[st]);                        // box consumed
         PROF_MARK(2)
@@ -975,6 +1033,11 @@ __global__ void __launch_bounds__(256, 3) post_kernel(const __grid_constant__ Re
     }
     // per-trace reduce on the last warps (they settle one unit fewer than the first ones)
     for (unsigned t = nw - 1 - wid; t < p.n_traces; t += nw) samples_trace(p, t, lane);
+    if (p.tierE && !p.rechain) {                        // Tier E of this stream pass, kept for re-thresholds
+        const size_t n4 = (size_t)p.n_sites * 4;
+        for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x)
+            p.tierE[i] = __ldcg(&p.table[(i >> 2) * SCL_NCOL + (i & 3)]);
+    }
     POST_T(1, atomicMax)
     grid_barrier(&p.ticket[1]);
     POST_T(2, atomicMax)
@@ -991,7 +1054,7 @@ __global__ void __launch_bounds__(256, 3) post_kernel(const __grid_constant__ Re
     if (!p.fuse_report) return;                                                           // phase C: a6
     grid_barrier(&p.ticket[3]);                             // every re-check done: leak frees final
     POST_T(4, atomicMax)
-    const ReportScratch rx{p.rbits, p.rlrate, p.rlsite, &p.ticket[5]};
+    const ReportScratch rx{p.rbits, p.rlrate, p.rlsite, &p.ticket[5], p.rsbcnt};
     report_grid_flags(p.fin, rx, wid, nw, lane);
     grid_barrier(&p.ticket[4]);
     report_grid_rows(p.fin, p.rows, rx, reinterpret_cast<unsigned long long*>(post_smem) + (threadIdx.x >> 5) * 32 * kRowWords,
@@ -1061,7 +1124,7 @@ replay_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         for (int x = tid; x < 2 * cap; x += kComputeWarps * 32) {    // flush Tier-E counters (allocs, frees)
             const int kind = x / cap, site = x % cap;
             const unsigned c = s.cnt[x];
-            if (c) {
+            if (c && (unsigned)site < p.n_sites) {                   // (an invalid site id is dropped)
                 unsigned long long* row = p.table + (size_t)site * SCL_NCOL;
                 atomicAdd(&row[SCL_COL_N_MALLOC + kind], (unsigned long long)c);
                 atomicAdd(&row[SCL_COL_MALLOC_BYTES + kind], (unsigned long long)s.blo[x]);

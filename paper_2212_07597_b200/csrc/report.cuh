@@ -184,8 +184,12 @@ __device__ void report_block(const FinalParams& p, scl_site_row* rows, ReportSme
     }
 }
 
-// ---- a6 spread over a whole grid (post_kernel, fused): warp w owns the 32 sites of word w.
-struct ReportScratch { unsigned* bits; double* lrate; unsigned* lsite; unsigned* nflag; };
+// ---- a6 spread over a whole grid (post_kernel, fused; or report_flags_kernel + report_rows_kernel
+// after a deferred finalize of a table above kReportSites): warp w owns the 32 sites of word w.
+// Any table size: bits has one word per 32 sites and sbcnt one flag count per kSuper words (both
+// zeroed before C1, like nflag), so the flagged sites before a word are <= n/2^15 + kSuper terms.
+constexpr unsigned kSuper = 1024;                              // bitmask words per superblock count
+struct ReportScratch { unsigned* bits; double* lrate; unsigned* lsite; unsigned* nflag; unsigned* sbcnt; };
 
 // C1: integer flags (bitmask word per warp), flagged sites (rate, site) appended to a global list.
 static __device__ void report_grid_flags(const FinalParams& p, const ReportScratch& x, unsigned wid, unsigned nw, int lane)
@@ -206,7 +210,7 @@ static __device__ void report_grid_flags(const FinalParams& p, const ReportScrat
             }
         }
         const unsigned word = __ballot_sync(kFull, fl);
-        if (lane == 0) x.bits[w] = word;
+        if (lane == 0) { x.bits[w] = word; if (word) atomicAdd(&x.sbcnt[w / kSuper], (unsigned)__popc(word)); }
     }
 }
 
@@ -221,7 +225,8 @@ static __device__ void report_grid_rows(const FinalParams& p, scl_site_row* rows
     const unsigned F = __ldcg(x.nflag);
     for (unsigned w = wid; w < nwd; w += nw) {
         unsigned fbw = 0;                                      // flagged sites before word w
-        for (unsigned q = (unsigned)lane; q < w; q += 32) fbw += __popc(__ldcg(&x.bits[q]));
+        for (unsigned q = (unsigned)lane; q < w / kSuper; q += 32) fbw += __ldcg(&x.sbcnt[q]);
+        for (unsigned q = w / kSuper * kSuper + (unsigned)lane; q < w; q += 32) fbw += __popc(__ldcg(&x.bits[q]));
         fbw = (unsigned)warp_sum((long long)fbw);
         const unsigned word = __ldcg(&x.bits[w]);
         const unsigned sidx = w * 32 + (unsigned)lane;
@@ -274,5 +279,7 @@ static __device__ void report_grid_rows(const FinalParams& p, scl_site_row* rows
         __syncwarp();
     }
 }
+
+cudaError_t launch_report_grid(const FinalParams& p, const ReportScratch& x, scl_site_row* rows, cudaStream_t st);
 
 }  // namespace scl

@@ -36,7 +36,10 @@ constexpr int kStages = 4;                    // TMA ring depth
 constexpr int kSlots = 6;                     // compute -> publisher unit summary ring (smem)
 constexpr int kBloomWords = 64;               // 2048-bit Bloom filter of freed pointers per chunk
 constexpr int kHot = 1024;                    // sites with shared-memory Tier-E counters (all 4 kinds)
-constexpr int kWarm = 2 * kHot;               // the same storage when n_sites > kHot: allocs and frees only
+constexpr int kWarm = 2 * kHot;               // the same storage when n_sites > kHot: allocs and frees only;
+                                              //   the other sites' events go to the cold-record stream
+constexpr int kRecChunk = 4096;               // cold-record stream: records per chunk (one warp's, at a time)
+constexpr int kColdSites = 28672;             // cold_hist_kernel: sites per range (2 kinds x 4 B = 224 KiB)
 constexpr long long kNeg = -(1ll << 62);      // "no event" sentinels for max / min
 constexpr long long kPos = (1ll << 62);
 constexpr unsigned long long kNoEp = ~0ull;
@@ -73,8 +76,6 @@ struct FinalParams {
     unsigned int n_sites;
     int formula;
     double elapsed_ns;
-    double* prob; double* rate; unsigned char* flag;
-    unsigned long long* key1; unsigned int* val;   // sort inputs
     unsigned long long* gate_out;     // [3] host-mapped pinned buffer: the gate sums (written by one thread)
     unsigned long long* prof;         // debug build only: phase timestamps of a6
 };
@@ -88,6 +89,7 @@ struct PrepParams {
     unsigned long long* summ; size_t summ_words;
     unsigned long long* run; size_t run_words;
     unsigned int* ticket;             // [8] (the replay kernel's counters; [0..6] zeroed here)
+    unsigned* rsbcnt; unsigned n_sb;  // a6 scratch superblock counts (zeroed here)
     unsigned long long* sbase;        // [n_traces]
     const unsigned long long* off;    // [n_traces + 1]
     const unsigned long long* sabs;   // [n_traces]
@@ -122,7 +124,8 @@ struct ReplayParams {
     int rechain;                      // runners only, over the handle's last stream pass (prepared by the host)
     PrepParams prep;                  // CTA 0 prepares the run; ticket[7] = epoch once done
     int fuse_report;                  // post_kernel runs a6 over all its blocks (fin -> rows)
-    unsigned* rbits;                  // [kReportSites/32] a6 scratch: flag bitmask words
+    unsigned* rbits;                  // [max(n_sites, kReportSites)/32] a6 scratch: flag bitmask words
+    unsigned* rsbcnt;                 //   flags per kSuper bitmask words (zeroed by the preparation)
     double* rlrate; unsigned* rlsite; //   flagged sites' rates and ids (kReportList)
     FinalParams fin;
     scl_site_row* rows;
@@ -139,6 +142,15 @@ struct ReplayParams {
     const unsigned long long* sbase;  // trace -> first sample slot
     scl_trace_summary* summ;          // [n_traces]
     unsigned long long* prof;         // debug build only (SCL_PROFILE): per-role cycle sums, else NULL
+    // cold-record stream (n_sites > kWarm): the meta word of every fast-path alloc / free of a site
+    // >= kWarm, in chunks of kRecChunk records taken by one compute warp at a time (cold_hist_kernel
+    // reduces them per site after the stream pass)
+    unsigned long long* crec;         // [crec_cap]
+    unsigned long long crec_cap;      // records (a multiple of kRecChunk)
+    unsigned long long* cctr;         // [2]: records allocated (chunk granules), pool exhausted flag (zeroed per run)
+    unsigned* crec_fill;              // [crec_cap / kRecChunk] records written to each allocated chunk
+    unsigned long long* covf;         // host-mapped: set when the pool was exhausted (the host grows it)
+    unsigned long long* tierE;        // [n_sites * 4] Tier-E columns of the stream pass (post pass copy; re-thresholds)
 };
 
 
@@ -212,16 +224,14 @@ cudaError_t launch_rate(const RateParams& p, int phase, cudaStream_t st);   // 0
 // launch wrappers (replay.cu)
 cudaError_t launch_load_stats(const scl_event* ev, const unsigned long long* off, unsigned n_traces,
                               unsigned long long n_events, unsigned n_sites, unsigned long long* sabs,
-                              unsigned long long* err, cudaStream_t st);
+                              unsigned long long* err, scl_event* dst, cudaStream_t st);
 cudaError_t launch_replay(const CUtensorMap* tmap, const ReplayParams& p, int grid, cudaStream_t st);
 cudaError_t launch_post(const ReplayParams& p, cudaStream_t st);
 cudaError_t launch_rechain(const ReplayParams& p, cudaStream_t st);   // runner warps alone
-cudaError_t launch_finalize(const FinalParams& p, cudaStream_t st);
+cudaError_t launch_cold_hist(const ReplayParams& p, cudaStream_t st);  // Tier E of the cold-record stream
+bool cold_hist_launched(const ReplayParams& p);
 bool report_fused(unsigned n_sites);   // a6 in one block (report_kernel) for tables this small
 cudaError_t launch_report(const FinalParams& p, scl_site_row* rows, cudaStream_t st);
-cudaError_t launch_rows(const unsigned long long* table, const double* prob, const double* rate,
-                        const unsigned char* flag, const unsigned int* order, unsigned n_sites,
-                        scl_site_row* rows, cudaStream_t st);
 size_t replay_smem_bytes();
 size_t replay_urec_bytes();            // bytes of one unit record
 int replay_occupancy(int* grid);

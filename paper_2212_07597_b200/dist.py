@@ -58,7 +58,9 @@ def replay_distributed(events, offsets, n_sites: int, T: int, rank: int, world: 
                        tick_ns: int = 1000, formula: int = 0, group=None):
     """Shard -> scl_trace_load -> scl_replay_run(defer) -> all-reduce -> scl_finalize.
     Every rank ends with the global report; samples stay rank-local."""
+    import torch
     from . import device_table_tensor, scl_finalize, scl_replay_run, scl_trace_load
+    torch.cuda.set_device(device)
     ev, off, rng = shard(events, offsets, rank, world)
     tr = scl_trace_load(ev, off, n_sites, device=device)
     r = scl_replay_run(T, tr, tick_ns=tick_ns, formula=formula, defer_finalize=True)
@@ -100,6 +102,7 @@ def replay_waves(events, offsets, n_sites: int, T: int, wave_events: int, device
     import torch
     from . import (device_table_tensor, scl_finalize, scl_replay_run, scl_samples, scl_trace_load,
                    scl_trace_reload, scl_trace_summaries)
+    torch.cuda.set_device(device)
     if world > 1:
         ev, off, rng = shard(events, offsets, rank, world)
     else:

@@ -206,18 +206,23 @@ def test_enumerated_traces_brute_force():
         off = np.zeros(len(traces) + 1, dtype=np.uint64)
         off[1:] = np.cumsum([len(t) for t in traces])
         r = oracle.replay(ev, off, 3, T)
+        M, Fr = [0, 0, 0], [0, 0, 0]                  # death-time leak scores summed over EVERY trace
         for t, tr in enumerate(traces):
             smp = r.trace_samples(t)
             _check_against_brute(tr, T, smp)
             m, f = leak_scores_by_death(tr, as_tuples(smp))
             for s in range(3):
-                assert int(r.site_table[s, 8]) >= 0
+                M[s] += m.get(s, 0)
+                Fr[s] += f.get(s, 0)
             # per-trace leak score: recompute from a single-trace replay
             rt = run_oracle(tr, T, n_sites=3) if t % 7 == 0 else None
             if rt is not None:
                 for s in range(3):
                     assert int(rt.site_table[s, 8]) == m.get(s, 0)
                     assert int(rt.site_table[s, 9]) == f.get(s, 0)
+        # the batched replay's leak columns are the sums of the independent per-trace scores
+        assert [int(x) for x in r.site_table[:, 8]] == M and [int(x) for x in r.site_table[:, 9]] == Fr
+        assert sum(M) > 0 and sum(Fr) > 0
 
 
 def test_random_traces_brute_force_and_mini():
