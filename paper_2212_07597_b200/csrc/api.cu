@@ -577,6 +577,7 @@ static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const sc
     if (!base) ensure_cold_pool(tr);
     p.crec = tr->d_crec; p.crec_cap = tr->crec_cap; p.cctr = tr->d_cctr; p.crec_fill = tr->d_crec_fill;
     p.covf = tr->h_covf;
+
     if (tr->n_sites > tr->cap_tierE) {
         cudaFree(tr->d_tierE); tr->d_tierE = nullptr; tr->cap_tierE = 0;
         if (cudaMalloc(&tr->d_tierE, (size_t)tr->n_sites * 32) != cudaSuccess) { cudaGetLastError(); if (fresh) scl_result_free(r); return fail(SCL_ENOMEM, "tier E"); }

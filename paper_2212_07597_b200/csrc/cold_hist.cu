@@ -26,8 +26,8 @@ __global__ void __launch_bounds__(1024, 1) cold_hist_kernel(const __grid_constan
     const unsigned long long used = min(ld_relaxed_u64(p.cctr), p.crec_cap);
     const unsigned long long nchunks = used / kRecChunk;
     auto one = [&](unsigned long long m) {
-        const unsigned site = ev_site(m) - lo, kind = ev_kind(m) & 1u;
-        if (site >= ns) return;                                   // another range (or an invalid id)
+        const unsigned site = ev_site(m) - lo, kind = ev_kind(m);
+        if (site >= ns || kind > 1) return;                       // another range, an invalid id, a pad record
         const unsigned long long size = ev_size(m);
         unsigned long long* row = p.table + (size_t)(site + lo) * SCL_NCOL;
         if (size < (1ull << 24)) {
@@ -44,31 +44,39 @@ __global__ void __launch_bounds__(1024, 1) cold_hist_kernel(const __grid_constan
             atomicAdd(&row[SCL_COL_MALLOC_BYTES + kind], size);
         }
     };
-    // two chunks per pass, each thread 2 x 16 B of each (8 records in flight per thread)
+    // two chunks per pass, each thread 2 x 16 B of each; the next pass's loads are issued before this
+    // pass's records are reduced (the records past a chunk's fill are read and ignored: the loads do
+    // not wait for the fill word)
     constexpr unsigned kPer = kRecChunk / 2 / 1024;              // 16-B loads per thread per chunk (2)
-    for (unsigned long long c0 = g; c0 < nchunks; c0 += 2ull * G) {
-        ulonglong2 v[2 * kPer];
-        unsigned fill[2];
+    auto load = [&](unsigned long long c0, ulonglong2* v, unsigned* fill) {
         #pragma unroll
         for (int q = 0; q < 2; ++q) {
             const unsigned long long c = c0 + (unsigned long long)q * G;
-            fill[q] = c < nchunks ? min(__ldcg(p.crec_fill + c), (unsigned)kRecChunk) : 0u;
-            const ulonglong2* src = reinterpret_cast<const ulonglong2*>(p.crec + c * kRecChunk);
+            const bool ok = c < nchunks;
+            fill[q] = ok ? min(__ldcg(p.crec_fill + c), (unsigned)kRecChunk) : 0u;
+            const ulonglong2* src = reinterpret_cast<const ulonglong2*>(p.crec + (ok ? c : 0) * kRecChunk);
             #pragma unroll
-            for (unsigned k = 0; k < kPer; ++k) {
-                const unsigned i = (threadIdx.x + k * 1024u) * 2u;
-                v[q * kPer + k] = i < fill[q] ? __ldcg(src + i / 2) : make_ulonglong2(0, 0);
-            }
+            for (unsigned k = 0; k < kPer; ++k)
+                v[q * kPer + k] = ok ? __ldcg(src + threadIdx.x + k * 1024u) : make_ulonglong2(0, 0);
         }
+    };
+    ulonglong2 v[2 * kPer], w[2 * kPer];
+    unsigned fv[2], fw[2];
+    load(g, v, fv);
+    for (unsigned long long c0 = g; c0 < nchunks; c0 += 2ull * G) {
+        load(c0 + 2ull * G, w, fw);                              // in flight while v is reduced
         #pragma unroll
         for (int q = 0; q < 2; ++q) {
             #pragma unroll
             for (unsigned k = 0; k < kPer; ++k) {
                 const unsigned i = (threadIdx.x + k * 1024u) * 2u;
-                if (i < fill[q]) one(v[q * kPer + k].x);
-                if (i + 1 < fill[q]) one(v[q * kPer + k].y);
+                if (i < fv[q]) one(v[q * kPer + k].x);
+                if (i + 1 < fv[q]) one(v[q * kPer + k].y);
             }
         }
+        #pragma unroll
+        for (int q = 0; q < 2 * (int)kPer; ++q) v[q] = w[q];
+        fv[0] = fw[0]; fv[1] = fw[1];
     }
     __syncthreads();
     for (unsigned i = threadIdx.x; i < 2 * ns; i += blockDim.x) {

@@ -46,7 +46,8 @@ struct __align__(16) Slot {          // compute -> publisher -> runners / post p
     unsigned bloom[kChunks][kBloomWords];
 };
 
-constexpr int kESlots = 4 * kHot + kComputeWarps * 32;
+constexpr int kTabSlots = 4 * kHot > 2 * kWarm ? 4 * kHot : 2 * kWarm;   // the two table layouts share storage
+constexpr int kESlots = kTabSlots + kComputeWarps * 32;              // + one sink slot per compute lane
 
 constexpr uint32_t kBloOff = kESlots * 4;   // byte distance cnt -> blo
 
@@ -78,7 +79,11 @@ __device__ __forceinline__ unsigned bloom_hash(unsigned long long ptr) {
 __device__ __forceinline__ unsigned bloom_word(unsigned long long ptr) { return bloom_hash(ptr) >> 26; }
 __device__ __forceinline__ unsigned bloom_mask(unsigned long long ptr) {
     const unsigned h = bloom_hash(ptr);
+#ifdef SCL_BLOOM1
+    return 1u << ((h >> 21) & 31u);
+#else
     return (1u << ((h >> 21) & 31u)) | (1u << ((h >> 16) & 31u));
+#endif
 }
 
 // Optional per-role cycle accounting (debug build with -DSCL_PROFILE only).
@@ -182,7 +187,7 @@ __device__ __forceinline__ void fast_row(const unsigned long long* ptr, const un
         } else {
             const bool h = af && (hi >> 11) < (unsigned)kWarm;
             cold |= (af && !h ? 1u : 0u) << j;
-            const uint32_t offw = ((hi >> 9) & (uint32_t)(4 * kWarm - 4)) | ((hi << 5) & (uint32_t)(4 * kWarm));
+            const uint32_t offw = ((hi >> 9) & (uint32_t)(4 * kWarm - 4)) | ((hi << (kWarmLog2 - 6)) & (uint32_t)(4 * kWarm));
             a = cnt_s + (h ? offw : dslot); add[j] = h ? lo : 0u;                // ((kind&1)*kWarm + site)*4
         }
         red_add(a, 1u);                                                       // a5 Tier E
@@ -235,6 +240,21 @@ __device__ __forceinline__ unsigned cold_records(const ReplayParams& p, ColdCurs
     #pragma unroll
     for (int j = 0; j < kEpt; ++j)
         if ((rec >> j) & 1u) { asm volatile("st.shared.u64 [%0], %1;" :: "r"(a), "l"(meta[j]) : "memory"); a += 8u; }
+#ifdef SCL_BULKREC
+    // an odd count is padded with a kind-3 record (cold_hist skips it): the bulk copy moves whole
+    // 16-B units to a 16-B aligned position
+    const unsigned totp = (tot + 1u) & ~1u;
+    if (lane == 0 && totp != tot) asm volatile("st.shared.u64 [%0], %1;" :: "r"(slice_s + 8u * tot), "l"(3ull << 40) : "memory");
+    fence_proxy_async_shared();                       // the staged records before the async-proxy read
+    __syncwarp();
+    if (lane == 0) {
+        bulk_s2g(p.crec + cc.base + cc.fill, reinterpret_cast<const void*>(__cvta_shared_to_generic(slice_s)), totp * 8u);
+        bulk_commit();
+        bulk_wait_read();                             // the slice is read: the box may be released
+    }
+    __syncwarp();
+    cc.fill += totp;
+#else
     __syncwarp();
     unsigned long long* dst = p.crec + cc.base + cc.fill;
     for (unsigned k = (unsigned)lane; k < tot; k += 32) {
@@ -243,6 +263,7 @@ __device__ __forceinline__ unsigned cold_records(const ReplayParams& p, ColdCurs
         dst[k] = v;
     }
     cc.fill += tot;
+#endif
     staged = true;
     return 0u;
 }
@@ -252,7 +273,7 @@ __device__ __forceinline__ unsigned cold_records(const ReplayParams& p, ColdCurs
 __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stage, int grp, int w8, int lane)
 {
     const uint32_t cnt_s = smem_u32(s.cnt);
-    const uint32_t dslot = (uint32_t)(4 * kHot + (grp * 8 + w8) * 32 + lane) * 4u;   // this lane's sink slot
+    const uint32_t dslot = (uint32_t)(kTabSlots + (grp * 8 + w8) * 32 + lane) * 4u;   // this lane's sink slot
     const bool all_hot = p.n_sites <= (unsigned)kHot;       // no cold site: no record stream
     ColdCursor cc{~0ull, (unsigned)kRecChunk};              // no chunk yet (taken at the first cold record)
     // this lane's row r = 32*w8 + lane of every box: its 8 swizzled 16-B chunks (chunk j at j ^ (r & 7))
@@ -457,6 +478,18 @@ __device__ __forceinline__ void store_rstate(RunState* rs, const RState& x, int 
     }
 }
 
+// Tier S of one sample (a5: n_growth / growth_bytes or n_decline / decline_bytes of the
+// sample's site -- a decline at the free's site, reading Q14) and, at an episode start, the site's
+// leak mallocs (the frees are counted by the reclaim pass).  Fire-and-forget L2 reductions
+// by the runner lane that takes the sample.
+__device__ __forceinline__ void sample_counters(const ReplayParams& p, unsigned site, bool growth, long long net, bool nm)
+{
+    unsigned long long* row = p.table + (size_t)site * SCL_NCOL;
+    atomicAdd(&row[growth ? SCL_COL_N_GROWTH : SCL_COL_N_DECLINE], 1ull);
+    atomicAdd(&row[growth ? SCL_COL_GROWTH_BYTES : SCL_COL_DECLINE_BYTES], (unsigned long long)(growth ? net : -net));
+    if (nm) atomicAdd(&row[SCL_COL_LEAK_MALLOCS], 1ull);
+}
+
 // A unit in which a sample fires: resolve it chunk by chunk (a3).  x: state before the unit
 // -> state after it.  Only chunks whose F range leaves (B-T, B+T) are read (lane l <-> row
 // 32c+l, 8 events); one combined warp scan gives each lane the footprint and the running
@@ -540,6 +573,7 @@ __device__ __forceinline__ void resolve_chunk32(const ReplayParams& p, const uns
                 smp.idx = (unsigned long long)(e0 + js); smp.net = net; smp.footprint = F;
                 smp.site = ev_site(ms); smp.kind = growth ? 0 : 1; smp.new_max = nm ? 1 : 0; smp.pad = 0;
                 p.samples[slot_s] = smp;
+                sample_counters(p, smp.site, growth, net, nm);
                 if (nm) { p.ep_flag[slot_s] = 0u; ep1 = slot_s + 1; eptr = ps; ++nep; }   // settled by the reclaim pass
                 ++n; B = F; Ms = llmax(Ms, F);            // "resets the counters"
                 h2 = clamp_i32(B + p.T - Fc); l2 = clamp_i32(B - p.T - Fc);
@@ -662,6 +696,7 @@ __device__ void resolve_unit(const ReplayParams& p, const Slot& S, RState& x, un
                     smp.idx = (unsigned long long)(e0 + js); smp.net = net; smp.footprint = F;
                     smp.site = ev_site(ms); smp.kind = growth ? 0 : 1; smp.new_max = nm ? 1 : 0; smp.pad = 0;
                     p.samples[slot_s] = smp;
+                    sample_counters(p, smp.site, growth, net, nm);
                     if (nm) { p.ep_flag[slot_s] = 0u; ep1 = slot_s + 1; eptr = ps; ++nep; }   // settled by the reclaim pass
                     ++n; B = F; Ms = llmax(Ms, F);            // "resets the counters"
                     from = (unsigned)js + 1;
@@ -779,9 +814,17 @@ __device__ void run_trace(const ReplayParams& p, RState& x, unsigned t, unsigned
         RPROF_ADD(14, clock64() - t_bat - t_res)
 #endif
         x.next += (unsigned)m;
-        if (x.next == nseg && lane == 0) {
+        if (x.next == nseg && lane == 0) {          // trace done: summary, trend end points, gate sums (Q10)
             scl_trace_summary* sm = &p.summ[t];
             sm->f_final = x.F; sm->hwm = x.M; sm->n_samples = x.n; sm->n_episodes = x.nep;
+            const long long ff = x.n ? __ldcg(&p.samples[sb].footprint) : 0, fl = x.n ? x.B : 0;
+            sm->f_first_sample = ff; sm->f_last_sample = fl;
+            if (x.n >= 2) {
+                unsigned long long* gate = p.table + (size_t)p.n_sites * SCL_NCOL;
+                atomicAdd(&gate[0], (unsigned long long)(fl - ff));
+                atomicAdd(&gate[1], (unsigned long long)(ff > 1 ? ff : 1));
+                atomicAdd(&gate[2], 1ull);
+            }
         }
     }
 }
@@ -798,7 +841,7 @@ __device__ void publisher_role(const ReplayParams& p, Smem& s, int lane)
         // units complete in order (almost): wait for unit j, take every complete unit after it,
         // copy each to its unit record and hand the shared-memory slot back right away (the copy
         // is in flight from registers), then ONE device-scope fence before the aggregate words
-        if (!mbar_try(&s.sdone[j % kSlots], (j / kSlots) & 1u)) {
+        if (!mbar_try_hint(&s.sdone[j % kSlots], (j / kSlots) & 1u, 2000u)) {
             const unsigned nu = ((volatile unsigned*)&s.n_units)[0];
             if (nu != kInvalid && j >= nu) { PROF_FLUSH(16) return; }
             PROF_MARK(0)
@@ -1031,8 +1074,6 @@ __global__ void __launch_bounds__(256, 3) post_kernel(const __grid_constant__ Re
             reclaim_unit(p, wid + (k0 + (unsigned)i) * nw, x, lane);
         }
     }
-    // per-trace reduce on the last warps (they settle one unit fewer than the first ones)
-    for (unsigned t = nw - 1 - wid; t < p.n_traces; t += nw) samples_trace(p, t, lane);
     if (p.tierE && !p.rechain) {                        // Tier E of this stream pass, kept for re-thresholds
         const size_t n4 = (size_t)p.n_sites * 4;
         for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x)
@@ -1052,6 +1093,17 @@ __global__ void __launch_bounds__(256, 3) post_kernel(const __grid_constant__ Re
     }
     POST_T(3, atomicMax)
     if (!p.fuse_report) return;                                                           // phase C: a6
+    if (p.n_sites <= kReportSites) {                        // small table: a6 in the block that finishes last
+        __shared__ unsigned last;
+        __syncthreads();
+        if (threadIdx.x == 0) { __threadfence(); last = atomicAdd(&p.ticket[3], 1u) == gridDim.x - 1; }
+        __syncthreads();
+        if (!last) return;
+        __threadfence();                                    // every block's leak frees before the reads below
+        report_block<256>(p.fin, p.rows, *reinterpret_cast<ReportSmem<256>*>(post_smem));
+        POST_T(5, atomicMax)
+        return;
+    }
     grid_barrier(&p.ticket[3]);                             // every re-check done: leak frees final
     POST_T(4, atomicMax)
     const ReportScratch rx{p.rbits, p.rlrate, p.rlsite, &p.ticket[5], p.rsbcnt};
@@ -1062,7 +1114,8 @@ __global__ void __launch_bounds__(256, 3) post_kernel(const __grid_constant__ Re
     POST_T(5, atomicMax)
 }
 
-constexpr size_t kPostStage = 8 * 32 * kRowWords * 8;          // a6 row staging: 8 warps x 32 rows
+constexpr size_t kPostStage = std::max<size_t>(8 * 32 * kRowWords * 8,      // a6 row staging: 8 warps x 32 rows,
+                                               report_smem_bytes<256>());     // or report_block in the last block
 
 cudaError_t launch_post(const ReplayParams& p, cudaStream_t st)
 {
@@ -1102,7 +1155,7 @@ replay_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0 && (smem_u32(smem_raw) & 1023u) != 0) __trap();     // the 128-B swizzle needs 1024-B alignment
 
-    for (int x = tid; x < 4 * kHot; x += kCtaThreads) { s.cnt[x] = 0; s.blo[x] = 0; }
+    for (int x = tid; x < kTabSlots; x += kCtaThreads) { s.cnt[x] = 0; s.blo[x] = 0; }
     if (tid == 0) {
         for (int i = 0; i < kStages; ++i) { mbar_init(&s.full[i], 1); mbar_init(&s.empty[i], 8 * 32); }
         for (int i = 0; i < kSlots; ++i) { mbar_init(&s.sempty[i], 1); mbar_init(&s.sdone[i], kChunks); }

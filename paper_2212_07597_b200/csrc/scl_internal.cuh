@@ -32,11 +32,18 @@ constexpr int kLBWarps = 3;                   // publisher + 2 runner warps (20 
 constexpr int kEmbeddedRunners = 2;           // warps 18-19 of every CTA run traces
 constexpr int kProducerWarp = kComputeWarps;
 constexpr int kCtaThreads = (kComputeWarps + 1 + kLBWarps) * 32;
-constexpr int kStages = 4;                    // TMA ring depth
+#ifndef SCL_STAGES
+#define SCL_STAGES 4
+#endif
+#ifndef SCL_WARM_LOG2
+#define SCL_WARM_LOG2 11
+#endif
+constexpr int kStages = SCL_STAGES;           // TMA ring depth
 constexpr int kSlots = 6;                     // compute -> publisher unit summary ring (smem)
 constexpr int kBloomWords = 64;               // 2048-bit Bloom filter of freed pointers per chunk
 constexpr int kHot = 1024;                    // sites with shared-memory Tier-E counters (all 4 kinds)
-constexpr int kWarm = 2 * kHot;               // the same storage when n_sites > kHot: allocs and frees only;
+constexpr int kWarmLog2 = SCL_WARM_LOG2;
+constexpr int kWarm = 1 << kWarmLog2;         // n_sites > kHot: the allocs and frees of the kWarm lowest site ids;
                                               //   the other sites' events go to the cold-record stream
 constexpr int kRecChunk = 4096;               // cold-record stream: records per chunk (one warp's, at a time)
 constexpr int kColdSites = 28672;             // cold_hist_kernel: sites per range (2 kinds x 4 B = 224 KiB)
@@ -147,7 +154,7 @@ struct ReplayParams {
     // reduces them per site after the stream pass)
     unsigned long long* crec;         // [crec_cap]
     unsigned long long crec_cap;      // records (a multiple of kRecChunk)
-    unsigned long long* cctr;         // [2]: records allocated (chunk granules), pool exhausted flag (zeroed per run)
+    unsigned long long* cctr;         // [2]: records allocated (chunk granules), spare (zeroed per run)
     unsigned* crec_fill;              // [crec_cap / kRecChunk] records written to each allocated chunk
     unsigned long long* covf;         // host-mapped: set when the pool was exhausted (the host grows it)
     unsigned long long* tierE;        // [n_sites * 4] Tier-E columns of the stream pass (post pass copy; re-thresholds)
@@ -155,33 +162,6 @@ struct ReplayParams {
 
 
 
-#ifdef __CUDACC__
-// Per-sample reduce of trace t by one warp: Tier-S columns, leak mallocs (one per episode start,
-// P:31-39; the frees are counted by the reclaim pass), footprint-trend endpoints and the gate
-// sums (reading Q10).
-__device__ __forceinline__ void samples_trace(const ReplayParams& p, unsigned t, int lane)
-{
-    unsigned long long* gate = p.table + (size_t)p.n_sites * SCL_NCOL;
-    const unsigned long long n = p.summ[t].n_samples, sb = p.sbase[t];
-    for (unsigned long long i = lane; i < n; i += 32) {
-        const scl_sample sm = p.samples[sb + i];
-        unsigned long long* row = p.table + (size_t)sm.site * SCL_NCOL;
-        if (sm.kind == 0) { atomicAdd(&row[SCL_COL_N_GROWTH], 1ull); atomicAdd(&row[SCL_COL_GROWTH_BYTES], (unsigned long long)sm.net); }
-        else              { atomicAdd(&row[SCL_COL_N_DECLINE], 1ull); atomicAdd(&row[SCL_COL_DECLINE_BYTES], (unsigned long long)(-sm.net)); }
-        if (sm.new_max) atomicAdd(&row[SCL_COL_LEAK_MALLOCS], 1ull);     // (frees: the reclaim pass)
-    }
-    if (lane == 0) {
-        long long ff = 0, fl = 0;
-        if (n > 0) { ff = p.samples[sb].footprint; fl = p.samples[sb + n - 1].footprint; }
-        p.summ[t].f_first_sample = ff; p.summ[t].f_last_sample = fl;
-        if (n >= 2) {
-            atomicAdd(&gate[0], (unsigned long long)(fl - ff));
-            atomicAdd(&gate[1], (unsigned long long)(ff > 1 ? ff : 1));
-            atomicAdd(&gate[2], 1ull);
-        }
-    }
-}
-#endif
 
 constexpr int kUCols = 4;               // per-unit byte sums: alloc, free, copy, managed alloc (rate.cu)
 

@@ -6,6 +6,8 @@ import torch
 import paper_2212_07597_b200 as scl, tracegen
 
 cfg = tracegen.CONFIGS[int(os.environ.get("CFG", "2"))]
+if os.environ.get("NT"):
+    cfg = cfg.with_traces(int(os.environ["NT"]))
 T = int(sys.argv[1]) if len(sys.argv) > 1 else cfg.T
 ev, off = tracegen.generate(cfg)
 tr = scl.scl_trace_load(ev, off, cfg.n_sites)
@@ -21,4 +23,4 @@ for _ in range(K):
     r = scl.scl_replay_run(T, tr, stream=st, out=r)
 b.record(st)
 torch.cuda.synchronize()
-print(f"T={T} step {a.elapsed_time(b) / K * 1e3:.1f} us  (events {'off' if os.environ.get('SCL_NO_EVENTS') else 'on'})")
+print(f"cfg{os.environ.get('CFG', '2')} nt={cfg.n_traces} T={T} step {a.elapsed_time(b) / K * 1e3:.1f} us  (events {'off' if os.environ.get('SCL_NO_EVENTS') else 'on'})")

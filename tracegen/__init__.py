@@ -70,7 +70,7 @@ SWEEP = (65537, 131101, 262147, 524309, 1048583, 2097169, 4194319, 8388617,
 CONFIGS = {
     1: Config("cfg1", 1, 10_000, 16, 0.8, 1, P_1MIB, 0.01, seed=20221215 + 1),
     2: Config("cfg2", 64, 1_000_000, 1_000, 0.8, 4, P_10MIB, 5.0e-5, seed=20221215 + 2),
-    3: Config("cfg3", 1024, 1_000_000, 50_000, 1.0, 16, P_10MIB, 4.0e-5, 100.0, seed=20221215 + 3),
+    3: Config("cfg3", 1024, 1_000_000, 50_000, 1.0, 16, P_10MIB, 1.6e-4, 100.0, seed=20221215 + 3),
     4: Config("cfg4", 8192, 4_000_000, 200_000, 1.2, 32, P_10MIB, 1.0e-5, seed=20221215 + 4),
     5: Config("cfg5", 256, 100_000_000, 10_000, 1.0, 8, 65537, 2.0e-6, heavy_tailed=True,
               seed=20221215 + 5, t_sweep=SWEEP),
