@@ -122,7 +122,16 @@ typedef struct {
                                 must make the matching call.  The library loads libnccl.so.2
                                 (already in the process, or from the system) on first use;
                                 SCL_ENCCL if it cannot or a collective fails. */
+    int chain_mode;          /* how the sampler's sequential chain (a3) is evaluated:
+                                SCL_CHAIN_AUTO (0, default): the library chooses;
+                                SCL_CHAIN_RUNNERS (1): one runner lane per trace, overlapped with
+                                the stream pass;  SCL_CHAIN_SPLIT (2): each trace cut into
+                                independent pieces at its sync events (|d| >= 2T-1: a sample from
+                                any state), the pieces chained in parallel
+                                after the stream pass (hwm_mode PREFIX only; SAMPLE mode always
+                                uses the runners).  Results are identical. */
 } scl_run_opts;
+enum { SCL_CHAIN_AUTO = 0, SCL_CHAIN_RUNNERS = 1, SCL_CHAIN_SPLIT = 2 };
 
 typedef struct scl_traces scl_traces;  /* opaque: device copy of events + offsets + segment plan */
 typedef struct scl_result scl_result;  /* opaque: samples, summaries, site table, report */

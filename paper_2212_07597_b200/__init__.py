@@ -50,7 +50,7 @@ class SclError(RuntimeError):
 class _RunOpts(ctypes.Structure):
     _fields_ = [("tick_ns", ctypes.c_uint64), ("hwm_mode", ctypes.c_int), ("formula", ctypes.c_int),
                 ("defer_finalize", ctypes.c_int), ("timing", ctypes.c_int), ("elapsed_ns", ctypes.c_uint64),
-                ("cuda_stream", ctypes.c_void_p), ("nccl_comm", ctypes.c_void_p)]
+                ("cuda_stream", ctypes.c_void_p), ("nccl_comm", ctypes.c_void_p), ("chain_mode", ctypes.c_int)]
 
 
 def _load():
@@ -201,19 +201,21 @@ def scl_trace_reload(traces: Traces, events, offsets, n_sites: int, validate: bo
 
 
 HWM_PREFIX, HWM_SAMPLE = 0, 1
+CHAIN_AUTO, CHAIN_RUNNERS, CHAIN_SPLIT = 0, 1, 2
 FORMULA_PAPER, FORMULA_TEXTBOOK = 0, 1
 
 
 def scl_replay_run(threshold: int, traces: Traces, tick_ns: int = 0, formula: int = 0,
                    defer_finalize: bool = False, elapsed_ns: int = 0, stream=None,
                    out: Result | None = None, timing: bool = False, hwm_mode: int = HWM_PREFIX,
-                   nccl_comm: int | None = None) -> Result:
+                   nccl_comm: int | None = None, chain_mode: int = 0) -> Result:
     """Replay all traces at threshold T; ``out`` (a previous Result of the same
     traces) is reused in place.  stream: torch.cuda.Stream / raw handle / None.
     timing: record CUDA events for scl_result_timing / scl_result_kernel_times."""
     o = _RunOpts()
     o.tick_ns, o.hwm_mode, o.formula = tick_ns, hwm_mode, formula
     o.defer_finalize, o.elapsed_ns, o.timing = int(defer_finalize), elapsed_ns, int(timing)
+    o.chain_mode = chain_mode
     if stream is not None:
         o.cuda_stream = getattr(stream, "cuda_stream", stream)
     if nccl_comm is not None:
@@ -227,12 +229,14 @@ def scl_replay_run(threshold: int, traces: Traces, tick_ns: int = 0, formula: in
 
 def scl_replay_rethreshold(threshold: int, traces: Traces, base: Result, tick_ns: int = 0, formula: int = 0,
                            defer_finalize: bool = False, elapsed_ns: int = 0, stream=None,
-                           out: Result | None = None, timing: bool = False, hwm_mode: int = HWM_PREFIX) -> Result:
+                           out: Result | None = None, timing: bool = False, hwm_mode: int = HWM_PREFIX,
+                           chain_mode: int = 0) -> Result:
     """The replay at another threshold over the handle's last stream pass (the run that gave
     ``base``): the events are not streamed again (K5, several thresholds in one read)."""
     o = _RunOpts()
     o.tick_ns, o.hwm_mode, o.formula = tick_ns, hwm_mode, formula
     o.defer_finalize, o.elapsed_ns, o.timing = int(defer_finalize), elapsed_ns, int(timing)
+    o.chain_mode = chain_mode
     if stream is not None:
         o.cuda_stream = getattr(stream, "cuda_stream", stream)
     r = out if out is not None else Result(traces)

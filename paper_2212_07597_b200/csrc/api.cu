@@ -66,6 +66,12 @@ struct scl_traces {
     // Tier-E columns of the last stream pass (written by its post pass; a re-threshold copies them)
     mutable unsigned long long* d_tierE = nullptr;
     mutable size_t cap_tierE = 0;
+    // chain split at sync events (pchain.cu): per unit and per piece, sized with the unit plan
+    mutable UnitStart* d_ust = nullptr;
+    mutable SyncInfo* d_sync = nullptr;
+    mutable PieceCount* d_pc = nullptr;
+    mutable PieceRun* d_pr = nullptr;
+    mutable size_t cap_pieces = 0;
 };
 
 constexpr int kRing = 128;
@@ -400,6 +406,7 @@ extern "C" void scl_traces_free(scl_traces* t) {
     cudaFree(t->d_tr_nseg); cudaFree(t->d_tr_base); cudaFree(t->d_run); cudaFree(t->d_uent); cudaFree(t->d_ticket);
     cudaFree(t->d_err); cudaFree(t->d_usum); cudaFree(t->d_ustart); cudaFree(t->d_ttot);
     cudaFree(t->d_crec); cudaFree(t->d_crec_fill); cudaFree(t->d_cctr); cudaFree(t->d_tierE);
+    cudaFree(t->d_ust); cudaFree(t->d_sync); cudaFree(t->d_pc); cudaFree(t->d_pr);
     if (t->h_covf) cudaFreeHost(t->h_covf);
     delete t;
 }
@@ -503,6 +510,18 @@ static void ensure_cold_pool(const scl_traces* tr) {
     tr->crec_cap = want;
 }
 
+// SCL_CHAIN_AUTO: split the chains at sync events when the runners' sequential chains would outlast
+// the stream pass they overlap: estimated samples of the longest trace (sum|d| / T, of which about
+// one in 16 survives the cancellation of allocs and frees in our workloads) at ~3 us per resolve,
+// against ~3.2 ns of stream per event per SM... (measured in profiles/r02_chain_split.txt).
+static bool split_pays(const scl_traces* tr, uint64_t T) {
+    uint64_t smax = 0;
+    for (uint32_t t = 0; t < tr->n_traces; ++t) smax = std::max<uint64_t>(smax, tr->h_sabs[t] / T);
+    const double chain_us = (double)smax / 16.0 * 3.0;
+    const double stream_us = (double)tr->n_events * 16.0 / 5.0e6;
+    return chain_us > stream_us;
+}
+
 static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const scl_run_opts* opts, scl_result** out,
                               const scl_result* base)
 {
@@ -584,6 +603,21 @@ static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const sc
         tr->cap_tierE = tr->n_sites;
     }
     p.tierE = tr->d_tierE;
+    if (o.chain_mode < SCL_CHAIN_AUTO || o.chain_mode > SCL_CHAIN_SPLIT) { if (fresh) scl_result_free(r); return fail(SCL_EINVAL, "bad chain_mode"); }
+    const bool split = o.hwm_mode == SCL_HWM_PREFIX && tr->n_segs > 0 &&
+                       (o.chain_mode == SCL_CHAIN_SPLIT || (o.chain_mode == SCL_CHAIN_AUTO && split_pays(tr, threshold)));
+    if (split) {
+        const size_t np = (size_t)tr->n_segs + tr->n_traces;
+        if (np > tr->cap_pieces) {
+            cudaFree(tr->d_ust); cudaFree(tr->d_sync); cudaFree(tr->d_pc); cudaFree(tr->d_pr);
+            tr->d_ust = nullptr; tr->d_sync = nullptr; tr->d_pc = nullptr; tr->d_pr = nullptr; tr->cap_pieces = 0;
+            if (cudaMalloc(&tr->d_ust, np * sizeof(UnitStart)) != cudaSuccess || cudaMalloc(&tr->d_sync, np * sizeof(SyncInfo)) != cudaSuccess ||
+                cudaMalloc(&tr->d_pc, np * sizeof(PieceCount)) != cudaSuccess || cudaMalloc(&tr->d_pr, np * sizeof(PieceRun)) != cudaSuccess)
+                { cudaGetLastError(); if (fresh) scl_result_free(r); return fail(SCL_ENOMEM, "chain pieces"); }
+            tr->cap_pieces = np;
+        }
+        p.no_chain = 1; p.ust = tr->d_ust; p.sync = tr->d_sync; p.pc = tr->d_pc; p.pr = tr->d_pr;
+    }
     PrepParams& pp = p.prep;                   // done by CTA 0 of the replay kernel
     pp.table = r->d_table; pp.table_words = (size_t)tr->n_sites * SCL_NCOL + 3;
     pp.summ = reinterpret_cast<unsigned long long*>(r->d_summ); pp.summ_words = (size_t)NT * sizeof(scl_trace_summary) / 8;
@@ -614,12 +648,13 @@ static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const sc
                                  cudaMemcpyDeviceToDevice, st));
         p.rechain = 1;
         p.n_runners = std::min<unsigned>(NT, (unsigned)r->grid * 8);
-        CU(launch_rechain(p, st));
-        r->nlaunch += tr->n_segs ? 1 : 0;
+        if (split) { CU(launch_pchain(p, st)); r->nlaunch += 5; }
+        else { CU(launch_rechain(p, st)); r->nlaunch += tr->n_segs ? 1 : 0; }
     } else {
         CU(launch_replay(&tr->tmap, p, r->grid, st));
         CU(launch_cold_hist(p, st));           // Tier E of the sites beyond the shared-memory table
         r->nlaunch += (tr->n_segs ? 1 : 0) + (cold_hist_launched(p) ? 1 : 0);
+        if (split) { CU(launch_pchain(p, st)); r->nlaunch += 5; }
     }
     if (tm) { CU(cudaEventRecord(r->kev[2 * ks + 1], st)); r->nrun += 1; }
     // a6 fused into the post pass when the run finalizes at once on a small table (not when the

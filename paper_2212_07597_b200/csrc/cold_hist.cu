@@ -28,6 +28,10 @@ __global__ void __launch_bounds__(1024, 1) cold_hist_kernel(const __grid_constan
     auto one = [&](unsigned long long m) {
         const unsigned site = ev_site(m) - lo, kind = ev_kind(m);
         if (site >= ns || kind > 1) return;                       // another range, an invalid id, a pad record
+#ifdef SCL_DIAG_NOATOM
+        if (site == 12345678u) ctab[0] = 1;
+        return;
+#endif
         const unsigned long long size = ev_size(m);
         unsigned long long* row = p.table + (size_t)(site + lo) * SCL_NCOL;
         if (size < (1ull << 24)) {

@@ -1,0 +1,389 @@
+// pchain.cu -- the threshold sampler's chain cut at sync events (a3 with hwm_mode PREFIX), so that
+// one trace's samples are found by many warps at once (dense thresholds, few traces per GPU).
+//
+// The sampler "resets the counters" after every sample (reading Q2): its state between
+// events is B, the footprint at the last sample, and a sample fires at the first event whose F leaves
+// (B - T, B + T).  An event with |d| >= 2T - 1 leaves that band from ANY state (|F - B| < T before
+// it), so it always takes a sample and the state after it is B = F there, whatever came before
+// (SURVEY §7.3, Appendix A W5).  Every other quantity of the chain is associative: F and the prefix
+// maximum M (so the new-maximum test F_i > M_(i-1) of PREFIX mode, reading Q3), the sample count and
+// the last episode start.  So each trace splits into independent PIECES: one from the trace start,
+// and one after the first sync event of every unit that has one, each ending at the first sync event
+// of a later unit (included) or at the trace end.  Five stream-ordered launches:
+//   pc_prefix   warp per trace: F at every unit start and the max F before it (unit aggregates);
+//   pc_sync     warp per unit: its first sync event (chunks whose F range spans >= 2T - 1 are read),
+//               F and max F through it;
+//   pc_run<0>   warp per piece: the exact chain over the piece, counting samples / episode starts;
+//   pc_combine  warp per trace: scan of the pieces' counts -> each piece's first sample slot and the
+//               episode entering it; the trace summary, trend end points and gate sums (Q10);
+//   pc_run<1>   warp per piece: the same chain again, writing samples, Tier S (a5), episode flags and
+//               the unit entries the reclaim pass reads (a4).
+// The walk inside a unit is replay_kernel.cu's resolve_unit with an event window (the piece's part of
+// the unit); its results are identical to the sequential runners' (checked against the oracle).
+#include <algorithm>
+#include "scl_internal.cuh"
+#include "ptx.cuh"
+
+namespace scl {
+
+// ---------------------------------------------------------------------------- pc_prefix
+__global__ void __launch_bounds__(128) pc_prefix_kernel(const __grid_constant__ ReplayParams p)
+{
+    const int lane = threadIdx.x & 31;
+    const unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const Slot* rec = reinterpret_cast<const Slot*>(p.urec);
+    for (unsigned t = w; t < p.n_traces; t += nw) {
+        const unsigned base = __ldg(p.tr_base + t), nseg = __ldg(p.tr_nseg + t);
+        long long F = 0, M = 0;                              // F before the next unit; max F so far (M_-1 = 0)
+        for (unsigned k0 = 0; k0 < nseg; k0 += 32) {
+            const unsigned k = k0 + (unsigned)lane;
+            long long us = 0, ux = kNeg;
+            if (k < nseg) { us = __ldcg(&rec[base + k].usum); ux = __ldcg(&rec[base + k].umx); }
+            long long ps = us, pm = ux;                      // combined inclusive scan (s1+s2, max(m1, s1+m2))
+            #pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const long long os = shfl_up_ll(ps, d), om = shfl_up_ll(pm, d);
+                if (lane >= d) { pm = llmax(om, os + pm); ps = os + ps; }
+            }
+            const long long pe = ps - us;                    // F at the unit start, relative to F
+            long long me = shfl_up_ll(pm, 1);
+            if (lane == 0) me = kNeg;
+            if (k < nseg) { UnitStart x; x.F0 = F + pe; x.M0 = llmax(M, me == kNeg ? kNeg : F + me); p.ust[base + k] = x; }
+            const long long ls = shfl_ll(ps, 31), lm = shfl_ll(pm, 31);
+            M = llmax(M, F + lm);
+            F += ls;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------- pc_sync
+// The unit's first event with |d| >= 2T - 1 (kind alloc / free, inside its trace).  A chunk can hold
+// one only if its F range, chunk start included, spans at least 2T - 1.
+__global__ void __launch_bounds__(128) pc_sync_kernel(const __grid_constant__ ReplayParams p)
+{
+    const int lane = threadIdx.x & 31;
+    const unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const Slot* rec = reinterpret_cast<const Slot*>(p.urec);
+    const unsigned long long thr = 2ull * (unsigned long long)p.T - 1ull;
+    for (unsigned u = w; u < p.n_segs; u += nw) {
+        const Slot& S = rec[u];
+        const long long sPc = __ldcg(&S.Pc[lane]), sax = __ldcg(&S.ax[lane]), san = __ldcg(&S.an[lane]);
+        const long long row_base = __ldcg(&S.info.row_base), off_t = __ldcg(&S.info.off_t), n_t = __ldcg(&S.info.n_t);
+        const UnitStart us = p.ust[u];
+        const long long span = llmax(sax, sPc) - llmin(san, sPc);
+        unsigned cand = __ballot_sync(kFull, span >= (long long)thr);
+        SyncInfo out; out.pos = -1; out.pad0 = 0; out.Fs = 0; out.Ms = 0; out.pad1 = 0;
+        while (cand) {
+            const int c = __ffs(cand) - 1;
+            cand &= cand - 1;
+            const long long row = row_base + (long long)c * 32 + lane;
+            unsigned long long rp[kEpt], rm[kEpt];
+            load_row_global(p.ev, row, rp, rm);
+            const long long e0 = row * kEpt - off_t;
+            long long run = 0, lmx = kNeg;
+            unsigned sy = 0;
+            #pragma unroll
+            for (int j = 0; j < kEpt; ++j) {
+                const long long ie = e0 + j;
+                const unsigned kind = ev_kind(rm[j]);
+                const bool af = ie >= 0 && ie < n_t && kind < 2;
+                const unsigned long long sz = ev_size(rm[j]);
+                run += af ? (kind == 0 ? (long long)sz : -(long long)sz) : 0;
+                if (af) lmx = llmax(lmx, run);
+                sy |= (af && sz >= thr ? 1u : 0u) << j;
+            }
+            const unsigned lm = __ballot_sync(kFull, sy != 0);
+            if (!lm) continue;
+            const int l0 = __ffs(lm) - 1;
+            // F and max F before lane l0's row: combined scan of the rows (sum, max prefix)
+            long long ssum = run, smax = lmx;
+            #pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const long long os = shfl_up_ll(ssum, d), om = shfl_up_ll(smax, d);
+                if (lane >= d) { smax = llmax(om, os + smax); ssum = os + ssum; }
+            }
+            const long long Fc = us.F0 + shfl_ll(sPc, c);
+            const long long Mc = llmax(us.M0, warp_max(lane < c ? us.F0 + sax : kNeg));   // max F before chunk c
+            const long long Fl = Fc + ssum - run;
+            long long Ml = shfl_up_ll(smax, 1);
+            Ml = lane == 0 ? Mc : llmax(Mc, Ml == kNeg ? kNeg : Fc + Ml);
+            if (lane == l0) {
+                const int j0 = __ffs(sy) - 1;
+                long long F = Fl, M = Ml;
+                #pragma unroll
+                for (int j = 0; j < kEpt; ++j) {
+                    if (j <= j0) {
+                        const long long ie = e0 + j;
+                        const unsigned kind = ev_kind(rm[j]);
+                        if (ie >= 0 && ie < n_t && kind < 2) {
+                            const long long sz = (long long)ev_size(rm[j]);
+                            F += kind == 0 ? sz : -sz;
+                            M = llmax(M, F);
+                        }
+                    }
+                }
+                out.pos = c * 256 + l0 * kEpt + j0; out.Fs = F; out.Ms = M;
+            }
+            out.pos = __shfl_sync(kFull, out.pos, l0); out.Fs = shfl_ll(out.Fs, l0); out.Ms = shfl_ll(out.Ms, l0);
+            break;
+        }
+        if (lane == 0) p.sync[u] = out;
+    }
+}
+
+// ---------------------------------------------------------------------------- pc_run
+struct PState {
+    long long B;                                  // footprint at the last sample (the counter's origin)
+    unsigned long long n, nep, lep, lep_ptr;      // samples, episode starts, last start (local index + 1), its ptr
+    long long ffirst;                             // footprint at the first sample
+    unsigned long long base, ep1, eptr;           // pass 2: first slot; the episode in progress (slot + 1) and ptr
+};
+
+// The samples of one unit inside a piece's window [wlo, whi) (unit positions).  Fu: F before the
+// unit's first event, Mu: max F before it.  As replay_kernel.cu resolve_unit (64-bit walk): the
+// chunks whose F range leaves (B - T, B + T) and meet the window are read (lane <-> row), one
+// combined scan gives every lane F and the running maximum before its row, and the lane holding the
+// first exit walks its events; events outside the window move F and M but take no sample.
+template <bool kWrite>
+__device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, long long Mu, unsigned wlo, unsigned whi,
+                           PState& x, int lane)
+{
+    const long long sPc = __ldcg(&S.Pc[lane]), sax = __ldcg(&S.ax[lane]), san = __ldcg(&S.an[lane]);
+    const long long row_base = __ldcg(&S.info.row_base), off_t = __ldcg(&S.info.off_t), n_t = __ldcg(&S.info.n_t);
+    const long long hiL = Fu + llmax(sax, sPc), loL = Fu + llmin(san, sPc);
+    const unsigned cb = (unsigned)lane * 256u;
+    const bool inwin = cb < whi && cb + 256u > wlo;
+    int cnext = 0;
+    for (;;) {
+        const unsigned ccm = __ballot_sync(kFull, lane >= cnext && inwin && (hiL >= x.B + p.T || loL <= x.B - p.T));
+        if (!ccm) break;
+        const int c = __ffs(ccm) - 1;
+        const long long row = row_base + (long long)c * 32 + lane;
+        unsigned long long rp[kEpt], rm[kEpt];
+        load_row_global(p.ev, row, rp, rm);
+        const long long Fc = Fu + shfl_ll(sPc, c);
+        const long long Mc = llmax(Mu, warp_max(lane < c ? Fu + sax : kNeg));        // max F before chunk c
+        const long long e0 = row * kEpt - off_t;                                     // trace index of the row
+        const unsigned q0 = (unsigned)c * 256u + (unsigned)lane * kEpt;              // unit position of the row
+        long long fe[kEpt], run = 0, lmx = kNeg, lmn = kPos;
+        unsigned live = 0;
+        #pragma unroll
+        for (int jj = 0; jj < kEpt; ++jj) {
+            const long long ie = e0 + jj;
+            const unsigned kind = ev_kind(rm[jj]);
+            const bool af = ie >= 0 && ie < n_t && kind < 2;
+            const long long sz = (long long)ev_size(rm[jj]);
+            run += af ? (kind == 0 ? sz : -sz) : 0;
+            fe[jj] = run;
+            if (af) {
+                lmx = llmax(lmx, run); lmn = llmin(lmn, run);
+                if (q0 + jj >= wlo && q0 + jj < whi) live |= 1u << jj;
+            }
+        }
+        long long ssum = run, smax = lmx;
+        #pragma unroll
+        for (int dd = 1; dd < 32; dd <<= 1) {
+            const long long os = shfl_up_ll(ssum, dd), om = shfl_up_ll(smax, dd);
+            if (lane >= dd) { smax = llmax(om, os + smax); ssum = os + ssum; }
+        }
+        const long long Fl = Fc + ssum - run;                                         // F before the lane's row
+        long long Ml = shfl_up_ll(smax, 1);
+        Ml = lane == 0 ? Mc : llmax(Mc, Ml == kNeg ? kNeg : Fc + Ml);                 // max F before it
+        int cur = 0;
+        for (;;) {
+            const unsigned cm = __ballot_sync(kFull, lane >= cur && live &&
+                                              (Fl + lmx >= x.B + p.T || Fl + lmn <= x.B - p.T));
+            if (!cm) break;
+            const int l0 = __ffs(cm) - 1;
+            if (lane == l0) {
+                unsigned from = 0;
+                for (;;) {
+                    unsigned ex = 0;
+                    #pragma unroll
+                    for (int jj = 0; jj < kEpt; ++jj) {
+                        const long long F = Fl + fe[jj];
+                        ex |= (F >= x.B + p.T || F <= x.B - p.T ? 1u : 0u) << jj;
+                    }
+                    ex &= live & ~((1u << from) - 1u);
+                    if (!ex) break;
+                    const int js = __ffs(ex) - 1;
+                    long long F = 0, Mp = Ml;
+                    unsigned long long ms = 0, ps = 0;
+                    #pragma unroll
+                    for (int jj = 0; jj < kEpt; ++jj) {
+                        if (jj < js) Mp = llmax(Mp, Fl + fe[jj]);
+                        if (jj == js) { F = Fl + fe[jj]; ms = rm[jj]; ps = rp[jj]; }
+                    }
+                    const long long net = F - x.B;                                    // the |A - F| counter
+                    const bool growth = net > 0;
+                    const bool nm = growth && F > Mp;                                  // new high-water mark (Q3)
+                    if (kWrite) {
+                        const unsigned long long slot = x.base + x.n;
+                        scl_sample smp;
+                        smp.idx = (unsigned long long)(e0 + js); smp.net = net; smp.footprint = F;
+                        smp.site = ev_site(ms); smp.kind = growth ? 0 : 1; smp.new_max = nm ? 1 : 0; smp.pad = 0;
+                        p.samples[slot] = smp;
+                        sample_counters(p, smp.site, growth, net, nm);
+                        if (nm) { p.ep_flag[slot] = 0u; x.ep1 = slot + 1; x.eptr = ps; }
+                    }
+                    if (nm) { ++x.nep; x.lep = x.n + 1; x.lep_ptr = ps; }
+                    if (x.n == 0) x.ffirst = F;
+                    ++x.n; x.B = F;                                                    // "resets the counters"
+                    from = (unsigned)js + 1;
+                }
+            }
+            x.B = shfl_ll(x.B, l0); x.n = __shfl_sync(kFull, x.n, l0); x.nep = __shfl_sync(kFull, x.nep, l0);
+            x.lep = __shfl_sync(kFull, x.lep, l0); x.lep_ptr = __shfl_sync(kFull, x.lep_ptr, l0);
+            x.ffirst = shfl_ll(x.ffirst, l0);
+            if (kWrite) { x.ep1 = __shfl_sync(kFull, x.ep1, l0); x.eptr = __shfl_sync(kFull, x.eptr, l0); }
+            cur = l0 + 1;
+        }
+        cnext = c + 1;
+    }
+    __syncwarp();
+}
+
+template <bool kWrite>
+__global__ void __launch_bounds__(128) pc_run_kernel(const __grid_constant__ ReplayParams p)
+{
+    const int lane = threadIdx.x & 31;
+    const unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const Slot* rec = reinterpret_cast<const Slot*>(p.urec);
+    const unsigned npieces = p.n_traces + p.n_segs;
+    for (unsigned id = w; id < npieces; id += nw) {
+        const bool tfirst = id < p.n_traces;
+        unsigned t, u0, wlo0;
+        long long B0;
+        if (tfirst) {
+            t = id;
+            if (__ldg(p.tr_nseg + t) == 0) { if (!kWrite && lane == 0) p.pc[id].active = 0; continue; }
+            u0 = __ldg(p.tr_base + t); wlo0 = 0; B0 = 0;
+        } else {
+            u0 = id - p.n_traces;
+            const SyncInfo sy = p.sync[u0];
+            if (sy.pos < 0) { if (!kWrite && lane == 0) p.pc[id].active = 0; continue; }
+            t = __ldcg(&rec[u0].info.t); wlo0 = (unsigned)sy.pos + 1; B0 = sy.Fs;
+        }
+        const unsigned uend = __ldg(p.tr_base + t) + __ldg(p.tr_nseg + t);
+        PState x{B0, 0, 0, 0, 0, 0, 0, 0, 0};
+        if (kWrite) { const PieceRun r = p.pr[id]; x.base = r.base; x.ep1 = r.ep1; x.eptr = r.eptr; }
+        for (unsigned u = u0; u < uend; ++u) {
+            const bool first = u == u0;
+            const unsigned wlo = first ? wlo0 : 0u;
+            unsigned whi = (unsigned)kUnit;
+            bool last = false;
+            if (!first || tfirst) {                          // the piece ends at this unit's first sync event
+                const int sp = p.sync[u].pos;
+                if (sp >= 0) { whi = (unsigned)sp + 1; last = true; }
+            }
+            const UnitStart us = p.ust[u];
+            const Slot& S = rec[u];
+            if (kWrite && wlo == 0 && lane == 0) {            // the state entering the unit (reclaim pass, a4)
+                UnitEntry* e = p.uent + u;
+                e->ep1 = x.ep1; e->eptr = x.eptr; e->s_in = x.base + x.n;
+            }
+            const long long umx = __ldcg(&S.umx), umn = __ldcg(&S.umn);
+            if (us.F0 + umx >= x.B + p.T || us.F0 + umn <= x.B - p.T)    // the F range can leave the band
+                piece_unit<kWrite>(p, S, us.F0, us.M0, wlo, whi, x, lane);
+            if (kWrite && whi == (unsigned)kUnit && lane == 0) p.uent[u].s_out = x.base + x.n;
+            if (last) break;
+        }
+        if (!kWrite && lane == 0) {
+            PieceCount c;
+            c.n = x.n; c.nep = x.nep; c.lep = x.lep; c.lep_ptr = x.lep_ptr; c.ffirst = x.ffirst; c.flast = x.B;
+            c.active = 1; c.pad = 0;
+            p.pc[id] = c;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------- pc_combine
+// Per trace, its pieces in order (the trace-first piece, then one per unit with a sync event): first
+// sample slot = sbase + the samples of the pieces before; the episode entering a piece = the last
+// episode start of the pieces before (slot + 1, pointer); the summary (f_final, hwm, n_samples,
+// n_episodes, trend end points) and the gate sums (reading Q10).
+__global__ void __launch_bounds__(128) pc_combine_kernel(const __grid_constant__ ReplayParams p)
+{
+    const int lane = threadIdx.x & 31;
+    const unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const Slot* rec = reinterpret_cast<const Slot*>(p.urec);
+    for (unsigned t = w; t < p.n_traces; t += nw) {
+        const unsigned base = __ldg(p.tr_base + t), nseg = __ldg(p.tr_nseg + t);
+        if (nseg == 0) continue;                             // summary zeroed by the preparation
+        const unsigned long long sb = p.sbase[t];
+        const PieceCount f = p.pc[t];
+        if (lane == 0) { PieceRun r; r.base = sb; r.ep1 = 0; r.eptr = 0; r.pad = 0; p.pr[t] = r; }
+        unsigned long long slot = sb + f.n, ep1 = f.lep ? sb + f.lep : 0, eptr = f.lep ? f.lep_ptr : 0, nep = f.nep;
+        long long ffirst = f.ffirst, flast = f.flast;
+        bool any = f.n > 0;
+        for (unsigned k0 = 0; k0 < nseg; k0 += 32) {
+            const unsigned u = base + k0 + (unsigned)lane;
+            const bool act = k0 + (unsigned)lane < nseg && p.sync[u].pos >= 0;
+            PieceCount c{};
+            if (act) c = p.pc[p.n_traces + u];
+            unsigned long long ns = act ? c.n : 0;
+            unsigned long long incl = ns;
+            #pragma unroll
+            for (int d = 1; d < 32; d <<= 1) { const unsigned long long o = __shfl_up_sync(kFull, incl, d); if (lane >= d) incl += o; }
+            const unsigned long long pbase = slot + incl - ns;
+            // the episode entering this lane's piece: the last episode start among the earlier lanes
+            const bool hep = act && c.lep != 0;
+            const unsigned long long my_ep1 = hep ? pbase + c.lep : 0, my_ptr = hep ? c.lep_ptr : 0;
+            int last = hep ? lane : -1;                      // inclusive max scan of the lanes with a start
+            #pragma unroll
+            for (int d = 1; d < 32; d <<= 1) { const int o = __shfl_up_sync(kFull, last, d); if (lane >= d) last = max(last, o); }
+            int prev = __shfl_up_sync(kFull, last, 1);
+            if (lane == 0) prev = -1;
+            const unsigned long long pe1 = __shfl_sync(kFull, my_ep1, prev < 0 ? 0 : prev);
+            const unsigned long long pep = __shfl_sync(kFull, my_ptr, prev < 0 ? 0 : prev);
+            if (act) {
+                PieceRun r; r.base = pbase; r.ep1 = prev < 0 ? ep1 : pe1; r.eptr = prev < 0 ? eptr : pep; r.pad = 0;
+                p.pr[p.n_traces + u] = r;
+            }
+            const int lastall = __shfl_sync(kFull, last, 31);
+            if (lastall >= 0) { ep1 = __shfl_sync(kFull, my_ep1, lastall); eptr = __shfl_sync(kFull, my_ptr, lastall); }
+            nep += (unsigned long long)warp_sum((long long)(act ? c.nep : 0));
+            // trend end points: the first / last piece (in order) that took a sample
+            const unsigned hs = __ballot_sync(kFull, act && c.n > 0);
+            if (hs) {
+                const long long ff = shfl_ll(c.ffirst, __ffs(hs) - 1), fl = shfl_ll(c.flast, 31 - __clz(hs));
+                if (!any) ffirst = ff;
+                flast = fl;
+                any = true;
+            }
+            slot = __shfl_sync(kFull, slot + incl, 31);
+        }
+        if (lane == 0) {
+            const unsigned ul = base + nseg - 1;
+            const UnitStart us = p.ust[ul];
+            scl_trace_summary* sm = &p.summ[t];
+            sm->f_final = us.F0 + __ldcg(&rec[ul].usum);
+            sm->hwm = llmax(us.M0, us.F0 + __ldcg(&rec[ul].umx));
+            const unsigned long long n = slot - sb;
+            sm->n_samples = n; sm->n_episodes = nep;
+            const long long ff = any ? ffirst : 0, fl = any ? flast : 0;
+            sm->f_first_sample = ff; sm->f_last_sample = fl;
+            if (n >= 2) {
+                unsigned long long* gate = p.table + (size_t)p.n_sites * SCL_NCOL;
+                atomicAdd(&gate[0], (unsigned long long)(fl - ff));
+                atomicAdd(&gate[1], (unsigned long long)(ff > 1 ? ff : 1));
+                atomicAdd(&gate[2], 1ull);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------- launch
+cudaError_t launch_pchain(const ReplayParams& p, cudaStream_t st)
+{
+    if (p.n_segs == 0) return cudaSuccess;
+    auto grid = [](unsigned warps) { return std::max(1u, std::min((warps + 3) / 4, 148u * 16)); };
+    pc_prefix_kernel<<<grid(p.n_traces), 128, 0, st>>>(p);
+    pc_sync_kernel<<<grid(p.n_segs), 128, 0, st>>>(p);
+    pc_run_kernel<false><<<grid(p.n_traces + p.n_segs), 128, 0, st>>>(p);
+    pc_combine_kernel<<<grid(p.n_traces), 128, 0, st>>>(p);
+    pc_run_kernel<true><<<grid(p.n_traces + p.n_segs), 128, 0, st>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace scl

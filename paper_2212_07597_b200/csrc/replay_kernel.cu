@@ -31,21 +31,6 @@
 
 namespace scl {
 
-struct SegInfo {                     // one unit ticket, as the producer resolved it
-    unsigned u, t, kraw, slot;       // ticket, trace, unit index (| last << 31), state slot
-    long long off_t, n_t, row_base;  // trace start, trace length, first global row of the unit
-    unsigned nbox, pad;              // boxes of this unit that overlap the trace
-};
-struct __align__(16) Slot {          // compute -> publisher -> runners / post pass: one unit
-    SegInfo info;
-    long long Pc[kChunks], ax[kChunks], an[kChunks];       // chunk prefix; max/min relative to the unit start
-                                                           // (before the compose: chunk sum, max, min
-                                                           // relative to the chunk start)
-    long long usum, umx, umn;                              // unit aggregate
-    unsigned pad0, pad1;
-    unsigned bloom[kChunks][kBloomWords];
-};
-
 constexpr int kTabSlots = 4 * kHot > 2 * kWarm ? 4 * kHot : 2 * kWarm;   // the two table layouts share storage
 constexpr int kESlots = kTabSlots + kComputeWarps * 32;              // + one sink slot per compute lane
 
@@ -102,16 +87,6 @@ __device__ __forceinline__ unsigned bloom_mask(unsigned long long ptr) {
 #define RPROF_ADD(i, v)
 #define PROF_TOUCH(v)
 #endif
-
-// The 8 events of one global row, through L2 (re-read path).  A row past the end of its trace
-// (a chunk's lanes beyond the last event, masked by the caller) is still read: the event buffer
-// carries 32 zeroed rows past its last row for exactly these lanes (scl_trace_load).
-__device__ __forceinline__ void load_row_global(const scl_event* ev, long long row,
-                                                unsigned long long* ptr, unsigned long long* meta) {
-    const ulonglong2* q = reinterpret_cast<const ulonglong2*>(ev + row * kEpt);
-    #pragma unroll
-    for (int j = 0; j < kEpt; ++j) { ulonglong2 v = __ldcg(q + j); ptr[j] = v.x; meta[j] = v.y; }
-}
 
 // ============================================================================ per-run preparation (CTA 0)
 __device__ void prepare_run(const ReplayParams& rp, unsigned long long* scratch)
@@ -235,6 +210,19 @@ __device__ __forceinline__ unsigned cold_records(const ReplayParams& p, ColdCurs
         cc.base = __shfl_sync(kFull, nb, 0); cc.fill = 0;
     }
     if (cc.base == ~0ull) return rec;                 // -> direct L2 reductions
+#ifdef SCL_DIAG_NOSTAGE
+    cc.fill += tot; return 0u;
+#endif
+#ifdef SCL_DIRECTREC
+    {   // lane-scattered stores of the records straight from registers (no staging)
+        unsigned long long* d = p.crec + cc.base + cc.fill + (incl - nc);
+        #pragma unroll
+        for (int j = 0; j < kEpt; ++j)
+            if ((rec >> j) & 1u) *d++ = meta[j];
+        cc.fill += tot;
+        return 0u;
+    }
+#endif
     __syncwarp();                                     // every lane's row is in registers
     uint32_t a = slice_s + 8u * (incl - nc);
     #pragma unroll
@@ -260,7 +248,11 @@ __device__ __forceinline__ unsigned cold_records(const ReplayParams& p, ColdCurs
     for (unsigned k = (unsigned)lane; k < tot; k += 32) {
         unsigned long long v;
         asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(slice_s + 8u * k) : "memory");
+#ifndef SCL_DIAG_NOSTORE
         dst[k] = v;
+#else
+        if (v == 0x1234567ull) dst[k] = v;
+#endif
     }
     cc.fill += tot;
 #endif
@@ -362,6 +354,9 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
                     }
                 }
             }
+#ifdef SCL_DIAG_NOREC
+            rec = 0;
+#endif
             if (!all_hot)                                     // (warp-collective; fallback -> L2)
                 cold |= cold_records(p, cc, meta, rec, smem_u32(boxp) + (uint32_t)w8 * 32u * 128u, lane, staged);
             while (cold) {                                    // cold site / huge size: L2 reductions
@@ -395,7 +390,9 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
             csum = shfl_ll(incl, 31);
         }
         if (lane == 0) { S.Pc[c] = csum; S.ax[c] = cmx; S.an[c] = cmn; }   // composed in place below
+#ifndef SCL_DIAG_NOFENCE
         if (staged) fence_proxy_async_shared();            // generic writes before the next TMA write of the box
+#endif
         __syncwarp();
         mbar_arrive(&s.empty[st]);                        // box consumed
         PROF_MARK(2)
@@ -476,18 +473,6 @@ __device__ __forceinline__ void store_rstate(RunState* rs, const RState& x, int 
         rs->F = x.F; rs->M = x.M; rs->B = x.B; rs->n = x.n; rs->nep = x.nep; rs->ep1 = x.ep1; rs->eptr = x.eptr;
         rs->Ms = x.Ms; rs->next = x.next;
     }
-}
-
-// Tier S of one sample (a5: n_growth / growth_bytes or n_decline / decline_bytes of the
-// sample's site -- a decline at the free's site, reading Q14) and, at an episode start, the site's
-// leak mallocs (the frees are counted by the reclaim pass).  Fire-and-forget L2 reductions
-// by the runner lane that takes the sample.
-__device__ __forceinline__ void sample_counters(const ReplayParams& p, unsigned site, bool growth, long long net, bool nm)
-{
-    unsigned long long* row = p.table + (size_t)site * SCL_NCOL;
-    atomicAdd(&row[growth ? SCL_COL_N_GROWTH : SCL_COL_N_DECLINE], 1ull);
-    atomicAdd(&row[growth ? SCL_COL_GROWTH_BYTES : SCL_COL_DECLINE_BYTES], (unsigned long long)(growth ? net : -net));
-    if (nm) atomicAdd(&row[SCL_COL_LEAK_MALLOCS], 1ull);
 }
 
 // A unit in which a sample fires: resolve it chunk by chunk (a3).  x: state before the unit
@@ -902,6 +887,7 @@ __device__ void publisher_role(const ReplayParams& p, Smem& s, int lane)
 // published, with the exact sequential state (kept in p.run between visits).
 __device__ void runner_role(const ReplayParams& p, unsigned ri, int lane)
 {
+    if (p.no_chain) return;                               // the chains run in the pchain kernels
     const unsigned ep_tag = p.epoch;
     const unsigned nr = p.n_runners;
     if (!p.rechain) wait_prepared(p);                     // runner states, sample bases: CTA 0

@@ -72,6 +72,21 @@ struct __align__(16) RunState {
 // sample slots [s_in, s_out) taken inside the unit.
 struct __align__(16) UnitEntry { unsigned long long ep1, eptr, s_in, s_out; };
 
+struct SegInfo {                     // one unit ticket, as the producer resolved it
+    unsigned u, t, kraw, slot;       // ticket, trace, unit index (| last << 31), state slot
+    long long off_t, n_t, row_base;  // trace start, trace length, first global row of the unit
+    unsigned nbox, pad;              // boxes of this unit that overlap the trace
+};
+struct __align__(16) Slot {          // compute -> publisher -> runners / post pass: one unit record (urec)
+    SegInfo info;
+    long long Pc[kChunks], ax[kChunks], an[kChunks];       // chunk prefix; max/min relative to the unit start
+                                                           // (before the compose: chunk sum, max, min
+                                                           // relative to the chunk start)
+    long long usum, umx, umn;                              // unit aggregate
+    unsigned pad0, pad1;
+    unsigned bloom[kChunks][kBloomWords];
+};
+
 // One unit ticket, resolved on the host at load time (one 32-B load per ticket).
 struct __align__(16) TicketInfo {
     long long off_t, n_t;             // trace start (global event index), trace length
@@ -158,10 +173,57 @@ struct ReplayParams {
     unsigned* crec_fill;              // [crec_cap / kRecChunk] records written to each allocated chunk
     unsigned long long* covf;         // host-mapped: set when the pool was exhausted (the host grows it)
     unsigned long long* tierE;        // [n_sites * 4] Tier-E columns of the stream pass (post pass copy; re-thresholds)
+    // chain split at sync events (pchain.cu; hwm_mode PREFIX): the embedded runners stand down
+    int no_chain;                     // 1: runner warps exit at once (the pchain kernels run the chains)
+    struct UnitStart* ust;            // [n_segs] F at each unit start, max F before it
+    struct SyncInfo* sync;            // [n_segs] the unit's first sync event (|d| >= 2T - 1)
+    struct PieceCount* pc;            // [n_traces + n_segs] pass-1 counts of every piece
+    struct PieceRun* pr;              // [n_traces + n_segs] pass-2 inputs (slot base, entering episode)
 };
 
+// Chain pieces (pchain.cu).  A sync event (|d| >= 2T - 1) takes a sample from
+// any counter state, after which the state is B = F there: each trace splits into independent
+// pieces, one starting at the trace start and one after the first sync event of every unit that
+// has one (piece id n_traces + unit), each ending at the first sync event of a later unit (included)
+// or at the trace end.
+struct UnitStart { long long F0, M0; };                  // F before the unit's first event; max F before it (M_-1 = 0)
+struct SyncInfo { long long Fs, Ms; int pos, pad0; long long pad1; };   // pos: unit position (-1: none); F, max F through it
+struct PieceCount {                                      // pass 1 (count) of one piece
+    unsigned long long n, nep;                           // samples, new-maximum samples (episode starts)
+    unsigned long long lep, lep_ptr;                     // local index + 1 of the last episode start (0: none), its pointer
+    long long ffirst, flast;                             // footprint at the first / last sample
+    unsigned long long active, pad;
+};
+struct PieceRun { unsigned long long base, ep1, eptr, pad; };   // pass 2: first slot; episode entering (slot + 1, 0 none)
+cudaError_t launch_pchain(const ReplayParams& p, cudaStream_t st);
 
 
+
+
+#ifdef __CUDACC__
+// The 8 events of one global row, through L2 (re-read path).  A row past the end of its trace
+// (a chunk's lanes beyond the last event, masked by the caller) is still read: the event buffer
+// carries 32 zeroed rows past its last row for exactly these lanes (scl_trace_load).
+__device__ __forceinline__ void load_row_global(const scl_event* ev, long long row,
+                                                unsigned long long* ptr, unsigned long long* meta) {
+    const ulonglong2* q = reinterpret_cast<const ulonglong2*>(ev + row * kEpt);
+    #pragma unroll
+    for (int j = 0; j < kEpt; ++j) { ulonglong2 v = __ldcg(q + j); ptr[j] = v.x; meta[j] = v.y; }
+}
+
+// Tier S of one sample (a5: n_growth / growth_bytes or n_decline / decline_bytes of the
+// sample's site -- a decline at the free's site, reading Q14) and, at an episode start, the site's
+// leak mallocs (the frees are counted by the reclaim pass).  Fire-and-forget L2 reductions
+// by the runner lane that takes the sample.
+__device__ __forceinline__ void sample_counters(const ReplayParams& p, unsigned site, bool growth, long long net, bool nm)
+{
+    unsigned long long* row = p.table + (size_t)site * SCL_NCOL;
+    atomicAdd(&row[growth ? SCL_COL_N_GROWTH : SCL_COL_N_DECLINE], 1ull);
+    atomicAdd(&row[growth ? SCL_COL_GROWTH_BYTES : SCL_COL_DECLINE_BYTES], (unsigned long long)(growth ? net : -net));
+    if (nm) atomicAdd(&row[SCL_COL_LEAK_MALLOCS], 1ull);
+}
+
+#endif
 
 constexpr int kUCols = 4;               // per-unit byte sums: alloc, free, copy, managed alloc (rate.cu)
 

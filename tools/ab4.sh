@@ -1,4 +1,4 @@
-# A/B/C/D step time of four builds (libscl_{A,B,C,D}.so) in one GPU session, 2 rounds
+# A/B/C/D device times of four builds (libscl_{A,B,C,D}.so) in one GPU session, 2 rounds
 for i in 1 2; do
-  for v in A B C D; do echo -n "$v "; SCL_LIB=paper_2212_07597_b200/libscl_$v.so timeout 180 python tools/step_time.py 2>&1 | tail -1; done
+  for v in A B C D; do SCL_LIB=paper_2212_07597_b200/libscl_$v.so timeout 180 python tools/kt.py 2>&1 | tail -1; done
 done
