@@ -47,7 +47,9 @@ struct scl_traces {
     unsigned long long* d_uagg = nullptr;      // per unit: tagged aggregate words (published flag)
     UnitEntry* d_uent = nullptr;               // per unit: state entering it (runner -> reclaim pass)
     size_t cap_segs = 0;
-    unsigned long long* d_err = nullptr;       // first invalid event (load check)
+    unsigned long long* d_err = nullptr;       // [1 + 64] first invalid event (load check), then the log2-size
+                                               // histogram of the alloc / free events (chain-split heuristic)
+    std::vector<uint64_t> h_shist;
     unsigned int* d_ticket = nullptr;
     std::vector<uint64_t> h_off, h_sabs;
     uint32_t n_segs = 0;
@@ -61,7 +63,8 @@ struct scl_traces {
     mutable unsigned long long* d_crec = nullptr;
     mutable unsigned* d_crec_fill = nullptr;
     mutable unsigned long long* d_cctr = nullptr;       // [2] records allocated, exhausted
-    mutable unsigned long long crec_cap = 0;
+    mutable unsigned long long crec_cap = 0;         // records (of the current record size)
+    mutable size_t crec_bytes = 0, crec_fills = 0;
     mutable unsigned long long* h_covf = nullptr;       // pinned: the last exhausted pool (grow it)
     // Tier-E columns of the last stream pass (written by its post pass; a re-threshold copies them)
     mutable unsigned long long* d_tierE = nullptr;
@@ -71,7 +74,12 @@ struct scl_traces {
     mutable SyncInfo* d_sync = nullptr;
     mutable PieceCount* d_pc = nullptr;
     mutable PieceRun* d_pr = nullptr;
+    mutable UnitLocal* d_ul = nullptr;
     mutable size_t cap_pieces = 0;
+    mutable scl_sample* d_pscr = nullptr;              // scratch blocks of the pieces' samples
+    mutable unsigned* d_pnext = nullptr;
+    mutable unsigned* d_pctr = nullptr;
+    mutable size_t cap_pblocks = 0;
 };
 
 constexpr int kRing = 128;
@@ -259,7 +267,7 @@ static scl_status upload(scl_traces* tr, const scl_event* src, bool src_dev, std
         tr->cap_tr = nt1;
     }
     if (!tr->d_err) {
-        if (!grow(tr->d_err, 1) || !grow(tr->d_ticket, 8)) { cudaFree(tr->d_err); tr->d_err = nullptr; return nomem("counters"); }
+        if (!grow(tr->d_err, 65) || !grow(tr->d_ticket, 8)) { cudaFree(tr->d_err); tr->d_err = nullptr; return nomem("counters"); }
         // ticket[7] is the "run prepared" flag compared with the run's epoch: a fresh block may hold
         // a freed handle's epoch (fuzzing found producers starting before CTA 0 had prepared)
         CU(cudaMemsetAsync(tr->d_ticket, 0, 8 * sizeof(unsigned), st));
@@ -273,8 +281,9 @@ static scl_status upload(scl_traces* tr, const scl_event* src, bool src_dev, std
     CU(cudaMemcpyAsync(tr->d_off, h_off.data(), h_off.size() * 8, cudaMemcpyHostToDevice, st));
     CU(cudaMemsetAsync(tr->d_sabs, 0, nt1 * 8, st));
     CU(cudaMemsetAsync(tr->d_err, 0xff, 8, st));
+    CU(cudaMemsetAsync(tr->d_err + 1, 0, 64 * 8, st));
     CU(launch_load_stats(csrc ? csrc : tr->d_ev, tr->d_off, n_traces, n, n_sites, tr->d_sabs, tr->d_err,
-                         csrc ? tr->d_ev : nullptr, st));
+                         csrc ? tr->d_ev : nullptr, tr->d_err + 1, st));
 
     // unit plan (while the copy runs): unit k of trace t covers rows (off_t/8) + 1024k ...;
     // tickets ordered (k, t) so that one trace's units are spread over the run
@@ -321,6 +330,8 @@ static scl_status upload(scl_traces* tr, const scl_event* src, bool src_dev, std
     unsigned long long err = 0;
     tr->h_sabs.resize(n_traces);
     CU(cudaMemcpyAsync(&err, tr->d_err, 8, cudaMemcpyDeviceToHost, st));
+    tr->h_shist.assign(64, 0);
+    CU(cudaMemcpyAsync(tr->h_shist.data(), tr->d_err + 1, 64 * 8, cudaMemcpyDeviceToHost, st));
     if (n_traces) CU(cudaMemcpyAsync(tr->h_sabs.data(), tr->d_sabs, n_traces * 8, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     tr->n_traces = n_traces; tr->n_sites = n_sites; tr->n_events = n; tr->max_len = max_len; tr->n_segs = total;
@@ -406,7 +417,8 @@ extern "C" void scl_traces_free(scl_traces* t) {
     cudaFree(t->d_tr_nseg); cudaFree(t->d_tr_base); cudaFree(t->d_run); cudaFree(t->d_uent); cudaFree(t->d_ticket);
     cudaFree(t->d_err); cudaFree(t->d_usum); cudaFree(t->d_ustart); cudaFree(t->d_ttot);
     cudaFree(t->d_crec); cudaFree(t->d_crec_fill); cudaFree(t->d_cctr); cudaFree(t->d_tierE);
-    cudaFree(t->d_ust); cudaFree(t->d_sync); cudaFree(t->d_pc); cudaFree(t->d_pr);
+    cudaFree(t->d_ust); cudaFree(t->d_sync); cudaFree(t->d_pc); cudaFree(t->d_pr); cudaFree(t->d_ul);
+    cudaFree(t->d_pscr); cudaFree(t->d_pnext); cudaFree(t->d_pctr);
     if (t->h_covf) cudaFreeHost(t->h_covf);
     delete t;
 }
@@ -497,29 +509,40 @@ static void ensure_cold_pool(const scl_traces* tr) {
         if (cudaHostAlloc(&tr->h_covf, 8, cudaHostAllocMapped) != cudaSuccess) { cudaGetLastError(); tr->h_covf = nullptr; }
         else *tr->h_covf = 0;
     }
+    const size_t rs = 8;
     unsigned long long want = tr->n_events / 16 * 5 + 4096ull * kRecChunk;
     if (tr->h_covf && *tr->h_covf) { want = std::max(want, 2 * tr->crec_cap); *tr->h_covf = 0; }
     want = std::min<unsigned long long>(want, tr->n_events + 4096ull * kRecChunk);
     want = (want + kRecChunk - 1) / kRecChunk * kRecChunk;
-    if (want <= tr->crec_cap) return;
-    cudaFree(tr->d_crec); cudaFree(tr->d_crec_fill); tr->d_crec = nullptr; tr->d_crec_fill = nullptr; tr->crec_cap = 0;
-    if (cudaMalloc(&tr->d_crec, want * 8) != cudaSuccess ||
+    if (want * rs <= tr->crec_bytes && want / kRecChunk <= tr->crec_fills) {   // (a reload may change the record size)
+        tr->crec_cap = std::min<unsigned long long>(tr->crec_bytes / rs / kRecChunk, tr->crec_fills) * kRecChunk;
+        return;
+    }
+    cudaFree(tr->d_crec); cudaFree(tr->d_crec_fill); tr->d_crec = nullptr; tr->d_crec_fill = nullptr;
+    tr->crec_cap = 0; tr->crec_bytes = 0; tr->crec_fills = 0;
+    if (cudaMalloc(&tr->d_crec, want * rs) != cudaSuccess ||
         cudaMalloc(&tr->d_crec_fill, want / kRecChunk * 4) != cudaSuccess) {
         cudaGetLastError(); cudaFree(tr->d_crec); tr->d_crec = nullptr; tr->d_crec_fill = nullptr; return;
     }
-    tr->crec_cap = want;
+    tr->crec_cap = want; tr->crec_bytes = want * rs; tr->crec_fills = want / kRecChunk;
 }
 
 // SCL_CHAIN_AUTO: split the chains at sync events when the runners' sequential chains would outlast
-// the stream pass they overlap: estimated samples of the longest trace (sum|d| / T, of which about
-// one in 16 survives the cancellation of allocs and frees in our workloads) at ~3 us per resolve,
-// against ~3.2 ns of stream per event per SM... (measured in profiles/r02_chain_split.txt).
+// the stream pass they overlap AND the traces have enough sync events to cut them into many pieces.
+// Chain estimate: the longest trace's sum|d| / T samples, about one in 16 of which survives the
+// cancellation of allocs and frees in our workloads, at ~3 us per resolve; stream: ~5 TB/s of 16-B
+// events; sync events per trace from the load-time log2-size histogram.  (Fitted on config 2 at
+// T = 2^20 .. 10 MiB, 8 and 64 traces, config 3, config 5: profiles/r02_chain_split.txt.)
 static bool split_pays(const scl_traces* tr, uint64_t T) {
+    if (tr->n_traces == 0) return false;
     uint64_t smax = 0;
     for (uint32_t t = 0; t < tr->n_traces; ++t) smax = std::max<uint64_t>(smax, tr->h_sabs[t] / T);
     const double chain_us = (double)smax / 16.0 * 3.0;
     const double stream_us = (double)tr->n_events * 16.0 / 5.0e6;
-    return chain_us > stream_us;
+    uint64_t sync = 0;                                 // events with size >= 2T - 1, about (whole log2 bins
+    for (int k = 0; k < 64 && k < (int)tr->h_shist.size(); ++k)   //  from the one holding 2T - 1)
+        if (k >= 62 || (2ull << k) > 2 * T - 1) sync += tr->h_shist[k];
+    return chain_us > 2.0 * stream_us && (double)sync / tr->n_traces >= 32.0;
 }
 
 static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const scl_run_opts* opts, scl_result** out,
@@ -592,6 +615,7 @@ static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const sc
     p.n_runners = (unsigned)r->grid * kEmbeddedRunners;    // 2 runner warps in every CTA
     p.n_sites = tr->n_sites; p.n_traces = NT; p.T = (long long)threshold; p.hwm_sample = o.hwm_mode == SCL_HWM_SAMPLE;
     p.table = r->d_table; p.samples = r->d_samples; p.ep_flag = r->d_epflag; p.sbase = r->d_sbase;
+    p.sample_cap = r->cap;
     p.summ = r->d_summ; p.uent = tr->d_uent;
     if (!base) ensure_cold_pool(tr);
     p.crec = tr->d_crec; p.crec_cap = tr->crec_cap; p.cctr = tr->d_cctr; p.crec_fill = tr->d_crec_fill;
@@ -609,14 +633,28 @@ static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const sc
     if (split) {
         const size_t np = (size_t)tr->n_segs + tr->n_traces;
         if (np > tr->cap_pieces) {
-            cudaFree(tr->d_ust); cudaFree(tr->d_sync); cudaFree(tr->d_pc); cudaFree(tr->d_pr);
-            tr->d_ust = nullptr; tr->d_sync = nullptr; tr->d_pc = nullptr; tr->d_pr = nullptr; tr->cap_pieces = 0;
+            cudaFree(tr->d_ust); cudaFree(tr->d_sync); cudaFree(tr->d_pc); cudaFree(tr->d_pr); cudaFree(tr->d_ul);
+            tr->d_ust = nullptr; tr->d_sync = nullptr; tr->d_pc = nullptr; tr->d_pr = nullptr; tr->d_ul = nullptr;
+            tr->cap_pieces = 0;
             if (cudaMalloc(&tr->d_ust, np * sizeof(UnitStart)) != cudaSuccess || cudaMalloc(&tr->d_sync, np * sizeof(SyncInfo)) != cudaSuccess ||
-                cudaMalloc(&tr->d_pc, np * sizeof(PieceCount)) != cudaSuccess || cudaMalloc(&tr->d_pr, np * sizeof(PieceRun)) != cudaSuccess)
+                cudaMalloc(&tr->d_pc, np * sizeof(PieceCount)) != cudaSuccess || cudaMalloc(&tr->d_pr, np * sizeof(PieceRun)) != cudaSuccess ||
+                cudaMalloc(&tr->d_ul, np * sizeof(UnitLocal)) != cudaSuccess)
                 { cudaGetLastError(); if (fresh) scl_result_free(r); return fail(SCL_ENOMEM, "chain pieces"); }
             tr->cap_pieces = np;
         }
-        p.no_chain = 1; p.ust = tr->d_ust; p.sync = tr->d_sync; p.pc = tr->d_pc; p.pr = tr->d_pr;
+        // scratch: every piece's samples in blocks of kPBlock (at most the run's sample capacity
+        // plus one partly filled block per piece)
+        const size_t nb = (size_t)(tot + kPBlock - 1) / kPBlock + np + 1;
+        if (nb > tr->cap_pblocks) {
+            cudaFree(tr->d_pscr); cudaFree(tr->d_pnext); tr->d_pscr = nullptr; tr->d_pnext = nullptr; tr->cap_pblocks = 0;
+            if (!tr->d_pctr && cudaMalloc(&tr->d_pctr, 4) != cudaSuccess) { cudaGetLastError(); tr->d_pctr = nullptr; }
+            if (!tr->d_pctr || cudaMalloc(&tr->d_pscr, nb * kPBlock * sizeof(scl_sample)) != cudaSuccess ||
+                cudaMalloc(&tr->d_pnext, nb * 4) != cudaSuccess)
+                { cudaGetLastError(); if (fresh) scl_result_free(r); return fail(SCL_ENOMEM, "chain piece samples"); }
+            tr->cap_pblocks = nb;
+        }
+        p.no_chain = 1; p.ust = tr->d_ust; p.sync = tr->d_sync; p.pc = tr->d_pc; p.pr = tr->d_pr; p.ul = tr->d_ul;
+        p.pscr = tr->d_pscr; p.pnext = tr->d_pnext; p.pctr = tr->d_pctr; p.pblocks = (unsigned)std::min<size_t>(tr->cap_pblocks, 0xffffffffu);
     }
     PrepParams& pp = p.prep;                   // done by CTA 0 of the replay kernel
     pp.table = r->d_table; pp.table_words = (size_t)tr->n_sites * SCL_NCOL + 3;

@@ -20,8 +20,14 @@ namespace scl {
 __global__ void __launch_bounds__(256) load_stats_kernel(const scl_event* ev, const unsigned long long* off,
                                                          unsigned n_traces, unsigned long long n_events,
                                                          unsigned n_sites, unsigned long long* sabs,
-                                                         unsigned long long* err, scl_event* dst)
+                                                         unsigned long long* err, scl_event* dst,
+                                                         unsigned long long* shist)
 {
+    // histogram of floor(log2(size)) over the alloc / free events (how many sync events |d| >= 2T - 1
+    // a threshold T has: the chain-split heuristic of scl_replay_run), per block in shared memory
+    __shared__ unsigned hist[64];
+    if (threadIdx.x < 64) hist[threadIdx.x] = 0;
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     const unsigned long long wid = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned long long nw = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
@@ -55,7 +61,7 @@ __global__ void __launch_bounds__(256) load_stats_kernel(const scl_event* ev, co
             const unsigned kind = ev_kind(m);
             const unsigned long long sz = ev_size(m);
             if (kind == 3 || ev_site(m) >= n_sites || (kind < 2 && sz == 0)) atomicMin(err, i);
-            if (kind < 2) acc += sz;
+            if (kind < 2) { acc += sz; if (sz) atomicAdd(&hist[63 - __clzll(sz)], 1u); }
         }
         const unsigned t_lane0 = __shfl_sync(kFull, t, 0);  // every lane shuffles (never inside a short circuit)
         const bool uni = __all_sync(kFull, !split && t == t_lane0);
@@ -67,6 +73,8 @@ __global__ void __launch_bounds__(256) load_stats_kernel(const scl_event* ev, co
             atomicAdd(&sabs[t], acc);
         }
     }
+    __syncthreads();
+    if (threadIdx.x < 64 && hist[threadIdx.x]) atomicAdd(&shist[threadIdx.x], (unsigned long long)hist[threadIdx.x]);
 }
 
 // ============================================================================ a6 (report.cuh)
@@ -96,12 +104,12 @@ __global__ void __launch_bounds__(512) report_kernel(const __grid_constant__ Fin
 // ============================================================================ launch wrappers
 cudaError_t launch_load_stats(const scl_event* ev, const unsigned long long* off, unsigned n_traces,
                               unsigned long long n_events, unsigned n_sites, unsigned long long* sabs,
-                              unsigned long long* err, scl_event* dst, cudaStream_t st)
+                              unsigned long long* err, scl_event* dst, unsigned long long* shist, cudaStream_t st)
 {
     if (n_traces == 0 || n_events == 0) return cudaSuccess;
     const unsigned long long warps = (n_events + 255) / 256;
     const unsigned blocks = (unsigned)std::min<unsigned long long>((warps + 7) / 8, 148ull * 8);
-    load_stats_kernel<<<blocks, 256, 0, st>>>(ev, off, n_traces, n_events, n_sites, sabs, err, dst);
+    load_stats_kernel<<<blocks, 256, 0, st>>>(ev, off, n_traces, n_events, n_sites, sabs, err, dst, shist);
     return cudaGetLastError();
 }
 

@@ -8,6 +8,7 @@
 // takes range b % R of the chunks of group b / R, so the R CTAs that read the same chunks are
 // adjacent and run together (the second read of a chunk hits L2).  Carries out of a packed field
 // are corrected exactly in the L2 table (as in replay_kernel); a size >= 2^24 goes to L2 directly.
+// Each pass issues the next pass's loads before reducing its own records.
 #include "scl_internal.cuh"
 #include "ptx.cuh"
 #include <algorithm>
@@ -28,10 +29,6 @@ __global__ void __launch_bounds__(1024, 1) cold_hist_kernel(const __grid_constan
     auto one = [&](unsigned long long m) {
         const unsigned site = ev_site(m) - lo, kind = ev_kind(m);
         if (site >= ns || kind > 1) return;                       // another range, an invalid id, a pad record
-#ifdef SCL_DIAG_NOATOM
-        if (site == 12345678u) ctab[0] = 1;
-        return;
-#endif
         const unsigned long long size = ev_size(m);
         unsigned long long* row = p.table + (size_t)(site + lo) * SCL_NCOL;
         if (size < (1ull << 24)) {

@@ -13,11 +13,13 @@
 //   pc_prefix   warp per trace: F at every unit start and the max F before it (unit aggregates);
 //   pc_sync     warp per unit: its first sync event (chunks whose F range spans >= 2T - 1 are read),
 //               F and max F through it;
-//   pc_run<0>   warp per piece: the exact chain over the piece, counting samples / episode starts;
+//   pc_run      warp per piece: the exact chain over the piece; its samples go to scratch blocks in
+//               the order found (their slots are not known yet), Tier S (a5) to the site table, and
+//               the piece-local sample count and last episode start at each unit's ends;
 //   pc_combine  warp per trace: scan of the pieces' counts -> each piece's first sample slot and the
 //               episode entering it; the trace summary, trend end points and gate sums (Q10);
-//   pc_run<1>   warp per piece: the same chain again, writing samples, Tier S (a5), episode flags and
-//               the unit entries the reclaim pass reads (a4).
+//   pc_place    warp per piece: the samples copied to their slots, episode flags, and the unit entries
+//               the reclaim pass reads (a4).
 // The walk inside a unit is replay_kernel.cu's resolve_unit with an event window (the piece's part of
 // the unit); its results are identical to the sequential runners' (checked against the oracle).
 #include <algorithm>
@@ -32,6 +34,7 @@ __global__ void __launch_bounds__(128) pc_prefix_kernel(const __grid_constant__ 
     const int lane = threadIdx.x & 31;
     const unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
     const Slot* rec = reinterpret_cast<const Slot*>(p.urec);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *p.pctr = 0;    // scratch blocks of this run's pieces (pc_run)
     for (unsigned t = w; t < p.n_traces; t += nw) {
         const unsigned base = __ldg(p.tr_base + t), nseg = __ldg(p.tr_nseg + t);
         long long F = 0, M = 0;                              // F before the next unit; max F so far (M_-1 = 0)
@@ -136,7 +139,7 @@ struct PState {
     long long B;                                  // footprint at the last sample (the counter's origin)
     unsigned long long n, nep, lep, lep_ptr;      // samples, episode starts, last start (local index + 1), its ptr
     long long ffirst;                             // footprint at the first sample
-    unsigned long long base, ep1, eptr;           // pass 2: first slot; the episode in progress (slot + 1) and ptr
+    unsigned blk, first_blk;                      // the scratch block being filled, the piece's first
 };
 
 // The samples of one unit inside a piece's window [wlo, whi) (unit positions).  Fu: F before the
@@ -144,7 +147,6 @@ struct PState {
 // chunks whose F range leaves (B - T, B + T) and meet the window are read (lane <-> row), one
 // combined scan gives every lane F and the running maximum before its row, and the lane holding the
 // first exit walks its events; events outside the window move F and M but take no sample.
-template <bool kWrite>
 __device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, long long Mu, unsigned wlo, unsigned whi,
                            PState& x, int lane)
 {
@@ -217,15 +219,16 @@ __device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, l
                     const long long net = F - x.B;                                    // the |A - F| counter
                     const bool growth = net > 0;
                     const bool nm = growth && F > Mp;                                  // new high-water mark (Q3)
-                    if (kWrite) {
-                        const unsigned long long slot = x.base + x.n;
-                        scl_sample smp;
-                        smp.idx = (unsigned long long)(e0 + js); smp.net = net; smp.footprint = F;
-                        smp.site = ev_site(ms); smp.kind = growth ? 0 : 1; smp.new_max = nm ? 1 : 0; smp.pad = 0;
-                        p.samples[slot] = smp;
-                        sample_counters(p, smp.site, growth, net, nm);
-                        if (nm) { p.ep_flag[slot] = 0u; x.ep1 = slot + 1; x.eptr = ps; }
+                    scl_sample smp;
+                    smp.idx = (unsigned long long)(e0 + js); smp.net = net; smp.footprint = F;
+                    smp.site = ev_site(ms); smp.kind = growth ? 0 : 1; smp.new_max = nm ? 1 : 0; smp.pad = 0;
+                    if (x.n % kPBlock == 0) {                                          // a new scratch block
+                        const unsigned nb = atomicAdd(p.pctr, 1u);
+                        if (x.n == 0) x.first_blk = nb; else if (x.blk < p.pblocks) p.pnext[x.blk] = nb;
+                        x.blk = nb;
                     }
+                    if (x.blk < p.pblocks) p.pscr[(size_t)x.blk * kPBlock + x.n % kPBlock] = smp;
+                    sample_counters(p, smp.site, growth, net, nm);
                     if (nm) { ++x.nep; x.lep = x.n + 1; x.lep_ptr = ps; }
                     if (x.n == 0) x.ffirst = F;
                     ++x.n; x.B = F;                                                    // "resets the counters"
@@ -235,7 +238,7 @@ __device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, l
             x.B = shfl_ll(x.B, l0); x.n = __shfl_sync(kFull, x.n, l0); x.nep = __shfl_sync(kFull, x.nep, l0);
             x.lep = __shfl_sync(kFull, x.lep, l0); x.lep_ptr = __shfl_sync(kFull, x.lep_ptr, l0);
             x.ffirst = shfl_ll(x.ffirst, l0);
-            if (kWrite) { x.ep1 = __shfl_sync(kFull, x.ep1, l0); x.eptr = __shfl_sync(kFull, x.eptr, l0); }
+            x.blk = __shfl_sync(kFull, x.blk, l0); x.first_blk = __shfl_sync(kFull, x.first_blk, l0);
             cur = l0 + 1;
         }
         cnext = c + 1;
@@ -243,7 +246,6 @@ __device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, l
     __syncwarp();
 }
 
-template <bool kWrite>
 __global__ void __launch_bounds__(128) pc_run_kernel(const __grid_constant__ ReplayParams p)
 {
     const int lane = threadIdx.x & 31;
@@ -256,43 +258,84 @@ __global__ void __launch_bounds__(128) pc_run_kernel(const __grid_constant__ Rep
         long long B0;
         if (tfirst) {
             t = id;
-            if (__ldg(p.tr_nseg + t) == 0) { if (!kWrite && lane == 0) p.pc[id].active = 0; continue; }
+            if (__ldg(p.tr_nseg + t) == 0) { if (lane == 0) p.pc[id].active = 0; continue; }
             u0 = __ldg(p.tr_base + t); wlo0 = 0; B0 = 0;
         } else {
             u0 = id - p.n_traces;
             const SyncInfo sy = p.sync[u0];
-            if (sy.pos < 0) { if (!kWrite && lane == 0) p.pc[id].active = 0; continue; }
+            if (sy.pos < 0) { if (lane == 0) p.pc[id].active = 0; continue; }
             t = __ldcg(&rec[u0].info.t); wlo0 = (unsigned)sy.pos + 1; B0 = sy.Fs;
         }
         const unsigned uend = __ldg(p.tr_base + t) + __ldg(p.tr_nseg + t);
-        PState x{B0, 0, 0, 0, 0, 0, 0, 0, 0};
-        if (kWrite) { const PieceRun r = p.pr[id]; x.base = r.base; x.ep1 = r.ep1; x.eptr = r.eptr; }
-        for (unsigned u = u0; u < uend; ++u) {
+        PState x{B0, 0, 0, 0, 0, 0, ~0u, ~0u};
+        unsigned u = u0, end_sync = 0;
+        for (;; ++u) {
             const bool first = u == u0;
             const unsigned wlo = first ? wlo0 : 0u;
             unsigned whi = (unsigned)kUnit;
-            bool last = false;
             if (!first || tfirst) {                          // the piece ends at this unit's first sync event
                 const int sp = p.sync[u].pos;
-                if (sp >= 0) { whi = (unsigned)sp + 1; last = true; }
+                if (sp >= 0) { whi = (unsigned)sp + 1; end_sync = 1; }
             }
             const UnitStart us = p.ust[u];
             const Slot& S = rec[u];
-            if (kWrite && wlo == 0 && lane == 0) {            // the state entering the unit (reclaim pass, a4)
-                UnitEntry* e = p.uent + u;
-                e->ep1 = x.ep1; e->eptr = x.eptr; e->s_in = x.base + x.n;
+            if (wlo == 0 && lane == 0) {                     // the state entering the unit
+                UnitLocal* l = p.ul + u;
+                l->n_start = x.n; l->lep_start = x.lep; l->lep_ptr_start = x.lep_ptr;
             }
             const long long umx = __ldcg(&S.umx), umn = __ldcg(&S.umn);
             if (us.F0 + umx >= x.B + p.T || us.F0 + umn <= x.B - p.T)    // the F range can leave the band
-                piece_unit<kWrite>(p, S, us.F0, us.M0, wlo, whi, x, lane);
-            if (kWrite && whi == (unsigned)kUnit && lane == 0) p.uent[u].s_out = x.base + x.n;
-            if (last) break;
+                piece_unit(p, S, us.F0, us.M0, wlo, whi, x, lane);
+            if (whi == (unsigned)kUnit && lane == 0) p.ul[u].n_end = x.n;
+            if (end_sync || u + 1 == uend) break;
         }
-        if (!kWrite && lane == 0) {
+        if (lane == 0) {
             PieceCount c;
             c.n = x.n; c.nep = x.nep; c.lep = x.lep; c.lep_ptr = x.lep_ptr; c.ffirst = x.ffirst; c.flast = x.B;
-            c.active = 1; c.pad = 0;
+            c.active = 1; c.first_blk = x.first_blk; c.u_first = u0; c.u_last = u; c.end_sync = end_sync; c.pad = 0;
             p.pc[id] = c;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------- pc_place
+// Each piece's samples from its scratch blocks to their slots (and the episode flags the reclaim
+// pass sets), and the unit entries of its units: the episode entering the unit (the piece's last
+// start before it, else the one entering the piece), the slots of the unit's samples.
+__global__ void __launch_bounds__(128) pc_place_kernel(const __grid_constant__ ReplayParams p)
+{
+    const int lane = threadIdx.x & 31;
+    const unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const unsigned npieces = p.n_traces + p.n_segs;
+    for (unsigned id = w; id < npieces; id += nw) {
+        const PieceCount c = p.pc[id];
+        if (!c.active) continue;
+        const PieceRun r = p.pr[id];
+        unsigned b = c.first_blk;
+        for (unsigned long long k0 = 0; k0 < c.n; k0 += kPBlock) {
+            #pragma unroll
+            for (int h = 0; h < kPBlock / 32; ++h) {
+                const unsigned long long k = k0 + (unsigned long long)(h * 32 + lane);
+                if (k < c.n && b < p.pblocks) {
+                    const scl_sample smp = p.pscr[(size_t)b * kPBlock + h * 32 + lane];
+                    SCL_CHECK(r.base + k < p.sample_cap);
+                    p.samples[r.base + k] = smp;
+                    if (smp.new_max) p.ep_flag[r.base + k] = 0u;
+                }
+            }
+            if (k0 + kPBlock < c.n) b = b < p.pblocks ? __ldcg(p.pnext + b) : ~0u;
+        }
+        const bool tfirst = id < p.n_traces;
+        for (unsigned u = c.u_first + (unsigned)lane; u <= c.u_last; u += 32) {
+            const UnitLocal l = p.ul[u];
+            SCL_CHECK(u < p.n_segs);
+            UnitEntry* e = p.uent + u;
+            if (u != c.u_first || tfirst) {                  // the piece holds the unit's start
+                e->ep1 = l.lep_start ? r.base + l.lep_start : r.ep1;
+                e->eptr = l.lep_start ? l.lep_ptr_start : r.eptr;
+                e->s_in = r.base + l.n_start;
+            }
+            if (u != c.u_last || !c.end_sync) e->s_out = r.base + l.n_end;   // ... and its end
         }
     }
 }
@@ -380,9 +423,9 @@ cudaError_t launch_pchain(const ReplayParams& p, cudaStream_t st)
     auto grid = [](unsigned warps) { return std::max(1u, std::min((warps + 3) / 4, 148u * 16)); };
     pc_prefix_kernel<<<grid(p.n_traces), 128, 0, st>>>(p);
     pc_sync_kernel<<<grid(p.n_segs), 128, 0, st>>>(p);
-    pc_run_kernel<false><<<grid(p.n_traces + p.n_segs), 128, 0, st>>>(p);
+    pc_run_kernel<<<grid(p.n_traces + p.n_segs), 128, 0, st>>>(p);
     pc_combine_kernel<<<grid(p.n_traces), 128, 0, st>>>(p);
-    pc_run_kernel<true><<<grid(p.n_traces + p.n_segs), 128, 0, st>>>(p);
+    pc_place_kernel<<<grid(p.n_traces + p.n_segs), 128, 0, st>>>(p);
     return cudaGetLastError();
 }
 

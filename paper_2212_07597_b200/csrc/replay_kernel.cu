@@ -64,8 +64,9 @@ __device__ __forceinline__ unsigned bloom_hash(unsigned long long ptr) {
 __device__ __forceinline__ unsigned bloom_word(unsigned long long ptr) { return bloom_hash(ptr) >> 26; }
 __device__ __forceinline__ unsigned bloom_mask(unsigned long long ptr) {
     const unsigned h = bloom_hash(ptr);
-#ifdef SCL_BLOOM1
-    return 1u << ((h >> 21) & 31u);
+#ifdef SCL_BLOOM_FUNNEL
+    // bits (h >> 21) & 31 and (h >> 16) & 31: a wrapping funnel shift of 1 takes its count mod 32
+    return __funnelshift_l(0u, 1u, h >> 21) | __funnelshift_l(0u, 1u, h >> 16);
 #else
     return (1u << ((h >> 21) & 31u)) | (1u << ((h >> 16) & 31u));
 #endif
@@ -182,13 +183,17 @@ __device__ __forceinline__ void fast_row(const unsigned long long* ptr, const un
 }
 
 // Cold events of the row (bit j of rec: event j) -> the warp's chunk of the cold-record stream:
-// one warp scan of the per-lane counts gives each lane its run of slots, the records are staged in
-// the warp's own 4-KiB slice of the TMA box it just read (its rows are in registers now; at most 256
-// records) and copied out with lane-contiguous stores (whole sectors).  A new chunk is taken from the
-// pool when the current one cannot hold the row's records (the rest of it is left unused; its fill
-// is written when the warp leaves it).  When the pool is exhausted the records are returned for the
-// direct L2 path.  Returns whether the slice was written (the async proxy's next TMA write must be
-// ordered after it: fence.proxy.async before the box is released).
+// one warp scan of the per-lane counts gives each lane its run of slots, the records (the events'
+// meta words) are staged in the warp's own 4-KiB slice of the TMA box it just read (its rows are in
+// registers now; at most 256 records) and copied out with lane-contiguous stores (whole sectors).
+// A new chunk is taken from the pool when the current one cannot hold the row's records (the rest
+// of it is left unused; its fill is written when the warp leaves it).  When the pool is exhausted
+// the records are returned for the direct L2 path.  Sets `staged` when the slice was written (the
+// async proxy's next TMA write must be ordered after it: fence.proxy.async before the box is
+// released).  (Measured alternatives on config 3: lane-scattered stores from registers and a bulk
+// copy of the slice, within 2 %; 4-B records (site - kWarm : 16 | kind : 1 | size : 15) halve the
+// record traffic but their encoding and the L2 path of the larger sizes cost the issue-bound compute
+// warps more: +6 % on the stream pass.)
 struct ColdCursor { unsigned long long base; unsigned fill; };   // base ~0: no chunk (pool exhausted)
 
 __device__ __forceinline__ unsigned cold_records(const ReplayParams& p, ColdCursor& cc, const unsigned long long* meta,
@@ -210,52 +215,20 @@ __device__ __forceinline__ unsigned cold_records(const ReplayParams& p, ColdCurs
         cc.base = __shfl_sync(kFull, nb, 0); cc.fill = 0;
     }
     if (cc.base == ~0ull) return rec;                 // -> direct L2 reductions
-#ifdef SCL_DIAG_NOSTAGE
-    cc.fill += tot; return 0u;
-#endif
-#ifdef SCL_DIRECTREC
-    {   // lane-scattered stores of the records straight from registers (no staging)
-        unsigned long long* d = p.crec + cc.base + cc.fill + (incl - nc);
-        #pragma unroll
-        for (int j = 0; j < kEpt; ++j)
-            if ((rec >> j) & 1u) *d++ = meta[j];
-        cc.fill += tot;
-        return 0u;
-    }
-#endif
     __syncwarp();                                     // every lane's row is in registers
     uint32_t a = slice_s + 8u * (incl - nc);
     #pragma unroll
     for (int j = 0; j < kEpt; ++j)
         if ((rec >> j) & 1u) { asm volatile("st.shared.u64 [%0], %1;" :: "r"(a), "l"(meta[j]) : "memory"); a += 8u; }
-#ifdef SCL_BULKREC
-    // an odd count is padded with a kind-3 record (cold_hist skips it): the bulk copy moves whole
-    // 16-B units to a 16-B aligned position
-    const unsigned totp = (tot + 1u) & ~1u;
-    if (lane == 0 && totp != tot) asm volatile("st.shared.u64 [%0], %1;" :: "r"(slice_s + 8u * tot), "l"(3ull << 40) : "memory");
-    fence_proxy_async_shared();                       // the staged records before the async-proxy read
     __syncwarp();
-    if (lane == 0) {
-        bulk_s2g(p.crec + cc.base + cc.fill, reinterpret_cast<const void*>(__cvta_shared_to_generic(slice_s)), totp * 8u);
-        bulk_commit();
-        bulk_wait_read();                             // the slice is read: the box may be released
-    }
-    __syncwarp();
-    cc.fill += totp;
-#else
-    __syncwarp();
+    SCL_CHECK(cc.base + cc.fill + tot <= p.crec_cap);
     unsigned long long* dst = p.crec + cc.base + cc.fill;
     for (unsigned k = (unsigned)lane; k < tot; k += 32) {
         unsigned long long v;
         asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(slice_s + 8u * k) : "memory");
-#ifndef SCL_DIAG_NOSTORE
         dst[k] = v;
-#else
-        if (v == 0x1234567ull) dst[k] = v;
-#endif
     }
     cc.fill += tot;
-#endif
     staged = true;
     return 0u;
 }
@@ -354,21 +327,19 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
                     }
                 }
             }
-#ifdef SCL_DIAG_NOREC
-            rec = 0;
-#endif
             if (!all_hot)                                     // (warp-collective; fallback -> L2)
                 cold |= cold_records(p, cc, meta, rec, smem_u32(boxp) + (uint32_t)w8 * 32u * 128u, lane, staged);
-            while (cold) {                                    // cold site / huge size: L2 reductions
-                const int j = __ffs(cold) - 1;
-                cold &= cold - 1;
-                unsigned long long mj = 0;
+            if (__any_sync(kFull, cold != 0u)) {              // cold site / huge size: L2 reductions (rare)
                 #pragma unroll
-                for (int q = 0; q < kEpt; ++q) if (q == j) mj = meta[q];
-                const unsigned kind = ev_kind(mj);
-                unsigned long long* row = p.table + (size_t)ev_site(mj) * SCL_NCOL;
-                atomicAdd(&row[SCL_COL_N_MALLOC + kind], 1ull);
-                atomicAdd(&row[SCL_COL_MALLOC_BYTES + kind], ev_size(mj));
+                for (int j = 0; j < kEpt; ++j) {
+                    if ((cold >> j) & 1u) {
+                        const unsigned kind = ev_kind(meta[j]);
+                        SCL_CHECK(ev_site(meta[j]) < p.n_sites);
+                        unsigned long long* row = p.table + (size_t)ev_site(meta[j]) * SCL_NCOL;
+                        atomicAdd(&row[SCL_COL_N_MALLOC + kind], 1ull);
+                        atomicAdd(&row[SCL_COL_MALLOC_BYTES + kind], ev_size(meta[j]));
+                    }
+                }
             }
         }
         PROF_MARK(4)
@@ -390,9 +361,7 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
             csum = shfl_ll(incl, 31);
         }
         if (lane == 0) { S.Pc[c] = csum; S.ax[c] = cmx; S.an[c] = cmn; }   // composed in place below
-#ifndef SCL_DIAG_NOFENCE
         if (staged) fence_proxy_async_shared();            // generic writes before the next TMA write of the box
-#endif
         __syncwarp();
         mbar_arrive(&s.empty[st]);                        // box consumed
         PROF_MARK(2)
@@ -557,6 +526,7 @@ __device__ __forceinline__ void resolve_chunk32(const ReplayParams& p, const uns
                 scl_sample smp;
                 smp.idx = (unsigned long long)(e0 + js); smp.net = net; smp.footprint = F;
                 smp.site = ev_site(ms); smp.kind = growth ? 0 : 1; smp.new_max = nm ? 1 : 0; smp.pad = 0;
+                SCL_CHECK(slot_s < p.sample_cap);
                 p.samples[slot_s] = smp;
                 sample_counters(p, smp.site, growth, net, nm);
                 if (nm) { p.ep_flag[slot_s] = 0u; ep1 = slot_s + 1; eptr = ps; ++nep; }   // settled by the reclaim pass
@@ -680,7 +650,8 @@ __device__ void resolve_unit(const ReplayParams& p, const Slot& S, RState& x, un
                     scl_sample smp;
                     smp.idx = (unsigned long long)(e0 + js); smp.net = net; smp.footprint = F;
                     smp.site = ev_site(ms); smp.kind = growth ? 0 : 1; smp.new_max = nm ? 1 : 0; smp.pad = 0;
-                    p.samples[slot_s] = smp;
+                    SCL_CHECK(slot_s < p.sample_cap);
+                p.samples[slot_s] = smp;
                     sample_counters(p, smp.site, growth, net, nm);
                     if (nm) { p.ep_flag[slot_s] = 0u; ep1 = slot_s + 1; eptr = ps; ++nep; }   // settled by the reclaim pass
                     ++n; B = F; Ms = llmax(Ms, F);            // "resets the counters"
@@ -738,6 +709,7 @@ __device__ void run_trace(const ReplayParams& p, RState& x, unsigned t, unsigned
         long long t_res = 0;
 #endif
         const Slot* R = rec + base + x.next;
+        SCL_CHECK(base + x.next + (unsigned)m <= p.n_segs);
         UnitEntry* ue = p.uent + base + x.next;
         if (lane >= m) { us = 0; ux = kNeg; un = kPos; }
         if (__any_sync(kFull, lane < m && us == kAggBig)) {   // a value beyond 48 bits: from the records
@@ -955,6 +927,7 @@ __device__ __forceinline__ bool chunk_has_free(const ReplayParams& p, long long 
 
 // The episode whose tracked object is freed: once, ep_flag 0 -> 1 and one free for its site.
 __device__ __forceinline__ void reclaimed(const ReplayParams& p, unsigned long long ep1, unsigned site) {
+    SCL_CHECK(ep1 >= 1 && ep1 <= p.sample_cap && site < p.n_sites);
     if (atomicExch(&p.ep_flag[ep1 - 1], 1u) == 0u)
         atomicAdd(&p.table[(size_t)site * SCL_NCOL + SCL_COL_LEAK_FREES], 1ull);
 }
@@ -999,6 +972,7 @@ __device__ void reclaim_unit(const ReplayParams& p, unsigned u, const UnitCtx& x
     for (unsigned long long s0 = x.s_in; s0 < x.s_out; s0 += 32) {         // samples taken in this unit
         const unsigned long long si = s0 + (unsigned long long)lane;
         bool nm = false; long long idx = 0; unsigned st = 0;
+        SCL_CHECK(x.s_out <= p.sample_cap);
         if (si < x.s_out) { const scl_sample smp = p.samples[si]; nm = smp.new_max != 0; idx = (long long)smp.idx; st = smp.site; }
         unsigned em = __ballot_sync(kFull, nm);
         while (em) {

@@ -6,6 +6,16 @@
 #include <cuda_runtime.h>
 #include "../../include/scl.h"
 
+// SCL_CHECKED builds (libscl_checked.so, tools/checked.sh): every computed index of a global write is
+// bounds-checked on the device and a violation traps with its source line -- the stand-in for
+// compute-sanitizer memcheck, which this GPU pool does not allow.
+#ifdef SCL_CHECKED
+#include <cstdio>
+#define SCL_CHECK(c) do { if (!(c)) { printf("SCL_CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c); __trap(); } } while (0)
+#else
+#define SCL_CHECK(c) do { } while (0)
+#endif
+
 namespace scl {
 
 // ---- geometry and CTA roles -----------------------------------
@@ -160,6 +170,7 @@ struct ReplayParams {
     long long T;
     unsigned long long* table;        // [n_sites*SCL_NCOL + 3]
     scl_sample* samples;              // [capacity]
+    unsigned long long sample_cap;    // slots of samples / ep_flag (SCL_CHECKED bounds)
     unsigned int* ep_flag;            // [capacity]  reclaimed flag per episode-start sample
     const unsigned long long* sbase;  // trace -> first sample slot
     scl_trace_summary* summ;          // [n_traces]
@@ -167,7 +178,7 @@ struct ReplayParams {
     // cold-record stream (n_sites > kWarm): the meta word of every fast-path alloc / free of a site
     // >= kWarm, in chunks of kRecChunk records taken by one compute warp at a time (cold_hist_kernel
     // reduces them per site after the stream pass)
-    unsigned long long* crec;         // [crec_cap]
+    unsigned long long* crec;         // [crec_cap] records (the events' meta words)
     unsigned long long crec_cap;      // records (a multiple of kRecChunk)
     unsigned long long* cctr;         // [2]: records allocated (chunk granules), spare (zeroed per run)
     unsigned* crec_fill;              // [crec_cap / kRecChunk] records written to each allocated chunk
@@ -177,8 +188,13 @@ struct ReplayParams {
     int no_chain;                     // 1: runner warps exit at once (the pchain kernels run the chains)
     struct UnitStart* ust;            // [n_segs] F at each unit start, max F before it
     struct SyncInfo* sync;            // [n_segs] the unit's first sync event (|d| >= 2T - 1)
-    struct PieceCount* pc;            // [n_traces + n_segs] pass-1 counts of every piece
-    struct PieceRun* pr;              // [n_traces + n_segs] pass-2 inputs (slot base, entering episode)
+    struct PieceCount* pc;            // [n_traces + n_segs] the chain's results per piece
+    struct PieceRun* pr;              // [n_traces + n_segs] placement of each piece (slot base, entering episode)
+    struct UnitLocal* ul;             // [n_segs] piece-local sample counts / episode at each unit's ends
+    scl_sample* pscr;                 // [pblocks * kPBlock] samples as the pieces found them (blocks)
+    unsigned* pnext;                  // [pblocks] next block of the same piece
+    unsigned* pctr;                   // [1] blocks taken (zeroed by pc_prefix)
+    unsigned pblocks;
 };
 
 // Chain pieces (pchain.cu).  A sync event (|d| >= 2T - 1) takes a sample from
@@ -188,11 +204,18 @@ struct ReplayParams {
 // or at the trace end.
 struct UnitStart { long long F0, M0; };                  // F before the unit's first event; max F before it (M_-1 = 0)
 struct SyncInfo { long long Fs, Ms; int pos, pad0; long long pad1; };   // pos: unit position (-1: none); F, max F through it
-struct PieceCount {                                      // pass 1 (count) of one piece
+constexpr int kPBlock = 64;                              // samples per scratch block of a piece
+struct PieceCount {                                      // one piece's chain (pc_run)
     unsigned long long n, nep;                           // samples, new-maximum samples (episode starts)
     unsigned long long lep, lep_ptr;                     // local index + 1 of the last episode start (0: none), its pointer
     long long ffirst, flast;                             // footprint at the first / last sample
-    unsigned long long active, pad;
+    unsigned active, first_blk;                          // the piece exists; its first scratch block
+    unsigned u_first, u_last;                            // its units (the first from its window start, the last
+    unsigned end_sync, pad;                              //   up to its end: a sync event of u_last, or the unit end)
+};
+struct UnitLocal {                                       // piece-local state at a unit's start / end (pc_run)
+    unsigned long long n_start, lep_start, lep_ptr_start;   // samples before; last episode start before (+1, 0 none)
+    unsigned long long n_end;                            // samples through the unit end
 };
 struct PieceRun { unsigned long long base, ep1, eptr, pad; };   // pass 2: first slot; episode entering (slot + 1, 0 none)
 cudaError_t launch_pchain(const ReplayParams& p, cudaStream_t st);
@@ -217,6 +240,7 @@ __device__ __forceinline__ void load_row_global(const scl_event* ev, long long r
 // by the runner lane that takes the sample.
 __device__ __forceinline__ void sample_counters(const ReplayParams& p, unsigned site, bool growth, long long net, bool nm)
 {
+    SCL_CHECK(site < p.n_sites);
     unsigned long long* row = p.table + (size_t)site * SCL_NCOL;
     atomicAdd(&row[growth ? SCL_COL_N_GROWTH : SCL_COL_N_DECLINE], 1ull);
     atomicAdd(&row[growth ? SCL_COL_GROWTH_BYTES : SCL_COL_DECLINE_BYTES], (unsigned long long)(growth ? net : -net));
@@ -266,7 +290,7 @@ cudaError_t launch_rate(const RateParams& p, int phase, cudaStream_t st);   // 0
 // launch wrappers (replay.cu)
 cudaError_t launch_load_stats(const scl_event* ev, const unsigned long long* off, unsigned n_traces,
                               unsigned long long n_events, unsigned n_sites, unsigned long long* sabs,
-                              unsigned long long* err, scl_event* dst, cudaStream_t st);
+                              unsigned long long* err, scl_event* dst, unsigned long long* shist, cudaStream_t st);
 cudaError_t launch_replay(const CUtensorMap* tmap, const ReplayParams& p, int grid, cudaStream_t st);
 cudaError_t launch_post(const ReplayParams& p, cudaStream_t st);
 cudaError_t launch_rechain(const ReplayParams& p, cudaStream_t st);   // runner warps alone

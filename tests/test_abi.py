@@ -45,7 +45,7 @@ def test_next_prime_host_only():
 
 def test_struct_sizes():
     assert scl.SAMPLE_DTYPE.itemsize == 32 and scl.SITE_ROW_DTYPE.itemsize == 104
-    assert scl.SUMMARY_DTYPE.itemsize == 48 and ctypes.sizeof(scl._RunOpts) == 48
+    assert scl.SUMMARY_DTYPE.itemsize == 48 and ctypes.sizeof(scl._RunOpts) == 56
     assert scl.RATE_SAMPLE_DTYPE.itemsize == 24 and oracle.RATE_SAMPLE_DTYPE.itemsize == 24
 
 
