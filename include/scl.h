@@ -230,6 +230,11 @@ scl_status scl_result_timing(const scl_result* r, float* replay_kernel_ms, float
  * without synchronising between them.  *n = number written (<= cap). */
 scl_status scl_result_kernel_times(const scl_result* r, float* ms, size_t cap, size_t* n);
 
+/* The same for the whole stream pass of each run: from the replay kernel's start to the end of the
+ * kernels that complete a1-a5 after it (the cold-site Tier-E reduce, the split chains) -- before
+ * the post pass.  Read independently of scl_result_kernel_times. */
+scl_status scl_result_pass_times(const scl_result* r, float* ms, size_t cap, size_t* n);
+
 /* Number of kernels the library launched for the result's last run and finalize (replay or
  * re-chain kernel, the cold-site Tier-E reduce when n_sites > 4096, the post pass, and the a6
  * kernels of a deferred finalize).  Host bookkeeping only: does not wait.

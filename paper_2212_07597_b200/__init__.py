@@ -19,7 +19,7 @@ from . import _build
 
 __all__ = ["SclError", "Traces", "Result", "scl_trace_load", "scl_trace_reload", "scl_replay_run", "scl_replay_rethreshold", "scl_replay_sweep", "scl_finalize",
            "scl_site_report", "scl_samples", "scl_trace_summaries", "scl_gate", "scl_result_device_table",
-           "scl_result_timing", "scl_result_kernel_times", "scl_result_launches", "scl_next_prime", "scl_traces_info", "EVENT_DTYPE", "SAMPLE_DTYPE",
+           "scl_result_timing", "scl_result_kernel_times", "scl_result_pass_times", "scl_result_launches", "scl_next_prime", "scl_traces_info", "EVENT_DTYPE", "SAMPLE_DTYPE",
            "SUMMARY_DTYPE", "SITE_ROW_DTYPE", "COLS", "device_table_tensor", "write_trace_file",
            "DOMAIN_DTYPE", "scl_sample_domains", "scl_trace_recon_error", "RATE_SAMPLE_DTYPE", "RATE_ALLOC_FREE", "RATE_COPY", "RateResult", "scl_rate_run", "scl_rate_counts",
            "scl_rate_samples", "scl_rate_site_counts", "scl_rate_timing"]
@@ -64,6 +64,7 @@ def _load():
         "scl_trace_reload": [P, P, P, U32, U32, I32, P],
         "scl_result_kernel_times": [P, P, SZ, P],
         "scl_result_launches": [P, P],
+        "scl_result_pass_times": [P, P, SZ, P],
         "scl_rate_run": [U64, U64, U32, P, P, P],
         "scl_sample_domains": [P, U32, P, SZ, P],
         "scl_trace_recon_error": [P, P, SZ, P],
@@ -351,6 +352,15 @@ def scl_result_kernel_times(r: Result) -> list:
     buf = (ctypes.c_float * 128)()
     n = ctypes.c_size_t()
     _check(lib.scl_result_kernel_times(r.handle, buf, 128, ctypes.byref(n)))
+    return [buf[i] for i in range(n.value)]
+
+
+def scl_result_pass_times(r: Result) -> list:
+    """Stream-pass durations (ms: replay kernel + the kernels completing a1-a5 after it) of the runs
+    enqueued with timing=True since the previous call (<= 128)."""
+    buf = (ctypes.c_float * 128)()
+    n = ctypes.c_size_t()
+    _check(lib.scl_result_pass_times(r.handle, buf, 128, ctypes.byref(n)))
     return [buf[i] for i in range(n.value)]
 
 

@@ -15,7 +15,7 @@ r = None
 for _ in range(3):
     r = scl.scl_replay_run(cfg.T, tr, stream=st, out=r)
 torch.cuda.synchronize()
-scl.scl_result_kernel_times(r)
+scl.scl_result_kernel_times(r); scl.scl_result_pass_times(r)
 K = 20
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 a.record(st)
@@ -24,5 +24,6 @@ for _ in range(K):
 b.record(st)
 torch.cuda.synchronize()
 ks = scl.scl_result_kernel_times(r)
+ps = scl.scl_result_pass_times(r)
 print(f"{os.environ.get('SCL_LIB','libscl.so').split('/')[-1]} cfg{os.environ.get('CFG','3')} nt={cfg.n_traces}: "
-      f"step {a.elapsed_time(b)/K*1e3:.1f} us, stream pass {sum(ks)/len(ks)*1e3:.1f} us")
+      f"step {a.elapsed_time(b)/K*1e3:.1f} us, replay kernel {sum(ks)/len(ks)*1e3:.1f} us, stream pass {sum(ps)/len(ps)*1e3:.1f} us")
