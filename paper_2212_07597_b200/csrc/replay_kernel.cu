@@ -61,7 +61,7 @@ size_t replay_smem_bytes() { return 1024 + (size_t)kStages * kSegBytes + sizeof(
 __device__ __forceinline__ unsigned bloom_hash(unsigned long long ptr) {
     return (unsigned)ptr * 0x9E3779B1u;
 }
-__device__ __forceinline__ unsigned bloom_word(unsigned long long ptr) { return bloom_hash(ptr) >> 26; }
+__device__ __forceinline__ unsigned bloom_word(unsigned long long ptr) { return bloom_hash(ptr) >> (32 - kBloomLog2); }
 __device__ __forceinline__ unsigned bloom_mask(unsigned long long ptr) {
     const unsigned h = bloom_hash(ptr);
 #ifdef SCL_BLOOM_FUNNEL
@@ -163,7 +163,7 @@ __device__ __forceinline__ void fast_row(const unsigned long long* ptr, const un
         } else {
             const bool h = af && (hi >> 11) < (unsigned)kWarm;
             cold |= (af && !h ? 1u : 0u) << j;
-            const uint32_t offw = ((hi >> 9) & (uint32_t)(4 * kWarm - 4)) | ((hi << (kWarmLog2 - 6)) & (uint32_t)(4 * kWarm));
+            const uint32_t offw = ((hi >> 9) & ~3u) + ((hi >> 8) & 1u) * (uint32_t)(4 * kWarm);   // (site < kWarm here)
             a = cnt_s + (h ? offw : dslot); add[j] = h ? lo : 0u;                // ((kind&1)*kWarm + site)*4
         }
         red_add(a, 1u);                                                       // a5 Tier E
@@ -199,6 +199,9 @@ struct ColdCursor { unsigned long long base; unsigned fill; };   // base ~0: no 
 __device__ __forceinline__ unsigned cold_records(const ReplayParams& p, ColdCursor& cc, const unsigned long long* meta,
                                                  unsigned rec, uint32_t slice_s, int lane, bool& staged)
 {
+#ifdef SCL_COLD_L2
+    return rec;                                       // (A/B: every cold event through two L2 reductions)
+#endif
     const unsigned nc = __popc(rec);
     unsigned incl = nc;
     #pragma unroll
@@ -269,7 +272,8 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
         PROF_MARK(1)
         Slot& S = s.slot[sl];
         const int c = g * 8 + w8;                         // chunk index within the unit
-        S.bloom[c][lane] = 0u; S.bloom[c][lane + 32] = 0u;
+        #pragma unroll
+        for (int q = 0; q < kBloomWords; q += 32) S.bloom[c][q + lane] = 0u;
         if (g == 0 && w8 == 0 && lane == 0) S.info = inf;
         __syncwarp();
         const uint32_t bl_s = smem_u32(&S.bloom[c][0]);
@@ -950,6 +954,17 @@ __device__ void reclaim_unit(const ReplayParams& p, unsigned u, const UnitCtx& x
         const bool pos = cb < send && cb + 32 * kEpt > sbeg && (S.bloom[lane][w] & msk) == msk;
         const unsigned cm = __ballot_sync(kFull, pos);
         if (!cm) return;
+#ifdef SCL_POST_INLINE
+        {                                                    // the exact re-checks here, in order
+            bool found = false;
+            for (unsigned c = cm; c && !found; c &= c - 1) {
+                const int ch = __ffs(c) - 1;
+                found = chunk_has_free(p, row_base + (long long)ch * 32, off_t, n_t, (unsigned)ch * 32 * kEpt, ptr, sbeg, send, lane);
+            }
+            if (found && lane == 0) reclaimed(p, ep1, site);
+            return;
+        }
+#endif
         unsigned base = 0;
         if (lane == 0) base = atomicAdd(&p.ticket[2], (unsigned)__popc(cm));
         base = __shfl_sync(kFull, base, 0);
@@ -1040,6 +1055,7 @@ __global__ void __launch_bounds__(256, 3) post_kernel(const __grid_constant__ Re
             p.tierE[i] = __ldcg(&p.table[(i >> 2) * SCL_NCOL + (i & 3)]);
     }
     POST_T(1, atomicMax)
+#ifndef SCL_POST_INLINE
     grid_barrier(&p.ticket[1]);
     POST_T(2, atomicMax)
     const unsigned ntask = min(ld_acquire(&p.ticket[2]), p.rtask_cap);
@@ -1051,6 +1067,7 @@ __global__ void __launch_bounds__(256, 3) post_kernel(const __grid_constant__ Re
         if (chunk_has_free(p, tk.row0, tk.off_t, tk.n_t, tk.pos0, tk.ptr, tk.sbeg, tk.send, lane) && lane == 0)
             reclaimed(p, tk.ep1, tk.site);
     }
+#endif
     POST_T(3, atomicMax)
     if (!p.fuse_report) return;                                                           // phase C: a6
     if (p.n_sites <= kReportSites) {                        // small table: a6 in the block that finishes last

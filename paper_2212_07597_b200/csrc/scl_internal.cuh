@@ -45,15 +45,18 @@ constexpr int kCtaThreads = (kComputeWarps + 1 + kLBWarps) * 32;
 #ifndef SCL_STAGES
 #define SCL_STAGES 4
 #endif
-#ifndef SCL_WARM_LOG2
-#define SCL_WARM_LOG2 11
+#ifndef SCL_WARM
+#define SCL_WARM 2048
+#endif
+#ifndef SCL_BLOOM_LOG2
+#define SCL_BLOOM_LOG2 6
 #endif
 constexpr int kStages = SCL_STAGES;           // TMA ring depth
 constexpr int kSlots = 6;                     // compute -> publisher unit summary ring (smem)
-constexpr int kBloomWords = 64;               // 2048-bit Bloom filter of freed pointers per chunk
+constexpr int kBloomLog2 = SCL_BLOOM_LOG2;
+constexpr int kBloomWords = 1 << kBloomLog2;  // Bloom filter of freed pointers per chunk (64 words: 2048 bits)
 constexpr int kHot = 1024;                    // sites with shared-memory Tier-E counters (all 4 kinds)
-constexpr int kWarmLog2 = SCL_WARM_LOG2;
-constexpr int kWarm = 1 << kWarmLog2;         // n_sites > kHot: the allocs and frees of the kWarm lowest site ids;
+constexpr int kWarm = SCL_WARM;               // n_sites > kHot: the allocs and frees of the kWarm lowest site ids;
                                               //   the other sites' events go to the cold-record stream
 constexpr int kRecChunk = 4096;               // cold-record stream: records per chunk (one warp's, at a time)
 constexpr int kColdSites = 28672;             // cold_hist_kernel: sites per range (2 kinds x 4 B = 224 KiB)

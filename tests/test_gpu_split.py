@@ -69,3 +69,24 @@ def test_split_sample_mode_uses_runners():
     tr = scl.scl_trace_load(ev, off, cfg.n_sites)
     r = scl.scl_replay_run(cfg.T, tr, chain_mode=SPLIT, hwm_mode=scl.HWM_SAMPLE)
     compare(ev, off, cfg.n_sites, cfg.T, r, hwm_mode=scl.HWM_SAMPLE)
+
+
+def test_launch_count_and_pass_times():
+    """scl_result_launches counts the library's kernels of the last run; the stream-pass time covers
+    the replay kernel and the kernels after it (cold-site Tier E, split chains)."""
+    for cfg, mode, want in ((tracegen.CONFIGS[2].with_traces(2), 1, 2),         # replay + post
+                            (tracegen.CONFIGS[3].with_traces(2), 1, 3),         # + cold_hist (50,000 sites)
+                            (tracegen.CONFIGS[2].with_traces(2), SPLIT, 7)):    # + 5 pchain kernels
+        ev, off = tracegen.generate(cfg)
+        tr = scl.scl_trace_load(ev, off, cfg.n_sites)
+        r = None
+        for _ in range(3):
+            r = scl.scl_replay_run(cfg.T, tr, out=r, timing=True, chain_mode=mode)
+        assert scl.scl_result_launches(r) == want
+        ks, ps = scl.scl_result_kernel_times(r), scl.scl_result_pass_times(r)
+        assert len(ks) == 3 and len(ps) == 3 and all(p >= k > 0 for k, p in zip(ks, ps))
+        rd = scl.scl_replay_run(cfg.T, tr, defer_finalize=True, chain_mode=mode)
+        scl.scl_finalize(rd, cfg.events_per_trace * 1000)
+        # deferred: the post pass without a6, then a6 in its own kernel(s): report_kernel, or
+        # report_flags + report_rows above 16,384 sites
+        assert scl.scl_result_launches(rd) == want + (1 if cfg.n_sites <= 16384 else 2)
