@@ -121,10 +121,12 @@ def replay(events: np.ndarray, offsets, n_sites: int, T: int, hwm_mode: int = HW
     cap = sample_bound(events, offsets, T)
     soff = np.zeros(n_traces + 1, dtype=np.uint64)
     soff[1:] = np.cumsum(cap)
-    samples = np.zeros(max(int(soff[-1]), 1), dtype=SAMPLE_DTYPE)
+    # slot buffers sized by the sample bound; only the slots the replay writes are read back (`keep`
+    # below), so they are not zero-filled (at dense thresholds the bound is many GB, the samples few)
+    samples = np.empty(max(int(soff[-1]), 1), dtype=SAMPLE_DTYPE)
     summ = np.zeros(n_traces, dtype=SUMMARY_DTYPE)
     table = np.zeros((n_sites, NCOL), dtype=np.uint64)
-    dom = np.zeros(len(samples), dtype=DOMAIN_DTYPE)
+    dom = np.empty(len(samples), dtype=DOMAIN_DTYPE)
     rc = lib.orc_replay_all(_ptr(events), _ptr(offsets), n_traces, n_sites, T, hwm_mode,
                             n_threads, _ptr(samples), _ptr(soff), _ptr(summ), _ptr(table), _ptr(dom))
     if rc != 0:
