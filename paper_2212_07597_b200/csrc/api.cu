@@ -50,6 +50,12 @@ struct scl_traces {
     unsigned long long* d_err = nullptr;       // [1 + 64] first invalid event (load check), then the log2-size
                                                // histogram of the alloc / free events (chain-split heuristic)
     std::vector<uint64_t> h_shist;
+    // site ids by frequency (n_sites > kHot): internal id = rank of the site in a strided sample of the
+    // events, so that the hottest sites land in the shared-memory Tier-E table whatever the caller's
+    // numbering; every output is mapped back to the caller's ids
+    unsigned* d_remap = nullptr;               // [n_sites] caller id -> internal id
+    std::vector<uint32_t> h_inv;               // internal id -> caller id (empty: identity)
+    bool remapped = false;
     unsigned int* d_ticket = nullptr;
     std::vector<uint64_t> h_off, h_sabs;
     uint32_t n_segs = 0;
@@ -95,7 +101,8 @@ struct scl_result {
     uint64_t elapsed_ns = 0;
     cudaStream_t stream = nullptr;
     // device
-    unsigned long long* d_table = nullptr;     // n_sites*NCOL + 3
+    unsigned long long* d_table = nullptr;     // n_sites*NCOL + 3, in the caller's site ids
+    unsigned long long* d_table_int = nullptr; // the same in internal ids (remapped handles; else == d_table)
     scl_sample* d_samples = nullptr; unsigned int* d_epflag = nullptr; size_t cap = 0;
     unsigned long long* d_sbase = nullptr;
     scl_trace_summary* d_summ = nullptr;
@@ -221,6 +228,50 @@ static scl_status validate_host(const scl_event* src, bool src_dev, const std::v
     return SCL_OK;
 }
 
+// Site ids by frequency (n_sites > kHot): count the sites of a strided sample of up to 2^21 alloc /
+// free events (host memory read in place, device memory through one strided copy), order the sites
+// by (sampled count desc, id asc) and upload caller -> internal.  No remap when that order is the
+// identity on the shared-memory table's range.  The remap is a permutation: every result is exact
+// whatever it is; it only decides which sites take the fast Tier-E path.
+static scl_status site_remap(scl_traces* tr, const scl_event* src, bool src_dev, uint64_t n, uint32_t n_sites,
+                             cudaStream_t st, bool& changed)
+{
+    tr->remapped = false; tr->h_inv.clear(); changed = false;
+    if (n_sites <= (uint32_t)kHot || n == 0) return SCL_OK;
+    const uint64_t want = 1ull << 21, stride = std::max<uint64_t>(1, n / want), m = (n + stride - 1) / stride;
+    std::vector<scl_event> smp;
+    const scl_event* hv = src;
+    if (src_dev) {
+        smp.resize(m);
+        CU(cudaMemcpy2DAsync(smp.data(), sizeof(scl_event), src, stride * sizeof(scl_event), sizeof(scl_event), m,
+                             cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        hv = smp.data();
+    }
+    std::vector<uint32_t> cnt(n_sites, 0);
+    for (uint64_t i = 0; i < m; ++i) {
+        const uint64_t meta = (src_dev ? hv[i] : hv[i * stride]).meta;
+        const uint32_t site = ev_site(meta);
+        if (site < n_sites && ev_kind(meta) < 2) ++cnt[site];
+    }
+    std::vector<uint32_t> order(n_sites);
+    for (uint32_t i = 0; i < n_sites; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return cnt[a] > cnt[b]; });
+    const uint32_t lim = std::min<uint32_t>(n_sites, (uint32_t)kWarm);
+    bool ident = true;                                // the table's range holds the same sites already?
+    for (uint32_t i = 0; i < lim && ident; ++i) ident = order[i] < lim;
+    if (ident) return SCL_OK;
+    std::vector<uint32_t> remap(n_sites);
+    for (uint32_t i = 0; i < n_sites; ++i) remap[order[i]] = i;
+    cudaFree(tr->d_remap); tr->d_remap = nullptr;
+    if (cudaMalloc(&tr->d_remap, (size_t)n_sites * 4) != cudaSuccess) { cudaGetLastError(); tr->d_remap = nullptr; return SCL_OK; }
+    CU(cudaMemcpyAsync(tr->d_remap, remap.data(), (size_t)n_sites * 4, cudaMemcpyHostToDevice, st));
+    CU(cudaStreamSynchronize(st));                    // (remap is a local vector)
+    tr->h_inv = std::move(order);
+    tr->remapped = true; changed = true;
+    return SCL_OK;
+}
+
 // Copy the events into the handle's device buffers (growing them if needed), run the load
 // statistics and build the unit plan.  Stream-ordered on st; one synchronisation at the end
 // (the host needs the per-trace sum |d| to size the sample buffer of each run).
@@ -277,8 +328,13 @@ static scl_status upload(scl_traces* tr, const scl_event* src, bool src_dev, std
     CU(cudaMemsetAsync(tr->d_sabs, 0, nt1 * 8, st));
     CU(cudaMemsetAsync(tr->d_err, 0xff, 8, st));
     CU(cudaMemsetAsync(tr->d_err + 1, 0, 64 * 8, st));
+    {
+        bool changed = false;
+        scl_status rs = site_remap(tr, src, src_dev, n, n_sites, st, changed);
+        if (rs != SCL_OK) { tr->n_traces = 0; tr->n_events = 0; tr->n_segs = 0; return rs; }
+    }
     CU(launch_load_stats(csrc ? csrc : tr->d_ev, tr->d_off, n_traces, n, n_sites, tr->d_sabs, tr->d_err,
-                         csrc ? tr->d_ev : nullptr, tr->d_err + 1, st));
+                         csrc ? tr->d_ev : nullptr, tr->d_err + 1, tr->remapped ? tr->d_remap : nullptr, st));
 
     // unit plan (while the copy runs): unit k of trace t covers rows (off_t/8) + 1024k ...;
     // tickets ordered (k, t) so that one trace's units are spread over the run
@@ -412,7 +468,7 @@ extern "C" void scl_traces_free(scl_traces* t) {
     cudaFree(t->d_tr_nseg); cudaFree(t->d_tr_base); cudaFree(t->d_run); cudaFree(t->d_uent); cudaFree(t->d_ticket);
     cudaFree(t->d_err); cudaFree(t->d_usum); cudaFree(t->d_ustart); cudaFree(t->d_ttot);
     cudaFree(t->d_crec); cudaFree(t->d_crec_fill); cudaFree(t->d_cctr); cudaFree(t->d_tierE);
-    cudaFree(t->d_ust); cudaFree(t->d_sync); cudaFree(t->d_pc); cudaFree(t->d_pr); cudaFree(t->d_ul);
+    cudaFree(t->d_ust); cudaFree(t->d_sync); cudaFree(t->d_pc); cudaFree(t->d_pr); cudaFree(t->d_ul); cudaFree(t->d_remap);
     cudaFree(t->d_pscr); cudaFree(t->d_pnext); cudaFree(t->d_pctr);
     if (t->h_covf) cudaFreeHost(t->h_covf);
     delete t;
@@ -428,6 +484,8 @@ extern "C" scl_status scl_traces_info(const scl_traces* t, uint64_t* n_events, u
 
 // ---------------------------------------------------------------- run
 static void free_result_buffers(scl_result* r) {
+    if (r->d_table_int != r->d_table) cudaFree(r->d_table_int);
+    r->d_table_int = nullptr;
     cudaFree(r->d_table); cudaFree(r->d_sbase); cudaFree(r->d_summ); cudaFree(r->d_rows);
     cudaFree(r->d_rbits); cudaFree(r->d_rsb);
     r->d_table = nullptr; r->d_sbase = nullptr; r->d_summ = nullptr; r->d_rows = nullptr;
@@ -463,6 +521,7 @@ static scl_status alloc_result(scl_result* r, const scl_traces* tr) {
     if (S <= r->cap_sites && nt <= r->cap_tr) return SCL_OK;
     free_result_buffers(r);
     CU(cudaMalloc(&r->d_table, (S * SCL_NCOL + 3) * 8));
+    CU(cudaMalloc(&r->d_table_int, (S * SCL_NCOL + 3) * 8));
     CU(cudaMalloc(&r->d_sbase, nt * 8));
     CU(cudaMalloc(&r->d_summ, nt * sizeof(scl_trace_summary)));
     const size_t nwd = (std::max<size_t>(S, kReportSites) + 31) / 32;
@@ -609,7 +668,8 @@ static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const sc
     p.ticket = tr->d_ticket; p.n_segs = tr->n_segs; p.epoch = tr->epoch;
     p.n_runners = (unsigned)r->grid * kEmbeddedRunners;    // 2 runner warps in every CTA
     p.n_sites = tr->n_sites; p.n_traces = NT; p.T = (long long)threshold; p.hwm_sample = o.hwm_mode == SCL_HWM_SAMPLE;
-    p.table = r->d_table; p.samples = r->d_samples; p.ep_flag = r->d_epflag; p.sbase = r->d_sbase;
+    unsigned long long* tab = tr->remapped ? r->d_table_int : r->d_table;   // the kernels' table (internal ids)
+    p.table = tab; p.samples = r->d_samples; p.ep_flag = r->d_epflag; p.sbase = r->d_sbase;
     p.sample_cap = r->cap;
     p.summ = r->d_summ; p.uent = tr->d_uent;
     if (!base) ensure_cold_pool(tr);
@@ -652,7 +712,7 @@ static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const sc
         p.pscr = tr->d_pscr; p.pnext = tr->d_pnext; p.pctr = tr->d_pctr; p.pblocks = (unsigned)std::min<size_t>(tr->cap_pblocks, 0xffffffffu);
     }
     PrepParams& pp = p.prep;                   // done by CTA 0 of the replay kernel
-    pp.table = r->d_table; pp.table_words = (size_t)tr->n_sites * SCL_NCOL + 3;
+    pp.table = tab; pp.table_words = (size_t)tr->n_sites * SCL_NCOL + 3;
     pp.summ = reinterpret_cast<unsigned long long*>(r->d_summ); pp.summ_words = (size_t)NT * sizeof(scl_trace_summary) / 8;
     pp.run = reinterpret_cast<unsigned long long*>(tr->d_run); pp.run_words = (size_t)NT * sizeof(RunState) / 8;
     pp.ticket = tr->d_ticket; pp.sbase = r->d_sbase; pp.off = tr->d_off; pp.sabs = tr->d_sabs;
@@ -677,7 +737,7 @@ static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const sc
                                                // post pass kept them (base's own table may be reduced since)
         CU(cudaMemsetAsync(pp.run, 0, pp.run_words * 8, st));
         if (tr->n_sites)
-            CU(cudaMemcpy2DAsync(r->d_table, SCL_NCOL * 8, tr->d_tierE, 4 * 8, 4 * 8, tr->n_sites,
+            CU(cudaMemcpy2DAsync(tab, SCL_NCOL * 8, tr->d_tierE, 4 * 8, 4 * 8, tr->n_sites,
                                  cudaMemcpyDeviceToDevice, st));
         p.rechain = 1;
         p.n_runners = std::min<unsigned>(NT, (unsigned)r->grid * 8);
@@ -698,13 +758,17 @@ static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const sc
     // a6 fused into the post pass when the run finalizes at once on a small table (not when the
     // table is first reduced across ranks)
     const bool reduce = o.nccl_comm != nullptr;
-    const bool fuse = !o.defer_finalize && !reduce;
+    const bool fuse = !o.defer_finalize && !reduce && !tr->remapped;   // (remapped: a6 after the permute)
     if (fuse) {
         p.fuse_report = 1; p.fin = final_params(r); p.rows = r->d_rows;
         p.rbits = r->d_rbits; p.rlrate = r->d_rlrate; p.rlsite = r->d_rlsite; p.rsbcnt = r->d_rsb;
     }
     CU(launch_post(p, st));
     r->nlaunch += 1;
+    if (tr->remapped) {                        // the table in the caller's site order (a6, the all-reduce)
+        CU(launch_permute_table(tab, r->d_table, tr->d_remap, tr->n_sites, st));
+        r->nlaunch += 1;
+    }
     if (tm) CU(cudaEventRecord(r->ev[1], st));
     if (fuse) {
         if (tm) CU(cudaEventRecord(r->ev[2], st));
@@ -817,9 +881,11 @@ extern "C" scl_status scl_samples(const scl_result* r, uint32_t trace, scl_sampl
     *n = cnt;
     if (cap == 0 || cnt == 0) return SCL_OK;
     if (!out) return fail(SCL_EINVAL, "out is NULL");
-    CU(cudaMemcpyAsync(out, r->d_samples + r->h_sbase[trace], std::min(cap, cnt) * sizeof(scl_sample),
-                       cudaMemcpyDeviceToHost, r->stream));
+    const size_t k = std::min(cap, cnt);
+    CU(cudaMemcpyAsync(out, r->d_samples + r->h_sbase[trace], k * sizeof(scl_sample), cudaMemcpyDeviceToHost, r->stream));
     CU(cudaStreamSynchronize(r->stream));
+    if (r->tr->remapped)                       // internal site ids -> the caller's
+        for (size_t i = 0; i < k; ++i) out[i].site = r->tr->h_inv[out[i].site];
     return SCL_OK;
 }
 
@@ -1114,9 +1180,11 @@ extern "C" scl_status scl_rate_samples(const scl_rate_result* r, uint32_t trace,
     if (cap == 0 || *n == 0) return SCL_OK;
     if (!out) return fail(SCL_EINVAL, "out is NULL");
     CU(cudaSetDevice(r->tr->device));
-    CU(cudaMemcpyAsync(out, r->d_samples + r->h_sbase[trace], std::min(cap, *n) * sizeof(scl_rate_sample),
-                       cudaMemcpyDeviceToHost, r->st));
+    const size_t k = std::min(cap, (size_t)*n);
+    CU(cudaMemcpyAsync(out, r->d_samples + r->h_sbase[trace], k * sizeof(scl_rate_sample), cudaMemcpyDeviceToHost, r->st));
     CU(cudaStreamSynchronize(r->st));
+    if (r->tr->remapped)                       // internal site ids -> the caller's
+        for (size_t i = 0; i < k; ++i) out[i].site = r->tr->h_inv[out[i].site];
     return SCL_OK;
 }
 
@@ -1126,6 +1194,13 @@ extern "C" scl_status scl_rate_site_counts(const scl_rate_result* r, uint64_t* c
     if (cap == 0) return SCL_OK;
     if (!counts) return fail(SCL_EINVAL, "counts is NULL");
     CU(cudaSetDevice(r->tr->device));
+    if (r->tr->remapped) {                     // per internal site -> per caller site
+        std::vector<uint64_t> tmp(*n);
+        CU(cudaMemcpyAsync(tmp.data(), r->d_site, *n * 8, cudaMemcpyDeviceToHost, r->st));
+        CU(cudaStreamSynchronize(r->st));
+        for (size_t i = 0; i < *n; ++i) if (r->tr->h_inv[i] < cap) counts[r->tr->h_inv[i]] = tmp[i];
+        return SCL_OK;
+    }
     CU(cudaMemcpyAsync(counts, r->d_site, std::min(cap, *n) * 8, cudaMemcpyDeviceToHost, r->st));
     CU(cudaStreamSynchronize(r->st));
     return SCL_OK;

@@ -21,7 +21,7 @@ __global__ void __launch_bounds__(256) load_stats_kernel(const scl_event* ev, co
                                                          unsigned n_traces, unsigned long long n_events,
                                                          unsigned n_sites, unsigned long long* sabs,
                                                          unsigned long long* err, scl_event* dst,
-                                                         unsigned long long* shist)
+                                                         unsigned long long* shist, const unsigned* remap)
 {
     // histogram of floor(log2(size)) over the alloc / free events (how many sync events |d| >= 2T - 1
     // a threshold T has: the chain-split heuristic of scl_replay_run), per block in shared memory
@@ -42,7 +42,20 @@ __global__ void __launch_bounds__(256) load_stats_kernel(const scl_event* ev, co
         ulonglong2 v[8];
         #pragma unroll
         for (int j = 0; j < 8; ++j) v[j] = i0 + j < n_events ? __ldcs(q + j) : make_ulonglong2(0, 0);
-        if (dst) {
+        if (remap) {                                         // site ids by load-time frequency (see upload)
+            ulonglong2* o = reinterpret_cast<ulonglong2*>((dst ? dst : const_cast<scl_event*>(ev)) + i0);
+            #pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (i0 + j < n_events) {
+                    const unsigned long long m = v[j].y;
+                    const unsigned site = ev_site(m);
+                    const unsigned long long m2 = site < n_sites
+                        ? (m & ((1ull << 43) - 1ull)) | ((unsigned long long)__ldg(remap + site) << 43) : m;
+                    if (dst) o[j] = make_ulonglong2(v[j].x, m2);
+                    else if (m2 != m) o[j].y = m2;
+                }
+            }
+        } else if (dst) {
             ulonglong2* o = reinterpret_cast<ulonglong2*>(dst + i0);
             #pragma unroll
             for (int j = 0; j < 8; ++j) if (i0 + j < n_events) o[j] = v[j];
@@ -104,12 +117,13 @@ __global__ void __launch_bounds__(512) report_kernel(const __grid_constant__ Fin
 // ============================================================================ launch wrappers
 cudaError_t launch_load_stats(const scl_event* ev, const unsigned long long* off, unsigned n_traces,
                               unsigned long long n_events, unsigned n_sites, unsigned long long* sabs,
-                              unsigned long long* err, scl_event* dst, unsigned long long* shist, cudaStream_t st)
+                              unsigned long long* err, scl_event* dst, unsigned long long* shist,
+                              const unsigned* remap, cudaStream_t st)
 {
     if (n_traces == 0 || n_events == 0) return cudaSuccess;
     const unsigned long long warps = (n_events + 255) / 256;
     const unsigned blocks = (unsigned)std::min<unsigned long long>((warps + 7) / 8, 148ull * 8);
-    load_stats_kernel<<<blocks, 256, 0, st>>>(ev, off, n_traces, n_events, n_sites, sabs, err, dst, shist);
+    load_stats_kernel<<<blocks, 256, 0, st>>>(ev, off, n_traces, n_events, n_sites, sabs, err, dst, shist, remap);
     return cudaGetLastError();
 }
 
@@ -125,6 +139,26 @@ cudaError_t launch_report(const FinalParams& p, scl_site_row* rows, cudaStream_t
         attr = true;
     }
     report_kernel<<<1, 512, report_smem_bytes<512>(), st>>>(p, rows);
+    return cudaGetLastError();
+}
+
+// The summable table in the caller's site order: tout[c] = tin[remap[c]] (+ the gate words).
+__global__ void __launch_bounds__(256) permute_table_kernel(const unsigned long long* tin, unsigned long long* tout,
+                                                            const unsigned* remap, unsigned n_sites)
+{
+    const size_t n = (size_t)n_sites * SCL_NCOL + 3;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const size_t c = i / SCL_NCOL;
+        tout[i] = c < n_sites ? __ldcg(tin + (size_t)__ldg(remap + c) * SCL_NCOL + i % SCL_NCOL) : __ldcg(tin + i);
+    }
+}
+
+cudaError_t launch_permute_table(const unsigned long long* tin, unsigned long long* tout, const unsigned* remap,
+                                 unsigned n_sites, cudaStream_t st)
+{
+    const size_t n = (size_t)n_sites * SCL_NCOL + 3;
+    const unsigned blocks = (unsigned)std::min<size_t>((n + 255) / 256, 148 * 16);
+    permute_table_kernel<<<blocks, 256, 0, st>>>(tin, tout, remap, n_sites);
     return cudaGetLastError();
 }
 

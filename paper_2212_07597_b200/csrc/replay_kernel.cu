@@ -273,7 +273,7 @@ __device__ void compute_role(const ReplayParams& p, Smem& s, unsigned char* stag
         Slot& S = s.slot[sl];
         const int c = g * 8 + w8;                         // chunk index within the unit
         #pragma unroll
-        for (int q = 0; q < kBloomWords; q += 32) S.bloom[c][q + lane] = 0u;
+        for (int q = 0; q < kBloomWords; q += 32) if (q + lane < kBloomWords) S.bloom[c][q + lane] = 0u;
         if (g == 0 && w8 == 0 && lane == 0) S.info = inf;
         __syncwarp();
         const uint32_t bl_s = smem_u32(&S.bloom[c][0]);

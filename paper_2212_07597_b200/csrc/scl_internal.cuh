@@ -49,12 +49,13 @@ constexpr int kCtaThreads = (kComputeWarps + 1 + kLBWarps) * 32;
 #define SCL_WARM 2048
 #endif
 #ifndef SCL_BLOOM_LOG2
-#define SCL_BLOOM_LOG2 6
+#define SCL_BLOOM_LOG2 5
 #endif
 constexpr int kStages = SCL_STAGES;           // TMA ring depth
 constexpr int kSlots = 6;                     // compute -> publisher unit summary ring (smem)
 constexpr int kBloomLog2 = SCL_BLOOM_LOG2;
-constexpr int kBloomWords = 1 << kBloomLog2;  // Bloom filter of freed pointers per chunk (64 words: 2048 bits)
+constexpr int kBloomWords = 1 << kBloomLog2;  // Bloom filter of freed pointers per chunk (32 words = 1024 bits; 64
+                                              //   measured 6-7 % slower on configs 2 and 3: the records and their zeroing)
 constexpr int kHot = 1024;                    // sites with shared-memory Tier-E counters (all 4 kinds)
 constexpr int kWarm = SCL_WARM;               // n_sites > kHot: the allocs and frees of the kWarm lowest site ids;
                                               //   the other sites' events go to the cold-record stream
@@ -293,7 +294,10 @@ cudaError_t launch_rate(const RateParams& p, int phase, cudaStream_t st);   // 0
 // launch wrappers (replay.cu)
 cudaError_t launch_load_stats(const scl_event* ev, const unsigned long long* off, unsigned n_traces,
                               unsigned long long n_events, unsigned n_sites, unsigned long long* sabs,
-                              unsigned long long* err, scl_event* dst, unsigned long long* shist, cudaStream_t st);
+                              unsigned long long* err, scl_event* dst, unsigned long long* shist,
+                              const unsigned* remap, cudaStream_t st);
+cudaError_t launch_permute_table(const unsigned long long* tin, unsigned long long* tout, const unsigned* remap,
+                                 unsigned n_sites, cudaStream_t st);
 cudaError_t launch_replay(const CUtensorMap* tmap, const ReplayParams& p, int grid, cudaStream_t st);
 cudaError_t launch_post(const ReplayParams& p, cudaStream_t st);
 cudaError_t launch_rechain(const ReplayParams& p, cudaStream_t st);   // runner warps alone
