@@ -82,11 +82,12 @@ def test_launch_count_and_pass_times():
         r = None
         for _ in range(3):
             r = scl.scl_replay_run(cfg.T, tr, out=r, timing=True, chain_mode=mode)
-        assert scl.scl_result_launches(r) == want
+        # (+3 if the load renumbered the sites: the table permute and an unfused two-kernel a6)
+        assert scl.scl_result_launches(r) in ((want,) if cfg.n_sites <= 1024 else (want, want + 3))
         ks, ps = scl.scl_result_kernel_times(r), scl.scl_result_pass_times(r)
         assert len(ks) == 3 and len(ps) == 3 and all(p >= k > 0 for k, p in zip(ks, ps))
         rd = scl.scl_replay_run(cfg.T, tr, defer_finalize=True, chain_mode=mode)
         scl.scl_finalize(rd, cfg.events_per_trace * 1000)
         # deferred: the post pass without a6, then a6 in its own kernel(s): report_kernel, or
         # report_flags + report_rows above 16,384 sites
-        assert scl.scl_result_launches(rd) == want + (1 if cfg.n_sites <= 16384 else 2)
+        assert scl.scl_result_launches(rd) in ((want + 1,) if cfg.n_sites <= 16384 else (want + 2, want + 3))
