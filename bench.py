@@ -437,8 +437,8 @@ def main():
                          "kernel": "scl::replay_kernel",
                          "kernel_ms": kern_avg, "peak_source": peak_src,
                          "stream_pass_ms": pass_avg,
-                         "stream_pass": "replay_kernel" + (" + cold_hist_kernel (Tier E of its cold-record stream)"
-                                                           if cold else "") + ": a1-a5 before the post pass",
+                         "stream_pass": "replay_kernel" + (" + cold_hist_kernel + cold_sum_kernel (Tier E of its "
+                                                           "cold-record stream)" if cold else "") + ": a1-a5 before the post pass",
                          "stream_pass_frac": alg_bytes / (pass_avg / 1e3) / 1e9 / peak,
                          "alg_bytes_per_launch": alg_bytes,
                          "alg_bytes_rule": "16 B/event read + 32 B/sample written + 80 B/site table flush",
@@ -448,7 +448,7 @@ def main():
             "e2e": e2e,
             "gpu_launches": launches * args.steps,
             "gpu_launches_note": "per step: replay_kernel (its CTA 0 prepares the run)" +
-                                 (", cold_hist_kernel" if cold else "") +
+                                 (", cold_hist_kernel, cold_sum_kernel" if cold else "") +
                                  ", post_kernel (reclaim + per-sample reduce + a6 grid-wide)" if world == 1 else
                                  ", post_kernel (reclaim + per-sample reduce), then after the all-reduce the a6 "
                                  "kernel(s): report_kernel, or report_flags + report_rows above 16,384 sites",

@@ -72,6 +72,8 @@ struct scl_traces {
     mutable unsigned long long crec_cap = 0;         // records (of the current record size)
     mutable size_t crec_bytes = 0, crec_fills = 0;
     mutable unsigned long long* h_covf = nullptr;       // pinned: the last exhausted pool (grow it)
+    mutable unsigned* d_cpart = nullptr;                // cold_hist's partial tables
+    mutable size_t cap_cpart = 0;
     // Tier-E columns of the last stream pass (written by its post pass; a re-threshold copies them)
     mutable unsigned long long* d_tierE = nullptr;
     mutable size_t cap_tierE = 0;
@@ -469,7 +471,7 @@ extern "C" void scl_traces_free(scl_traces* t) {
     cudaFree(t->d_ev); cudaFree(t->d_off); cudaFree(t->d_sabs); cudaFree(t->d_tk); cudaFree(t->d_urec); cudaFree(t->d_uagg);
     cudaFree(t->d_tr_nseg); cudaFree(t->d_tr_base); cudaFree(t->d_run); cudaFree(t->d_uent); cudaFree(t->d_ticket);
     cudaFree(t->d_err); cudaFree(t->d_usum); cudaFree(t->d_ustart); cudaFree(t->d_ttot);
-    cudaFree(t->d_crec); cudaFree(t->d_crec_fill); cudaFree(t->d_cctr); cudaFree(t->d_tierE);
+    cudaFree(t->d_crec); cudaFree(t->d_crec_fill); cudaFree(t->d_cctr); cudaFree(t->d_tierE); cudaFree(t->d_cpart);
     cudaFree(t->d_ust); cudaFree(t->d_sync); cudaFree(t->d_pc); cudaFree(t->d_pr); cudaFree(t->d_ul); cudaFree(t->d_remap);
     cudaFree(t->d_pscr); cudaFree(t->d_pnext); cudaFree(t->d_pctr);
     if (t->h_covf) cudaFreeHost(t->h_covf);
@@ -564,6 +566,16 @@ static void ensure_cold_pool(const scl_traces* tr) {
         cudaMemset(tr->d_cctr, 0, 16);
         if (cudaHostAlloc(&tr->h_covf, 8, cudaHostAllocMapped) != cudaSuccess) { cudaGetLastError(); tr->h_covf = nullptr; }
         else *tr->h_covf = 0;
+    }
+    {   // cold_hist's partial tables: one per CTA (R ranges x G groups <= max(SMs, R))
+        int grid = 0;
+        replay_occupancy(&grid);
+        const size_t np = std::max<size_t>((size_t)grid, cold_ranges(tr->n_sites)) * 2 * kColdSites;
+        if (np > tr->cap_cpart) {
+            cudaFree(tr->d_cpart); tr->d_cpart = nullptr; tr->cap_cpart = 0;
+            if (cudaMalloc(&tr->d_cpart, np * 4) != cudaSuccess) { cudaGetLastError(); tr->d_cpart = nullptr; }
+            else tr->cap_cpart = np;
+        }
     }
     const size_t rs = 8;
     unsigned long long want = tr->n_events / 16 * 5 + 4096ull * kRecChunk;
@@ -676,6 +688,7 @@ static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const sc
     p.summ = r->d_summ; p.uent = tr->d_uent;
     if (!base) ensure_cold_pool(tr);
     p.crec = tr->d_crec; p.crec_cap = tr->crec_cap; p.cctr = tr->d_cctr; p.crec_fill = tr->d_crec_fill;
+    p.cpart = tr->d_cpart;
     p.covf = tr->h_covf;
 
     if (tr->n_sites > tr->cap_tierE) {
@@ -749,7 +762,7 @@ static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const sc
         CU(launch_replay(&tr->tmap, p, r->grid, st));
         if (tm) CU(cudaEventRecord(r->kev[3 * ks + 1], st));
         CU(launch_cold_hist(p, st));           // Tier E of the sites beyond the shared-memory table
-        r->nlaunch += (tr->n_segs ? 1 : 0) + (cold_hist_launched(p) ? 1 : 0);
+        r->nlaunch += (tr->n_segs ? 1 : 0) + cold_hist_launches(p);
         if (split) { CU(launch_pchain(p, st)); r->nlaunch += 5; }
     }
     if (tm) {

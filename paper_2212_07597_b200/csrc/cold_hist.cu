@@ -80,18 +80,52 @@ __global__ void __launch_bounds__(1024, 1) cold_hist_kernel(const __grid_constan
         fv[0] = fw[0]; fv[1] = fw[1];
     }
     __syncthreads();
-    for (unsigned i = threadIdx.x; i < 2 * ns; i += blockDim.x) {
+    // the CTA's partial table goes out with plain coalesced stores; cold_sum_kernel adds the G partials
+    // of each range (one L2 atomic pair per word of every CTA cost ~70 us on config 3: 13.6 M reductions)
+    if (p.cpart) {
+        uint4* dst = reinterpret_cast<uint4*>(p.cpart + (size_t)blockIdx.x * 2 * kColdSites);
+        const uint4* srcw = reinterpret_cast<const uint4*>(ctab);
+        for (unsigned i = threadIdx.x; i < 2 * (unsigned)kColdSites / 4; i += blockDim.x) dst[i] = srcw[i];
+        return;
+    }
+    for (unsigned i = threadIdx.x; i < 2 * ns; i += blockDim.x) {     // (no partial-table buffer: L2 atomics)
         const unsigned kind = i / ns, site = i % ns;
-        const unsigned w = ctab[kind * kColdSites + site];
-        if (w) {
+        const unsigned cw = ctab[kind * kColdSites + site];
+        if (cw) {
             unsigned long long* row = p.table + (size_t)(site + lo) * SCL_NCOL;
-            atomicAdd(&row[SCL_COL_N_MALLOC + kind], (unsigned long long)(w >> 24));
-            atomicAdd(&row[SCL_COL_MALLOC_BYTES + kind], (unsigned long long)(w & 0xFFFFFFu));
+            atomicAdd(&row[SCL_COL_N_MALLOC + kind], (unsigned long long)(cw >> 24));
+            atomicAdd(&row[SCL_COL_MALLOC_BYTES + kind], (unsigned long long)(cw & 0xFFFFFFu));
+        }
+    }
+}
+
+// Sum of the G partial tables of every range -> the site table (thread per (range, kind, site); the
+// partials of one word are G apart).  No other kernel writes Tier E of the cold sites at this point,
+// so the add needs no atomic.
+__global__ void __launch_bounds__(256) cold_sum_kernel(const __grid_constant__ ReplayParams p, unsigned R, unsigned G)
+{
+    const size_t n = (size_t)R * 2 * kColdSites;
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (size_t)gridDim.x * blockDim.x) {
+        const unsigned r = (unsigned)(idx / (2 * kColdSites)), k = (unsigned)(idx % (2 * kColdSites));
+        const unsigned kind = k / kColdSites, site = k % kColdSites;
+        const unsigned lo = (unsigned)kWarm + r * (unsigned)kColdSites;
+        if (lo + site >= p.n_sites) continue;
+        unsigned long long cnt = 0, bytes = 0;
+        for (unsigned g = 0; g < G; ++g) {
+            const unsigned w = __ldcg(p.cpart + ((size_t)g * R + r) * 2 * kColdSites + k);
+            cnt += w >> 24; bytes += w & 0xFFFFFFu;
+        }
+        if (cnt | bytes) {
+            unsigned long long* row = p.table + (size_t)(lo + site) * SCL_NCOL;
+            row[SCL_COL_N_MALLOC + kind] += cnt;
+            row[SCL_COL_MALLOC_BYTES + kind] += bytes;
         }
     }
 }
 
 bool cold_hist_launched(const ReplayParams& p) { return p.n_sites > (unsigned)kWarm && p.n_segs > 0; }
+unsigned cold_hist_launches(const ReplayParams& p) { return cold_hist_launched(p) ? (p.cpart ? 2u : 1u) : 0u; }
+unsigned cold_ranges(unsigned n_sites) { return n_sites > (unsigned)kWarm ? (n_sites - kWarm + kColdSites - 1) / kColdSites : 0; }
 
 cudaError_t launch_cold_hist(const ReplayParams& p, cudaStream_t st)
 {
@@ -105,9 +139,13 @@ cudaError_t launch_cold_hist(const ReplayParams& p, cudaStream_t st)
         cudaError_t e = cudaFuncSetAttribute(cold_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) { nsm = 0; return e; }
     }
-    const unsigned R = (p.n_sites - kWarm + kColdSites - 1) / kColdSites;
+    const unsigned R = cold_ranges(p.n_sites);
     const unsigned G = std::max(1u, (unsigned)nsm / R);
     cold_hist_kernel<<<R * G, 1024, smem, st>>>(p, R);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || !p.cpart) return e;
+    const size_t n = (size_t)R * 2 * kColdSites;
+    cold_sum_kernel<<<(unsigned)std::min<size_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(p, R, G);
     return cudaGetLastError();
 }
 

@@ -1073,10 +1073,13 @@ __global__ void __launch_bounds__(256, 3) post_kernel(const __grid_constant__ Re
     if (p.n_sites <= kReportSites) {                        // small table: a6 in the block that finishes last
         __shared__ unsigned last;
         __syncthreads();
-        if (threadIdx.x == 0) { __threadfence(); last = atomicAdd(&p.ticket[3], 1u) == gridDim.x - 1; }
+        if (threadIdx.x == 0) {
+            __threadfence();                                // this block's leak frees before its arrival
+            last = atomicAdd(&p.ticket[3], 1u) == gridDim.x - 1;
+            if (last) fence_acquire();                      // every block's leak frees before the reads below
+        }
         __syncthreads();
         if (!last) return;
-        __threadfence();                                    // every block's leak frees before the reads below
         report_block<256>(p.fin, p.rows, *reinterpret_cast<ReportSmem<256>*>(post_smem));
         POST_T(5, atomicMax)
         return;

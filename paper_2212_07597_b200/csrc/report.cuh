@@ -64,7 +64,11 @@ template <int NT> constexpr size_t report_smem_bytes() { return sizeof(ReportSme
 // consecutive sites take consecutive ranks: their rows are staged in shared memory and written
 // with lane-contiguous stores.  Four sites per thread and pass are in flight at once (the passes
 // are latency-bound).  n_sites <= kReportSites; blockDim.x == NT.
-constexpr int kRU = 1;
+#ifndef SCL_RU
+#define SCL_RU 1
+#endif
+constexpr int kRU = SCL_RU;                  // sites per thread and pass in flight: pass 2 (rows)
+constexpr int kRU1 = 4;                      //   and pass 1 (two words per site: flags)
 template <int NT>
 __device__ void report_block(const FinalParams& p, scl_site_row* rows, ReportSmem<NT>& sm)
 {
@@ -79,10 +83,10 @@ __device__ void report_block(const FinalParams& p, scl_site_row* rows, ReportSme
     if (tid == 0) { sm.nflag = 0; gate_copy(p); }
     __syncthreads();
     RPT_T(0)
-    for (unsigned base = 0; base < S; base += kRU * NT) {    // pass 1: flags (integer only), flagged list
-        unsigned long long m[kRU], f[kRU];
+    for (unsigned base = 0; base < S; base += kRU1 * NT) {    // pass 1: flags (integer only), flagged list
+        unsigned long long m[kRU1], f[kRU1];
         #pragma unroll
-        for (int k = 0; k < kRU; ++k) {
+        for (int k = 0; k < kRU1; ++k) {
             const unsigned sidx = base + k * NT + tid;
             m[k] = f[k] = 0;
             if (sidx < S) {
@@ -91,7 +95,7 @@ __device__ void report_block(const FinalParams& p, scl_site_row* rows, ReportSme
             }
         }
         #pragma unroll
-        for (int k = 0; k < kRU; ++k) {
+        for (int k = 0; k < kRU1; ++k) {
             const unsigned sidx = base + k * NT + tid;
             const bool fl = sidx < S && open && site_over(p, m[k], f[k]);
             if (fl) {

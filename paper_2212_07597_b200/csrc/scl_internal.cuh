@@ -187,6 +187,7 @@ struct ReplayParams {
     unsigned long long* cctr;         // [2]: records allocated (chunk granules), spare (zeroed per run)
     unsigned* crec_fill;              // [crec_cap / kRecChunk] records written to each allocated chunk
     unsigned long long* covf;         // host-mapped: set when the pool was exhausted (the host grows it)
+    unsigned* cpart;                  // [max(nsm, R) * 2 * kColdSites] cold_hist's partial tables
     unsigned long long* tierE;        // [n_sites * 4] Tier-E columns of the stream pass (post pass copy; re-thresholds)
     // chain split at sync events (pchain.cu; hwm_mode PREFIX): the embedded runners stand down
     int no_chain;                     // 1: runner warps exit at once (the pchain kernels run the chains)
@@ -303,6 +304,8 @@ cudaError_t launch_post(const ReplayParams& p, cudaStream_t st);
 cudaError_t launch_rechain(const ReplayParams& p, cudaStream_t st);   // runner warps alone
 cudaError_t launch_cold_hist(const ReplayParams& p, cudaStream_t st);  // Tier E of the cold-record stream
 bool cold_hist_launched(const ReplayParams& p);
+unsigned cold_hist_launches(const ReplayParams& p);   // kernels of launch_cold_hist (hist + partial sum)
+unsigned cold_ranges(unsigned n_sites);       // cold_hist ranges of kColdSites sites
 bool report_fused(unsigned n_sites);   // a6 in one block (report_kernel) for tables this small
 cudaError_t launch_report(const FinalParams& p, scl_site_row* rows, cudaStream_t st);
 size_t replay_smem_bytes();

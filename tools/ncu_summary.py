@@ -49,7 +49,7 @@ if alg and "dram__bytes_read.sum" in d:
     traffic = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
     t = num("gpu__time_duration.sum")
     tu = d["gpu__time_duration.sum"][0]
-    secs = t * {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1}.get(tu, 1e-9)
+    secs = t * {"nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3, "second": 1, "s": 1}.get(tu, 1e-9)
     print()
     print(f"# algorithmic bytes per launch {alg:.0f}; dram traffic {traffic:.0f} = {100 * traffic / alg:.1f}% of algorithmic;"
           f" {alg / secs / 1e9:.0f} GB/s algorithmic under ncu (cold, serialised)")
