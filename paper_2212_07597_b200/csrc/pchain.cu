@@ -221,7 +221,8 @@ __device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, l
                     const bool nm = growth && F > Mp;                                  // new high-water mark (Q3)
                     scl_sample smp;
                     smp.idx = (unsigned long long)(e0 + js); smp.net = net; smp.footprint = F;
-                    smp.site = ev_site(ms); smp.kind = growth ? 0 : 1; smp.new_max = nm ? 1 : 0; smp.pad = 0;
+                    smp.site = ev_site(ms); smp.kind = growth ? 0 : 1; smp.new_max = nm ? 1 : 0;
+                    smp.pad = nm && ev_size(ms) >= kBloomBig ? 1 : 0;                  // (pc_place: episode flag bit 1)
                     if (x.n % kPBlock == 0) {                                          // a new scratch block
                         const unsigned nb = atomicAdd(p.pctr, 1u);
                         if (x.n == 0) x.first_blk = nb; else if (x.blk < p.pblocks) p.pnext[x.blk] = nb;
@@ -317,10 +318,11 @@ __global__ void __launch_bounds__(128) pc_place_kernel(const __grid_constant__ R
             for (int h = 0; h < kPBlock / 32; ++h) {
                 const unsigned long long k = k0 + (unsigned long long)(h * 32 + lane);
                 if (k < c.n && b < p.pblocks) {
-                    const scl_sample smp = p.pscr[(size_t)b * kPBlock + h * 32 + lane];
+                    scl_sample smp = p.pscr[(size_t)b * kPBlock + h * 32 + lane];
                     SCL_CHECK(r.base + k < p.sample_cap);
+                    if (smp.new_max) p.ep_flag[r.base + k] = smp.pad ? 2u : 0u;   // the tracked object >= kBloomBig
+                    smp.pad = 0;
                     p.samples[r.base + k] = smp;
-                    if (smp.new_max) p.ep_flag[r.base + k] = 0u;
                 }
             }
             if (k0 + kPBlock < c.n) b = b < p.pblocks ? __ldcg(p.pnext + b) : ~0u;

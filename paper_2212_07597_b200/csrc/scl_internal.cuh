@@ -54,6 +54,7 @@ constexpr int kCtaThreads = (kComputeWarps + 1 + kLBWarps) * 32;
 constexpr int kStages = SCL_STAGES;           // TMA ring depth
 constexpr int kSlots = 6;                     // compute -> publisher unit summary ring (smem)
 constexpr int kBloomLog2 = SCL_BLOOM_LOG2;
+constexpr unsigned kBloomBig = 4096;          // the filter's halves: frees under / from this size (replay_kernel.cu)
 constexpr int kBloomWords = 1 << kBloomLog2;  // Bloom filter of freed pointers per chunk (32 words = 1024 bits; 64
                                               //   measured 6-7 % slower on configs 2 and 3: the records and their zeroing)
 constexpr int kHot = 1024;                    // sites with shared-memory Tier-E counters (all 4 kinds)
