@@ -26,23 +26,25 @@ __global__ void __launch_bounds__(1024, 1) cold_hist_kernel(const __grid_constan
     __syncthreads();
     const unsigned long long used = min(ld_relaxed_u64(p.cctr), p.crec_cap);
     const unsigned long long nchunks = used / kRecChunk;
-    auto one = [&](unsigned long long m) {
-        const unsigned site = ev_site(m) - lo, kind = ev_kind(m);
-        if (site >= ns || kind > 1) return;                       // another range, an invalid id, a pad record
-        const unsigned long long size = ev_size(m);
-        unsigned long long* row = p.table + (size_t)(site + lo) * SCL_NCOL;
-        if (size < (1ull << 24)) {
-            const unsigned ad = (1u << 24) + (unsigned)size;
+    auto one = [&](unsigned long long m) {                       // one record (an alloc or a free)
+        const unsigned hi = (unsigned)(m >> 32), lo32 = (unsigned)m;
+        const unsigned site = (hi >> 11) - lo;
+        if (site >= ns) return;                                   // another range (or an invalid id)
+        const unsigned kind = (hi >> 8) & 1u;
+        if ((hi & 0xFFu) == 0 && lo32 < (1u << 24)) {             // size < 2^24: the packed word
+            const unsigned ad = (1u << 24) + lo32;
             const unsigned o = atomicAdd(&ctab[kind * kColdSites + site], ad);
-            const unsigned c1 = ((o & 0xFFFFFFu) + (unsigned)size) >> 24;
-            const unsigned w = (unsigned)(((unsigned long long)o + ad) >> 32);
-            if (c1 | w) {
+            if ((o & 0xFFFFFFu) + lo32 > 0xFFFFFFu || o > ~ad) {  // rare: a field carried -- exact fix in L2
+                const unsigned c1 = ((o & 0xFFFFFFu) + lo32) >> 24;
+                const unsigned w = (unsigned)(((unsigned long long)o + ad) >> 32);
+                unsigned long long* row = p.table + (size_t)(site + lo) * SCL_NCOL;
                 atomicAdd(&row[SCL_COL_N_MALLOC + kind], ((unsigned long long)w << 8) - c1);
                 if (c1) atomicAdd(&row[SCL_COL_MALLOC_BYTES + kind], 1ull << 24);
             }
         } else {
+            unsigned long long* row = p.table + (size_t)(site + lo) * SCL_NCOL;
             atomicAdd(&row[SCL_COL_N_MALLOC + kind], 1ull);
-            atomicAdd(&row[SCL_COL_MALLOC_BYTES + kind], size);
+            atomicAdd(&row[SCL_COL_MALLOC_BYTES + kind], ev_size(m));
         }
     };
     // two chunks per pass, each thread 2 x 16 B of each; the next pass's loads are issued before this

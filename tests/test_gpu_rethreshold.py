@@ -70,3 +70,29 @@ def test_rethreshold_all_empty_and_deferred_finalize():
     r = scl.scl_replay_rethreshold(65537, tr, base, defer_finalize=True, tick_ns=1000)
     scl.scl_finalize(r, oracle.elapsed_ns(off, 1000))
     compare(ev, off, cfg.n_sites, 65537, r)
+
+
+def test_rethreshold_after_an_all_reduced_base():
+    """a base whose table was all-reduced (here: two identical 'ranks', the table
+    doubled in place as a SUM all-reduce would) must not leak the other rank's Tier E into a
+    re-threshold: the re-chained result is this rank's alone until it is reduced itself."""
+    cfg = tracegen.CONFIGS[2].with_traces(4)
+    ev, off = tracegen.generate(cfg)
+    tr = scl.scl_trace_load(ev, off, cfg.n_sites)
+    el = cfg.events_per_trace * 1000
+    base = scl.scl_replay_run(cfg.T, tr, defer_finalize=True)
+    tab = scl.device_table_tensor(base)
+    tab.add_(tab.clone())                                  # the SUM all-reduce of two equal shards
+    scl.scl_finalize(base, el)
+    ref1 = oracle.replay(ev, off, cfg.n_sites, cfg.T).site_table
+    assert np.array_equal(scl.device_table_tensor(base).cpu().numpy()[:cfg.n_sites * 10].reshape(-1, 10)
+                          .astype(np.uint64), 2 * ref1)
+    T2 = 1048583
+    r2 = scl.scl_replay_rethreshold(T2, tr, base, defer_finalize=True)
+    ref2 = oracle.replay(ev, off, cfg.n_sites, T2).site_table
+    t2 = scl.device_table_tensor(r2)
+    assert np.array_equal(t2.cpu().numpy()[:cfg.n_sites * 10].reshape(-1, 10).astype(np.uint64), ref2)
+    t2.add_(t2.clone())
+    scl.scl_finalize(r2, el)
+    rows = scl.scl_site_report(r2)
+    assert np.array_equal(rows["col"][np.argsort(rows["site"])], 2 * ref2)
