@@ -170,7 +170,11 @@ __device__ __forceinline__ void fast_row(const unsigned long long* ptr, const un
         } else {
             const bool h = af && (hi >> 11) < (unsigned)kWarm;
             cold |= (af && !h ? 1u : 0u) << j;
-            const uint32_t offw = ((hi >> 9) & ~3u) + ((hi >> 8) & 1u) * (uint32_t)(4 * kWarm);   // (site < kWarm here)
+            uint32_t offw;                                                    // ((kind&1)*kWarm + site)*4
+            if constexpr ((kWarm & (kWarm - 1)) == 0)                         // (site < kWarm when used)
+                offw = ((hi >> 9) & (uint32_t)(4 * kWarm - 4)) | (((hi >> 8) & 1u) * (uint32_t)(4 * kWarm));
+            else
+                offw = ((hi >> 9) & ~3u) + ((hi >> 8) & 1u) * (uint32_t)(4 * kWarm);
             a = cnt_s + (h ? offw : dslot); add[j] = h ? lo : 0u;                // ((kind&1)*kWarm + site)*4
         }
         red_add(a, 1u);                                                       // a5 Tier E
@@ -880,12 +884,14 @@ __device__ void runner_role(const ReplayParams& p, unsigned ri, int lane)
     unsigned long long my_sb = 0;
     if ((unsigned)lane < cnt) { my_nseg = __ldg(p.tr_nseg + my_t); my_base = __ldg(p.tr_base + my_t); my_sb = p.sbase[my_t]; }
     PROF_DECL
-    for (;;) {
+    unsigned nap = 64;                                    // polling back-off (ns): units are published every
+    for (;;) {                                            //   few us per CTA; the polls cost the stream issue slots
         const bool alive = (unsigned)lane < cnt && my_next < my_nseg;
         if (!__any_sync(kFull, alive)) break;
         const bool ready = alive && (ld_relaxed_u64(p.uagg + (size_t)(my_base + my_next) * 4 + 2) & 0xffffu) == (ep_tag & 0xffffu);
         unsigned rm = __ballot_sync(kFull, ready);
-        if (!rm) { PROF_MARK(0) __nanosleep(64); continue; }
+        if (!rm) { PROF_MARK(0) __nanosleep(nap); nap = min(nap * 2u, (unsigned)SCL_RUNNER_NAP); continue; }
+        nap = 64;
         fence_acquire();
         PROF_MARK(0)
         while (rm) {

@@ -48,6 +48,9 @@ constexpr int kCtaThreads = (kComputeWarps + 1 + kLBWarps) * 32;
 #ifndef SCL_WARM
 #define SCL_WARM 2048
 #endif
+#ifndef SCL_RUNNER_NAP
+#define SCL_RUNNER_NAP 1024
+#endif
 #ifndef SCL_BLOOM_LOG2
 #define SCL_BLOOM_LOG2 5
 #endif

@@ -46,6 +46,7 @@ class Config:
     seed: int = 0
     t_sweep: tuple = ()          # config 5: thresholds of the sweep
     copy_lambda: float = 0.0     # per-step probability of a copy event (NEXT-3 copy volume); 0: none
+    leak_T: int = 0              # planted leak sizes U[leak_T/4, leak_T]; 0: the config's T
 
     @property
     def n_events(self) -> int:
@@ -56,7 +57,7 @@ class Config:
 
     def ctype(self) -> _Cfg:
         return _Cfg(self.n_traces, self.n_sites, self.events_per_trace, self.zipf_s,
-                    self.n_planted, int(self.heavy_tailed), self.T, self.leak_lambda,
+                    self.n_planted, int(self.heavy_tailed), self.leak_T or self.T, self.leak_lambda,
                     self.leak_rate_spread, self.seed, self.copy_lambda)
 
 
@@ -72,7 +73,7 @@ CONFIGS = {
     2: Config("cfg2", 64, 1_000_000, 1_000, 0.8, 4, P_10MIB, 5.0e-5, seed=20221215 + 2),
     3: Config("cfg3", 1024, 1_000_000, 50_000, 1.0, 16, P_10MIB, 1.6e-4, 100.0, seed=20221215 + 3),
     4: Config("cfg4", 8192, 4_000_000, 200_000, 1.2, 32, P_10MIB, 1.0e-5, seed=20221215 + 4),
-    5: Config("cfg5", 256, 100_000_000, 10_000, 1.0, 8, 65537, 2.0e-6, heavy_tailed=True,
+    5: Config("cfg5", 256, 100_000_000, 10_000, 1.0, 8, 65537, 8.0e-6, heavy_tailed=True, leak_T=1 << 26,
               seed=20221215 + 5, t_sweep=SWEEP),
 }
 
