@@ -142,22 +142,49 @@ struct PState {
     unsigned blk, first_blk;                      // the scratch block being filled, the piece's first
 };
 
+// Per warp of pc_run: the current row's absolute F after each event, the max F before it, and the
+// event words, event-major ([j][lane]) so that a dynamic event index is one shared-memory load.
+struct RowStage {
+    long long F[kEpt][32], M[kEpt][32];
+    unsigned long long meta[kEpt][32], ptr[kEpt][32];
+};
+
+constexpr long long kI32Min = -2147483648ll, kI32Max = 2147483647ll;
+
+// Lane mask of the events j of a row whose F (as f[j] relative to the row start) leaves the band:
+// f >= hi or f <= lo.
+template <typename V>
+__device__ __forceinline__ unsigned band_exits(const V (&f)[kEpt], V hi, V lo)
+{
+    unsigned ex = 0;
+    #pragma unroll
+    for (int j = 0; j < kEpt; ++j) ex |= (f[j] >= hi || f[j] <= lo ? 1u : 0u) << j;
+    return ex;
+}
+
 // The samples of one unit inside a piece's window [wlo, whi) (unit positions).  Fu: F before the
-// unit's first event, Mu: max F before it.  As replay_kernel.cu resolve_unit (64-bit walk): the
-// chunks whose F range leaves (B - T, B + T) and meet the window are read (lane <-> row), one
-// combined scan gives every lane F and the running maximum before its row, and the lane holding the
-// first exit walks its events; events outside the window move F and M but take no sample.
+// unit's first event, Mu: max F before it.  The chunks whose F range leaves (B - T, B + T) and meet
+// the window are read (lane <-> row); one combined scan gives every lane F and the running maximum
+// before its row.  Then, per chunk:
+//   (1) the sample positions, in order: every lane tests its row's events against the band around
+//       B, the first lane with an exit holds the next sample, B becomes F there (the only state that
+//       crosses lanes; ~60 warp instructions per sample, the 32-bit compare when the rows allow);
+//   (2) the samples' records, lane-parallel: slot = an exclusive scan of the lanes' counts, the
+//       counter before each one = F at the sample before it (reading Q2), the new-maximum test
+//       against the max F before the event (Q3).
+// Events outside the window move F and M but take no sample.
 __device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, long long Mu, unsigned wlo, unsigned whi,
-                           PState& x, int lane)
+                           PState& x, int lane, RowStage& st)
 {
     const long long sPc = __ldcg(&S.Pc[lane]), sax = __ldcg(&S.ax[lane]), san = __ldcg(&S.an[lane]);
     const long long row_base = __ldcg(&S.info.row_base), off_t = __ldcg(&S.info.off_t), n_t = __ldcg(&S.info.n_t);
     const long long hiL = Fu + llmax(sax, sPc), loL = Fu + llmin(san, sPc);
+    const long long T = (long long)p.T;
     const unsigned cb = (unsigned)lane * 256u;
     const bool inwin = cb < whi && cb + 256u > wlo;
     int cnext = 0;
     for (;;) {
-        const unsigned ccm = __ballot_sync(kFull, lane >= cnext && inwin && (hiL >= x.B + p.T || loL <= x.B - p.T));
+        const unsigned ccm = __ballot_sync(kFull, lane >= cnext && inwin && (hiL >= x.B + T || loL <= x.B - T));
         if (!ccm) break;
         const int c = __ffs(ccm) - 1;
         const long long row = row_base + (long long)c * 32 + lane;
@@ -191,60 +218,109 @@ __device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, l
         const long long Fl = Fc + ssum - run;                                         // F before the lane's row
         long long Ml = shfl_up_ll(smax, 1);
         Ml = lane == 0 ? Mc : llmax(Mc, Ml == kNeg ? kNeg : Fc + Ml);                 // max F before it
-        int cur = 0;
-        for (;;) {
-            const unsigned cm = __ballot_sync(kFull, lane >= cur && live &&
-                                              (Fl + lmx >= x.B + p.T || Fl + lmn <= x.B - p.T));
-            if (!cm) break;
-            const int l0 = __ffs(cm) - 1;
-            if (lane == l0) {
-                unsigned from = 0;
-                for (;;) {
-                    unsigned ex = 0;
-                    #pragma unroll
-                    for (int jj = 0; jj < kEpt; ++jj) {
-                        const long long F = Fl + fe[jj];
-                        ex |= (F >= x.B + p.T || F <= x.B - p.T ? 1u : 0u) << jj;
-                    }
-                    ex &= live & ~((1u << from) - 1u);
-                    if (!ex) break;
-                    const int js = __ffs(ex) - 1;
-                    long long F = 0, Mp = Ml;
-                    unsigned long long ms = 0, ps = 0;
-                    #pragma unroll
-                    for (int jj = 0; jj < kEpt; ++jj) {
-                        if (jj < js) Mp = llmax(Mp, Fl + fe[jj]);
-                        if (jj == js) { F = Fl + fe[jj]; ms = rm[jj]; ps = rp[jj]; }
-                    }
-                    const long long net = F - x.B;                                    // the |A - F| counter
-                    const bool growth = net > 0;
-                    const bool nm = growth && F > Mp;                                  // new high-water mark (Q3)
-                    scl_sample smp;
-                    smp.idx = (unsigned long long)(e0 + js); smp.net = net; smp.footprint = F;
-                    smp.site = ev_site(ms); smp.kind = growth ? 0 : 1; smp.new_max = nm ? 1 : 0;
-                    smp.pad = nm && ev_size(ms) >= kBloomBig ? 1 : 0;                  // (pc_place: episode flag bit 1)
-                    if (x.n % kPBlock == 0) {                                          // a new scratch block
-                        const unsigned nb = atomicAdd(p.pctr, 1u);
-                        if (x.n == 0) x.first_blk = nb; else if (x.blk < p.pblocks) p.pnext[x.blk] = nb;
-                        x.blk = nb;
-                    }
-                    if (x.blk < p.pblocks) p.pscr[(size_t)x.blk * kPBlock + x.n % kPBlock] = smp;
-                    sample_counters(p, smp.site, growth, net, nm);
-                    if (nm) { ++x.nep; x.lep = x.n + 1; x.lep_ptr = ps; }
-                    if (x.n == 0) x.ffirst = F;
-                    ++x.n; x.B = F;                                                    // "resets the counters"
-                    from = (unsigned)js + 1;
-                }
+        // stage the row: F after each event, the max F before it, the event words
+        {
+            long long m = Ml;
+            #pragma unroll
+            for (int jj = 0; jj < kEpt; ++jj) {
+                const long long F = Fl + fe[jj];
+                st.F[jj][lane] = F; st.M[jj][lane] = m;
+                st.meta[jj][lane] = rm[jj]; st.ptr[jj][lane] = rp[jj];
+                m = llmax(m, F);
             }
-            x.B = shfl_ll(x.B, l0); x.n = __shfl_sync(kFull, x.n, l0); x.nep = __shfl_sync(kFull, x.nep, l0);
-            x.lep = __shfl_sync(kFull, x.lep, l0); x.lep_ptr = __shfl_sync(kFull, x.lep_ptr, l0);
-            x.ffirst = shfl_ll(x.ffirst, l0);
-            x.blk = __shfl_sync(kFull, x.blk, l0); x.first_blk = __shfl_sync(kFull, x.first_blk, l0);
-            cur = l0 + 1;
         }
+        __syncwarp();
+        // ---- (1) the sample positions, in order
+        unsigned smask = 0;
+        {
+            // every f[j] lies in [min(0, lmn), max(0, lmx)]: int32 compares are exact when that range
+            // is within +-2^30 and the band edges are clamped to the int32 range
+            const bool n32 = __all_sync(kFull, lmx <= (1ll << 30) && lmn >= -(1ll << 30));
+            int f32[kEpt];
+            #pragma unroll
+            for (int jj = 0; jj < kEpt; ++jj) f32[jj] = (int)fe[jj];
+            long long B = x.B;
+            int cl = 0;
+            unsigned cfrom = 0;
+            for (;;) {
+                const long long hi = B + T - Fl, lo = B - T - Fl;
+                unsigned ex;
+                if (n32) ex = band_exits(f32, (int)llmin(llmax(hi, kI32Min), kI32Max), (int)llmin(llmax(lo, kI32Min), kI32Max));
+                else ex = band_exits(fe, hi, lo);
+                ex &= live & (lane > cl ? ~0u : lane == cl ? ~0u << cfrom : 0u);
+                const unsigned m = __ballot_sync(kFull, ex != 0);
+                if (!m) break;
+                const int l0 = __ffs(m) - 1;
+                const int js = __shfl_sync(kFull, __ffs(ex) - 1, l0);
+                B = st.F[js][l0];                                                     // "resets the counters"
+                if (lane == l0) smask |= 1u << js;
+                cl = l0; cfrom = (unsigned)js + 1u;
+            }
+        }
+        // ---- (2) the samples' records, lane-parallel
+        const unsigned cnt = __popc(smask);
+        unsigned incl = cnt;
+        #pragma unroll
+        for (int d = 1; d < 32; d <<= 1) { const unsigned o = __shfl_up_sync(kFull, incl, d); if (lane >= d) incl += o; }
+        const unsigned tot = __shfl_sync(kFull, incl, 31);
+        if (tot) {
+            const unsigned long long n0 = x.n;
+            const unsigned long long have = (n0 + kPBlock - 1) / kPBlock, need = (n0 + tot + kPBlock - 1) / kPBlock;
+            unsigned nb0 = 0;
+            if (need > have) {                                       // new scratch blocks, contiguous and linked
+                if (lane == 0) {
+                    nb0 = atomicAdd(p.pctr, (unsigned)(need - have));
+                    if (n0 == 0) x.first_blk = nb0; else if (x.blk < p.pblocks) p.pnext[x.blk] = nb0;
+                    for (unsigned k = 1; k < (unsigned)(need - have); ++k)
+                        if (nb0 + k - 1 < p.pblocks) p.pnext[nb0 + k - 1] = nb0 + k;
+                }
+                nb0 = __shfl_sync(kFull, nb0, 0);
+                x.first_blk = __shfl_sync(kFull, x.first_blk, 0);
+            }
+            // the counter's origin before this lane's first sample: F at the last sample of an earlier
+            // lane, else the state entering the chunk
+            int last = smask ? lane : -1;
+            #pragma unroll
+            for (int d = 1; d < 32; d <<= 1) { const int o = __shfl_up_sync(kFull, last, d); if (lane >= d) last = max(last, o); }
+            int prev = __shfl_up_sync(kFull, last, 1);
+            if (lane == 0) prev = -1;
+            const long long myLastF = st.F[smask ? 31 - __clz(smask) : 0][lane];
+            const long long myFirstF = st.F[smask ? __ffs(smask) - 1 : 0][lane];
+            long long Bp = shfl_ll(myLastF, prev < 0 ? 0 : prev);
+            if (prev < 0) Bp = x.B;
+            unsigned long long n = n0 + incl - cnt;
+            unsigned long long nep = 0, lep = 0, lep_ptr = 0;
+            for (unsigned sm = smask; sm; sm &= sm - 1) {
+                const int j = __ffs(sm) - 1;
+                const long long F = st.F[j][lane], Mp = st.M[j][lane];
+                const unsigned long long ms = st.meta[j][lane];
+                const long long net = F - Bp;                                         // the |A - F| counter
+                const bool growth = net > 0;
+                const bool nm = growth && F > Mp;                                     // new high-water mark (Q3)
+                scl_sample smp;
+                smp.idx = (unsigned long long)(e0 + j); smp.net = net; smp.footprint = F;
+                smp.site = ev_site(ms); smp.kind = growth ? 0 : 1; smp.new_max = nm ? 1 : 0;
+                smp.pad = nm && ev_size(ms) >= kBloomBig ? 1 : 0;                     // (pc_place: episode flag bit 1)
+                const unsigned long long bi = n / kPBlock;
+                const unsigned blk = bi < have ? x.blk : nb0 + (unsigned)(bi - have);
+                if (blk < p.pblocks) p.pscr[(size_t)blk * kPBlock + n % kPBlock] = smp;
+                sample_counters(p, smp.site, growth, net, nm);
+                if (nm) { ++nep; lep = n + 1; lep_ptr = st.ptr[j][lane]; }
+                Bp = F; ++n;
+            }
+            x.nep += (unsigned long long)warp_sum((long long)nep);
+            const unsigned lm = __ballot_sync(kFull, lep != 0);
+            if (lm) { const int ll = 31 - __clz(lm); x.lep = __shfl_sync(kFull, lep, ll); x.lep_ptr = __shfl_sync(kFull, lep_ptr, ll); }
+            const unsigned sl = __ballot_sync(kFull, smask != 0);
+            if (n0 == 0) x.ffirst = shfl_ll(myFirstF, __ffs(sl) - 1);
+            x.B = shfl_ll(myLastF, 31 - __clz(sl));
+            const unsigned long long bl = (n0 + tot - 1) / kPBlock;
+            x.blk = bl < have ? x.blk : nb0 + (unsigned)(bl - have);
+            x.n = n0 + tot;
+        }
+        __syncwarp();                                                                 // (st is rewritten next chunk)
         cnext = c + 1;
     }
-    __syncwarp();
 }
 
 __global__ void __launch_bounds__(128) pc_run_kernel(const __grid_constant__ ReplayParams p)
@@ -253,6 +329,7 @@ __global__ void __launch_bounds__(128) pc_run_kernel(const __grid_constant__ Rep
     const unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
     const Slot* rec = reinterpret_cast<const Slot*>(p.urec);
     const unsigned npieces = p.n_traces + p.n_segs;
+    __shared__ RowStage stage[4];
     for (unsigned id = w; id < npieces; id += nw) {
         const bool tfirst = id < p.n_traces;
         unsigned t, u0, wlo0;
@@ -286,7 +363,7 @@ __global__ void __launch_bounds__(128) pc_run_kernel(const __grid_constant__ Rep
             }
             const long long umx = __ldcg(&S.umx), umn = __ldcg(&S.umn);
             if (us.F0 + umx >= x.B + p.T || us.F0 + umn <= x.B - p.T)    // the F range can leave the band
-                piece_unit(p, S, us.F0, us.M0, wlo, whi, x, lane);
+                piece_unit(p, S, us.F0, us.M0, wlo, whi, x, lane, stage[threadIdx.x >> 5]);
             if (whi == (unsigned)kUnit && lane == 0) p.ul[u].n_end = x.n;
             if (end_sync || u + 1 == uend) break;
         }

@@ -1,7 +1,7 @@
 """Randomised GPU-vs-oracle fuzzing (not part of the test suite: minutes of GPU time).  Each case keeps
 the previous case's re-threshold result (and so its handle) alive, which varies the allocation layout:
 that is how an unguarded read past the event buffer showed up (case 141 of seed 2).
-python tools/fuzz.py N_CASES SEED"""
+python tools/fuzz.py N_CASES SEED   (FUZZ_CHAIN=1/2: force the runners / the chain split)"""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
@@ -12,6 +12,7 @@ from parity import compare
 n_cases, seed = int(sys.argv[1]), int(sys.argv[2])
 rng = np.random.default_rng(seed)
 _keep = []
+chain = int(os.environ.get("FUZZ_CHAIN", "0"))
 t0 = time.time()
 for case in range(n_cases):
     n_traces = int(rng.integers(1, 40))
@@ -39,11 +40,11 @@ for case in range(n_cases):
         open("gpurun_out/fuzz_cur.txt", "w").write(desc + "\n")
     try:
         tr = scl.scl_trace_load(ev, off, n_sites)
-        r = scl.scl_replay_run(T, tr, tick_ns=1000, hwm_mode=hwm, formula=formula)
+        r = scl.scl_replay_run(T, tr, tick_ns=1000, hwm_mode=hwm, formula=formula, chain_mode=chain)
         compare(ev, off, n_sites, T, r, hwm_mode=hwm, formula=formula)
         T2 = int(rng.choice([3, 1031, 1048583]))
         if not os.environ.get("FUZZ_NO_RT"):
-            r2 = scl.scl_replay_rethreshold(T2, tr, r, tick_ns=1000, hwm_mode=hwm, formula=formula)
+            r2 = scl.scl_replay_rethreshold(T2, tr, r, tick_ns=1000, hwm_mode=hwm, formula=formula, chain_mode=chain)
             compare(ev, off, n_sites, T2, r2, hwm_mode=hwm, formula=formula)
             _keep.append(r2) if len(_keep) < 1 else (_keep.pop(), _keep.append(r2))
     except (AssertionError, scl.SclError) as e:
