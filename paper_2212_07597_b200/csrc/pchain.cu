@@ -26,6 +26,7 @@
 #include "scl_internal.cuh"
 #include "ptx.cuh"
 
+
 namespace scl {
 
 // ---------------------------------------------------------------------------- pc_prefix
@@ -146,8 +147,15 @@ struct PState {
 // event words, event-major ([j][lane]) so that a dynamic event index is one shared-memory load.
 struct RowStage {
     long long F[kEpt][32], M[kEpt][32];
-    unsigned long long meta[kEpt][32], ptr[kEpt][32];
+    unsigned long long meta[kEpt][32];
 };
+
+// Bits j of [a, b) within [0, kEpt).
+__device__ __forceinline__ unsigned bit_range(long long a, long long b)
+{
+    const unsigned aa = (unsigned)llmin(llmax(a, 0), kEpt), bb = (unsigned)llmin(llmax(b, 0), kEpt);
+    return bb > aa ? ((1u << bb) - 1u) & ~((1u << aa) - 1u) : 0u;
+}
 
 constexpr long long kI32Min = -2147483648ll, kI32Max = 2147483647ll;
 
@@ -188,27 +196,30 @@ __device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, l
         if (!ccm) break;
         const int c = __ffs(ccm) - 1;
         const long long row = row_base + (long long)c * 32 + lane;
-        unsigned long long rp[kEpt], rm[kEpt];
-        load_row_global(p.ev, row, rp, rm);
+        unsigned long long rm[kEpt];
+        load_row_meta(p.ev, row, rm);
         const long long Fc = Fu + shfl_ll(sPc, c);
         const long long Mc = llmax(Mu, warp_max(lane < c ? Fu + sax : kNeg));        // max F before chunk c
         const long long e0 = row * kEpt - off_t;                                     // trace index of the row
-        const unsigned q0 = (unsigned)c * 256u + (unsigned)lane * kEpt;              // unit position of the row
-        long long fe[kEpt], run = 0, lmx = kNeg, lmn = kPos;
-        unsigned live = 0;
-        #pragma unroll
+        const long long q0 = (long long)c * 256 + (long long)lane * kEpt;            // unit position of the row
+        // the row's events inside the trace and inside the window, as bit masks (bit j: event j)
+        const unsigned tm = bit_range(-e0, n_t - e0), wm = bit_range((long long)wlo - q0, (long long)whi - q0);
+        long long fe[kEpt], run = 0, lmx = kNeg;                 // F after event j relative to the row start;
+        unsigned live = 0, big = 0;                              //   its max (a non-alloc/free event repeats
+        #pragma unroll                                           //   the F before it, which changes no max)
         for (int jj = 0; jj < kEpt; ++jj) {
-            const long long ie = e0 + jj;
-            const unsigned kind = ev_kind(rm[jj]);
-            const bool af = ie >= 0 && ie < n_t && kind < 2;
+            const unsigned mh = (unsigned)(rm[jj] >> 32);
+            const unsigned kind = (mh >> 8) & 3u;
+            const bool af = ((tm >> jj) & 1u) && kind < 2;
             const long long sz = (long long)ev_size(rm[jj]);
-            run += af ? (kind == 0 ? sz : -sz) : 0;
+            const long long neg = kind == 1 ? -1ll : 0ll;
+            run += af ? (sz ^ neg) - neg : 0ll;
             fe[jj] = run;
-            if (af) {
-                lmx = llmax(lmx, run); lmn = llmin(lmn, run);
-                if (q0 + jj >= wlo && q0 + jj < whi) live |= 1u << jj;
-            }
+            lmx = llmax(lmx, run);
+            big |= (mh & 0xFFu) | ((unsigned)rm[jj] >> 27);      // a size >= 2^27
+            live |= (af ? 1u : 0u) << jj;
         }
+        live &= wm;
         long long ssum = run, smax = lmx;
         #pragma unroll
         for (int dd = 1; dd < 32; dd <<= 1) {
@@ -218,14 +229,13 @@ __device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, l
         const long long Fl = Fc + ssum - run;                                         // F before the lane's row
         long long Ml = shfl_up_ll(smax, 1);
         Ml = lane == 0 ? Mc : llmax(Mc, Ml == kNeg ? kNeg : Fc + Ml);                 // max F before it
-        // stage the row: F after each event, the max F before it, the event words
+        // stage the row: F after each event, the max F before it, the meta word
         {
             long long m = Ml;
             #pragma unroll
             for (int jj = 0; jj < kEpt; ++jj) {
                 const long long F = Fl + fe[jj];
-                st.F[jj][lane] = F; st.M[jj][lane] = m;
-                st.meta[jj][lane] = rm[jj]; st.ptr[jj][lane] = rp[jj];
+                st.F[jj][lane] = F; st.M[jj][lane] = m; st.meta[jj][lane] = rm[jj];
                 m = llmax(m, F);
             }
         }
@@ -233,9 +243,9 @@ __device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, l
         // ---- (1) the sample positions, in order
         unsigned smask = 0;
         {
-            // every f[j] lies in [min(0, lmn), max(0, lmx)]: int32 compares are exact when that range
-            // is within +-2^30 and the band edges are clamped to the int32 range
-            const bool n32 = __all_sync(kFull, lmx <= (1ll << 30) && lmn >= -(1ll << 30));
+            // with every size < 2^27, |f[j]| < 2^30: int32 compares are exact when the band edges are
+            // clamped to the int32 range
+            const bool n32 = __all_sync(kFull, big == 0);
             int f32[kEpt];
             #pragma unroll
             for (int jj = 0; jj < kEpt; ++jj) f32[jj] = (int)fe[jj];
@@ -305,7 +315,7 @@ __device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, l
                 const unsigned blk = bi < have ? x.blk : nb0 + (unsigned)(bi - have);
                 if (blk < p.pblocks) p.pscr[(size_t)blk * kPBlock + n % kPBlock] = smp;
                 sample_counters(p, smp.site, growth, net, nm);
-                if (nm) { ++nep; lep = n + 1; lep_ptr = st.ptr[j][lane]; }
+                if (nm) { ++nep; lep = n + 1; lep_ptr = __ldcg(&p.ev[row * kEpt + j].ptr); }
                 Bp = F; ++n;
             }
             x.nep += (unsigned long long)warp_sum((long long)nep);
@@ -323,7 +333,10 @@ __device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, l
     }
 }
 
-__global__ void __launch_bounds__(128) pc_run_kernel(const __grid_constant__ ReplayParams p)
+#ifndef SCL_PCRUN_MINB
+#define SCL_PCRUN_MINB 1
+#endif
+__global__ void __launch_bounds__(128, SCL_PCRUN_MINB) pc_run_kernel(const __grid_constant__ ReplayParams p)
 {
     const int lane = threadIdx.x & 31;
     const unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;

@@ -951,9 +951,27 @@ __device__ __forceinline__ void reclaimed(const ReplayParams& p, unsigned long l
 
 struct UnitCtx { long long row_base, off_t, n_t; unsigned long long ep1, eptr, s_in, s_out; };
 
-__device__ void reclaim_unit(const ReplayParams& p, unsigned u, const UnitCtx& x, int lane)
+constexpr int kBloomRow = kBloomWords + 1;                  // staged filter row, padded: word w of the
+constexpr size_t kPostBloom = 8 * 32 * kBloomRow * 4;       //   32 chunks in 32 banks; 8 warps per block
+
+// sb: the warp's shared-memory slice for the unit's 32 chunk filters.
+__device__ void reclaim_unit(const ReplayParams& p, unsigned u, const UnitCtx& x, int lane, unsigned* sb)
 {
     const Slot& S = reinterpret_cast<const Slot*>(p.urec)[u];
+    const bool staged = x.s_out >= x.s_in + 8;               // many segments: stage the filters (few
+    if (staged) {                                            //   segments: one word per chunk, from L2)
+        // lane = chunk: its filter, one 128-B row
+        const uint4* src = reinterpret_cast<const uint4*>(&S.bloom[lane][0]);
+        uint4 v[kBloomWords / 4];
+        #pragma unroll
+        for (int k = 0; k < kBloomWords / 4; ++k) v[k] = __ldcg(src + k);
+        #pragma unroll
+        for (int k = 0; k < kBloomWords / 4; ++k) {
+            unsigned* d = sb + lane * kBloomRow + 4 * k;
+            d[0] = v[k].x; d[1] = v[k].y; d[2] = v[k].z; d[3] = v[k].w;
+        }
+        __syncwarp();
+    }
     const long long row_base = x.row_base, off_t = x.off_t, n_t = x.n_t;
     const long long g0 = row_base * kEpt;                    // global event index of unit position 0
     unsigned long long ep1 = x.ep1, ptr = x.eptr;            // current segment: episode (slot + 1), pointer, start
@@ -965,7 +983,8 @@ __device__ void reclaim_unit(const ReplayParams& p, unsigned u, const UnitCtx& x
         if (!ep1 || send <= sbeg) return;
         const unsigned w = bloom_word(ptr, big), msk = bloom_mask(ptr);
         const unsigned cb = (unsigned)lane * 32 * kEpt;
-        const bool pos = cb < send && cb + 32 * kEpt > sbeg && (S.bloom[lane][w] & msk) == msk;
+        const unsigned bw = staged ? sb[lane * kBloomRow + w] : __ldcg(&S.bloom[lane][w]);
+        const bool pos = cb < send && cb + 32 * kEpt > sbeg && (bw & msk) == msk;
         const unsigned cm = __ballot_sync(kFull, pos);
         if (!cm) return;
 #ifdef SCL_POST_INLINE
@@ -1003,6 +1022,8 @@ __device__ void reclaim_unit(const ReplayParams& p, unsigned u, const UnitCtx& x
         bool nm = false; long long idx = 0; unsigned st = 0;
         SCL_CHECK(x.s_out <= p.sample_cap);
         if (si < x.s_out) { const scl_sample smp = p.samples[si]; nm = smp.new_max != 0; idx = (long long)smp.idx; st = smp.site; }
+        ulonglong2 evl = make_ulonglong2(0, 0);              // every episode's tracked object, loaded at once
+        if (nm) evl = __ldcg(reinterpret_cast<const ulonglong2*>(p.ev + off_t + idx));
         unsigned em = __ballot_sync(kFull, nm);
         while (em) {
             const int e = __ffs(em) - 1;
@@ -1011,10 +1032,8 @@ __device__ void reclaim_unit(const ReplayParams& p, unsigned u, const UnitCtx& x
             const unsigned pos = (unsigned)(off_t + ie - g0);
             segment(pos);
             ep1 = s0 + (unsigned long long)e + 1;
-            {
-                const ulonglong2 evt = __ldcg(reinterpret_cast<const ulonglong2*>(p.ev + off_t + ie));
-                ptr = evt.x; big = ev_size(evt.y) >= kBloomBig;
-            }
+            ptr = __shfl_sync(kFull, evl.x, e);
+            big = ev_size(__shfl_sync(kFull, evl.y, e)) >= kBloomBig;
             site = __shfl_sync(kFull, st, e);
             sbeg = pos;
         }
@@ -1063,7 +1082,8 @@ __global__ void __launch_bounds__(256, 3) post_kernel(const __grid_constant__ Re
             x.row_base = shfl_ll(c.row_base, i); x.off_t = shfl_ll(c.off_t, i); x.n_t = shfl_ll(c.n_t, i);
             x.ep1 = __shfl_sync(kFull, c.ep1, i); x.eptr = __shfl_sync(kFull, c.eptr, i);
             x.s_in = __shfl_sync(kFull, c.s_in, i); x.s_out = __shfl_sync(kFull, c.s_out, i);
-            reclaim_unit(p, wid + (k0 + (unsigned)i) * nw, x, lane);
+            reclaim_unit(p, wid + (k0 + (unsigned)i) * nw, x, lane,
+                         reinterpret_cast<unsigned*>(post_smem) + (threadIdx.x >> 5) * 32 * kBloomRow);
         }
     }
     if (p.tierE && !p.rechain) {                        // Tier E of this stream pass, kept for re-thresholds
@@ -1111,13 +1131,14 @@ __global__ void __launch_bounds__(256, 3) post_kernel(const __grid_constant__ Re
     POST_T(5, atomicMax)
 }
 
-constexpr size_t kPostStage = std::max<size_t>(8 * 32 * kRowWords * 8,      // a6 row staging: 8 warps x 32 rows,
-                                               report_smem_bytes<256>());     // or report_block in the last block
+constexpr size_t kPostStage = std::max<size_t>(std::max<size_t>(8 * 32 * kRowWords * 8,   // a6 row staging: 8 warps x 32
+                                                                report_smem_bytes<256>()),  // rows, or report_block in the
+                                               kPostBloom);                                 // last block; phase A's filters
 
 cudaError_t launch_post(const ReplayParams& p, cudaStream_t st)
 {
     static int occ = 0, nsm = 0;
-    const size_t smem = p.fuse_report ? kPostStage : 0;
+    const size_t smem = p.fuse_report ? kPostStage : kPostBloom;
     static int occ_fused = 0;
     if (!occ) {
         int dev = 0;
@@ -1126,7 +1147,7 @@ cudaError_t launch_post(const ReplayParams& p, cudaStream_t st)
         cudaError_t e = cudaFuncSetAttribute(post_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)kPostStage);
         if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, post_kernel, 256, 0);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, post_kernel, 256, kPostBloom);
         if (e != cudaSuccess) return e;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_fused, post_kernel, 256, kPostStage);
         if (e != cudaSuccess) return e;

@@ -243,6 +243,12 @@ __device__ __forceinline__ void load_row_global(const scl_event* ev, long long r
     for (int j = 0; j < kEpt; ++j) { ulonglong2 v = __ldcg(q + j); ptr[j] = v.x; meta[j] = v.y; }
 }
 
+__device__ __forceinline__ void load_row_meta(const scl_event* ev, long long row, unsigned long long* meta) {
+    const scl_event* q = ev + row * kEpt;
+    #pragma unroll
+    for (int j = 0; j < kEpt; ++j) meta[j] = __ldcg(&q[j].meta);
+}
+
 // Tier S of one sample (a5: n_growth / growth_bytes or n_decline / decline_bytes of the
 // sample's site -- a decline at the free's site, reading Q14) and, at an episode start, the site's
 // leak mallocs (the frees are counted by the reclaim pass).  Fire-and-forget L2 reductions
