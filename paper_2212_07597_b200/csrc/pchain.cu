@@ -143,10 +143,10 @@ struct PState {
     unsigned blk, first_blk;                      // the scratch block being filled, the piece's first
 };
 
-// Per warp of pc_run: the current row's absolute F after each event, the max F before it, and the
-// event words, event-major ([j][lane]) so that a dynamic event index is one shared-memory load.
+// Per warp of pc_run: the current row's absolute F after each event, the max F before it relative
+// to the row start, and the meta words, event-major ([j][lane]) so that a dynamic event index is one shared-memory load.
 struct RowStage {
-    long long F[kEpt][32], M[kEpt][32];
+    long long F[kEpt][32], P[kEpt][32];
     unsigned long long meta[kEpt][32];
 };
 
@@ -204,9 +204,9 @@ __device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, l
         const long long q0 = (long long)c * 256 + (long long)lane * kEpt;            // unit position of the row
         // the row's events inside the trace and inside the window, as bit masks (bit j: event j)
         const unsigned tm = bit_range(-e0, n_t - e0), wm = bit_range((long long)wlo - q0, (long long)whi - q0);
-        long long fe[kEpt], run = 0, lmx = kNeg;                 // F after event j relative to the row start;
-        unsigned live = 0, big = 0;                              //   its max (a non-alloc/free event repeats
-        #pragma unroll                                           //   the F before it, which changes no max)
+        long long fe[kEpt], run = 0;                             // F after event j relative to the row start
+        unsigned live = 0, big = 0;
+        #pragma unroll
         for (int jj = 0; jj < kEpt; ++jj) {
             const unsigned mh = (unsigned)(rm[jj] >> 32);
             const unsigned kind = (mh >> 8) & 3u;
@@ -215,11 +215,27 @@ __device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, l
             const long long neg = kind == 1 ? -1ll : 0ll;
             run += af ? (sz ^ neg) - neg : 0ll;
             fe[jj] = run;
-            lmx = llmax(lmx, run);
             big |= (mh & 0xFFu) | ((unsigned)rm[jj] >> 27);      // a size >= 2^27
             live |= (af ? 1u : 0u) << jj;
         }
         live &= wm;
+        // with every size < 2^27, |fe| < 2^30: int32 maxima and band compares (the band edges clamped to
+        // the int32 range) are exact
+        const bool n32 = __all_sync(kFull, big == 0);
+        // the max of fe before each event, from 0 (the F before the row, which is <= the max F before
+        // it; a non-alloc/free event repeats the F before it: neither changes a maximum) -> st.P
+        long long lmx;
+        if (n32) {
+            int m = 0;
+            #pragma unroll
+            for (int jj = 0; jj < kEpt; ++jj) { st.P[jj][lane] = m; m = max(m, (int)fe[jj]); }
+            lmx = m;
+        } else {
+            long long m = 0;
+            #pragma unroll
+            for (int jj = 0; jj < kEpt; ++jj) { st.P[jj][lane] = m; m = llmax(m, fe[jj]); }
+            lmx = m;
+        }
         long long ssum = run, smax = lmx;
         #pragma unroll
         for (int dd = 1; dd < 32; dd <<= 1) {
@@ -228,24 +244,14 @@ __device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, l
         }
         const long long Fl = Fc + ssum - run;                                         // F before the lane's row
         long long Ml = shfl_up_ll(smax, 1);
-        Ml = lane == 0 ? Mc : llmax(Mc, Ml == kNeg ? kNeg : Fc + Ml);                 // max F before it
-        // stage the row: F after each event, the max F before it, the meta word
-        {
-            long long m = Ml;
-            #pragma unroll
-            for (int jj = 0; jj < kEpt; ++jj) {
-                const long long F = Fl + fe[jj];
-                st.F[jj][lane] = F; st.M[jj][lane] = m; st.meta[jj][lane] = rm[jj];
-                m = llmax(m, F);
-            }
-        }
+        Ml = lane == 0 ? Mc : llmax(Mc, Fc + Ml);                                     // max F before it
+        // stage the row: F after each event, the meta word
+        #pragma unroll
+        for (int jj = 0; jj < kEpt; ++jj) { st.F[jj][lane] = Fl + fe[jj]; st.meta[jj][lane] = rm[jj]; }
         __syncwarp();
         // ---- (1) the sample positions, in order
         unsigned smask = 0;
         {
-            // with every size < 2^27, |f[j]| < 2^30: int32 compares are exact when the band edges are
-            // clamped to the int32 range
-            const bool n32 = __all_sync(kFull, big == 0);
             int f32[kEpt];
             #pragma unroll
             for (int jj = 0; jj < kEpt; ++jj) f32[jj] = (int)fe[jj];
@@ -302,7 +308,7 @@ __device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, l
             unsigned long long nep = 0, lep = 0, lep_ptr = 0;
             for (unsigned sm = smask; sm; sm &= sm - 1) {
                 const int j = __ffs(sm) - 1;
-                const long long F = st.F[j][lane], Mp = st.M[j][lane];
+                const long long F = st.F[j][lane], Mp = llmax(Ml, Fl + st.P[j][lane]);   // max F before it
                 const unsigned long long ms = st.meta[j][lane];
                 const long long net = F - Bp;                                         // the |A - F| counter
                 const bool growth = net > 0;
