@@ -190,6 +190,9 @@ __device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, l
     const long long T = (long long)p.T;
     const unsigned cb = (unsigned)lane * 256u;
     const bool inwin = cb < whi && cb + 256u > wlo;
+    long long cmx = Fu + sax;                                // max F through each chunk (inclusive scan)
+    #pragma unroll
+    for (int d = 1; d < 32; d <<= 1) { const long long o = shfl_up_ll(cmx, d); if (lane >= d) cmx = llmax(cmx, o); }
     int cnext = 0;
     for (;;) {
         const unsigned ccm = __ballot_sync(kFull, lane >= cnext && inwin && (hiL >= x.B + T || loL <= x.B - T));
@@ -199,7 +202,8 @@ __device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, l
         unsigned long long rm[kEpt];
         load_row_meta(p.ev, row, rm);
         const long long Fc = Fu + shfl_ll(sPc, c);
-        const long long Mc = llmax(Mu, warp_max(lane < c ? Fu + sax : kNeg));        // max F before chunk c
+        const long long cm1 = shfl_ll(cmx, c > 0 ? c - 1 : 0);
+        const long long Mc = c > 0 ? llmax(Mu, cm1) : Mu;                             // max F before chunk c
         const long long e0 = row * kEpt - off_t;                                     // trace index of the row
         const long long q0 = (long long)c * 256 + (long long)lane * kEpt;            // unit position of the row
         // the row's events inside the trace and inside the window, as bit masks (bit j: event j)
@@ -215,12 +219,12 @@ __device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, l
             const long long neg = kind == 1 ? -1ll : 0ll;
             run += af ? (sz ^ neg) - neg : 0ll;
             fe[jj] = run;
-            big |= (mh & 0xFFu) | ((unsigned)rm[jj] >> 27);      // a size >= 2^27
+            big |= (mh & 0xFFu) | ((unsigned)rm[jj] >> 22);      // a size >= 2^22
             live |= (af ? 1u : 0u) << jj;
         }
         live &= wm;
-        // with every size < 2^27, |fe| < 2^30: int32 maxima and band compares (the band edges clamped to
-        // the int32 range) are exact
+        // with every size of the chunk < 2^22, |fe| < 2^25 and the chunk's prefix sums < 2^30: int32 sums,
+        // maxima and band compares (the band edges clamped to the int32 range) are exact
         const bool n32 = __all_sync(kFull, big == 0);
         // the max of fe before each event, from 0 (the F before the row, which is <= the max F before
         // it; a non-alloc/free event repeats the F before it: neither changes a maximum) -> st.P
@@ -236,15 +240,26 @@ __device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, l
             for (int jj = 0; jj < kEpt; ++jj) { st.P[jj][lane] = m; m = llmax(m, fe[jj]); }
             lmx = m;
         }
-        long long ssum = run, smax = lmx;
-        #pragma unroll
-        for (int dd = 1; dd < 32; dd <<= 1) {
-            const long long os = shfl_up_ll(ssum, dd), om = shfl_up_ll(smax, dd);
-            if (lane >= dd) { smax = llmax(om, os + smax); ssum = os + ssum; }
+        long long ssum, smax;                                    // combined scan of the rows: (sum, max prefix)
+        if (n32) {
+            int s32 = (int)run, m32 = (int)lmx;
+            #pragma unroll
+            for (int dd = 1; dd < 32; dd <<= 1) {
+                const int os = __shfl_up_sync(kFull, s32, dd), om = __shfl_up_sync(kFull, m32, dd);
+                if (lane >= dd) { m32 = max(om, os + m32); s32 = os + s32; }
+            }
+            ssum = s32; smax = __shfl_up_sync(kFull, m32, 1);
+        } else {
+            ssum = run; smax = lmx;
+            #pragma unroll
+            for (int dd = 1; dd < 32; dd <<= 1) {
+                const long long os = shfl_up_ll(ssum, dd), om = shfl_up_ll(smax, dd);
+                if (lane >= dd) { smax = llmax(om, os + smax); ssum = os + ssum; }
+            }
+            smax = shfl_up_ll(smax, 1);
         }
         const long long Fl = Fc + ssum - run;                                         // F before the lane's row
-        long long Ml = shfl_up_ll(smax, 1);
-        Ml = lane == 0 ? Mc : llmax(Mc, Fc + Ml);                                     // max F before it
+        const long long Ml = lane == 0 ? Mc : llmax(Mc, Fc + smax);                   // max F before it
         // stage the row: F after each event, the meta word
         #pragma unroll
         for (int jj = 0; jj < kEpt; ++jj) { st.F[jj][lane] = Fl + fe[jj]; st.meta[jj][lane] = rm[jj]; }
