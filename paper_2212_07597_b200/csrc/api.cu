@@ -717,7 +717,7 @@ static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const sc
         const size_t nb = (size_t)(tot + kPBlock - 1) / kPBlock + np + 1;
         if (nb > tr->cap_pblocks) {
             cudaFree(tr->d_pscr); cudaFree(tr->d_pnext); tr->d_pscr = nullptr; tr->d_pnext = nullptr; tr->cap_pblocks = 0;
-            if (!tr->d_pctr && cudaMalloc(&tr->d_pctr, 4) != cudaSuccess) { cudaGetLastError(); tr->d_pctr = nullptr; }
+            if (!tr->d_pctr && cudaMalloc(&tr->d_pctr, 8) != cudaSuccess) { cudaGetLastError(); tr->d_pctr = nullptr; }
             if (!tr->d_pctr || cudaMalloc(&tr->d_pscr, nb * kPBlock * sizeof(scl_sample)) != cudaSuccess ||
                 cudaMalloc(&tr->d_pnext, nb * 4) != cudaSuccess)
                 { cudaGetLastError(); if (fresh) scl_result_free(r); return fail(SCL_ENOMEM, "chain piece samples"); }

@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(128) pc_prefix_kernel(const __grid_constant__ 
     const int lane = threadIdx.x & 31;
     const unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
     const Slot* rec = reinterpret_cast<const Slot*>(p.urec);
-    if (blockIdx.x == 0 && threadIdx.x == 0) *p.pctr = 0;    // scratch blocks of this run's pieces (pc_run)
+    if (blockIdx.x == 0 && threadIdx.x < 2) p.pctr[threadIdx.x] = 0;   // pc_run's scratch blocks and pieces
     for (unsigned t = w; t < p.n_traces; t += nw) {
         const unsigned base = __ldg(p.tr_base + t), nseg = __ldg(p.tr_nseg + t);
         long long F = 0, M = 0;                              // F before the next unit; max F so far (M_-1 = 0)
@@ -360,11 +360,15 @@ __device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, l
 __global__ void __launch_bounds__(128, SCL_PCRUN_MINB) pc_run_kernel(const __grid_constant__ ReplayParams p)
 {
     const int lane = threadIdx.x & 31;
-    const unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
     const Slot* rec = reinterpret_cast<const Slot*>(p.urec);
     const unsigned npieces = p.n_traces + p.n_segs;
     __shared__ RowStage stage[4];
-    for (unsigned id = w; id < npieces; id += nw) {
+    // pieces are taken one at a time from a counter (their lengths vary; a resident grid)
+    for (;;) {
+        unsigned id = 0;
+        if (lane == 0) id = atomicAdd(p.pctr + 1, 1u);
+        id = __shfl_sync(kFull, id, 0);
+        if (id >= npieces) break;
         const bool tfirst = id < p.n_traces;
         unsigned t, u0, wlo0;
         long long B0;
@@ -536,7 +540,16 @@ cudaError_t launch_pchain(const ReplayParams& p, cudaStream_t st)
     auto grid = [](unsigned warps) { return std::max(1u, std::min((warps + 3) / 4, 148u * 16)); };
     pc_prefix_kernel<<<grid(p.n_traces), 128, 0, st>>>(p);
     pc_sync_kernel<<<grid(p.n_segs), 128, 0, st>>>(p);
-    pc_run_kernel<<<grid(p.n_traces + p.n_segs), 128, 0, st>>>(p);
+    static int run_blocks = 0;                               // resident pc_run blocks (it takes pieces from a counter)
+    if (!run_blocks) {
+        int dev = 0, nsm = 0, occ = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pc_run_kernel, 128, 0);
+        if (e != cudaSuccess) return e;
+        run_blocks = std::max(1, occ) * nsm;
+    }
+    pc_run_kernel<<<std::min(grid(p.n_traces + p.n_segs), (unsigned)run_blocks), 128, 0, st>>>(p);
     pc_combine_kernel<<<grid(p.n_traces), 128, 0, st>>>(p);
     pc_place_kernel<<<grid(p.n_traces + p.n_segs), 128, 0, st>>>(p);
     return cudaGetLastError();

@@ -202,7 +202,7 @@ struct ReplayParams {
     struct UnitLocal* ul;             // [n_segs] piece-local sample counts / episode at each unit's ends
     scl_sample* pscr;                 // [pblocks * kPBlock] samples as the pieces found them (blocks)
     unsigned* pnext;                  // [pblocks] next block of the same piece
-    unsigned* pctr;                   // [1] blocks taken (zeroed by pc_prefix)
+    unsigned* pctr;                   // [2] scratch blocks taken, pieces taken (zeroed by pc_prefix)
     unsigned pblocks;
 };
 
