@@ -756,14 +756,14 @@ static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const sc
                                  cudaMemcpyDeviceToDevice, st));
         p.rechain = 1;
         p.n_runners = std::min<unsigned>(NT, (unsigned)r->grid * 8);
-        if (split) { CU(launch_pchain(p, st)); r->nlaunch += 5; }
+        if (split) { CU(launch_pchain(p, st)); r->nlaunch += 4; }
         else { CU(launch_rechain(p, st)); r->nlaunch += tr->n_segs ? 1 : 0; }
     } else {
         CU(launch_replay(&tr->tmap, p, r->grid, st));
         if (tm) CU(cudaEventRecord(r->kev[3 * ks + 1], st));
         CU(launch_cold_hist(p, st));           // Tier E of the sites beyond the shared-memory table
         r->nlaunch += (tr->n_segs ? 1 : 0) + cold_hist_launches(p);
-        if (split) { CU(launch_pchain(p, st)); r->nlaunch += 5; }
+        if (split) { CU(launch_pchain(p, st)); r->nlaunch += 4; }
     }
     if (tm) {
         if (base) CU(cudaEventRecord(r->kev[3 * ks + 1], st));   // (no replay kernel: the re-chain)

@@ -9,10 +9,11 @@
 // maximum M (so the new-maximum test F_i > M_(i-1) of PREFIX mode, reading Q3), the sample count and
 // the last episode start.  So each trace splits into independent PIECES: one from the trace start,
 // and one after the first sync event of every unit that has one, each ending at the first sync event
-// of a later unit (included) or at the trace end.  Five stream-ordered launches:
-//   pc_prefix   warp per trace: F at every unit start and the max F before it (unit aggregates);
-//   pc_sync     warp per unit: its first sync event (chunks whose F range spans >= 2T - 1 are read),
-//               F and max F through it;
+// of a later unit (included) or at the trace end.  Four stream-ordered launches:
+//   pc_scan     = pc_prefix (warp per trace: F at every unit start and the max F before it, from the
+//               unit aggregates) and, in the other blocks of the same launch, pc_sync (warp per unit:
+//               its first sync event -- chunks whose F range spans >= 2T - 1 are read -- and F through
+//               it relative to the unit start);
 //   pc_run      warp per piece: the exact chain over the piece; its samples go to scratch blocks in
 //               the order found (their slots are not known yet), Tier S (a5) to the site table, and
 //               the piece-local sample count and last episode start at each unit's ends;
@@ -30,12 +31,13 @@
 namespace scl {
 
 // ---------------------------------------------------------------------------- pc_prefix
-__global__ void __launch_bounds__(128) pc_prefix_kernel(const __grid_constant__ ReplayParams p)
+// (blocks [0, nb) of the pc_scan launch)
+__device__ void pc_prefix(const ReplayParams& p, unsigned blk, unsigned nb)
 {
     const int lane = threadIdx.x & 31;
-    const unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const unsigned w = (blk * blockDim.x + threadIdx.x) >> 5, nw = (nb * blockDim.x) >> 5;
     const Slot* rec = reinterpret_cast<const Slot*>(p.urec);
-    if (blockIdx.x == 0 && threadIdx.x < 2) p.pctr[threadIdx.x] = 0;   // pc_run's scratch blocks and pieces
+    if (blk == 0 && threadIdx.x < 2) p.pctr[threadIdx.x] = 0;            // pc_run's scratch blocks and pieces
     for (unsigned t = w; t < p.n_traces; t += nw) {
         const unsigned base = __ldg(p.tr_base + t), nseg = __ldg(p.tr_nseg + t);
         long long F = 0, M = 0;                              // F before the next unit; max F so far (M_-1 = 0)
@@ -61,30 +63,31 @@ __global__ void __launch_bounds__(128) pc_prefix_kernel(const __grid_constant__ 
 }
 
 // ---------------------------------------------------------------------------- pc_sync
-// The unit's first event with |d| >= 2T - 1 (kind alloc / free, inside its trace).  A chunk can hold
-// one only if its F range, chunk start included, spans at least 2T - 1.
-__global__ void __launch_bounds__(128) pc_sync_kernel(const __grid_constant__ ReplayParams p)
+// The unit's first event with |d| >= 2T - 1 (kind alloc / free, inside its trace) and F there,
+// relative to the unit start (pc_run adds the unit's F0: this pass does not wait for pc_prefix).  A
+// chunk can hold one only if its F range, chunk start included, spans at least 2T - 1.
+// (blocks [nb0, gridDim.x) of the pc_scan launch)
+__device__ void pc_sync(const ReplayParams& p, unsigned blk, unsigned nb)
 {
     const int lane = threadIdx.x & 31;
-    const unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const unsigned w = (blk * blockDim.x + threadIdx.x) >> 5, nw = (nb * blockDim.x) >> 5;
     const Slot* rec = reinterpret_cast<const Slot*>(p.urec);
     const unsigned long long thr = 2ull * (unsigned long long)p.T - 1ull;
     for (unsigned u = w; u < p.n_segs; u += nw) {
         const Slot& S = rec[u];
         const long long sPc = __ldcg(&S.Pc[lane]), sax = __ldcg(&S.ax[lane]), san = __ldcg(&S.an[lane]);
         const long long row_base = __ldcg(&S.info.row_base), off_t = __ldcg(&S.info.off_t), n_t = __ldcg(&S.info.n_t);
-        const UnitStart us = p.ust[u];
         const long long span = llmax(sax, sPc) - llmin(san, sPc);
         unsigned cand = __ballot_sync(kFull, span >= (long long)thr);
-        SyncInfo out; out.pos = -1; out.pad0 = 0; out.Fs = 0; out.Ms = 0; out.pad1 = 0;
+        SyncInfo out; out.pos = -1; out.pad0 = 0; out.Fs = 0; out.pad1 = 0; out.pad2 = 0;
         while (cand) {
             const int c = __ffs(cand) - 1;
             cand &= cand - 1;
             const long long row = row_base + (long long)c * 32 + lane;
-            unsigned long long rp[kEpt], rm[kEpt];
-            load_row_global(p.ev, row, rp, rm);
+            unsigned long long rm[kEpt];
+            load_row_meta(p.ev, row, rm);
             const long long e0 = row * kEpt - off_t;
-            long long run = 0, lmx = kNeg;
+            long long run = 0;
             unsigned sy = 0;
             #pragma unroll
             for (int j = 0; j < kEpt; ++j) {
@@ -93,27 +96,19 @@ __global__ void __launch_bounds__(128) pc_sync_kernel(const __grid_constant__ Re
                 const bool af = ie >= 0 && ie < n_t && kind < 2;
                 const unsigned long long sz = ev_size(rm[j]);
                 run += af ? (kind == 0 ? (long long)sz : -(long long)sz) : 0;
-                if (af) lmx = llmax(lmx, run);
                 sy |= (af && sz >= thr ? 1u : 0u) << j;
             }
             const unsigned lm = __ballot_sync(kFull, sy != 0);
             if (!lm) continue;
             const int l0 = __ffs(lm) - 1;
-            // F and max F before lane l0's row: combined scan of the rows (sum, max prefix)
-            long long ssum = run, smax = lmx;
+            // F before lane l0's row, relative to the unit start: scan of the row sums
+            long long ssum = run;
             #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const long long os = shfl_up_ll(ssum, d), om = shfl_up_ll(smax, d);
-                if (lane >= d) { smax = llmax(om, os + smax); ssum = os + ssum; }
-            }
-            const long long Fc = us.F0 + shfl_ll(sPc, c);
-            const long long Mc = llmax(us.M0, warp_max(lane < c ? us.F0 + sax : kNeg));   // max F before chunk c
-            const long long Fl = Fc + ssum - run;
-            long long Ml = shfl_up_ll(smax, 1);
-            Ml = lane == 0 ? Mc : llmax(Mc, Ml == kNeg ? kNeg : Fc + Ml);
+            for (int d = 1; d < 32; d <<= 1) { const long long os = shfl_up_ll(ssum, d); if (lane >= d) ssum += os; }
+            const long long Fl = shfl_ll(sPc, c) + ssum - run;
             if (lane == l0) {
                 const int j0 = __ffs(sy) - 1;
-                long long F = Fl, M = Ml;
+                long long F = Fl;
                 #pragma unroll
                 for (int j = 0; j < kEpt; ++j) {
                     if (j <= j0) {
@@ -122,17 +117,22 @@ __global__ void __launch_bounds__(128) pc_sync_kernel(const __grid_constant__ Re
                         if (ie >= 0 && ie < n_t && kind < 2) {
                             const long long sz = (long long)ev_size(rm[j]);
                             F += kind == 0 ? sz : -sz;
-                            M = llmax(M, F);
                         }
                     }
                 }
-                out.pos = c * 256 + l0 * kEpt + j0; out.Fs = F; out.Ms = M;
+                out.pos = c * 256 + l0 * kEpt + j0; out.Fs = F;
             }
-            out.pos = __shfl_sync(kFull, out.pos, l0); out.Fs = shfl_ll(out.Fs, l0); out.Ms = shfl_ll(out.Ms, l0);
+            out.pos = __shfl_sync(kFull, out.pos, l0); out.Fs = shfl_ll(out.Fs, l0);
             break;
         }
         if (lane == 0) p.sync[u] = out;
     }
+}
+
+__global__ void __launch_bounds__(128) pc_scan_kernel(const __grid_constant__ ReplayParams p, unsigned nbp)
+{
+    if (blockIdx.x < nbp) pc_prefix(p, blockIdx.x, nbp);
+    else pc_sync(p, blockIdx.x - nbp, gridDim.x - nbp);
 }
 
 // ---------------------------------------------------------------------------- pc_run
@@ -205,9 +205,11 @@ __device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, l
         const long long cm1 = shfl_ll(cmx, c > 0 ? c - 1 : 0);
         const long long Mc = c > 0 ? llmax(Mu, cm1) : Mu;                             // max F before chunk c
         const long long e0 = row * kEpt - off_t;                                     // trace index of the row
-        const long long q0 = (long long)c * 256 + (long long)lane * kEpt;            // unit position of the row
+        const unsigned q0 = (unsigned)c * 256u + (unsigned)lane * kEpt;              // unit position of the row
         // the row's events inside the trace and inside the window, as bit masks (bit j: event j)
-        const unsigned tm = bit_range(-e0, n_t - e0), wm = bit_range((long long)wlo - q0, (long long)whi - q0);
+        const unsigned tm = e0 >= 0 && e0 + kEpt <= n_t ? 0xFFu : bit_range(-e0, n_t - e0);
+        const unsigned wm = q0 >= wlo && q0 + kEpt <= whi ? 0xFFu
+                          : bit_range((long long)wlo - (long long)q0, (long long)whi - (long long)q0);
         long long fe[kEpt], run = 0;                             // F after event j relative to the row start
         unsigned live = 0, big = 0;
         #pragma unroll
@@ -380,31 +382,53 @@ __global__ void __launch_bounds__(128, SCL_PCRUN_MINB) pc_run_kernel(const __gri
             u0 = id - p.n_traces;
             const SyncInfo sy = p.sync[u0];
             if (sy.pos < 0) { if (lane == 0) p.pc[id].active = 0; continue; }
-            t = __ldcg(&rec[u0].info.t); wlo0 = (unsigned)sy.pos + 1; B0 = sy.Fs;
+            t = __ldcg(&rec[u0].info.t); wlo0 = (unsigned)sy.pos + 1; B0 = p.ust[u0].F0 + sy.Fs;
         }
         const unsigned uend = __ldg(p.tr_base + t) + __ldg(p.tr_nseg + t);
         PState x{B0, 0, 0, 0, 0, 0, ~0u, ~0u};
-        unsigned u = u0, end_sync = 0;
-        for (;; ++u) {
-            const bool first = u == u0;
-            const unsigned wlo = first ? wlo0 : 0u;
-            unsigned whi = (unsigned)kUnit;
-            if (!first || tfirst) {                          // the piece ends at this unit's first sync event
-                const int sp = p.sync[u].pos;
-                if (sp >= 0) { whi = (unsigned)sp + 1; end_sync = 1; }
+        unsigned end_sync = 0, ulast = uend - 1;
+        // the piece's units 32 at a time (lane = unit): one load of their start F, F range and first sync
+        // event; a unit whose range stays inside the band around B (and holds no sync event, and is not
+        // the piece's first unit after a sync event) passes the state through unchanged and is not walked
+        for (unsigned u = u0; u < uend && !end_sync; u += 32) {
+            const unsigned ub = u + (unsigned)lane;
+            const bool valid = ub < uend;
+            long long hiU = kNeg, loU = kPos;
+            int sp = -1;
+            if (valid) {
+                const long long F0 = p.ust[ub].F0;
+                hiU = F0 + __ldcg(&rec[ub].umx); loU = F0 + __ldcg(&rec[ub].umn);
+                if (ub != u0 || tfirst) sp = p.sync[ub].pos;  // the piece ends at this unit's first sync event
             }
-            const UnitStart us = p.ust[u];
-            const Slot& S = rec[u];
-            if (wlo == 0 && lane == 0) {                     // the state entering the unit
-                UnitLocal* l = p.ul + u;
-                l->n_start = x.n; l->lep_start = x.lep; l->lep_ptr_start = x.lep_ptr;
+            const bool opener = ub == u0 && !tfirst;          // starts after the sync event: window [wlo0, ...)
+            unsigned k = 0;                                   // lanes of the batch handled
+            for (;;) {
+                const bool need = valid && (unsigned)lane >= k &&
+                                  (sp >= 0 || opener || hiU >= x.B + p.T || loU <= x.B - p.T);
+                const unsigned nmask = __ballot_sync(kFull, need);
+                const unsigned kn = nmask ? (unsigned)(__ffs(nmask) - 1) : 32u;
+                if (valid && (unsigned)lane >= k && (unsigned)lane < kn) {   // passed through
+                    UnitLocal* l = p.ul + ub;
+                    l->n_start = x.n; l->lep_start = x.lep; l->lep_ptr_start = x.lep_ptr; l->n_end = x.n;
+                }
+                if (kn == 32u) break;
+                const unsigned uw = u + kn;
+                const unsigned wlo = uw == u0 ? wlo0 : 0u;
+                const int spk = __shfl_sync(kFull, sp, (int)kn);
+                unsigned whi = (unsigned)kUnit;
+                if (spk >= 0) { whi = (unsigned)spk + 1; end_sync = 1; }
+                if (wlo == 0 && lane == 0) {                  // the state entering the unit
+                    UnitLocal* l = p.ul + uw;
+                    l->n_start = x.n; l->lep_start = x.lep; l->lep_ptr_start = x.lep_ptr;
+                }
+                const UnitStart us = p.ust[uw];
+                piece_unit(p, rec[uw], us.F0, us.M0, wlo, whi, x, lane, stage[threadIdx.x >> 5]);
+                if (whi == (unsigned)kUnit && lane == 0) p.ul[uw].n_end = x.n;
+                if (end_sync) { ulast = uw; break; }
+                k = kn + 1;
             }
-            const long long umx = __ldcg(&S.umx), umn = __ldcg(&S.umn);
-            if (us.F0 + umx >= x.B + p.T || us.F0 + umn <= x.B - p.T)    // the F range can leave the band
-                piece_unit(p, S, us.F0, us.M0, wlo, whi, x, lane, stage[threadIdx.x >> 5]);
-            if (whi == (unsigned)kUnit && lane == 0) p.ul[u].n_end = x.n;
-            if (end_sync || u + 1 == uend) break;
         }
+        const unsigned u = ulast;
         if (lane == 0) {
             PieceCount c;
             c.n = x.n; c.nep = x.nep; c.lep = x.lep; c.lep_ptr = x.lep_ptr; c.ffirst = x.ffirst; c.flast = x.B;
@@ -538,8 +562,8 @@ cudaError_t launch_pchain(const ReplayParams& p, cudaStream_t st)
 {
     if (p.n_segs == 0) return cudaSuccess;
     auto grid = [](unsigned warps) { return std::max(1u, std::min((warps + 3) / 4, 148u * 16)); };
-    pc_prefix_kernel<<<grid(p.n_traces), 128, 0, st>>>(p);
-    pc_sync_kernel<<<grid(p.n_segs), 128, 0, st>>>(p);
+    const unsigned nbp = grid(p.n_traces);                   // pc_prefix and pc_sync are independent: one launch
+    pc_scan_kernel<<<nbp + grid(p.n_segs), 128, 0, st>>>(p, nbp);
     static int run_blocks = 0;                               // resident pc_run blocks (it takes pieces from a counter)
     if (!run_blocks) {
         int dev = 0, nsm = 0, occ = 0;

@@ -212,7 +212,7 @@ struct ReplayParams {
 // has one (piece id n_traces + unit), each ending at the first sync event of a later unit (included)
 // or at the trace end.
 struct UnitStart { long long F0, M0; };                  // F before the unit's first event; max F before it (M_-1 = 0)
-struct SyncInfo { long long Fs, Ms; int pos, pad0; long long pad1; };   // pos: unit position (-1: none); F, max F through it
+struct SyncInfo { long long Fs, pad2; int pos, pad0; long long pad1; };  // pos: unit position (-1: none); F through it, relative to the unit start
 constexpr int kPBlock = 64;                              // samples per scratch block of a piece
 struct PieceCount {                                      // one piece's chain (pc_run)
     unsigned long long n, nep;                           // samples, new-maximum samples (episode starts)

@@ -76,7 +76,7 @@ def test_launch_count_and_pass_times():
     the replay kernel and the kernels after it (cold-site Tier E, split chains)."""
     for cfg, mode, want in ((tracegen.CONFIGS[2].with_traces(2), 1, 2),         # replay + post
                             (tracegen.CONFIGS[3].with_traces(2), 1, 4),         # + cold_hist + cold_sum (50,000 sites)
-                            (tracegen.CONFIGS[2].with_traces(2), SPLIT, 7)):    # + 5 pchain kernels
+                            (tracegen.CONFIGS[2].with_traces(2), SPLIT, 6)):    # + 4 pchain kernels
         ev, off = tracegen.generate(cfg)
         tr = scl.scl_trace_load(ev, off, cfg.n_sites)
         r = None
