@@ -11,5 +11,7 @@ timeout 1500 python -m pytest tests -m gpu -x -q --deselect tests/test_gpu_fulls
 echo "== checked build: tools/fuzz.py $N cases, seeds 1 and 2"
 timeout 1200 python tools/fuzz.py $N 1 2>&1 | tail -2
 timeout 1200 python tools/fuzz.py $N 2 2>&1 | tail -2
+echo "== checked build: tools/fuzz.py $N cases with the chain split forced, seed 3"
+FUZZ_CHAIN=2 timeout 1200 python tools/fuzz.py $N 3 2>&1 | tail -2
 echo "== checked build: tools/sanitize.py"
 timeout 900 python tools/sanitize.py 2>&1 | tail -4
