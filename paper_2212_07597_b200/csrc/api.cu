@@ -241,20 +241,21 @@ static scl_status site_remap(scl_traces* tr, const scl_event* src, bool src_dev,
     tr->remapped = false; tr->h_inv.clear(); changed = false;
     if (n_sites <= (uint32_t)kHot || n == 0) return SCL_OK;
     const uint64_t want = 1ull << 21, stride = std::max<uint64_t>(1, n / want), m = (n + stride - 1) / stride;
-    std::vector<scl_event> smp;
-    const scl_event* hv = src;
-    if (src_dev) {
-        smp.resize(m);
-        CU(cudaMemcpy2DAsync(smp.data(), sizeof(scl_event), src, stride * sizeof(scl_event), sizeof(scl_event), m,
-                             cudaMemcpyDeviceToHost, st));
-        CU(cudaStreamSynchronize(st));
-        hv = smp.data();
-    }
     std::vector<uint32_t> cnt(n_sites, 0);
-    for (uint64_t i = 0; i < m; ++i) {
-        const uint64_t meta = (src_dev ? hv[i] : hv[i * stride]).meta;
-        const uint32_t site = ev_site(meta);
-        if (site < n_sites && ev_kind(meta) < 2) ++cnt[site];
+    if (src_dev) {                                    // counted on the device, n_sites words back
+        unsigned* d_cnt = nullptr;
+        if (cudaMallocAsync(&d_cnt, (size_t)n_sites * 4, st) != cudaSuccess) { cudaGetLastError(); return SCL_OK; }
+        CU(cudaMemsetAsync(d_cnt, 0, (size_t)n_sites * 4, st));
+        CU(launch_site_sample(src, stride, m, n_sites, d_cnt, st));
+        CU(cudaMemcpyAsync(cnt.data(), d_cnt, (size_t)n_sites * 4, cudaMemcpyDeviceToHost, st));
+        CU(cudaFreeAsync(d_cnt, st));
+        CU(cudaStreamSynchronize(st));
+    } else {
+        for (uint64_t i = 0; i < m; ++i) {
+            const uint64_t meta = src[i * stride].meta;
+            const uint32_t site = ev_site(meta);
+            if (site < n_sites && ev_kind(meta) < 2) ++cnt[site];
+        }
     }
     std::vector<uint32_t> order(n_sites);
     for (uint32_t i = 0; i < n_sites; ++i) order[i] = i;

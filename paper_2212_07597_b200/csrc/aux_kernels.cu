@@ -127,6 +127,29 @@ cudaError_t launch_load_stats(const scl_event* ev, const unsigned long long* off
     return cudaGetLastError();
 }
 
+// Load-time site frequencies (the site renumbering, api.cu site_remap) from a device source: every
+// stride-th event's site (allocs and frees), counted in cnt[n_sites] -- one kernel and one small
+// copy back instead of a strided 16-B-row copy of the sample to the host.
+__global__ void site_sample_kernel(const scl_event* src, unsigned long long stride, unsigned long long m,
+                                   unsigned n_sites, unsigned* cnt)
+{
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long meta = __ldg(&src[i * stride].meta);
+        const unsigned site = ev_site(meta);
+        if (site < n_sites && ev_kind(meta) < 2) atomicAdd(&cnt[site], 1u);
+    }
+}
+
+cudaError_t launch_site_sample(const scl_event* src, unsigned long long stride, unsigned long long m,
+                               unsigned n_sites, unsigned* cnt, cudaStream_t st)
+{
+    if (m == 0) return cudaSuccess;
+    const unsigned blocks = (unsigned)std::min<unsigned long long>((m + 255) / 256, 148ull * 8);
+    site_sample_kernel<<<blocks, 256, 0, st>>>(src, stride, m, n_sites, cnt);
+    return cudaGetLastError();
+}
+
 bool report_fused(unsigned n_sites) { return n_sites <= kReportSites; }
 
 cudaError_t launch_report(const FinalParams& p, scl_site_row* rows, cudaStream_t st)

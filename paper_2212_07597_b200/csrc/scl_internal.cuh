@@ -307,6 +307,8 @@ cudaError_t launch_load_stats(const scl_event* ev, const unsigned long long* off
                               unsigned long long n_events, unsigned n_sites, unsigned long long* sabs,
                               unsigned long long* err, scl_event* dst, unsigned long long* shist,
                               const unsigned* remap, cudaStream_t st);
+cudaError_t launch_site_sample(const scl_event* src, unsigned long long stride, unsigned long long m,
+                               unsigned n_sites, unsigned* cnt, cudaStream_t st);
 cudaError_t launch_permute_table(const unsigned long long* tin, unsigned long long* tout, const unsigned* remap,
                                  unsigned n_sites, cudaStream_t st);
 cudaError_t launch_replay(const CUtensorMap* tmap, const ReplayParams& p, int grid, cudaStream_t st);
