@@ -60,6 +60,7 @@ struct scl_traces {
     std::vector<uint64_t> h_off, h_sabs;
     uint32_t n_segs = 0;
     mutable unsigned int epoch = 0;
+    mutable uint32_t zc_arrivals = 0;          // CTAs of the replay launches since ticket[8] was zeroed
     CUtensorMap tmap;
     // rate sampler (lazy, per loaded traces): alloc / free / copy bytes per unit, before each unit, per trace
     mutable unsigned long long *d_usum = nullptr, *d_ustart = nullptr, *d_ttot = nullptr;
@@ -316,10 +317,10 @@ static scl_status upload(scl_traces* tr, const scl_event* src, bool src_dev, std
         tr->cap_tr = nt1;
     }
     if (!tr->d_err) {
-        if (!grow(tr->d_err, 65) || !grow(tr->d_ticket, 8)) { cudaFree(tr->d_err); tr->d_err = nullptr; return nomem("counters"); }
+        if (!grow(tr->d_err, 65) || !grow(tr->d_ticket, 10)) { cudaFree(tr->d_err); tr->d_err = nullptr; return nomem("counters"); }
         // ticket[7] is the "run prepared" flag compared with the run's epoch: a fresh block may hold
         // a freed handle's epoch (fuzzing found producers starting before CTA 0 had prepared)
-        CU(cudaMemsetAsync(tr->d_ticket, 0, 8 * sizeof(unsigned), st));
+        CU(cudaMemsetAsync(tr->d_ticket, 0, 10 * sizeof(unsigned), st));
     }
     // A device source is copied by the statistics pass itself (one read of the source, one write to
     // HBM -- the events are not read back).  Host memory takes the DMA copy, then the statistics pass
@@ -666,7 +667,7 @@ static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const sc
     // epoch-tagged unit aggregate words: no per-run clear
     // (the aggregate words carry the low 16 bits: cleared, and tag 0 skipped, once per 2^16 runs)
     if (!base) {                               // a new stream pass (a re-threshold reads the last one)
-        if (tr->epoch >= (1u << 30)) { tr->epoch = 0; CU(cudaMemsetAsync(tr->d_ticket, 0, 8 * 4, st)); }   // no stale "prepared"
+        if (tr->epoch >= (1u << 30)) { tr->epoch = 0; tr->zc_arrivals = 0; CU(cudaMemsetAsync(tr->d_ticket, 0, 10 * 4, st)); }   // no stale "prepared"
         if (((tr->epoch + 1) & 0xffffu) == 0) { CU(cudaMemsetAsync(tr->d_uagg, 0, tr->cap_segs * 32, st)); tr->epoch += 1; }
         if (tr->epoch == 0) CU(cudaMemsetAsync(tr->d_uagg, 0, tr->cap_segs * 32, st));
         tr->epoch += 1;
@@ -760,7 +761,9 @@ static scl_status replay_impl(uint64_t threshold, const scl_traces* tr, const sc
         if (split) { CU(launch_pchain(p, st)); r->nlaunch += 4; }
         else { CU(launch_rechain(p, st)); r->nlaunch += tr->n_segs ? 1 : 0; }
     } else {
+        p.zc_target = tr->zc_arrivals + (uint32_t)r->grid;      // every CTA of every launch arrives once
         CU(launch_replay(&tr->tmap, p, r->grid, st));
+        if (tr->n_segs) tr->zc_arrivals += (uint32_t)r->grid;
         if (tm) CU(cudaEventRecord(r->kev[3 * ks + 1], st));
         CU(launch_cold_hist(p, st));           // Tier E of the sites beyond the shared-memory table
         r->nlaunch += (tr->n_segs ? 1 : 0) + cold_hist_launches(p);

@@ -96,14 +96,27 @@ __device__ __forceinline__ unsigned bloom_mask(unsigned long long ptr) {
 #define PROF_TOUCH(v)
 #endif
 
-// ============================================================================ per-run preparation (CTA 0)
-__device__ void prepare_run(const ReplayParams& rp, unsigned long long* scratch)
+// ============================================================================ per-run preparation
+// Every CTA zeroes its slice of the site table, trace summaries and runner states, then arrives on
+// ticket[8] (never reset between launches: the host passes the count after this launch's arrivals,
+// zc_target); wait_prepared also waits for all arrivals.  (One CTA zeroing config 3's 4-MB table
+// held every producer ~20 us.)
+__device__ void zero_slice(const ReplayParams& rp)
+{
+    const PrepParams& p = rp.prep;
+    const size_t tid = threadIdx.x, nth = blockDim.x, b = blockIdx.x, nb = gridDim.x;
+    auto slice = [&](unsigned long long* a, size_t n) {
+        for (size_t i = n * b / nb + tid, hi = n * (b + 1) / nb; i < hi; i += nth) a[i] = 0;
+    };
+    slice(p.table, p.table_words); slice(p.summ, p.summ_words); slice(p.run, p.run_words);
+    __syncthreads();
+    if (tid == 0) { __threadfence(); atomicAdd(rp.ticket + 8, 1u); }
+}
+
+__device__ void prepare_run(const ReplayParams& rp, unsigned long long* scratch)   // CTA 0
 {
     const PrepParams& p = rp.prep;
     const unsigned tid = threadIdx.x, nth = blockDim.x;
-    for (size_t i = tid; i < p.table_words; i += nth) p.table[i] = 0;
-    for (size_t i = tid; i < p.summ_words; i += nth) p.summ[i] = 0;
-    for (size_t i = tid; i < p.run_words; i += nth) p.run[i] = 0;
     if (tid < 7) p.ticket[tid] = 0;
     if (tid < 2 && rp.cctr) rp.cctr[tid] = 0;              // cold-record pool: allocated, exhausted
     for (unsigned i = tid; i < p.n_sb; i += nth) p.rsbcnt[i] = 0;
@@ -132,6 +145,7 @@ __device__ void prepare_run(const ReplayParams& rp, unsigned long long* scratch)
 
 __device__ __forceinline__ void wait_prepared(const ReplayParams& p) {
     while (ld_relaxed(&p.ticket[7]) != p.epoch) __nanosleep(32);
+    while ((int)(ld_relaxed(&p.ticket[8]) - p.zc_target) < 0) __nanosleep(32);
     fence_acquire();
 }
 
@@ -1182,6 +1196,7 @@ replay_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         asm volatile("prefetch.tensormap [%0];" :: "l"((uint64_t)&tmap) : "memory");
     }
     __syncthreads();
+    zero_slice(p);
     if (blockIdx.x == 0) prepare_run(p, reinterpret_cast<unsigned long long*>(stage));   // stage: not in use yet
 
     // register rebalancing per warpgroup (launch: 96/thread): the four compute warpgroups give 16

@@ -172,6 +172,7 @@ struct ReplayParams {
     unsigned int n_segs;
     unsigned int n_runners;           // gridDim.x * kEmbeddedRunners
     unsigned int epoch;               // run number on this traces handle (ready tag)
+    unsigned int zc_target;           // ticket[8] once every CTA of this replay launch zeroed its slice
     unsigned int n_sites;
     unsigned int n_traces;
     int hwm_sample;                   // 1: new maximum against earlier sample footprints (SCL_HWM_SAMPLE)
