@@ -147,7 +147,7 @@ struct PState {
 // to the row start, and the meta words, event-major ([j][lane]) so that a dynamic event index is one shared-memory load.
 struct RowStage {
     long long F[kEpt][32], P[kEpt][32];
-    unsigned long long meta[kEpt][32];
+    unsigned long long meta[kEpt][33];                   // (padded: the transposing stores below)
 };
 
 // Bits j of [a, b) within [0, kEpt).
@@ -200,7 +200,18 @@ __device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, l
         const int c = __ffs(ccm) - 1;
         const long long row = row_base + (long long)c * 32 + lane;
         unsigned long long rm[kEpt];
-        load_row_meta(p.ev, row, rm);
+        {   // the chunk's 256 meta words with coalesced loads (lane l: events 32k + l), transposed to
+            // rows through the stage (event 32k + l is event l % 8 of row 4k + l / 8)
+            const scl_event* cev = p.ev + (row_base + (long long)c * 32) * kEpt;
+            unsigned long long v[kEpt];
+            #pragma unroll
+            for (int k = 0; k < kEpt; ++k) v[k] = __ldcg(&cev[k * 32 + lane].meta);
+            #pragma unroll
+            for (int k = 0; k < kEpt; ++k) st.meta[lane & 7][4 * k + (lane >> 3)] = v[k];
+            __syncwarp();
+            #pragma unroll
+            for (int jj = 0; jj < kEpt; ++jj) rm[jj] = st.meta[jj][lane];
+        }
         const long long Fc = Fu + shfl_ll(sPc, c);
         const long long cm1 = shfl_ll(cmx, c > 0 ? c - 1 : 0);
         const long long Mc = c > 0 ? llmax(Mu, cm1) : Mu;                             // max F before chunk c
@@ -262,9 +273,9 @@ __device__ void piece_unit(const ReplayParams& p, const Slot& S, long long Fu, l
         }
         const long long Fl = Fc + ssum - run;                                         // F before the lane's row
         const long long Ml = lane == 0 ? Mc : llmax(Mc, Fc + smax);                   // max F before it
-        // stage the row: F after each event, the meta word
+        // stage the row: F after each event (the meta words are staged already)
         #pragma unroll
-        for (int jj = 0; jj < kEpt; ++jj) { st.F[jj][lane] = Fl + fe[jj]; st.meta[jj][lane] = rm[jj]; }
+        for (int jj = 0; jj < kEpt; ++jj) st.F[jj][lane] = Fl + fe[jj];
         __syncwarp();
         // ---- (1) the sample positions, in order
         unsigned smask = 0;
