@@ -67,7 +67,7 @@ __device__ void pc_prefix(const ReplayParams& p, unsigned blk, unsigned nb)
 // relative to the unit start (pc_run adds the unit's F0: this pass does not wait for pc_prefix).  A
 // chunk can hold one only if its F range, chunk start included, spans at least 2T - 1.
 // (blocks [nb0, gridDim.x) of the pc_scan launch)
-__device__ void pc_sync(const ReplayParams& p, unsigned blk, unsigned nb)
+__device__ void pc_sync(const ReplayParams& p, unsigned blk, unsigned nb, unsigned long long (*tb)[33])
 {
     const int lane = threadIdx.x & 31;
     const unsigned w = (blk * blockDim.x + threadIdx.x) >> 5, nw = (nb * blockDim.x) >> 5;
@@ -85,7 +85,18 @@ __device__ void pc_sync(const ReplayParams& p, unsigned blk, unsigned nb)
             cand &= cand - 1;
             const long long row = row_base + (long long)c * 32 + lane;
             unsigned long long rm[kEpt];
-            load_row_meta(p.ev, row, rm);
+            {   // coalesced loads of the chunk's meta words, transposed to rows (as in pc_run)
+                const scl_event* cev = p.ev + (row_base + (long long)c * 32) * kEpt;
+                unsigned long long v[kEpt];
+                #pragma unroll
+                for (int k = 0; k < kEpt; ++k) v[k] = __ldcg(&cev[k * 32 + lane].meta);
+                __syncwarp();
+                #pragma unroll
+                for (int k = 0; k < kEpt; ++k) tb[lane & 7][4 * k + (lane >> 3)] = v[k];
+                __syncwarp();
+                #pragma unroll
+                for (int jj = 0; jj < kEpt; ++jj) rm[jj] = tb[jj][lane];
+            }
             const long long e0 = row * kEpt - off_t;
             long long run = 0;
             unsigned sy = 0;
@@ -131,8 +142,9 @@ __device__ void pc_sync(const ReplayParams& p, unsigned blk, unsigned nb)
 
 __global__ void __launch_bounds__(128) pc_scan_kernel(const __grid_constant__ ReplayParams p, unsigned nbp)
 {
+    __shared__ unsigned long long tb[4][kEpt][33];           // pc_sync: per-warp transposition buffer
     if (blockIdx.x < nbp) pc_prefix(p, blockIdx.x, nbp);
-    else pc_sync(p, blockIdx.x - nbp, gridDim.x - nbp);
+    else pc_sync(p, blockIdx.x - nbp, gridDim.x - nbp, tb[threadIdx.x >> 5]);
 }
 
 // ---------------------------------------------------------------------------- pc_run

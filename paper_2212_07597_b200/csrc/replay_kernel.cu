@@ -943,15 +943,18 @@ __device__ void runner_role(const ReplayParams& p, unsigned ri, int lane)
 __device__ __forceinline__ bool chunk_has_free(const ReplayParams& p, long long row0, long long off_t, long long n_t,
                                                unsigned pos0, unsigned long long ptr, unsigned sbeg, unsigned send, int lane)
 {
-    const long long row = row0 + lane;
-    unsigned long long rp[kEpt], rm[kEpt];
-    load_row_global(p.ev, row, rp, rm);
+    // the chunk's 256 events with coalesced loads: lane l reads events 32k + l (no row order needed)
+    const ulonglong2* cev = reinterpret_cast<const ulonglong2*>(p.ev + row0 * kEpt);
+    ulonglong2 v[kEpt];
+    #pragma unroll
+    for (int k = 0; k < kEpt; ++k) v[k] = __ldcg(cev + k * 32 + lane);
     bool hit = false;
     #pragma unroll
-    for (int jj = 0; jj < kEpt; ++jj) {
-        const long long ie = row * kEpt + jj - off_t;
-        const unsigned q = pos0 + (unsigned)lane * kEpt + jj;
-        hit |= rp[jj] == ptr && q >= sbeg && q < send && ie >= 0 && ie < n_t && ev_kind(rm[jj]) == 1;
+    for (int k = 0; k < kEpt; ++k) {
+        const unsigned e = (unsigned)(k * 32 + lane);
+        const long long ie = row0 * kEpt + e - off_t;
+        const unsigned q = pos0 + e;
+        hit |= v[k].x == ptr && q >= sbeg && q < send && ie >= 0 && ie < n_t && ev_kind(v[k].y) == 1;
     }
     return __any_sync(kFull, hit);
 }
