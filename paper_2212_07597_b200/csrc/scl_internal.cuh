@@ -239,9 +239,12 @@ cudaError_t launch_pchain(const ReplayParams& p, cudaStream_t st);
 // carries 32 zeroed rows past its last row for exactly these lanes (scl_trace_load).
 __device__ __forceinline__ void load_row_global(const scl_event* ev, long long row,
                                                 unsigned long long* ptr, unsigned long long* meta) {
-    const ulonglong2* q = reinterpret_cast<const ulonglong2*>(ev + row * kEpt);
+    // 32-B loads (two events each, LDG.256 on sm_100): each sector of the row is requested once
+    const scl_event* q = ev + row * kEpt;
     #pragma unroll
-    for (int j = 0; j < kEpt; ++j) { ulonglong2 v = __ldcg(q + j); ptr[j] = v.x; meta[j] = v.y; }
+    for (int j = 0; j < kEpt; j += 2)
+        asm volatile("ld.global.v4.u64 {%0, %1, %2, %3}, [%4];"
+                     : "=l"(ptr[j]), "=l"(meta[j]), "=l"(ptr[j + 1]), "=l"(meta[j + 1]) : "l"(q + j));
 }
 
 __device__ __forceinline__ void load_row_meta(const scl_event* ev, long long row, unsigned long long* meta) {
